@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark: sparse MTTKRP HBM GB/s & CP-ALS ms/iter at R=16 (BASELINE.json).
+
+One "step" = one CP-ALS iteration over the resident tensor: an MTTKRP for
+every mode plus the ALS glue (Gram/Hadamard/Cholesky/solve/normalise/fit) and,
+for N > 1 ranks, the NCCL exchange of each updated factor -- every row of
+SURVEY.md §8(a) that repeats per iteration (a3-a9).  Ingest (a1) and
+build_perm (a2) are one-time setup, timed separately and reported in
+"setup".  Default workload: the NELL-2-shaped config (BASELINE configs[2],
+where the metric's HBM-fraction target is stated), R=16, fp64.
+
+value = B_model bytes of the step's MTTKRPs (per-gather north
+star byte model) / device time per step, whole job; ms_per_step = CP-ALS
+ms/iteration.  Launch: `python bench.py --gpus N --steps K --warmup W`
+(N > 1 under torch.distributed.run, one rank per GPU, NCCL).
+`--impl reference` times the CPU oracle (the reference arm for this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+from paper_1809_09175_b200 import metrics  # noqa: E402
+
+METRIC = "sparse MTTKRP HBM GB/s & CP-ALS ms/iter at R=16, 1/2/4/8 B200"
+FALLBACK_HBM = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback (GB/s)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="sptk", choices=["sptk", "reference"])
+    ap.add_argument("--config", default="nell2", choices=list(synth.CONFIGS))
+    ap.add_argument("--rank", type=int, default=16)
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU seconds for the oracle baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        j = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def traffic_for(workload_key: str):
+    """ncu DRAM bytes per MTTKRP launch from the committed capture, if any."""
+    try:
+        j = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return j.get(workload_key)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ clocks
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+           0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [s[0] for s in self.samples]
+        mask = 0
+        for s in self.samples:
+            mask |= s[2]
+        reasons = [name for bit, name in REASONS.items() if mask & bit and name != "gpu_idle"]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ oracle leg
+def oracle_sample_rate(c, R: int, target_s: float, np_dtype):
+    """Time the oracle (row-owned OpenMP form, as it stands) on a bounded
+    sample of the workload: the first P_s nonzeros of the same generator
+    stream, full-size factors.  Returns (GB/s under B_model, threads, desc)."""
+    import oracle
+    A = [synth.factor(c.seed_f, c.N, m, int(I), R).astype(np_dtype).astype(np.float64)
+         for m, I in enumerate(c.dims)]
+
+    def run(Ps):
+        idx, vals = synth.tensor(c.seed, c.dims, Ps, c.dist)
+        vals = vals.astype(np_dtype).astype(np.float64)
+        perms = [oracle.perm(idx, n, int(I)) for n, I in enumerate(c.dims)]
+        t0 = time.perf_counter()
+        nt = 1
+        for n in range(c.N):
+            _, nt = oracle.mttkrp_omp(c.dims, idx, vals, A, n, perms[n][0], perms[n][1])
+        dt = time.perf_counter() - t0
+        s_v = np.dtype(np_dtype).itemsize
+        b = sum(metrics.b_model(c.N, Ps, R, int(I), s_v) for I in c.dims)
+        return b, dt, nt
+
+    Ps = min(c.nnz, 1_000_000)
+    b, dt, nt = run(Ps)
+    if dt < target_s and Ps < c.nnz:
+        Ps = int(min(c.nnz, Ps * max(1.0, target_s / max(dt, 1e-3))))
+        b, dt, nt = run(Ps)
+    desc = (f"first {Ps:,} of {c.nnz:,} nonzeros of the {c.name} generator stream, full-size "
+            f"factors, MTTKRP of all {c.N} modes (oracle_mttkrp_omp: counting-sort perm + "
+            f"row-owned OpenMP; perm not timed); {dt:.2f} s")
+    return b / dt / 1e9, nt, desc, Ps, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    c = synth.CONFIGS[args.config]
+    np_dtype = np.float64 if args.dtype == "f64" else np.float32
+    per_step = max(1.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    vals = []
+    desc = cores = None
+    for k in range(args.warmup + args.steps):
+        gbs, cores, desc, Ps, dt = oracle_sample_rate(c, args.rank, per_step, np_dtype)
+        if k >= args.warmup:
+            vals.append(gbs)
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+        "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": workload_name(c, args.rank, args.dtype)},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_name(c, R, dtype):
+    d = "x".join(str(x) for x in c.dims)
+    return f"{c.name}-shaped {c.N}-way {d}, {c.nnz:,} nnz, {c.dist}, R={R}, {dtype}"
+
+
+# ------------------------------------------------------------------ GPU leg
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1809_09175_b200 as sp
+    from synth import device as sdev
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = sp.comm_from_process_group() if world > 1 else None
+
+    c = synth.CONFIGS[args.config]
+    R = args.rank
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    s_v = 8 if args.dtype == "f64" else 4
+    stream = torch.cuda.current_stream()
+
+    # ---- setup: generate (device), ingest, build perms (timed, not in the step)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    e0, e1, e2 = ev(), ev(), ev()
+    e0.record()
+    idx_d, val_d = sdev.tensor(c.seed, c.dims, c.nnz, c.dist, dtype=tdt)
+    e1.record()
+    t = sp.sptensor_create(c.dims, idx_d, val_d)
+    e2.record()
+    torch.cuda.synchronize()
+    del idx_d, val_d
+    perm_ms = []
+    for n in range(c.N):
+        a, b = ev(), ev()
+        a.record()
+        sp.build_perm(t, n)
+        b.record()
+        torch.cuda.synchronize()
+        perm_ms.append(a.elapsed_time(b))
+    F = [sdev.factor(c.seed_f, c.N, m, I, R, dtype=tdt) for m, I in enumerate(c.dims)]
+
+    # per-rank share of the work (row-range sharding) for the byte model
+    bounds, pos = [], []
+    for n, I in enumerate(c.dims):
+        rp = torch.empty(I + 1, dtype=torch.int32, device="cuda")
+        sp.get_rowptr(t, n, rp)
+        rph = rp.cpu().numpy().view(np.uint32)
+        bd = sp.partition_rows(rph, world)
+        bounds.append(bd)
+        pos.append((int(rph[bd[rank]]), int(rph[bd[rank + 1]])))
+    bm_total = sum(metrics.b_model(c.N, c.nnz, R, I, s_v) for I in c.dims)
+    bm_rank = sum(metrics.b_model(c.N, pos[n][1] - pos[n][0], R,
+                                  int(bounds[n][rank + 1] - bounds[n][rank]), s_v)
+                  for n in range(c.N))
+
+    def step():
+        return sp.cp_als(t, R, 1, F, init=F, comm=comm, trace=False)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device time, CUDA events on the launching stream)
+    sp.profile_reset()
+    sp.profile_enable(True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        start, end = ev(), ev()
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+        end.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    sp.profile_enable(False)
+    prof = sp.profile_read()
+    ms = start.elapsed_time(end) / args.steps
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = bm_total / (ms_max * 1e-3) / 1e9
+
+    # dominant kernel (MTTKRP) roofline on this rank
+    mttkrp_ms_launch = prof["mttkrp_ms"] / max(1, prof["mttkrp_launches"])
+    achieved = (bm_rank / c.N) / (mttkrp_ms_launch * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    key = f"{args.config}_R{R}_{args.dtype}"
+    traffic = traffic_for(key)
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        Fh = [torch.empty((I, R), dtype=tdt).pin_memory() for I in c.dims]
+        for m in range(c.N):
+            Fh[m].copy_(F[m].cpu())
+        for _ in range(2):
+            sp.cp_als(t, R, 1, Fh, init=Fh, comm=comm, trace=False)
+        barrier()
+        torch.cuda.synchronize()
+        a, b = ev(), ev()
+        a.record(stream)
+        for _ in range(args.steps):
+            sp.cp_als(t, R, 1, Fh, init=Fh, comm=comm, trace=False)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms = a.elapsed_time(b) / args.steps
+        et = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        fbytes = sum(I * R * s_v for I in c.dims)
+        e2e = {"value": bm_total / (float(et.item()) * 1e-3) / 1e9, "unit": "GB/s",
+               "ms_per_step": float(et.item()), "h2d_bytes_per_step": fbytes,
+               "d2h_bytes_per_step": fbytes + 8,
+               "path": "sptk_cp_als(max_iters=1) with pinned HOST factor buffers: H2D of all "
+                       "factors, one ALS iteration, D2H of the factors and the fit, per step; "
+                       "the tensor is ingested once (setup)"}
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        gbs, cores, desc, Ps, dt = oracle_sample_rate(
+            c, R, args.cpu_seconds, np.float64 if args.dtype == "f64" else np.float32)
+        cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": args.dtype, "data": "synthetic",
+            "config": {
+                "workload": workload_name(c, R, args.dtype), "dims": list(c.dims),
+                "nnz": c.nnz, "R": R, "dist": c.dist, "seed": c.seed, "seed_f": c.seed_f,
+                "step": "one CP-ALS iteration (MTTKRP all modes + glue + exchange)",
+                "parallelism": f"row-range shard x{world}" if world > 1 else "single GPU",
+                "l2": "inputs larger than L2 (records %.2f GB + perms %.2f GB vs 126 MB L2); "
+                      "factor matrices (%.1f MB) are L2-resident by design" % (
+                          c.nnz * (32 if args.dtype == 'f64' or c.N > 3 else 16) / 1e9,
+                          c.N * c.nnz * 4 / 1e9, sum(I * R * s_v for I in c.dims) / 1e6),
+            },
+            "cp_als_ms_per_iter": ms_max,
+            "mttkrp_ms_per_mode": mttkrp_ms_launch,
+            "b_model_bytes_per_step": bm_total,
+            "gflops": sum(metrics.flops(c.N, c.nnz, R) for _ in c.dims) / (ms_max * 1e-3) / 1e9,
+            "setup": {"generate_ms": e0.elapsed_time(e1), "create_ms": e1.elapsed_time(e2),
+                      "build_perm_ms": perm_ms,
+                      "sort_to_iteration_ratio": sum(perm_ms) / ms_max},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "mttkrp_fast_kernel (permuted traversal)",
+                         "bytes_model": "B_model per launch = P(N*4+s_v) + P(N-1)R*s_v + I_n*R*s_v "
+                                        "(per-gather, SURVEY 8(d)); can exceed HBM peak when "
+                                        "gathers hit L2 (P:716)",
+                         "peak_source": peak_src,
+                         "frac_of_8TBps": achieved / 8000.0},
+            "clocks": clk.summary(),
+            "gpu_launches": prof["kernel_launches"],
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    t.close()
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

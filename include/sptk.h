@@ -1,0 +1,193 @@
+/*
+ * sptk.h -- C ABI of the B200-native sparse MTTKRP / CP-ALS library
+ * (libsptk.so), the hot path of arXiv 1809.09175 (GenTen, "Sparse Tensor
+ * Decomposition Algorithms for Performance Portability").
+ *
+ * Citations: P:NNN = line of the paper text (reference PAPER.md), with the
+ * section / equation / figure named; S:NNN = line of the CPU-program SPEC.md
+ * (interfaces only).  Design and readings: DESIGN.md.
+ *
+ * Conventions (all calls):
+ *  - Every call returns sptk_status (0 = SPTK_OK).  On error a thread-local
+ *    message is available from sptk_last_error().  Precondition violations
+ *    never abort.  After SPTK_ECUDA the handle is poisoned (every later call
+ *    on it returns SPTK_ECUDA).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Device work is stream-ordered on it; calls return without
+ *    synchronising unless stated.
+ *  - "device or host" pointers are classified with cudaPointerGetAttributes:
+ *    host (pageable or pinned) memory is staged through device buffers inside
+ *    the call (that call then synchronises `stream`).
+ *  - Factor matrices are row-major I_m x R ("row-wise memory
+ *    layout"), element type = the tensor's dtype, caller-owned.
+ *  - Limits: 1 <= nmodes <= 6 (cp_als: >= 2); 1 <= dims[m] < 2^32;
+ *    0 <= nnz < 2^32; R >= 1.  Indices are 0-based (Z2).
+ *  - A handle is immutable after sptk_build_perm and may be shared by
+ *    concurrent sptk_mttkrp calls on different streams; it is not
+ *    thread-safe during create / build_perm / cp_als.
+ */
+#ifndef SPTK_H
+#define SPTK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { SPTK_F32 = 1, SPTK_F64 = 2 } sptk_dtype;
+typedef enum { SPTK_IDX_I64 = 1, SPTK_IDX_U32 = 2 } sptk_idx_type;
+
+typedef enum {
+    SPTK_OK = 0,
+    SPTK_EINVAL = 1,       /* bad argument (null pointer, dtype mismatch, shape) */
+    SPTK_ERANGE = 2,       /* a coordinate >= dims[m] (or < 0) */
+    SPTK_EDUP = 3,         /* reserved: duplicate coordinate under a DUP_ERROR policy */
+    SPTK_ENOPERM = 4,      /* sptk_build_perm(mode) has not been run */
+    SPTK_ENOMEM = 5,       /* device allocation failed */
+    SPTK_ECUDA = 6,        /* CUDA runtime error (handle poisoned) */
+    SPTK_ENCCL = 7,        /* NCCL missing or failed */
+    SPTK_ESINGULAR = 8,    /* Cholesky of Gamma failed after the ridge retry */
+    SPTK_EZERONORM = 9,    /* ||X|| = 0 in cp_als */
+    SPTK_EUNSUPPORTED = 10 /* outside the limits above */
+} sptk_status;
+
+typedef struct sptk_tensor_s *sptk_tensor; /* opaque; owns device records, perms, rowptrs */
+typedef struct sptk_comm_s *sptk_comm;     /* opaque; owns an ncclComm_t */
+
+/* Library version string, e.g. "sptk 0.1 sm_100a". */
+const char *sptk_version(void);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char *sptk_last_error(void);
+
+/* ---------------------------------------------------------------- tensor */
+
+/* Create a COO sparse tensor ("a P-vector of real values and a
+ * P x d vector of coordinates"; COO).
+ *   nmodes   d (1..6)
+ *   dims     host int64[nmodes], I_m >= 1
+ *   nnz      P >= 0 (0 = empty tensor)
+ *   idx      device or host, nnz x nmodes row-major, 0-based; element type
+ *            itype (int64 or uint32).  May be NULL iff nnz == 0.
+ *   vals     device or host, nnz values of `dtype`.  NULL iff nnz == 0.
+ *   flags    0 (duplicates allowed: MTTKRP is linear in X; Z3)
+ *   out      receives the handle
+ * Copies the input into packed device records {value, idx[d]} (16 or 32 B)
+ * after validating 0 <= idx < dims (SPTK_ERANGE otherwise) -- the caller may
+ * free its buffers when the call returns.  Also caches ||X||^2.  Synchronises
+ * `stream` once (reading the validation flag). */
+sptk_status sptk_sptensor_create(int nmodes, const int64_t *dims, int64_t nnz,
+                                 const void *idx, sptk_idx_type itype, const void *vals,
+                                 sptk_dtype dtype, unsigned flags, void *stream,
+                                 sptk_tensor *out);
+
+/* Free all device memory owned by the handle (NULL is a no-op). */
+sptk_status sptk_sptensor_destroy(sptk_tensor t);
+
+/* Shape query: any output pointer may be NULL; dims receives nmodes values. */
+sptk_status sptk_sptensor_info(sptk_tensor t, int *nmodes, int64_t *dims, int64_t *nnz,
+                               sptk_dtype *dtype);
+
+/* Device bytes owned by the handle (records + perms + rowptrs + workspace). */
+sptk_status sptk_sptensor_device_bytes(sptk_tensor t, int64_t *bytes);
+
+/* Build the mode-`mode` permutation (mode = -1: all modes).  P:513-515 (§5
+ * "Permutation approach"): "a permutation array for each mode that sorts the
+ * tensor nonzeros in increasing index along that mode"; the sort is STABLE
+ * (ties keep storage order), so the permutation is unique.
+ * Also builds rowptr_n[I_n+1] (start of each mode-n row in permuted order).
+ * On-GPU LSD radix sort; temporary device memory ~16 B x nnz. */
+sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream);
+
+/* Copy perm_n (uint32[nnz]) / rowptr_n (uint32[I_n + 1]) to `out` (device or
+ * host).  SPTK_ENOPERM if build_perm(mode) has not run. */
+sptk_status sptk_get_perm(sptk_tensor t, int mode, uint32_t *out, void *stream);
+sptk_status sptk_get_rowptr(sptk_tensor t, int mode, uint32_t *out, void *stream);
+
+/* ---------------------------------------------------------------- MTTKRP */
+
+/* Mode-n MTTKRP, Eq. (2):
+ *   out(k, j) = lambda_j * sum_{i : l_in = k} x_i * prod_{m != n} A_m(l_im, j)
+ * computed by permuted traversal (§5, Fig. mttkrp_perm): nonzeros
+ * are visited in perm_n order, a row is accumulated in registers and written
+ * when the mode-n index changes -- plain store for rows interior to a
+ * worker's block, atomic add for a block's first/last row.
+ *   mode     n in [0, nmodes)
+ *   R        rank (columns), >= 1
+ *   factors  HOST array of nmodes DEVICE pointers, factors[m] is I_m x R
+ *            row-major of the tensor's dtype; factors[mode] is ignored (may
+ *            be NULL)
+ *   lambda   device R-vector or NULL (= all ones; Z1)
+ *   out      device I_n x R, overwritten (rows without nonzeros are exactly 0;
+ *            S:239)
+ *   comm     NULL: single GPU.  Otherwise each rank computes the rows of its
+ *            contiguous row range (sptk_partition_rows over rowptr_n) and the
+ *            full `out` is replicated on every rank by NCCL broadcasts.
+ * Result equals Eq. (2) up to floating-point summation order (atomics).
+ * SPTK_ENOPERM if build_perm(mode) has not run. */
+sptk_status sptk_mttkrp(sptk_tensor t, int mode, int64_t R, const void *const *factors,
+                        const void *lambda, void *out, sptk_comm comm, void *stream);
+
+/* ---------------------------------------------------------------- CP-ALS */
+
+/* CP-ALS (the paper omits the algorithm and defers to Kolda &
+ * Bader): textbook alternating least squares, readings in DESIGN.md §2.
+ * For it < max_iters, for n = 0..N-1: V = MTTKRP(n); Gamma = Hadamard of
+ * A_m^T A_m (m != n); A_n = V Gamma^{-1} (Cholesky; one ridge retry with
+ * 1e-12 tr(Gamma)/R); lambda = column 2-norms; normalise.  fit = 1 - ||X - M||
+ * / ||X|| after each iteration; stop when tol > 0 and |fit - fit_prev| < tol.
+ *   init        HOST array of nmodes pointers (device or host) with the
+ *               initial factors, or NULL: A_m(r, c) = U[0,1) drawn from the
+ *               counter generator of DESIGN.md §3 with seed `seed`
+ *               (stream nmodes+1+m, counter r*R+c).  init[m] may equal
+ *               factors_out[m] (in place).
+ *   factors_out HOST array of nmodes pointers (device or host), I_m x R each
+ *   lambda_out  R values (device or host) or NULL
+ *   fit_out, iters_out   host scalars or NULL
+ *   fit_trace   host double[max_iters] or NULL
+ *   comm        NULL or a communicator (row-range sharding of every mode;
+ *               factors replicated on all ranks)
+ * Requires nmodes >= 2.  Builds missing perms.  Synchronises `stream` once
+ * per iteration (the fit).  SPTK_EZERONORM if ||X|| = 0; SPTK_ESINGULAR if
+ * Gamma stays singular. */
+sptk_status sptk_cp_als(sptk_tensor t, int64_t R, int max_iters, double tol, uint64_t seed,
+                        const void *const *init, void *const *factors_out, void *lambda_out,
+                        double *fit_out, int *iters_out, double *fit_trace, sptk_comm comm,
+                        void *stream);
+
+/* --------------------------------------------------------- multi-GPU */
+
+/* Fill `id128` (128 bytes, host) with a new NCCL unique id (rank 0 only;
+ * broadcast it to the other ranks out of band, e.g. torch.distributed). */
+sptk_status sptk_comm_unique_id(void *id128);
+
+/* Create / destroy a communicator over `nranks` processes (one GPU each;
+ * the current CUDA device is used).  Collective: every rank must call it. */
+sptk_status sptk_comm_create(const void *id128, int nranks, int rank, sptk_comm *out);
+sptk_status sptk_comm_destroy(sptk_comm c);
+
+/* Host-only (no GPU needed): split rows [0, In) into nranks contiguous ranges
+ * of near-equal nonzero counts.  rowptr (host, In+1 entries, non-decreasing,
+ * rowptr[0] = 0, rowptr[In] = nnz).  bounds (host, nranks+1): rank g owns rows
+ * [bounds[g], bounds[g+1]) and positions [rowptr[bounds[g]],
+ * rowptr[bounds[g+1]]).  bounds[g] = min{ r : rowptr[r] >= ceil(g*nnz/nranks) }
+ * for 0 < g < nranks, bounds[0] = 0, bounds[nranks] = In. */
+sptk_status sptk_partition_rows(const uint32_t *rowptr, int64_t In, int nranks,
+                                int64_t *bounds);
+
+/* ---------------------------------------------------------- measurement */
+
+/* When enabled, the library brackets every MTTKRP kernel launch with CUDA
+ * events on its launch stream and accumulates the elapsed time (read after
+ * the stream is synchronised).  Launch counters count every kernel the
+ * library launches.  Not thread-safe; for benchmarking. */
+sptk_status sptk_profile_enable(int on);
+sptk_status sptk_profile_reset(void);
+sptk_status sptk_profile_read(double *mttkrp_ms, int64_t *mttkrp_launches,
+                              int64_t *kernel_launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPTK_H */

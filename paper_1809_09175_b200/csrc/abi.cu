@@ -1,0 +1,325 @@
+// abi.cu -- C ABI entry points for tensors, perms, partitioning, profiling.
+// The ABI is declared (with citations) in include/sptk.h.
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+
+#include "common.cuh"
+
+namespace sptk {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string &msg) { g_err = msg; }
+sptk_status fail(sptk_status st, const std::string &msg) {
+    g_err = msg;
+    return st;
+}
+sptk_status cuda_fail(cudaError_t e, const char *what) {
+    g_err = std::string("CUDA error '") + cudaGetErrorString(e) + "' in " + what;
+    return SPTK_ECUDA;
+}
+
+Profile &profile() {
+    static Profile p;
+    return p;
+}
+
+sptk_status mttkrp_span_begin(cudaStream_t s, cudaEvent_t *b) {
+    *b = nullptr;
+    if (!profile().on) return SPTK_OK;
+    SPTK_CUDA(cudaEventCreate(b));
+    SPTK_CUDA(cudaEventRecord(*b, s));
+    return SPTK_OK;
+}
+sptk_status mttkrp_span_end(cudaStream_t s, cudaEvent_t b) {
+    if (!profile().on || !b) return SPTK_OK;
+    cudaEvent_t e;
+    SPTK_CUDA(cudaEventCreate(&e));
+    SPTK_CUDA(cudaEventRecord(e, s));
+    profile().pending.push_back({b, e});
+    profile().mttkrp_launches += 1;
+    return SPTK_OK;
+}
+
+int dev_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+            sms <= 0)
+            sms = kNumSMs;
+    }
+    return sms;
+}
+
+sptk_status DevBuf::reserve(size_t n) {
+    if (n <= bytes && p) return SPTK_OK;
+    release();
+    if (n == 0) return SPTK_OK;
+    cudaError_t e = cudaMalloc(&p, n);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        return fail(SPTK_ENOMEM, "cudaMalloc of " + std::to_string(n) + " bytes failed: " +
+                                     cudaGetErrorString(e));
+    }
+    bytes = n;
+    return SPTK_OK;
+}
+
+bool is_device_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ------------------------------------------------------------ kernels: sum
+// Deterministic fixed-order sum of `n` doubles with one block.
+__global__ void sum_f64_kernel(const double *__restrict__ in, int64_t n, double *__restrict__ out) {
+    __shared__ double sh[256];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += in[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
+sptk_status launch_sum_f64(const double *in, int64_t n, double *out, cudaStream_t s) {
+    sum_f64_kernel<<<1, 256, 0, s>>>(in, n, out);
+    count_launch();
+    SPTK_CUDA(cudaGetLastError());
+    return SPTK_OK;
+}
+
+}  // namespace sptk
+
+using namespace sptk;
+
+#define CHECK_HANDLE(t)                                                                \
+    do {                                                                               \
+        if (!(t)) return fail(SPTK_EINVAL, "null tensor handle");                      \
+        if ((t)->poisoned) return fail(SPTK_ECUDA, "tensor handle poisoned by an earlier CUDA error"); \
+    } while (0)
+
+extern "C" {
+
+const char *sptk_version(void) { return "sptk 0.1 sm_100a"; }
+
+const char *sptk_last_error(void) { return g_err.c_str(); }
+
+sptk_status sptk_sptensor_create(int nmodes, const int64_t *dims, int64_t nnz, const void *idx,
+                                 sptk_idx_type itype, const void *vals, sptk_dtype dtype,
+                                 unsigned flags, void *stream, sptk_tensor *out) {
+    if (!out) return fail(SPTK_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (nmodes < 1 || nmodes > kMaxModes)
+        return fail(SPTK_EUNSUPPORTED, "nmodes must be in [1, 6]");
+    if (!dims) return fail(SPTK_EINVAL, "dims is NULL");
+    for (int m = 0; m < nmodes; ++m)
+        if (dims[m] < 1 || dims[m] >= (int64_t(1) << 32))
+            return fail(SPTK_EUNSUPPORTED, "dims[m] must be in [1, 2^32)");
+    if (nnz < 0) return fail(SPTK_EINVAL, "nnz < 0");
+    if (nnz >= (int64_t(1) << 32)) return fail(SPTK_EUNSUPPORTED, "nnz must be < 2^32");
+    if (dtype != SPTK_F32 && dtype != SPTK_F64) return fail(SPTK_EINVAL, "bad dtype");
+    if (itype != SPTK_IDX_I64 && itype != SPTK_IDX_U32) return fail(SPTK_EINVAL, "bad idx type");
+    if (flags != 0) return fail(SPTK_EUNSUPPORTED, "flags must be 0 (duplicates allowed)");
+    if (nnz > 0 && (!idx || !vals)) return fail(SPTK_EINVAL, "idx/vals NULL with nnz > 0");
+
+    cudaStream_t s = (cudaStream_t)stream;
+    sptk_tensor t = new (std::nothrow) sptk_tensor_s();
+    if (!t) return fail(SPTK_ENOMEM, "host allocation failed");
+    t->N = nmodes;
+    for (int m = 0; m < nmodes; ++m) t->dims[m] = dims[m];
+    t->P = nnz;
+    t->dtype = dtype;
+    t->rec_bytes = record_bytes(dtype, nmodes);
+    cudaGetDevice(&t->device);
+
+    sptk_status st = SPTK_OK;
+    if (nnz > 0) {
+        DevBuf sidx, svals, flag;
+        const size_t ib = (itype == SPTK_IDX_I64 ? 8 : 4) * (size_t)nnz * nmodes;
+        const size_t vb = (size_t)dtype_bytes(dtype) * nnz;
+        const void *didx = idx, *dvals = vals;
+        if ((st = t->rec.reserve((size_t)t->rec_bytes * nnz)) != SPTK_OK) goto bad;
+        if (!is_device_ptr(idx)) {
+            if ((st = sidx.reserve(ib)) != SPTK_OK) goto bad;
+            if (cudaMemcpyAsync(sidx.p, idx, ib, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+                st = cuda_fail(cudaGetLastError(), "H2D idx");
+                goto bad;
+            }
+            didx = sidx.p;
+        }
+        if (!is_device_ptr(vals)) {
+            if ((st = svals.reserve(vb)) != SPTK_OK) goto bad;
+            if (cudaMemcpyAsync(svals.p, vals, vb, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+                st = cuda_fail(cudaGetLastError(), "H2D vals");
+                goto bad;
+            }
+            dvals = svals.p;
+        }
+        if ((st = flag.reserve(16)) != SPTK_OK) goto bad;
+        int *d_flag = flag.as<int>();
+        double *d_norm = reinterpret_cast<double *>(flag.as<char>() + 8);
+        if (cudaMemsetAsync(d_flag, 0, 8, s) != cudaSuccess) {
+            st = cuda_fail(cudaGetLastError(), "memset flag");
+            goto bad;
+        }
+        if ((st = launch_pack(t, didx, itype, dvals, d_flag, d_norm, s)) != SPTK_OK) goto bad;
+        struct {
+            int flag;
+            int pad;
+            double norm;
+        } h;
+        if (cudaMemcpyAsync(&h, flag.p, 16, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess) {
+            st = cuda_fail(cudaGetLastError(), "create: reading validation flag");
+            goto bad;
+        }
+        if (h.flag) {
+            st = fail(SPTK_ERANGE, "a coordinate is outside [0, dims[m])");
+            goto bad;
+        }
+        t->normX2 = h.norm;
+    }
+    *out = t;
+    return SPTK_OK;
+bad:
+    delete t;
+    return st;
+}
+
+sptk_status sptk_sptensor_destroy(sptk_tensor t) {
+    if (!t) return SPTK_OK;
+    delete t;
+    return SPTK_OK;
+}
+
+sptk_status sptk_sptensor_info(sptk_tensor t, int *nmodes, int64_t *dims, int64_t *nnz,
+                               sptk_dtype *dtype) {
+    if (!t) return fail(SPTK_EINVAL, "null tensor handle");
+    if (nmodes) *nmodes = t->N;
+    if (dims)
+        for (int m = 0; m < t->N; ++m) dims[m] = t->dims[m];
+    if (nnz) *nnz = t->P;
+    if (dtype) *dtype = t->dtype;
+    return SPTK_OK;
+}
+
+sptk_status sptk_sptensor_device_bytes(sptk_tensor t, int64_t *bytes) {
+    if (!t || !bytes) return fail(SPTK_EINVAL, "null argument");
+    int64_t b = t->rec.bytes;
+    for (int m = 0; m < t->N; ++m) b += t->perm[m].bytes + t->rowptr[m].bytes;
+    const ALSWork &w = t->als;
+    b += w.V.bytes + w.G.bytes + w.L.bytes + w.partial.bytes + w.colsq.bytes + w.lam.bytes +
+         w.scal.bytes + w.stage.bytes + w.lamT.bytes;
+    *bytes = b;
+    return SPTK_OK;
+}
+
+sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream) {
+    CHECK_HANDLE(t);
+    if (mode < -1 || mode >= t->N) return fail(SPTK_EINVAL, "mode out of range");
+    cudaStream_t s = (cudaStream_t)stream;
+    for (int m = (mode < 0 ? 0 : mode); m < (mode < 0 ? t->N : mode + 1); ++m) {
+        sptk_status st = build_perm_mode(t, m, s);
+        if (st == SPTK_ECUDA) t->poisoned = true;
+        if (st != SPTK_OK) return st;
+    }
+    return SPTK_OK;
+}
+
+static sptk_status copy_out(void *out, const void *src, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return SPTK_OK;
+    const bool dev = is_device_ptr(out);
+    SPTK_CUDA(cudaMemcpyAsync(out, src, bytes,
+                              dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    if (!dev) SPTK_CUDA(cudaStreamSynchronize(s));
+    return SPTK_OK;
+}
+
+sptk_status sptk_get_perm(sptk_tensor t, int mode, uint32_t *out, void *stream) {
+    CHECK_HANDLE(t);
+    if (mode < 0 || mode >= t->N) return fail(SPTK_EINVAL, "mode out of range");
+    if (!t->has_perm[mode]) return fail(SPTK_ENOPERM, "build_perm(mode) has not run");
+    if (t->P > 0 && !out) return fail(SPTK_EINVAL, "out is NULL");
+    return copy_out(out, t->perm[mode].p, sizeof(uint32_t) * (size_t)t->P, (cudaStream_t)stream);
+}
+
+sptk_status sptk_get_rowptr(sptk_tensor t, int mode, uint32_t *out, void *stream) {
+    CHECK_HANDLE(t);
+    if (mode < 0 || mode >= t->N) return fail(SPTK_EINVAL, "mode out of range");
+    if (!t->has_perm[mode]) return fail(SPTK_ENOPERM, "build_perm(mode) has not run");
+    if (!out) return fail(SPTK_EINVAL, "out is NULL");
+    return copy_out(out, t->rowptr[mode].p, sizeof(uint32_t) * (size_t)(t->dims[mode] + 1),
+                    (cudaStream_t)stream);
+}
+
+sptk_status sptk_partition_rows(const uint32_t *rowptr, int64_t In, int nranks,
+                                int64_t *bounds) {
+    if (!rowptr || !bounds || In < 1 || nranks < 1)
+        return fail(SPTK_EINVAL, "partition_rows: bad argument");
+    const uint64_t P = rowptr[In];
+    bounds[0] = 0;
+    bounds[nranks] = In;
+    for (int g = 1; g < nranks; ++g) {
+        const uint64_t target = (P * (uint64_t)g + (uint64_t)nranks - 1) / (uint64_t)nranks;
+        // min r with rowptr[r] >= target (rowptr non-decreasing)
+        const uint32_t *it = std::lower_bound(rowptr, rowptr + In + 1, (uint32_t)target);
+        int64_t r = it - rowptr;
+        if (r > In) r = In;
+        if (r < bounds[g - 1]) r = bounds[g - 1];
+        bounds[g] = r;
+    }
+    return SPTK_OK;
+}
+
+sptk_status sptk_profile_enable(int on) {
+    profile().on = on != 0;
+    return SPTK_OK;
+}
+
+sptk_status sptk_profile_reset(void) {
+    Profile &p = profile();
+    for (auto &e : p.pending) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    p.pending.clear();
+    p.mttkrp_ms = 0.0;
+    p.mttkrp_launches = 0;
+    p.launches = 0;
+    return SPTK_OK;
+}
+
+sptk_status sptk_profile_read(double *mttkrp_ms, int64_t *mttkrp_launches,
+                              int64_t *kernel_launches) {
+    Profile &p = profile();
+    for (auto &e : p.pending) {
+        float ms = 0.f;
+        SPTK_CUDA(cudaEventSynchronize(e.second));
+        SPTK_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
+        p.mttkrp_ms += ms;
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    p.pending.clear();
+    if (mttkrp_ms) *mttkrp_ms = p.mttkrp_ms;
+    if (mttkrp_launches) *mttkrp_launches = p.mttkrp_launches;
+    if (kernel_launches) *kernel_launches = p.launches;
+    return SPTK_OK;
+}
+
+}  // extern "C"

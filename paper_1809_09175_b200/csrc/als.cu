@@ -1,0 +1,519 @@
+// als.cu -- CP-ALS glue and the sptk_cp_als driver.
+// The paper omits the algorithm ("Details are omitted here") and
+// defers to Kolda & Bader; these are the textbook steps (DESIGN.md §2
+// readings Z11, Z12):
+//   per mode n:  V = MTTKRP(X, A, n)          (mttkrp.cuh, lambda = NULL)
+//                Gamma = Hadamard_{m!=n} G_m  (G_m = A_m^T A_m, cached)
+//                Gamma = L L^T                (one block; ridge retry)
+//                A_n = V Gamma^{-1}           (per-row triangular solves)
+//                lambda_j = ||A_n(:,j)||_2, normalise (zero column -> e_1)
+//                G_n = A_n^T A_n
+//   per iteration: fit = 1 - sqrt(max(0, ||X||^2 + ||M||^2 - 2<X,M>)) / ||X||
+//                <X,M> = sum_j lambda_j sum_k A_{N-1}(k,j) V(k,j)
+//                ||M||^2 = lambda^T (Hadamard_m G_m) lambda
+// All reductions are fixed-order (per-block partials, then an in-order sum),
+// so a run is bit-reproducible; one 16-byte D2H (fit, status) per iteration.
+// Multi-GPU: each rank solves its own row range of every mode, the R column
+// sums of squares and <X,M> partials are all-reduced, the rows broadcast.
+#include <math.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace sptk {
+
+constexpr int kMaxAlsRank = 128;
+
+// ---------------------------------------------------------------- kernels
+// Counter generator of DESIGN.md §3 (same text as synth/), for init = NULL.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+template <typename T>
+__global__ void init_factor_kernel(uint64_t seed, uint64_t stream, int64_t n, T *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t d = splitmix64(seed ^ ((uint64_t)i * 0x9E3779B97F4A7C15ull) ^
+                                      (stream * 0xD1B54A32D192ED03ull));
+        out[i] = (T)((double)(d >> 11) * 0x1.0p-53);
+    }
+}
+
+// partial[b][e] = sum over the rows of block b of A(k,a) A(k,c), e = a*R + c
+template <typename T>
+__global__ void __launch_bounds__(256)
+    gram_partial_kernel(const T *__restrict__ A, int64_t I, int R, int64_t rows_per_block,
+                        double *__restrict__ partial) {
+    constexpr int TR = 32;  // rows staged per tile
+    extern __shared__ double tile[];  // TR x R
+    const int RR = R * R;
+    const int64_t r0 = blockIdx.x * rows_per_block;
+    const int64_t r1 = min(I, r0 + rows_per_block);
+    for (int e0 = 0; e0 < RR; e0 += 256 * 16) {
+        double acc[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+        for (int64_t rt = r0; rt < r1; rt += TR) {
+            const int nr = (int)min((int64_t)TR, r1 - rt);
+            __syncthreads();
+            for (int x = threadIdx.x; x < nr * R; x += blockDim.x)
+                tile[x] = (double)A[rt * R + x];
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const int e = e0 + k * 256 + threadIdx.x;
+                if (e < RR) {
+                    const int a = e / R, c = e % R;
+                    double s = acc[k];
+                    for (int r = 0; r < nr; ++r) s += tile[r * R + a] * tile[r * R + c];
+                    acc[k] = s;
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int e = e0 + k * 256 + threadIdx.x;
+            if (e < RR) partial[(int64_t)blockIdx.x * RR + e] = acc[k];
+        }
+    }
+}
+
+// out[e] = sum_b partial[b][e]  (fixed order)
+__global__ void reduce_partials_kernel(const double *__restrict__ partial, int nb, int ne,
+                                       double *__restrict__ out) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int b = 0; b < nb; ++b) s += partial[(int64_t)b * ne + e];
+        out[e] = s;
+    }
+}
+
+// partial[b][j] = sum over rows of block b of X(k,j) * Y(k,j)
+template <typename T>
+__global__ void __launch_bounds__(256)
+    coldot_partial_kernel(const T *__restrict__ X, const T *__restrict__ Y, int64_t r0,
+                          int64_t r1, int R, int64_t rows_per_block, double *__restrict__ partial) {
+    __shared__ double sh[256];
+    const int lanes = 256 / R;  // row lanes per column (R <= 256)
+    const int j = threadIdx.x % R, l = threadIdx.x / R;
+    const int64_t b0 = r0 + blockIdx.x * rows_per_block;
+    const int64_t b1 = min(r1, b0 + rows_per_block);
+    double s = 0.0;
+    if (l < lanes)
+        for (int64_t k = b0 + l; k < b1; k += lanes)
+            s += (double)X[k * R + j] * (double)Y[k * R + j];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x < R) {
+        double t = 0.0;
+        for (int q = 0; q < lanes; ++q) t += sh[q * R + threadIdx.x];
+        partial[(int64_t)blockIdx.x * R + threadIdx.x] = t;
+    }
+}
+
+// Gamma = Hadamard_{m != n} G_m, then L L^T = Gamma (+ ridge retry), one block.
+__global__ void __launch_bounds__(256)
+    gamma_chol_kernel(const double *__restrict__ G, int N, int n, int R, double *__restrict__ Lout,
+                      int *__restrict__ status) {
+    extern __shared__ double L[];  // R x R
+    __shared__ int bad;
+    __shared__ double ridge;
+    auto gamma = [&](int i, int j) {
+        double h = 1.0;
+        for (int m = 0; m < N; ++m)
+            if (m != n) h *= G[(int64_t)m * R * R + i * R + j];
+        return h;
+    };
+    if (threadIdx.x == 0) ridge = 0.0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        for (int x = threadIdx.x; x < R * R; x += blockDim.x) L[x] = 0.0;
+        if (threadIdx.x == 0) bad = 0;
+        __syncthreads();
+        for (int j = 0; j < R; ++j) {
+            if (threadIdx.x == 0) {
+                double d = gamma(j, j) + ridge;
+                for (int k = 0; k < j; ++k) d -= L[j * R + k] * L[j * R + k];
+                if (!(d > 0.0)) {
+                    bad = 1;
+                    d = 1.0;
+                }
+                L[j * R + j] = sqrt(d);
+            }
+            __syncthreads();
+            const double ljj = L[j * R + j];
+            for (int i = j + 1 + threadIdx.x; i < R; i += blockDim.x) {
+                double s = gamma(i, j);
+                for (int k = 0; k < j; ++k) s -= L[i * R + k] * L[j * R + k];
+                L[i * R + j] = s / ljj;
+            }
+            __syncthreads();
+        }
+        if (!bad) break;
+        if (threadIdx.x == 0) {
+            double tr = 0.0;
+            for (int j = 0; j < R; ++j) tr += gamma(j, j);
+            ridge = 1e-12 * (tr / (double)R);
+        }
+        __syncthreads();
+        if (attempt == 1 && threadIdx.x == 0) atomicOr(status, 1);
+    }
+    for (int x = threadIdx.x; x < R * R; x += blockDim.x) Lout[x] = L[x];
+}
+
+// A(k,:) = V(k,:) Gamma^{-1}: forward then back substitution, one row per thread.
+template <typename T>
+__global__ void row_solve_kernel(const T *__restrict__ V, int64_t r0, int64_t r1, int R,
+                                 const double *__restrict__ Lg, T *__restrict__ A) {
+    extern __shared__ double sm[];
+    double *L = sm;             // R x R
+    double *x = sm + R * R;     // R x blockDim (column-major by thread)
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) L[e] = Lg[e];
+    __syncthreads();
+    const int64_t k = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= r1) return;
+    const int bd = blockDim.x, t = threadIdx.x;
+    for (int i = 0; i < R; ++i) {
+        double s = (double)V[k * R + i];
+        for (int q = 0; q < i; ++q) s -= L[i * R + q] * x[q * bd + t];
+        x[i * bd + t] = s / L[i * R + i];
+    }
+    for (int i = R - 1; i >= 0; --i) {
+        double s = x[i * bd + t];
+        for (int q = i + 1; q < R; ++q) s -= L[q * R + i] * x[q * bd + t];
+        x[i * bd + t] = s / L[i * R + i];
+    }
+    for (int i = 0; i < R; ++i) A[k * R + i] = (T)x[i * bd + t];
+}
+
+// lambda_j = sqrt(colsq_j)
+__global__ void lambda_kernel(const double *__restrict__ colsq, int R, double *__restrict__ lam) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < R) lam[j] = sqrt(colsq[j]);
+}
+
+template <typename T>
+__global__ void normalize_kernel(T *__restrict__ A, int64_t r0, int64_t r1, int R,
+                                 const double *__restrict__ lam) {
+    const int64_t n = (r1 - r0) * R;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = r0 + i / R;
+        const int j = (int)(i % R);
+        const double l = lam[j];
+        T *a = A + k * R + j;
+        if (l == 0.0) *a = (T)(k == 0 ? 1.0 : 0.0);
+        else *a = (T)((double)*a / l);
+    }
+}
+
+// fit from s_j = sum_k A_{N-1}(k,j) V(k,j), lambda, G_m  -> out[0]
+__global__ void __launch_bounds__(256)
+    fit_kernel(const double *__restrict__ s, const double *__restrict__ lam,
+               const double *__restrict__ G, int N, int R, double normX2,
+               double *__restrict__ out) {
+    __shared__ double sh[256];
+    double acc = 0.0;
+    for (int a = threadIdx.x; a < R; a += blockDim.x)
+        for (int b = 0; b < R; ++b) {
+            double h = 1.0;
+            for (int m = 0; m < N; ++m) h *= G[(int64_t)m * R * R + a * R + b];
+            acc += lam[a] * h * lam[b];
+        }
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double normM2 = sh[0];
+        double inner = 0.0;
+        for (int j = 0; j < R; ++j) inner += lam[j] * s[j];
+        double res2 = normX2 + normM2 - 2.0 * inner;
+        if (res2 < 0.0) res2 = 0.0;
+        out[0] = 1.0 - sqrt(res2) / sqrt(normX2);
+        out[1] = inner;
+        out[2] = normM2;
+    }
+}
+
+template <typename T>
+__global__ void cast_kernel(const double *__restrict__ in, int n, T *__restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (T)in[i];
+}
+
+// ---------------------------------------------------------------- host
+static int grid_for(int64_t n, int per = 256) {
+    int64_t b = (n + per - 1) / per;
+    const int64_t cap = (int64_t)dev_sms() * 8;
+    if (b > cap) b = cap;
+    return b < 1 ? 1 : (int)b;
+}
+
+struct AlsCtx {
+    sptk_tensor t;
+    int64_t R;
+    cudaStream_t s;
+    sptk_comm comm;
+    std::vector<void *> A;                 // device factor pointers
+    std::vector<std::vector<int64_t>> b;   // per-mode row bounds (comm)
+    int nblocks;                           // partial-sum blocks
+};
+
+template <typename T>
+static sptk_status gram(AlsCtx &c, int m) {
+    sptk_tensor t = c.t;
+    ALSWork &w = t->als;
+    const int R = (int)c.R;
+    const int64_t I = t->dims[m];
+    int nb = (int)std::min<int64_t>(c.nblocks, (I + 31) / 32);
+    const int64_t rpb = (I + nb - 1) / nb;
+    nb = (int)((I + rpb - 1) / rpb);
+    const size_t sm = sizeof(double) * 32 * R;
+    gram_partial_kernel<T><<<nb, 256, sm, c.s>>>(static_cast<const T *>(c.A[m]), I, R, rpb,
+                                                 w.partial.as<double>());
+    reduce_partials_kernel<<<grid_for(R * R), 256, 0, c.s>>>(
+        w.partial.as<double>(), nb, R * R, w.G.as<double>() + (int64_t)m * R * R);
+    count_launch(2);
+    SPTK_CUDA(cudaGetLastError());
+    return SPTK_OK;
+}
+
+// colsum_j = sum_{k in [r0,r1)} X(k,j) Y(k,j) -> out (device, R doubles)
+template <typename T>
+static sptk_status coldot(AlsCtx &c, const T *X, const T *Y, int64_t r0, int64_t r1,
+                          double *out) {
+    const int R = (int)c.R;
+    ALSWork &w = c.t->als;
+    const int64_t n = r1 - r0;
+    if (n <= 0) {
+        SPTK_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * R, c.s));
+        return SPTK_OK;
+    }
+    int nb = (int)std::min<int64_t>(c.nblocks, (n + 63) / 64);
+    const int64_t rpb = (n + nb - 1) / nb;
+    nb = (int)((n + rpb - 1) / rpb);
+    coldot_partial_kernel<T><<<nb, 256, 0, c.s>>>(X, Y, r0, r1, R, rpb, w.partial.as<double>());
+    reduce_partials_kernel<<<grid_for(R), 256, 0, c.s>>>(w.partial.as<double>(), nb, R, out);
+    count_launch(2);
+    SPTK_CUDA(cudaGetLastError());
+    return SPTK_OK;
+}
+
+template <typename T>
+static sptk_status als_iteration(AlsCtx &c, double *fit_host, int *status_host) {
+    sptk_tensor t = c.t;
+    ALSWork &w = t->als;
+    const int N = t->N, R = (int)c.R;
+    const bool multi = c.comm && c.comm->nranks > 1;
+    double *colsq = w.colsq.as<double>();
+    double *lam = w.lam.as<double>();
+    double *scal = w.scal.as<double>();
+    int *status = reinterpret_cast<int *>(scal + 8);
+    T *V = w.V.as<T>();
+    for (int n = 0; n < N; ++n) {
+        const int64_t r0 = multi ? c.b[n][c.comm->rank] : 0;
+        const int64_t r1 = multi ? c.b[n][c.comm->rank + 1] : t->dims[n];
+        SPTK_TRY(mttkrp_launch(t, n, c.R, c.A.data(), nullptr, V, r0, r1, c.s));
+        gamma_chol_kernel<<<1, 256, sizeof(double) * R * R, c.s>>>(w.G.as<double>(), N, n, R,
+                                                                 w.L.as<double>(), status);
+        count_launch();
+        SPTK_CUDA(cudaGetLastError());
+        T *An = static_cast<T *>(c.A[n]);
+        if (r1 > r0) {
+            const int bd = R <= 64 ? 128 : 32;
+            const size_t sm = sizeof(double) * ((size_t)R * R + (size_t)R * bd);
+            row_solve_kernel<T><<<(unsigned)((r1 - r0 + bd - 1) / bd), bd, sm, c.s>>>(
+                V, r0, r1, R, w.L.as<double>(), An);
+            count_launch();
+            SPTK_CUDA(cudaGetLastError());
+        }
+        SPTK_TRY(coldot<T>(c, An, An, r0, r1, colsq));
+        if (multi) SPTK_TRY(comm_allreduce_f64(c.comm, colsq, R, c.s));
+        lambda_kernel<<<1, 128, 0, c.s>>>(colsq, R, lam);
+        if (r1 > r0) normalize_kernel<T><<<grid_for((r1 - r0) * R), 256, 0, c.s>>>(An, r0, r1, R, lam);
+        count_launch(2);
+        SPTK_CUDA(cudaGetLastError());
+        if (multi) SPTK_TRY(comm_bcast_rows(c.comm, An, c.R, t->dtype, c.b[n].data(), c.s));
+        SPTK_TRY(gram<T>(c, n));
+    }
+    // fit (last mode's V and A)
+    const int n = N - 1;
+    const int64_t r0 = multi ? c.b[n][c.comm->rank] : 0;
+    const int64_t r1 = multi ? c.b[n][c.comm->rank + 1] : t->dims[n];
+    SPTK_TRY(coldot<T>(c, static_cast<const T *>(c.A[n]), V, r0, r1, colsq));
+    if (multi) SPTK_TRY(comm_allreduce_f64(c.comm, colsq, R, c.s));
+    fit_kernel<<<1, 256, 0, c.s>>>(colsq, lam, w.G.as<double>(), N, R, t->normX2, scal);
+    count_launch();
+    SPTK_CUDA(cudaGetLastError());
+    double h[9];
+    SPTK_CUDA(cudaMemcpyAsync(h, scal, sizeof(double) * 9, cudaMemcpyDeviceToHost, c.s));
+    SPTK_CUDA(cudaStreamSynchronize(c.s));
+    *fit_host = h[0];
+    int st;
+    memcpy(&st, &h[8], sizeof(int));
+    *status_host = st;
+    return SPTK_OK;
+}
+
+template <typename T>
+static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double tol, uint64_t seed,
+                               const void *const *init, void *const *factors_out,
+                               void *lambda_out, double *fit_out, int *iters_out,
+                               double *fit_trace, sptk_comm comm, cudaStream_t s) {
+    const int N = t->N;
+    const size_t es = sizeof(T);
+    ALSWork &w = t->als;
+    int64_t Imax = 0, Isum = 0;
+    for (int m = 0; m < N; ++m) {
+        Imax = std::max(Imax, t->dims[m]);
+        Isum += t->dims[m];
+    }
+    AlsCtx c;
+    c.t = t;
+    c.R = R;
+    c.s = s;
+    c.comm = comm;
+    c.nblocks = dev_sms() * 2;
+    SPTK_TRY(w.V.reserve(es * Imax * R));
+    SPTK_TRY(w.G.reserve(sizeof(double) * N * R * R));
+    SPTK_TRY(w.L.reserve(sizeof(double) * R * R));
+    SPTK_TRY(w.partial.reserve(sizeof(double) * (size_t)c.nblocks * R * R));
+    SPTK_TRY(w.colsq.reserve(sizeof(double) * R));
+    SPTK_TRY(w.lam.reserve(sizeof(double) * R));
+    SPTK_TRY(w.scal.reserve(sizeof(double) * 16));
+    SPTK_TRY(w.lamT.reserve(es * R));
+    SPTK_CUDA(cudaMemsetAsync(w.scal.p, 0, sizeof(double) * 16, s));
+    w.R = R;
+
+    // factor storage: caller's device buffers, or staging for host buffers
+    std::vector<bool> host_out(N);
+    bool any_host = false;
+    for (int m = 0; m < N; ++m) {
+        host_out[m] = !is_device_ptr(factors_out[m]);
+        any_host = any_host || host_out[m];
+    }
+    if (any_host) SPTK_TRY(w.stage.reserve(es * Isum * R));
+    c.A.resize(N);
+    {
+        char *st = w.stage.as<char>();
+        for (int m = 0; m < N; ++m) {
+            if (host_out[m]) {
+                c.A[m] = st;
+                st += es * t->dims[m] * R;
+            } else {
+                c.A[m] = factors_out[m];
+            }
+        }
+    }
+    for (int m = 0; m < N; ++m) {
+        const size_t bytes = es * t->dims[m] * R;
+        if (!init || !init[m]) {
+            init_factor_kernel<T><<<grid_for(t->dims[m] * R), 256, 0, s>>>(
+                seed, (uint64_t)(N + 1 + m), t->dims[m] * R, static_cast<T *>(c.A[m]));
+            count_launch();
+            SPTK_CUDA(cudaGetLastError());
+        } else if (init[m] != c.A[m]) {
+            SPTK_CUDA(cudaMemcpyAsync(c.A[m], init[m], bytes, cudaMemcpyDefault, s));
+        }
+    }
+    for (int m = 0; m < N; ++m)
+        if (!t->has_perm[m]) SPTK_TRY(build_perm_mode(t, m, s));
+    const bool multi = comm && comm->nranks > 1;
+    if (multi) {
+        c.b.assign(N, std::vector<int64_t>(comm->nranks + 1));
+        for (int m = 0; m < N; ++m) {
+            SPTK_TRY(host_rowptr(t, m, s));
+            SPTK_TRY(sptk_partition_rows(t->host_rowptr[m].data(), t->dims[m], comm->nranks,
+                                         c.b[m].data()));
+        }
+    }
+    for (int m = 0; m < N; ++m) SPTK_TRY(gram<T>(c, m));
+
+    double fit = 0.0, fit_prev = 0.0;
+    int it = 0;
+    sptk_status st = SPTK_OK;
+    for (it = 0; it < max_iters; ++it) {
+        int bad = 0;
+        st = als_iteration<T>(c, &fit, &bad);
+        if (st != SPTK_OK) break;
+        if (bad) {
+            st = fail(SPTK_ESINGULAR, "Gamma is singular after the ridge retry");
+            break;
+        }
+        if (fit_trace) fit_trace[it] = fit;
+        if (tol > 0.0 && fabs(fit - fit_prev) < tol) {
+            ++it;
+            break;
+        }
+        fit_prev = fit;
+    }
+    if (fit_out) *fit_out = fit;
+    if (iters_out) *iters_out = it;
+    if (st != SPTK_OK) return st;
+    if (max_iters == 0) {  // lambda = ones
+        SPTK_CUDA(cudaMemsetAsync(w.lam.p, 0, sizeof(double) * R, s));
+        std::vector<double> ones(R, 1.0);
+        SPTK_CUDA(cudaMemcpyAsync(w.lam.p, ones.data(), sizeof(double) * R,
+                                  cudaMemcpyHostToDevice, s));
+        SPTK_CUDA(cudaStreamSynchronize(s));
+    }
+    for (int m = 0; m < N; ++m)
+        if (host_out[m])
+            SPTK_CUDA(cudaMemcpyAsync(factors_out[m], c.A[m], es * t->dims[m] * R,
+                                      cudaMemcpyDeviceToHost, s));
+    if (lambda_out) {
+        cast_kernel<T><<<(unsigned)((R + 127) / 128), 128, 0, s>>>(w.lam.as<double>(), (int)R,
+                                                                  w.lamT.as<T>());
+        count_launch();
+        SPTK_CUDA(cudaGetLastError());
+        SPTK_CUDA(cudaMemcpyAsync(lambda_out, w.lamT.p, es * R, cudaMemcpyDefault, s));
+    }
+    if (any_host || (lambda_out && !is_device_ptr(lambda_out)))
+        SPTK_CUDA(cudaStreamSynchronize(s));
+    return SPTK_OK;
+}
+
+}  // namespace sptk
+
+using namespace sptk;
+
+extern "C" sptk_status sptk_cp_als(sptk_tensor t, int64_t R, int max_iters, double tol,
+                                   uint64_t seed, const void *const *init,
+                                   void *const *factors_out, void *lambda_out, double *fit_out,
+                                   int *iters_out, double *fit_trace, sptk_comm comm,
+                                   void *stream) {
+    if (!t) return fail(SPTK_EINVAL, "null tensor handle");
+    if (t->poisoned) return fail(SPTK_ECUDA, "tensor handle poisoned by an earlier CUDA error");
+    if (t->N < 2) return fail(SPTK_EUNSUPPORTED, "cp_als needs nmodes >= 2");
+    if (R < 1) return fail(SPTK_EINVAL, "R must be >= 1");
+    if (R > kMaxAlsRank) return fail(SPTK_EUNSUPPORTED, "cp_als supports R <= 128");
+    if (max_iters < 0) return fail(SPTK_EINVAL, "max_iters < 0");
+    if (!factors_out) return fail(SPTK_EINVAL, "factors_out is NULL");
+    for (int m = 0; m < t->N; ++m)
+        if (!factors_out[m]) return fail(SPTK_EINVAL, "factors_out[m] is NULL");
+    if (!(t->normX2 > 0.0)) return fail(SPTK_EZERONORM, "||X|| = 0");
+    cudaStream_t s = (cudaStream_t)stream;
+    // row_solve shared memory can exceed the 48 KB default for R > 64
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(row_solve_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(row_solve_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(gamma_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    sptk_status st =
+        t->dtype == SPTK_F64
+            ? cp_als_impl<double>(t, R, max_iters, tol, seed, init, factors_out, lambda_out,
+                                  fit_out, iters_out, fit_trace, comm, s)
+            : cp_als_impl<float>(t, R, max_iters, tol, seed, init, factors_out, lambda_out,
+                                 fit_out, iters_out, fit_trace, comm, s);
+    if (st == SPTK_ECUDA) t->poisoned = true;
+    return st;
+}

@@ -1,0 +1,129 @@
+// common.cuh -- shared internals of libsptk (handle, errors, launch helpers).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sptk.h"
+
+namespace sptk {
+
+constexpr int kMaxModes = 6;
+constexpr int kNumSMs = 148;  // B200; the runtime value is queried in dev_sms()
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string &msg);
+sptk_status fail(sptk_status st, const std::string &msg);
+sptk_status cuda_fail(cudaError_t e, const char *what);
+
+#define SPTK_CUDA(expr)                                                        \
+    do {                                                                       \
+        cudaError_t _e = (expr);                                               \
+        if (_e != cudaSuccess) return ::sptk::cuda_fail(_e, #expr);            \
+    } while (0)
+
+#define SPTK_TRY(expr)                                                         \
+    do {                                                                       \
+        sptk_status _s = (expr);                                               \
+        if (_s != SPTK_OK) return _s;                                          \
+    } while (0)
+
+// ------------------------------------------------------------------ profile
+struct Profile {
+    bool on = false;
+    int64_t launches = 0;         // every kernel launched by the library
+    int64_t mttkrp_launches = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;  // mttkrp spans
+    double mttkrp_ms = 0.0;
+};
+Profile &profile();
+inline void count_launch(int n = 1) { profile().launches += n; }
+sptk_status mttkrp_span_begin(cudaStream_t s, cudaEvent_t *b);
+sptk_status mttkrp_span_end(cudaStream_t s, cudaEvent_t b);
+
+int dev_sms();
+
+// ------------------------------------------------------------------ memory
+// RAII device buffer (cudaMallocAsync-free, plain cudaMalloc for large,
+// long-lived buffers; workspaces are kept in the handle).
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    sptk_status reserve(size_t n);  // grows (contents not kept)
+    template <typename T> T *as() const { return static_cast<T *>(p); }
+};
+
+bool is_device_ptr(const void *p);
+
+// ------------------------------------------------------------------ tensor
+struct ALSWork {
+    int64_t R = 0;
+    DevBuf V;         // Imax x R (T)
+    DevBuf G;         // N x R x R (f64) Gram matrices
+    DevBuf L;         // R x R (f64) Cholesky factor of Gamma
+    DevBuf partial;   // per-block partial sums (f64)
+    DevBuf colsq;     // R (f64)
+    DevBuf lam;       // R (f64)
+    DevBuf scal;      // small f64 scalars (status, inner, fit ...)
+    DevBuf stage;     // host<->device staging for factors
+    DevBuf lamT;      // R (T) lambda in tensor dtype
+};
+
+}  // namespace sptk
+
+struct sptk_tensor_s {
+    int N = 0;
+    int64_t dims[sptk::kMaxModes] = {0};
+    int64_t P = 0;
+    sptk_dtype dtype = SPTK_F64;
+    int rec_bytes = 32;
+    sptk::DevBuf rec;                           // packed records
+    sptk::DevBuf perm[sptk::kMaxModes];         // uint32[P]
+    sptk::DevBuf rowptr[sptk::kMaxModes];       // uint32[I_n + 1]
+    bool has_perm[sptk::kMaxModes] = {false};
+    std::vector<uint32_t> host_rowptr[sptk::kMaxModes];  // for partitioning (lazy)
+    double normX2 = 0.0;
+    bool poisoned = false;
+    int device = 0;
+    sptk::ALSWork als;
+};
+
+struct sptk_comm_s {
+    void *nccl = nullptr;  // ncclComm_t
+    int nranks = 1;
+    int rank = 0;
+};
+
+namespace sptk {
+
+// record layout: value first, then nmodes uint32 indices, padded to 16/32 B
+inline int record_bytes(sptk_dtype dt, int N) {
+    const int vb = dt == SPTK_F64 ? 8 : 4;
+    return (vb + 4 * N <= 16) ? 16 : 32;
+}
+inline int dtype_bytes(sptk_dtype dt) { return dt == SPTK_F64 ? 8 : 4; }
+
+// --- kernels implemented in the .cu files (host launchers) ---
+sptk_status launch_pack(sptk_tensor t, const void *idx, sptk_idx_type itype, const void *vals,
+                        int *d_flag, double *d_normsq, cudaStream_t s);
+sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s);
+sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const *factors,
+                          const void *lambda, void *out, int64_t row_begin, int64_t row_end,
+                          cudaStream_t s);
+sptk_status host_rowptr(sptk_tensor t, int mode, cudaStream_t s);
+sptk_status comm_bcast_rows(sptk_comm c, void *buf, int64_t R, sptk_dtype dt,
+                            const int64_t *bounds, cudaStream_t s);
+sptk_status comm_allreduce_f64(sptk_comm c, double *buf, int64_t count, cudaStream_t s);
+
+}  // namespace sptk

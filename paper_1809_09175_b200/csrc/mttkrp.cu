@@ -1,0 +1,132 @@
+// mttkrp.cu -- host side of sptk_mttkrp: dispatch on (dtype, N, R), column
+// tiles, row-range (multi-GPU) launches.  Kernels: mttkrp.cuh.
+#include <stdlib.h>
+
+#include "mttkrp.cuh"
+
+namespace sptk {
+
+static int64_t run_length() {
+    static int64_t run = 0;
+    if (!run) {
+        const char *e = getenv("SPTK_RUN");
+        run = e ? atoll(e) : 256;
+        if (run < 2) run = 2;
+        run = (run + 1) / 2 * 2;  // multiple of the unroll (2)
+    }
+    return run;
+}
+
+static int pow2ceil(int x) {
+    int g = 1;
+    while (g < x) g <<= 1;
+    return g;
+}
+
+static bool aligned32(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; }
+
+sptk_status host_rowptr(sptk_tensor t, int mode, cudaStream_t s) {
+    std::vector<uint32_t> &h = t->host_rowptr[mode];
+    if (!h.empty()) return SPTK_OK;
+    h.resize((size_t)t->dims[mode] + 1);
+    SPTK_CUDA(cudaMemcpyAsync(h.data(), t->rowptr[mode].p, sizeof(uint32_t) * h.size(),
+                              cudaMemcpyDeviceToHost, s));
+    SPTK_CUDA(cudaStreamSynchronize(s));
+    return SPTK_OK;
+}
+
+sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const *factors,
+                          const void *lambda, void *out, int64_t row_begin, int64_t row_end,
+                          cudaStream_t s) {
+    const int64_t In = t->dims[mode];
+    const size_t es = dtype_bytes(t->dtype);
+    if (row_end <= row_begin) return SPTK_OK;
+    SPTK_CUDA(cudaMemsetAsync(static_cast<char *>(out) + (size_t)row_begin * R * es, 0,
+                              (size_t)(row_end - row_begin) * R * es, s));
+    int64_t pb = 0, pe = t->P;
+    if (row_begin != 0 || row_end != In) {
+        SPTK_TRY(host_rowptr(t, mode, s));
+        pb = t->host_rowptr[mode][row_begin];
+        pe = t->host_rowptr[mode][row_end];
+    }
+    if (pe <= pb) return SPTK_OK;
+
+    MttkrpArgs a{};
+    a.rec = t->rec.as<uint8_t>();
+    a.perm = t->perm[mode].as<uint32_t>();
+    a.pos_begin = pb;
+    a.pos_end = pe;
+    a.run = run_length();
+    a.ld = R;
+    a.mode = mode;
+    a.N = t->N;
+    a.rb = t->rec_bytes;
+    for (int m = 0; m < t->N; ++m) a.A[m] = (m == mode) ? nullptr : factors[m];
+    a.lambda = lambda;
+    a.out = out;
+    const int64_t workers = (pe - pb + a.run - 1) / a.run;
+
+    const int V = 32 / (int)es;
+    bool fast = t->N >= 3 && t->N <= 5 && R % V == 0 && aligned32(out) &&
+                (!lambda || aligned32(lambda));
+    for (int m = 0; m < t->N && fast; ++m)
+        if (m != mode && !aligned32(factors[m])) fast = false;
+
+    cudaEvent_t ev;
+    SPTK_TRY(mttkrp_span_begin(s, &ev));
+    if (fast) {
+        const int64_t tile = 32 * V;
+        for (int64_t c0 = 0; c0 < R; c0 += tile) {
+            a.col0 = (int)c0;
+            a.ncols = (int)((R - c0) < tile ? (R - c0) : tile);
+            const int G = pow2ceil(a.ncols / V);
+            if (t->dtype == SPTK_F64) SPTK_TRY(launch_fast<double>(t->N, G, t->rec_bytes, a, workers, s));
+            else SPTK_TRY(launch_fast<float>(t->N, G, t->rec_bytes, a, workers, s));
+        }
+    } else {
+        const int G = R <= 16 ? 4 : 32;
+        const int64_t tile = (int64_t)G * 4;
+        for (int64_t c0 = 0; c0 < R; c0 += tile) {
+            a.col0 = (int)c0;
+            a.ncols = (int)((R - c0) < tile ? (R - c0) : tile);
+            if (t->dtype == SPTK_F64) SPTK_TRY(launch_generic<double>(G, a, workers, s));
+            else SPTK_TRY(launch_generic<float>(G, a, workers, s));
+        }
+    }
+    SPTK_TRY(mttkrp_span_end(s, ev));
+    return SPTK_OK;
+}
+
+}  // namespace sptk
+
+using namespace sptk;
+
+extern "C" sptk_status sptk_mttkrp(sptk_tensor t, int mode, int64_t R,
+                                   const void *const *factors, const void *lambda, void *out,
+                                   sptk_comm comm, void *stream) {
+    if (!t) return fail(SPTK_EINVAL, "null tensor handle");
+    if (t->poisoned) return fail(SPTK_ECUDA, "tensor handle poisoned by an earlier CUDA error");
+    if (mode < 0 || mode >= t->N) return fail(SPTK_EINVAL, "mode out of range");
+    if (R < 1 || R > (int64_t(1) << 20)) return fail(SPTK_EINVAL, "R must be in [1, 2^20]");
+    if (!factors || !out) return fail(SPTK_EINVAL, "factors/out is NULL");
+    for (int m = 0; m < t->N; ++m)
+        if (m != mode && !factors[m]) return fail(SPTK_EINVAL, "factors[m] is NULL");
+    if (!t->has_perm[mode]) return fail(SPTK_ENOPERM, "build_perm(mode) has not run");
+    cudaStream_t s = (cudaStream_t)stream;
+    sptk_status st;
+    if (!comm || comm->nranks == 1) {
+        st = mttkrp_launch(t, mode, R, factors, lambda, out, 0, t->dims[mode], s);
+    } else {
+        st = host_rowptr(t, mode, s);
+        std::vector<int64_t> b(comm->nranks + 1);
+        if (st == SPTK_OK)
+            st = sptk_partition_rows(t->host_rowptr[mode].data(), t->dims[mode], comm->nranks,
+                                     b.data());
+        if (st == SPTK_OK)
+            st = mttkrp_launch(t, mode, R, factors, lambda, out, b[comm->rank],
+                               b[comm->rank + 1], s);
+        if (st == SPTK_OK) st = comm_bcast_rows(comm, out, R, t->dtype, b.data(), s);
+    }
+    if (st == SPTK_ECUDA) t->poisoned = true;
+    return st;
+}

@@ -1,0 +1,299 @@
+// mttkrp.cuh -- the hot-path kernel: permuted-traversal COO MTTKRP
+// (SURVEY §8(a) rows a3-a7), Eq. (2) of the paper computed by the
+// permutation approach of §5 (Fig. mttkrp_perm):
+//
+//   "Each thread within a team iterates over a given block size of tensor
+//    nonzeros and writes its contribution to the resulting factor matrix only
+//    when the mode-n coordinate changes.  This must be an atomic-write if the
+//    mode-n index is equal to the first or last index of the block ...;
+//    otherwise, it is a regular (non-atomic) write."
+//
+// B200 mapping:
+//   * a "worker" is a group of G lanes (G = R*sizeof(T)/32 rounded up to a
+//     power of two); its lanes span the R columns, each lane owning V = 32 B /
+//     sizeof(T) consecutive columns, so one factor row is one coalesced run of
+//     256-bit loads (LDG.E.ENL2.256) across the group;
+//   * each worker owns a contiguous run of `run` permuted positions (the
+//     paper's NZPTM block);
+//   * per position i: p = perm_n[i] (sequential), the 16/32-byte record
+//     {x_p, l_p*} (one random aligned load, L1::no_allocate), then the N-1
+//     factor rows A_m(l_pm, cols) (random 256-bit gathers: the dominant
+//     traffic), Hadamard product times x_p in registers, accumulated while
+//     the row is unchanged;
+//   * on a row change the register row is flushed: plain vector store for a
+//     row interior to the run (owned by this worker alone), red.global.add
+//     (fp64 scalar / fp32 .v4) for the run's first and last rows;
+//   * lambda (NULL = ones) is applied once per flush (Z1);
+//   * U positions are processed per step with the perm entries for the next
+//     step prefetched, so several records and 2U factor rows are in flight.
+// The generic kernel (any N <= 6, any R) uses scalar loads with runtime
+// record offsets and column tiles; same write discipline.
+#pragma once
+#include "common.cuh"
+
+namespace sptk {
+
+constexpr uint32_t kNoRow = 0xffffffffu;
+
+struct MttkrpArgs {
+    const uint8_t *rec;
+    const uint32_t *perm;
+    int64_t pos_begin, pos_end;  // permuted positions handled by this launch
+    int64_t run;                 // positions per worker
+    int64_t ld;                  // row stride of factors and out (= R)
+    int col0, ncols;             // column tile
+    int mode, N, rb;             // runtime mode / order / record bytes
+    const void *A[kMaxModes];    // factor matrices (A[mode] unused)
+    const void *lambda;          // NULL = ones
+    void *out;
+};
+
+// ----------------------------------------------------------------- loads
+__device__ __forceinline__ void ld_rec32(const void *p, uint32_t (&r)[8]) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                   "=r"(r[6]), "=r"(r[7])
+                 : "l"(p));
+}
+__device__ __forceinline__ void ld_rec16(const void *p, uint32_t (&r)[8]) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "l"(p));
+    r[4] = r[5] = r[6] = r[7] = 0;
+}
+__device__ __forceinline__ void ld_row(const double *p, double (&r)[4]) {
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+                 : "l"(p));
+}
+__device__ __forceinline__ void ld_row(const float *p, float (&r)[8]) {
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
+                   "=f"(r[6]), "=f"(r[7])
+                 : "l"(p));
+}
+__device__ __forceinline__ void st_row(double *p, const double (&r)[4]) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(r[0]), "d"(r[1]),
+                 "d"(r[2]), "d"(r[3])
+                 : "memory");
+}
+__device__ __forceinline__ void st_row(float *p, const float (&r)[8]) {
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r[0]),
+                 "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7])
+                 : "memory");
+}
+__device__ __forceinline__ void red_row(double *p, const double (&r)[4]) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+        asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p + v), "d"(r[v]) : "memory");
+}
+__device__ __forceinline__ void red_row(float *p, const float (&r)[8]) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(r[0]), "f"(r[1]),
+                 "f"(r[2]), "f"(r[3])
+                 : "memory");
+    asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p + 4), "f"(r[4]),
+                 "f"(r[5]), "f"(r[6]), "f"(r[7])
+                 : "memory");
+}
+
+template <typename T> __device__ __forceinline__ T rec_val(const uint32_t (&w)[8]);
+template <> __device__ __forceinline__ double rec_val<double>(const uint32_t (&w)[8]) {
+    return __hiloint2double((int)w[1], (int)w[0]);
+}
+template <> __device__ __forceinline__ float rec_val<float>(const uint32_t (&w)[8]) {
+    return __uint_as_float(w[0]);
+}
+
+// ------------------------------------------------------- fast kernel body
+// T, N (3..5), MODE (< N) and G (lanes per worker) are compile-time; the
+// column tile is [col0, col0 + ncols) with ncols <= G*V and ncols % V == 0.
+template <typename T, int N, int MODE, int G, int U, int RB>
+__device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
+    constexpr int V = 32 / sizeof(T);
+    constexpr int OFF = sizeof(T) / 4;  // first index word in a record
+    const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t worker = gtid / G;
+    const int q = (int)(gtid % G);
+    const int64_t s = a.pos_begin + worker * a.run;
+    if (s >= a.pos_end) return;
+    const int64_t e = min(s + a.run, a.pos_end);
+    const bool lane_on = q * V < a.ncols;
+    const int c = a.col0 + q * V;
+    const uint8_t *__restrict__ rec = a.rec;
+    const uint32_t *__restrict__ perm = a.perm;
+    T *__restrict__ out = static_cast<T *>(a.out);
+
+    T lam[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) lam[v] = T(1);
+    if (a.lambda && lane_on) ld_row(static_cast<const T *>(a.lambda) + c, lam);
+
+    T acc[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = T(0);
+    uint32_t cur = kNoRow, first = kNoRow;
+
+    auto flush = [&](uint32_t row, bool atomic) {
+        if (!lane_on) return;
+        T o[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) o[v] = acc[v] * lam[v];
+        T *dst = out + (int64_t)row * a.ld + c;
+        if (atomic) red_row(dst, o);
+        else st_row(dst, o);
+    };
+
+    uint32_t pn[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) pn[u] = (s + u < e) ? __ldg(perm + s + u) : kNoRow;
+
+    for (int64_t i = s; i < e; i += U) {
+        uint32_t p[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) p[u] = pn[u];
+#pragma unroll
+        for (int u = 0; u < U; ++u) pn[u] = (i + U + u < e) ? __ldg(perm + i + U + u) : kNoRow;
+
+        uint32_t w[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (p[u] != kNoRow) {
+                if constexpr (RB == 32) ld_rec32(rec + (size_t)p[u] * 32, w[u]);
+                else ld_rec16(rec + (size_t)p[u] * 16, w[u]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) w[u][k] = 0;
+            }
+        }
+        T f[U][N][V];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int m = 0; m < N; ++m)
+                if (m != MODE) {
+                    if (p[u] != kNoRow && lane_on)
+                        ld_row(static_cast<const T *>(a.A[m]) + (int64_t)w[u][OFF + m] * a.ld + c,
+                               f[u][m]);
+                    else
+#pragma unroll
+                        for (int v = 0; v < V; ++v) f[u][m][v] = T(0);
+                }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (p[u] == kNoRow) continue;
+            const uint32_t row = w[u][OFF + MODE];
+            if (row != cur) {
+                if (cur != kNoRow) flush(cur, cur == first);
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[v] = T(0);
+                if (first == kNoRow) first = row;
+                cur = row;
+            }
+            const T x = rec_val<T>(w[u]);
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                T t = x;
+#pragma unroll
+                for (int m = 0; m < N; ++m)
+                    if (m != MODE) t *= f[u][m][v];
+                acc[v] += t;
+            }
+        }
+    }
+    if (cur != kNoRow) flush(cur, true);
+}
+
+template <typename T, int N, int G, int U, int RB>
+__global__ void __launch_bounds__(256) mttkrp_fast_kernel(const MttkrpArgs a) {
+    if constexpr (N >= 1) if (a.mode == 0) { mttkrp_fast_body<T, N, 0, G, U, RB>(a); return; }
+    if constexpr (N >= 2) if (a.mode == 1) { mttkrp_fast_body<T, N, 1, G, U, RB>(a); return; }
+    if constexpr (N >= 3) if (a.mode == 2) { mttkrp_fast_body<T, N, 2, G, U, RB>(a); return; }
+    if constexpr (N >= 4) if (a.mode == 3) { mttkrp_fast_body<T, N, 3, G, U, RB>(a); return; }
+    if constexpr (N >= 5) if (a.mode == 4) { mttkrp_fast_body<T, N, 4, G, U, RB>(a); return; }
+}
+
+// ---------------------------------------------------- generic kernel
+// Any N <= 6, any mode, any column tile: lane q of a G-lane worker owns
+// columns col0 + q + G*k (k < NV), scalar loads, runtime record offsets.
+template <typename T, int G, int NV>
+__global__ void __launch_bounds__(256) mttkrp_generic_kernel(const MttkrpArgs a) {
+    constexpr int U = 2;
+    const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t worker = gtid / G;
+    const int q = (int)(gtid % G);
+    const int64_t s = a.pos_begin + worker * a.run;
+    if (s >= a.pos_end) return;
+    const int64_t e = min(s + a.run, a.pos_end);
+    const int N = a.N, mode = a.mode, rb = a.rb;
+    const int off = sizeof(T) / 4;
+    const uint8_t *__restrict__ rec = a.rec;
+    T *__restrict__ out = static_cast<T *>(a.out);
+    bool on[NV];
+    int col[NV];
+    T lam[NV], acc[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        col[k] = a.col0 + q + G * k;
+        on[k] = q + G * k < a.ncols;
+        lam[k] = (a.lambda && on[k]) ? static_cast<const T *>(a.lambda)[col[k]] : T(1);
+        acc[k] = T(0);
+    }
+    uint32_t cur = kNoRow, first = kNoRow;
+    auto flush = [&](uint32_t row, bool atomic) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            if (!on[k]) continue;
+            T *dst = out + (int64_t)row * a.ld + col[k];
+            const T o = acc[k] * lam[k];
+            if (atomic) atomicAdd(dst, o);
+            else *dst = o;
+        }
+    };
+    for (int64_t i = s; i < e; i += U) {
+        uint32_t p[U], row[U];
+        T x[U];
+        T t[U][NV];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            p[u] = (i + u < e) ? __ldg(a.perm + i + u) : kNoRow;
+            if (p[u] == kNoRow) continue;
+            const uint8_t *r = rec + (size_t)p[u] * rb;
+            x[u] = __ldg(reinterpret_cast<const T *>(r));
+            const uint32_t *ix = reinterpret_cast<const uint32_t *>(r) + off;
+            row[u] = __ldg(ix + mode);
+#pragma unroll
+            for (int k = 0; k < NV; ++k) t[u][k] = x[u];
+#pragma unroll
+            for (int m = 0; m < kMaxModes; ++m) {
+                if (m >= N || m == mode) continue;
+                const T *Am = static_cast<const T *>(a.A[m]) + (int64_t)__ldg(ix + m) * a.ld;
+#pragma unroll
+                for (int k = 0; k < NV; ++k)
+                    if (on[k]) t[u][k] *= __ldg(Am + col[k]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (p[u] == kNoRow) continue;
+            if (row[u] != cur) {
+                if (cur != kNoRow) flush(cur, cur == first);
+#pragma unroll
+                for (int k = 0; k < NV; ++k) acc[k] = T(0);
+                if (first == kNoRow) first = row[u];
+                cur = row[u];
+            }
+#pragma unroll
+            for (int k = 0; k < NV; ++k) acc[k] += t[u][k];
+        }
+    }
+    if (cur != kNoRow) flush(cur, true);
+}
+
+// launchers (instantiated per dtype in mttkrp_f64.cu / mttkrp_f32.cu)
+template <typename T>
+sptk_status launch_fast(int N, int G, int rb, const MttkrpArgs &a, int64_t workers,
+                        cudaStream_t s);
+template <typename T>
+sptk_status launch_generic(int G, const MttkrpArgs &a, int64_t workers, cudaStream_t s);
+
+}  // namespace sptk

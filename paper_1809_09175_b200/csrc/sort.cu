@@ -1,0 +1,342 @@
+// sort.cu -- build_perm: per-mode permutation arrays
+// (§5: "a permutation array for each mode that sorts the tensor
+// nonzeros in increasing index along that mode"), built on the GPU by a
+// STABLE least-significant-digit radix sort of (key = l_in, value = i).
+// Stability (P:584 names a *stable* sort) makes the permutation unique.
+//
+// Per digit pass (<= 8 bits, ceil(bits(I_n - 1) / passes) bits each):
+//   upsweep    per-tile digit histograms          counts[digit][tile]
+//   scan       exclusive scan of counts (digit-major) -> global offsets
+//   downsweep  stable scatter: inside a 4096-key tile, warp w owns keys
+//              [w*512, w*512+512) and ranks equal digits with __match_any_sync
+//              in rounds of 32, so equal keys keep their storage order.
+// Then rowptr_n[r] = first sorted position with key >= r (boundary kernel).
+#include "common.cuh"
+
+namespace sptk {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;                              // keys per thread
+constexpr int kSortTile = kSortThreads * kSortItems;        // 4096
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kWarpChunk = kSortTile / kSortWarps;          // 512 keys per warp
+constexpr int kScanChunk = 4096;
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// key of element i for the current pass
+template <bool FROM_REC>
+__device__ __forceinline__ uint32_t load_key(const uint32_t *__restrict__ keys,
+                                             const uint8_t *__restrict__ rec, int rb, int kw,
+                                             int64_t i) {
+    if constexpr (FROM_REC)
+        return __ldg(reinterpret_cast<const uint32_t *>(rec + (size_t)i * rb) + kw);
+    else
+        return __ldg(keys + i);
+}
+
+template <bool FROM_REC>
+__global__ void __launch_bounds__(kSortThreads)
+    radix_upsweep(const uint32_t *__restrict__ keys, const uint8_t *__restrict__ rec, int rb,
+                  int kw, int64_t P, int shift, int dbits, int64_t ntiles,
+                  uint32_t *__restrict__ counts) {
+    __shared__ uint32_t hist[256];
+    const int nd = 1 << dbits;
+    for (int d = threadIdx.x; d < nd; d += blockDim.x) hist[d] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+    const uint32_t mask = (uint32_t)nd - 1;
+#pragma unroll 4
+    for (int k = 0; k < kSortItems; ++k) {
+        const int64_t i = base + k * kSortThreads + threadIdx.x;
+        const bool valid = i < P;
+        const uint32_t digit = valid ? (load_key<FROM_REC>(keys, rec, rb, kw, i) >> shift) & mask
+                                     : 0xffffffffu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, digit);
+        if (valid && (peers & lanemask_lt()) == 0) atomicAdd(&hist[digit], __popc(peers));
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < nd; d += blockDim.x)
+        counts[(int64_t)d * ntiles + blockIdx.x] = hist[d];
+}
+
+template <bool FROM_REC, bool WRITE_KEYS>
+__global__ void __launch_bounds__(kSortThreads)
+    radix_downsweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
+                    const uint8_t *__restrict__ rec, int rb, int kw, int64_t P, int shift,
+                    int dbits, int64_t ntiles, const uint32_t *__restrict__ offsets,
+                    uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out) {
+    __shared__ uint32_t whist[kSortWarps][256];
+    const int nd = 1 << dbits;
+    const uint32_t mask = (uint32_t)nd - 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int d = lane; d < nd; d += 32) whist[warp][d] = 0;
+    __syncwarp();
+    const int64_t base = (int64_t)blockIdx.x * kSortTile + (int64_t)warp * kWarpChunk;
+    uint32_t key[kSortItems], val[kSortItems];
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        const int64_t i = base + r * 32 + lane;
+        if (i < P) {
+            key[r] = load_key<FROM_REC>(keys_in, rec, rb, kw, i);
+            val[r] = FROM_REC ? (uint32_t)i : __ldg(vals_in + i);
+        } else {
+            key[r] = 0xffffffffu;
+            val[r] = 0;
+        }
+    }
+    // A: per-warp digit histogram of its 512-key sub-chunk
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        const bool valid = base + r * 32 + lane < P;
+        const uint32_t digit = valid ? (key[r] >> shift) & mask : 0xffffffffu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, digit);
+        if (valid && (peers & lt) == 0) whist[warp][digit] += __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // B: per-warp starting offsets = tile offset + earlier warps' counts
+    for (int d = threadIdx.x; d < nd; d += blockDim.x) {
+        uint32_t run = offsets[(int64_t)d * ntiles + blockIdx.x];
+#pragma unroll
+        for (int w = 0; w < kSortWarps; ++w) {
+            const uint32_t c = whist[w][d];
+            whist[w][d] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    // C: stable scatter, rounds in storage order
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        const bool valid = base + r * 32 + lane < P;
+        const uint32_t digit = valid ? (key[r] >> shift) & mask : 0xffffffffu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, digit);
+        uint32_t pos = 0;
+        if (valid) pos = whist[warp][digit] + __popc(peers & lt);
+        __syncwarp();
+        if (valid && (peers & lt) == 0) whist[warp][digit] += __popc(peers);
+        __syncwarp();
+        if (valid) {
+            if constexpr (WRITE_KEYS) keys_out[pos] = key[r];
+            vals_out[pos] = val[r];
+        }
+    }
+}
+
+// ------------------------------------------------------------ exclusive scan
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+    }
+    return v;
+}
+
+// block-wide exclusive scan of one value per thread (256 threads); returns total
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *excl) {
+    __shared__ uint32_t wsum[kSortWarps];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t inc = warp_incl_scan(v);
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    uint32_t wpre = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) {
+        const uint32_t s = wsum[w];
+        if (w < warp) wpre += s;
+        total += s;
+    }
+    __syncthreads();
+    *excl = wpre + inc - v;
+    return total;
+}
+
+__global__ void __launch_bounds__(256) scan_chunk_sums(const uint32_t *__restrict__ in, int64_t n,
+                                                       uint32_t *__restrict__ bsum) {
+    const int64_t base = (int64_t)blockIdx.x * kScanChunk;
+    uint32_t s = 0;
+    for (int k = threadIdx.x; k < kScanChunk; k += blockDim.x) {
+        const int64_t i = base + k;
+        if (i < n) s += in[i];
+    }
+    __shared__ uint32_t sh[256];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) bsum[blockIdx.x] = sh[0];
+}
+
+__global__ void __launch_bounds__(256) scan_block_sums(uint32_t *__restrict__ bsum, int64_t nb) {
+    uint32_t carry = 0;
+    for (int64_t b0 = 0; b0 < nb; b0 += 256) {
+        const int64_t i = b0 + threadIdx.x;
+        const uint32_t v = i < nb ? bsum[i] : 0;
+        uint32_t ex;
+        const uint32_t tot = block_excl_scan(v, &ex);
+        if (i < nb) bsum[i] = carry + ex;
+        carry += tot;
+    }
+}
+
+// in-place allowed (in == out)
+__global__ void __launch_bounds__(256) scan_chunk_apply(const uint32_t *in, int64_t n,
+                                                        const uint32_t *__restrict__ bsum,
+                                                        uint32_t *out) {
+    const int64_t base = (int64_t)blockIdx.x * kScanChunk;
+    constexpr int per = kScanChunk / 256;  // 16 contiguous items per thread
+    uint32_t v[per];
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < per; ++k) {
+        const int64_t i = base + threadIdx.x * per + k;
+        v[k] = i < n ? in[i] : 0;
+        s += v[k];
+    }
+    uint32_t ex;
+    block_excl_scan(s, &ex);
+    uint32_t run = bsum[blockIdx.x] + ex;
+#pragma unroll
+    for (int k = 0; k < per; ++k) {
+        const int64_t i = base + threadIdx.x * per + k;
+        if (i < n) out[i] = run;
+        run += v[k];
+    }
+}
+
+static sptk_status exclusive_scan(uint32_t *data, int64_t n, DevBuf &tmp, cudaStream_t s) {
+    if (n == 0) return SPTK_OK;
+    const int64_t nb = (n + kScanChunk - 1) / kScanChunk;
+    SPTK_TRY(tmp.reserve(sizeof(uint32_t) * nb));
+    scan_chunk_sums<<<(unsigned)nb, 256, 0, s>>>(data, n, tmp.as<uint32_t>());
+    scan_block_sums<<<1, 256, 0, s>>>(tmp.as<uint32_t>(), nb);
+    scan_chunk_apply<<<(unsigned)nb, 256, 0, s>>>(data, n, tmp.as<uint32_t>(), data);
+    count_launch(3);
+    SPTK_CUDA(cudaGetLastError());
+    return SPTK_OK;
+}
+
+// ------------------------------------------------------------ rowptr / iota
+// rowptr[r] = first sorted position whose key >= r (binary search per row;
+// balanced for any gap structure, including long runs of empty rows)
+__global__ void rowptr_from_sorted(const uint32_t *__restrict__ keys, int64_t P, int64_t In,
+                                   uint32_t *__restrict__ rowptr) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= In;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = P;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)__ldg(keys + mid) < r) lo = mid + 1;
+            else hi = mid;
+        }
+        rowptr[r] = (uint32_t)lo;
+    }
+}
+
+__global__ void iota_kernel(uint32_t *__restrict__ out, int64_t P) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (uint32_t)i;
+}
+
+__global__ void fill_u32(uint32_t *__restrict__ out, int64_t n, uint32_t v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = v;
+}
+
+static int grid_for(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    const int64_t cap = (int64_t)dev_sms() * 16;
+    if (b > cap) b = cap;
+    return b < 1 ? 1 : (int)b;
+}
+
+sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s) {
+    const int64_t P = t->P, In = t->dims[mode];
+    SPTK_TRY(t->perm[mode].reserve(sizeof(uint32_t) * (P > 0 ? P : 1)));
+    SPTK_TRY(t->rowptr[mode].reserve(sizeof(uint32_t) * (In + 1)));
+    uint32_t *perm = t->perm[mode].as<uint32_t>();
+    uint32_t *rowptr = t->rowptr[mode].as<uint32_t>();
+    t->host_rowptr[mode].clear();
+    if (P == 0) {
+        SPTK_CUDA(cudaMemsetAsync(rowptr, 0, sizeof(uint32_t) * (In + 1), s));
+        t->has_perm[mode] = true;
+        return SPTK_OK;
+    }
+    int bits = 0;
+    while (bits < 32 && ((uint64_t)(In - 1) >> bits) != 0) ++bits;
+    if (bits == 0) {  // I_n = 1: every key is 0, the stable order is the identity
+        iota_kernel<<<grid_for(P), 256, 0, s>>>(perm, P);
+        fill_u32<<<1, 32, 0, s>>>(rowptr, 1, 0u);
+        fill_u32<<<1, 32, 0, s>>>(rowptr + 1, 1, (uint32_t)P);
+        count_launch(3);
+        SPTK_CUDA(cudaGetLastError());
+        t->has_perm[mode] = true;
+        return SPTK_OK;
+    }
+    const int npass = (bits + 7) / 8;
+    const int dbits = (bits + npass - 1) / npass;
+    const int64_t ntiles = (P + kSortTile - 1) / kSortTile;
+    DevBuf kA, kB, vA, counts, tmp;
+    SPTK_TRY(kA.reserve(sizeof(uint32_t) * P));
+    SPTK_TRY(kB.reserve(sizeof(uint32_t) * P));
+    SPTK_TRY(vA.reserve(sizeof(uint32_t) * P));
+    SPTK_TRY(counts.reserve(sizeof(uint32_t) * ntiles * (1 << dbits)));
+    // ping-pong: vals end in `perm` after the last pass
+    uint32_t *kin = nullptr, *vin = nullptr;
+    uint32_t *kbuf[2] = {kA.as<uint32_t>(), kB.as<uint32_t>()};
+    uint32_t *vbuf[2] = {vA.as<uint32_t>(), perm};
+    const int kw = dtype_bytes(t->dtype) / 4 + mode;
+    const uint8_t *rec = t->rec.as<uint8_t>();
+    const int rb = t->rec_bytes;
+    for (int p = 0; p < npass; ++p) {
+        const int shift = p * dbits;
+        const int db = (shift + dbits > bits) ? bits - shift : dbits;
+        const bool first = p == 0;
+        // vals of the last pass land in `perm`; in/out buffers differ every pass
+        uint32_t *kout = kbuf[(npass - 1 - p) & 1];
+        uint32_t *vout = vbuf[((npass - 1 - p) & 1) ^ 1];
+        if (first)
+            radix_upsweep<true><<<(unsigned)ntiles, kSortThreads, 0, s>>>(
+                nullptr, rec, rb, kw, P, shift, db, ntiles, counts.as<uint32_t>());
+        else
+            radix_upsweep<false><<<(unsigned)ntiles, kSortThreads, 0, s>>>(
+                kin, nullptr, rb, kw, P, shift, db, ntiles, counts.as<uint32_t>());
+        count_launch();
+        SPTK_CUDA(cudaGetLastError());
+        SPTK_TRY(exclusive_scan(counts.as<uint32_t>(), ntiles * ((int64_t)1 << db), tmp, s));
+        if (first)
+            radix_downsweep<true, true><<<(unsigned)ntiles, kSortThreads, 0, s>>>(
+                nullptr, nullptr, rec, rb, kw, P, shift, db, ntiles, counts.as<uint32_t>(), kout,
+                vout);
+        else
+            radix_downsweep<false, true><<<(unsigned)ntiles, kSortThreads, 0, s>>>(
+                kin, vin, nullptr, rb, kw, P, shift, db, ntiles, counts.as<uint32_t>(), kout,
+                vout);
+        count_launch();
+        SPTK_CUDA(cudaGetLastError());
+        kin = kout;
+        vin = vout;
+    }
+    // kin = sorted keys, vin = perm
+    rowptr_from_sorted<<<grid_for(In + 1), 256, 0, s>>>(kin, P, In, rowptr);
+    count_launch();
+    SPTK_CUDA(cudaGetLastError());
+    // temporaries are freed when this returns: order the frees after the work
+    SPTK_CUDA(cudaStreamSynchronize(s));
+    t->has_perm[mode] = true;
+    return SPTK_OK;
+}
+
+}  // namespace sptk

@@ -1,0 +1,69 @@
+"""Device-side generator (libsynth.so, built from synth/gen.cu): writes the
+same inputs as the numpy functions in synth/__init__.py straight into CUDA
+memory (torch tensors).  Input generation only -- no method arithmetic."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import POW2_COEFFS, PowerLawParams
+
+_LIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsynth.so")
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB):
+            raise RuntimeError(f"{_LIB} missing: run `python -m paper_1809_09175_b200.build`")
+        L = C.CDLL(_LIB)
+        p, u64, i, i64, d = C.c_void_p, C.c_uint64, C.c_int, C.c_int64, C.c_double
+        L.synth_coords.argtypes = [u64, i, i, C.c_uint32, u64, i64, i, d, u64, u64, p, p, p]
+        L.synth_values.argtypes = [u64, i, u64, i64, i, p, p]
+        L.synth_factor.argtypes = [u64, i, i, i64, i64, i, p, p]
+        _lib = L
+    return _lib
+
+
+_COEFFS = np.ascontiguousarray(POW2_COEFFS)
+
+
+def _stream():
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
+def tensor(seed: int, dims, P: int, dist: str = "uniform", i0: int = 0, dtype=None,
+           device="cuda"):
+    """(idx uint32-as-int32 [P,N] on device, vals [P] on device)."""
+    import torch
+    dtype = dtype or torch.float64
+    N = len(dims)
+    idx = torch.empty((P, N), dtype=torch.int32, device=device)
+    vals = torch.empty(P, dtype=dtype, device=device)
+    if P == 0:
+        return idx, vals
+    for m, I in enumerate(dims):
+        pl = PowerLawParams.for_dim(int(I)) if dist == "powerlaw" else PowerLawParams(0.0, 0, 0)
+        st = lib().synth_coords(seed, m, N, int(I), i0, P, 1 if dist == "powerlaw" else 0,
+                                pl.L, pl.a, pl.b, _COEFFS.ctypes.data, idx.data_ptr(), _stream())
+        if st:
+            raise RuntimeError(f"synth_coords failed: cuda error {st}")
+    st = lib().synth_values(seed, N, i0, P, int(dtype == torch.float32), vals.data_ptr(), _stream())
+    if st:
+        raise RuntimeError(f"synth_values failed: cuda error {st}")
+    return idx, vals
+
+
+def factor(seed_f: int, N: int, m: int, I: int, R: int, dtype=None, device="cuda"):
+    import torch
+    dtype = dtype or torch.float64
+    out = torch.empty((I, R), dtype=dtype, device=device)
+    st = lib().synth_factor(seed_f, N, m, I, R, int(dtype == torch.float32), out.data_ptr(),
+                            _stream())
+    if st:
+        raise RuntimeError(f"synth_factor failed: cuda error {st}")
+    return out

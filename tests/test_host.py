@@ -1,0 +1,99 @@
+"""CPU-only tests of the product's host side: the C-ABI library loads and
+exports every symbol include/sptk.h declares, host-only logic (row
+partitioning, argument validation that fails before any CUDA call), the byte
+models, and the input generator's determinism."""
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+import synth
+from paper_1809_09175_b200 import metrics
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = json.load(open(os.path.join(ROOT, "tests", "golden", "spec_examples.json")))
+
+
+@pytest.fixture(scope="module")
+def sp():
+    import paper_1809_09175_b200 as sp
+    from paper_1809_09175_b200 import build
+    build.build()
+    sp.lib()
+    return sp
+
+
+def test_library_exports_every_header_symbol(sp):
+    header = open(os.path.join(ROOT, "include", "sptk.h")).read()
+    header = re.sub(r"/\*.*?\*/", "", header, flags=re.S)          # drop comments
+    declared = set(re.findall(r"\b(sptk_[a-z_0-9]+)\s*\(", header))
+    assert len(declared) >= 18
+    lib = sp.lib()
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(sp.EXPORTS) == declared
+    assert "sm_100a" in sp.version()
+
+
+def test_partition_rows_definition(sp):
+    rng = np.random.default_rng(0)
+    for In, nr in [(1, 1), (1, 4), (10, 3), (1000, 8), (50, 2)]:
+        counts = rng.integers(0, 20, In)
+        if In > 3:
+            counts[3] = 500          # one hot row
+        rowptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.uint32)
+        b = sp.partition_rows(rowptr, nr)
+        P = int(rowptr[-1])
+        assert b[0] == 0 and b[-1] == In and np.all(np.diff(b) >= 0)
+        for g in range(1, nr):
+            target = -(-P * g // nr)
+            expect = int(np.searchsorted(rowptr, target, side="left"))
+            assert b[g] == min(expect, In)
+
+
+def test_create_validation_before_cuda(sp):
+    with pytest.raises(sp.SptkError) as e:
+        sp.sptensor_create([], np.zeros((0, 0), np.int64), np.zeros(0))
+    assert e.value.name == "EUNSUPPORTED"
+    with pytest.raises(sp.SptkError) as e:
+        sp.sptensor_create([3, 0], np.zeros((1, 2), np.int64), np.zeros(1))
+    assert e.value.name == "EUNSUPPORTED"
+    with pytest.raises(sp.SptkError) as e:
+        sp.sptensor_create([2] * 7, np.zeros((1, 7), np.int64), np.zeros(1))
+    assert e.value.name == "EUNSUPPORTED"
+    with pytest.raises(ValueError):
+        sp.sptensor_create([2, 2], np.zeros((3, 2), np.int64), np.zeros(2))
+
+
+def test_metrics_golden():
+    for key in ("storage_base", "storage_small"):
+        g = GOLD[key]
+        assert metrics.storage_bytes(g["d"], g["P"], g["s_r"], g["s_o"], False) == g["base"], g["cite"]
+        assert metrics.storage_bytes(g["d"], g["P"], g["s_r"], g["s_o"], True) == g["with_perm"], g["cite"]
+    g = GOLD["bandwidth_model"]
+    assert metrics.paper_bandwidth(g["d"], g["R"], g["P"], g["s_r"], g["s_o"], g["t"]) == pytest.approx(
+        g["bytes_per_s"], rel=1e-12), g["cite"]
+    for d, R, f in GOLD["flops_spec"]["cases"]:
+        assert metrics.flops_spec(d, R) == f
+    # C3 f64 R=16 B_model = 21.3 GB per mode (avg over modes)
+    c = synth.CONFIGS["nell2"]
+    bm = np.mean([metrics.b_model(3, c.nnz, 16, I, 8) for I in c.dims])
+    assert bm == pytest.approx(21.3e9, rel=0.01)
+
+
+def test_synth_deterministic_and_ranges():
+    a = synth.tensor(5, (7, 9, 1), 1000, "uniform")
+    b = synth.tensor(5, (7, 9, 1), 1000, "uniform")
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert a[0][:, 0].max() == 6 and a[0][:, 2].max() == 0
+    assert (a[1] > 0).all() and (a[1] <= 1).all()
+    # the chunked generation is the same stream
+    c = synth.tensor(5, (7, 9, 1), 600, "uniform", i0=400)
+    assert np.array_equal(c[0], a[0][400:])
+    p = synth.tensor(6, (1400, 2), 20000, "powerlaw")[0][:, 0]
+    top = np.bincount(p).max() / len(p)
+    assert abs(top - np.log(2) / np.log(1401)) < 0.01    # Zipf(1) head mass
+    f = synth.factor(3, 3, 1, 5, 4)
+    assert f.shape == (5, 4) and (f >= 0).all() and (f < 1).all()
