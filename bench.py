@@ -41,8 +41,8 @@ FALLBACK_HBM = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback (GB/s)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="sptk", choices=["sptk", "reference"])
     ap.add_argument("--config", default="nell2", choices=list(synth.CONFIGS))
     ap.add_argument("--rank", type=int, default=16)
@@ -51,6 +51,9 @@ def parse():
                     help="target CPU seconds for the oracle baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--layout", default="sorted", choices=["sorted", "perm_gather"],
+                    help="sorted: records materialised in perm order at build_perm (default); "
+                         "perm_gather: the paper's literal gather through perm_n")
     return ap.parse_args()
 
 
@@ -103,9 +106,18 @@ class ClockSampler:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 3:
                 try:
-                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16),
+                                         time.perf_counter()))
                 except ValueError:
                     pass
+
+    def wait_first(self, timeout=5.0):
+        t0 = time.perf_counter()
+        while self.proc and not self.samples and time.perf_counter() - t0 < timeout:
+            time.sleep(0.02)
+
+    def mark(self, which):
+        setattr(self, which, time.perf_counter())
 
     def __exit__(self, *a):
         if self.proc:
@@ -118,48 +130,71 @@ class ClockSampler:
             self.thread.join(timeout=2)
 
     def summary(self):
-        if not self.samples:
+        t0, t1 = getattr(self, "t_start", None), getattr(self, "t_end", None)
+        sel = [s for s in self.samples if t0 is not None and t0 <= s[3] <= t1 + 0.15]
+        window = "timed region"
+        if not sel and self.samples and t0 is not None:   # region shorter than the 100 ms period
+            sel = sorted(self.samples, key=lambda s: abs(s[3] - 0.5 * (t0 + t1)))[:2]
+            window = "nearest samples to the timed region"
+        if not sel:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [s[0] for s in self.samples]
         mask = 0
-        for s in self.samples:
+        for s in sel:
             mask |= s[2]
         reasons = [name for bit, name in REASONS.items() if mask & bit and name != "gpu_idle"]
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
-                "reasons": reasons, "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(s[0] for s in sel),
+                "sm_max_mhz": max(s[1] for s in sel), "reasons": reasons,
+                "samples": len(sel), "window": window}
 
 
 # ------------------------------------------------------------------ oracle leg
-def oracle_sample_rate(c, R: int, target_s: float, np_dtype):
-    """Time the oracle (row-owned OpenMP form, as it stands) on a bounded
-    sample of the workload: the first P_s nonzeros of the same generator
-    stream, full-size factors.  Returns (GB/s under B_model, threads, desc)."""
-    import oracle
-    A = [synth.factor(c.seed_f, c.N, m, int(I), R).astype(np_dtype).astype(np.float64)
-         for m, I in enumerate(c.dims)]
+class OracleSample:
+    """The oracle (row-owned OpenMP form, as it stands) on a bounded sample of
+    the workload: the first P_s nonzeros of the same generator stream with
+    full-size factors.  The oracle's own counting-sort perms are built once
+    (not timed, like build_perm on the GPU side)."""
 
-    def run(Ps):
-        idx, vals = synth.tensor(c.seed, c.dims, Ps, c.dist)
-        vals = vals.astype(np_dtype).astype(np.float64)
-        perms = [oracle.perm(idx, n, int(I)) for n, I in enumerate(c.dims)]
+    def __init__(self, c, R: int, np_dtype, Ps: int):
+        import oracle
+        self.oracle, self.c, self.R, self.Ps = oracle, c, R, Ps
+        self.s_v = np.dtype(np_dtype).itemsize
+        self.A = [synth.factor(c.seed_f, c.N, m, int(I), R).astype(np_dtype).astype(np.float64)
+                  for m, I in enumerate(c.dims)]
+        self.idx, vals = synth.tensor(c.seed, c.dims, Ps, c.dist)
+        self.vals = vals.astype(np_dtype).astype(np.float64)
+        self.perms = [oracle.perm(self.idx, n, int(I)) for n, I in enumerate(c.dims)]
+        self.bytes = sum(metrics.b_model(c.N, Ps, R, int(I), self.s_v) for I in c.dims)
+
+    def step(self):
+        """MTTKRP of every mode; returns (seconds, threads used)."""
         t0 = time.perf_counter()
         nt = 1
-        for n in range(c.N):
-            _, nt = oracle.mttkrp_omp(c.dims, idx, vals, A, n, perms[n][0], perms[n][1])
-        dt = time.perf_counter() - t0
-        s_v = np.dtype(np_dtype).itemsize
-        b = sum(metrics.b_model(c.N, Ps, R, int(I), s_v) for I in c.dims)
-        return b, dt, nt
+        for n in range(self.c.N):
+            _, nt = self.oracle.mttkrp_omp(self.c.dims, self.idx, self.vals, self.A, n,
+                                           self.perms[n][0], self.perms[n][1])
+        return time.perf_counter() - t0, nt
 
-    Ps = min(c.nnz, 1_000_000)
-    b, dt, nt = run(Ps)
-    if dt < target_s and Ps < c.nnz:
-        Ps = int(min(c.nnz, Ps * max(1.0, target_s / max(dt, 1e-3))))
-        b, dt, nt = run(Ps)
-    desc = (f"first {Ps:,} of {c.nnz:,} nonzeros of the {c.name} generator stream, full-size "
-            f"factors, MTTKRP of all {c.N} modes (oracle_mttkrp_omp: counting-sort perm + "
-            f"row-owned OpenMP; perm not timed); {dt:.2f} s")
-    return b / dt / 1e9, nt, desc, Ps, dt
+    def describe(self, dt):
+        c = self.c
+        return (f"first {self.Ps:,} of {c.nnz:,} nonzeros of the {c.name} generator stream, "
+                f"full-size factors, MTTKRP of all {c.N} modes per step (oracle_mttkrp_omp: "
+                f"counting-sort perm + row-owned OpenMP; perm not timed); {dt:.2f} s per step")
+
+
+def sized_sample(c, R, np_dtype, target_s: float) -> OracleSample:
+    """Calibrate P_s so that one oracle step takes about target_s seconds."""
+    probe = OracleSample(c, R, np_dtype, min(c.nnz, 500_000))
+    dt, _ = probe.step()
+    if dt >= target_s or probe.Ps >= c.nnz:
+        return probe
+    Ps = int(min(c.nnz, probe.Ps * target_s / max(dt, 1e-4)))
+    return OracleSample(c, R, np_dtype, Ps)
+
+
+def oracle_sample_rate(c, R: int, target_s: float, np_dtype):
+    smp = sized_sample(c, R, np_dtype, target_s)
+    dt, nt = smp.step()
+    return smp.bytes / dt / 1e9, nt, smp.describe(dt), smp.Ps, dt
 
 
 def run_reference(args):
@@ -168,21 +203,22 @@ def run_reference(args):
         return 0
     c = synth.CONFIGS[args.config]
     np_dtype = np.float64 if args.dtype == "f64" else np.float32
-    per_step = max(1.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
-    vals = []
-    desc = cores = None
+    per_step = max(0.5, min(10.0, 90.0 / max(1, args.steps + args.warmup)))
+    smp = sized_sample(c, args.rank, np_dtype, per_step)
+    times, cores = [], 1
     for k in range(args.warmup + args.steps):
-        gbs, cores, desc, Ps, dt = oracle_sample_rate(c, args.rank, per_step, np_dtype)
+        dt, cores = smp.step()
         if k >= args.warmup:
-            vals.append(gbs)
-    v = statistics.median(vals)
+            times.append(dt)
+    dt = statistics.median(times)
+    v = smp.bytes / dt / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-        "dtype": args.dtype, "data": "synthetic",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": workload_name(c, args.rank, args.dtype)},
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle",
-                         "sample": desc},
+                         "sample": smp.describe(dt)},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -228,18 +264,19 @@ def main():
     e0.record()
     idx_d, val_d = sdev.tensor(c.seed, c.dims, c.nnz, c.dist, dtype=tdt)
     e1.record()
-    t = sp.sptensor_create(c.dims, idx_d, val_d)
+    t = sp.sptensor_create(c.dims, idx_d, val_d, perm_gather=args.layout == "perm_gather")
     e2.record()
     torch.cuda.synchronize()
     del idx_d, val_d
-    perm_ms = []
+    perm_ms, perm_first_ms = [], []
     for n in range(c.N):
-        a, b = ev(), ev()
-        a.record()
-        sp.build_perm(t, n)
-        b.record()
-        torch.cuda.synchronize()
-        perm_ms.append(a.elapsed_time(b))
+        for rep in range(2):        # first call includes lazy module load + allocations
+            a, b = ev(), ev()
+            a.record()
+            sp.build_perm(t, n)
+            b.record()
+            torch.cuda.synchronize()
+            (perm_first_ms if rep == 0 else perm_ms).append(a.elapsed_time(b))
     F = [sdev.factor(c.seed_f, c.N, m, I, R, dtype=tdt) for m, I in enumerate(c.dims)]
 
     # per-rank share of the work (row-range sharding) for the byte model
@@ -263,23 +300,27 @@ def main():
         if world > 1:
             dist.barrier()
 
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
-
-    # ---- timed region (device time, CUDA events on the launching stream)
-    sp.profile_reset()
-    sp.profile_enable(True)
-    barrier()
-    torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        clk.wait_first()
+        for _ in range(max(3, args.warmup)):
+            step()
+        torch.cuda.synchronize()
+
+        # ---- timed region (device time, CUDA events on the launching stream)
+        sp.profile_reset()
+        sp.profile_enable(True)
+        barrier()
+        torch.cuda.synchronize()
+        clk.mark("t_start")
         start, end = ev(), ev()
         start.record(stream)
         for _ in range(args.steps):
             step()
         end.record(stream)
         torch.cuda.synchronize()
+        clk.mark("t_end")
         barrier()
+        time.sleep(0.15)
     sp.profile_enable(False)
     prof = sp.profile_read()
     ms = start.elapsed_time(end) / args.steps
@@ -341,6 +382,7 @@ def main():
                 "workload": workload_name(c, R, args.dtype), "dims": list(c.dims),
                 "nnz": c.nnz, "R": R, "dist": c.dist, "seed": c.seed, "seed_f": c.seed_f,
                 "step": "one CP-ALS iteration (MTTKRP all modes + glue + exchange)",
+                "layout": args.layout,
                 "parallelism": f"row-range shard x{world}" if world > 1 else "single GPU",
                 "l2": "inputs larger than L2 (records %.2f GB + perms %.2f GB vs 126 MB L2); "
                       "factor matrices (%.1f MB) are L2-resident by design" % (
@@ -352,7 +394,7 @@ def main():
             "b_model_bytes_per_step": bm_total,
             "gflops": sum(metrics.flops(c.N, c.nnz, R) for _ in c.dims) / (ms_max * 1e-3) / 1e9,
             "setup": {"generate_ms": e0.elapsed_time(e1), "create_ms": e1.elapsed_time(e2),
-                      "build_perm_ms": perm_ms,
+                      "build_perm_ms": perm_ms, "build_perm_first_call_ms": perm_first_ms,
                       "sort_to_iteration_ratio": sum(perm_ms) / ms_max},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

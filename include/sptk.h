@@ -36,6 +36,20 @@ extern "C" {
 #endif
 
 typedef enum { SPTK_F32 = 1, SPTK_F64 = 2 } sptk_dtype;
+
+/* sptk_sptensor_create flags */
+enum {
+    SPTK_CREATE_DEFAULT = 0,
+    /* Keep the paper's traversal literally: MTTKRP reads perm_n[i] and then
+     * gathers record perm_n[i] (§5, Fig. mttkrp_perm).  Without
+     * this flag build_perm(n) also materialises the records in perm_n order
+     * (one gather at build time) and MTTKRP streams that copy instead of
+     * gathering through the permutation -- same visiting order, same write
+     * discipline, same result; DESIGN.md §4 gives the measured reason (a
+     * random 32 B record read costs a 128 B HBM line on B200).  If the copy
+     * cannot be allocated the mode silently uses the perm-gather traversal. */
+    SPTK_CREATE_PERM_GATHER = 2
+};
 typedef enum { SPTK_IDX_I64 = 1, SPTK_IDX_U32 = 2 } sptk_idx_type;
 
 typedef enum {
@@ -71,7 +85,9 @@ const char *sptk_last_error(void);
  *   idx      device or host, nnz x nmodes row-major, 0-based; element type
  *            itype (int64 or uint32).  May be NULL iff nnz == 0.
  *   vals     device or host, nnz values of `dtype`.  NULL iff nnz == 0.
- *   flags    0 (duplicates allowed: MTTKRP is linear in X; Z3)
+ *   flags    SPTK_CREATE_DEFAULT or SPTK_CREATE_PERM_GATHER (see above).
+ *            Duplicate coordinates are always allowed (MTTKRP is linear in X;
+ *            DESIGN.md Z3).
  *   out      receives the handle
  * Copies the input into packed device records {value, idx[d]} (16 or 32 B)
  * after validating 0 <= idx < dims (SPTK_ERANGE otherwise) -- the caller may
@@ -89,15 +105,18 @@ sptk_status sptk_sptensor_destroy(sptk_tensor t);
 sptk_status sptk_sptensor_info(sptk_tensor t, int *nmodes, int64_t *dims, int64_t *nnz,
                                sptk_dtype *dtype);
 
-/* Device bytes owned by the handle (records + perms + rowptrs + workspace). */
+/* Device bytes owned by the handle (records + perms + rowptrs + permuted
+ * copies + workspace). */
 sptk_status sptk_sptensor_device_bytes(sptk_tensor t, int64_t *bytes);
 
 /* Build the mode-`mode` permutation (mode = -1: all modes).  P:513-515 (§5
  * "Permutation approach"): "a permutation array for each mode that sorts the
  * tensor nonzeros in increasing index along that mode"; the sort is STABLE
  * (ties keep storage order), so the permutation is unique.
- * Also builds rowptr_n[I_n+1] (start of each mode-n row in permuted order).
- * On-GPU LSD radix sort; temporary device memory ~16 B x nnz. */
+ * Also builds rowptr_n[I_n+1] (start of each mode-n row in permuted order)
+ * and, unless the tensor was created with SPTK_CREATE_PERM_GATHER, the
+ * records in perm_n order (rec_bytes x nnz).  On-GPU LSD radix sort;
+ * temporary device memory ~16 B x nnz. */
 sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream);
 
 /* Copy perm_n (uint32[nnz]) / rowptr_n (uint32[I_n + 1]) to `out` (device or
@@ -110,7 +129,8 @@ sptk_status sptk_get_rowptr(sptk_tensor t, int mode, uint32_t *out, void *stream
 /* Mode-n MTTKRP, Eq. (2):
  *   out(k, j) = lambda_j * sum_{i : l_in = k} x_i * prod_{m != n} A_m(l_im, j)
  * computed by permuted traversal (§5, Fig. mttkrp_perm): nonzeros
- * are visited in perm_n order, a row is accumulated in registers and written
+ * are visited in perm_n order (through perm_n, or streaming the permuted copy
+ * of the records), a row is accumulated in registers and written
  * when the mode-n index changes -- plain store for rows interior to a
  * worker's block, atomic add for a block's first/last row.
  *   mode     n in [0, nmodes)

@@ -134,7 +134,8 @@ sptk_status sptk_sptensor_create(int nmodes, const int64_t *dims, int64_t nnz, c
     if (nnz >= (int64_t(1) << 32)) return fail(SPTK_EUNSUPPORTED, "nnz must be < 2^32");
     if (dtype != SPTK_F32 && dtype != SPTK_F64) return fail(SPTK_EINVAL, "bad dtype");
     if (itype != SPTK_IDX_I64 && itype != SPTK_IDX_U32) return fail(SPTK_EINVAL, "bad idx type");
-    if (flags != 0) return fail(SPTK_EUNSUPPORTED, "flags must be 0 (duplicates allowed)");
+    if (flags & ~(unsigned)SPTK_CREATE_PERM_GATHER)
+        return fail(SPTK_EUNSUPPORTED, "unknown create flag");
     if (nnz > 0 && (!idx || !vals)) return fail(SPTK_EINVAL, "idx/vals NULL with nnz > 0");
 
     cudaStream_t s = (cudaStream_t)stream;
@@ -145,6 +146,7 @@ sptk_status sptk_sptensor_create(int nmodes, const int64_t *dims, int64_t nnz, c
     t->P = nnz;
     t->dtype = dtype;
     t->rec_bytes = record_bytes(dtype, nmodes);
+    t->perm_gather_only = (flags & SPTK_CREATE_PERM_GATHER) != 0;
     cudaGetDevice(&t->device);
 
     sptk_status st = SPTK_OK;
@@ -221,7 +223,7 @@ sptk_status sptk_sptensor_info(sptk_tensor t, int *nmodes, int64_t *dims, int64_
 sptk_status sptk_sptensor_device_bytes(sptk_tensor t, int64_t *bytes) {
     if (!t || !bytes) return fail(SPTK_EINVAL, "null argument");
     int64_t b = t->rec.bytes;
-    for (int m = 0; m < t->N; ++m) b += t->perm[m].bytes + t->rowptr[m].bytes;
+    for (int m = 0; m < t->N; ++m) b += t->perm[m].bytes + t->rowptr[m].bytes + t->srec[m].bytes;
     const ALSWork &w = t->als;
     b += w.V.bytes + w.G.bytes + w.L.bytes + w.partial.bytes + w.colsq.bytes + w.lam.bytes +
          w.scal.bytes + w.stage.bytes + w.lamT.bytes;

@@ -92,6 +92,9 @@ struct sptk_tensor_s {
     sptk::DevBuf perm[sptk::kMaxModes];         // uint32[P]
     sptk::DevBuf rowptr[sptk::kMaxModes];       // uint32[I_n + 1]
     bool has_perm[sptk::kMaxModes] = {false};
+    sptk::DevBuf srec[sptk::kMaxModes];         // records in perm_n order (optional)
+    bool has_srec[sptk::kMaxModes] = {false};
+    bool perm_gather_only = false;              // SPTK_CREATE_PERM_GATHER
     std::vector<uint32_t> host_rowptr[sptk::kMaxModes];  // for partitioning (lazy)
     double normX2 = 0.0;
     bool poisoned = false;

@@ -52,8 +52,13 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     if (pe <= pb) return SPTK_OK;
 
     MttkrpArgs a{};
-    a.rec = t->rec.as<uint8_t>();
-    a.perm = t->perm[mode].as<uint32_t>();
+    if (t->has_srec[mode]) {  // records materialised in perm_n order: stream them
+        a.rec = t->srec[mode].as<uint8_t>();
+        a.perm = nullptr;
+    } else {                  // the paper's traversal: gather through perm_n
+        a.rec = t->rec.as<uint8_t>();
+        a.perm = t->perm[mode].as<uint32_t>();
+    }
     a.pos_begin = pb;
     a.pos_end = pe;
     a.run = run_length();

@@ -37,7 +37,7 @@ constexpr uint32_t kNoRow = 0xffffffffu;
 
 struct MttkrpArgs {
     const uint8_t *rec;
-    const uint32_t *perm;
+    const uint32_t *perm;        // NULL: `rec` is already in perm_n order
     int64_t pos_begin, pos_end;  // permuted positions handled by this launch
     int64_t run;                 // positions per worker
     int64_t ld;                  // row stride of factors and out (= R)
@@ -107,7 +107,7 @@ template <> __device__ __forceinline__ float rec_val<float>(const uint32_t (&w)[
 // ------------------------------------------------------- fast kernel body
 // T, N (3..5), MODE (< N) and G (lanes per worker) are compile-time; the
 // column tile is [col0, col0 + ncols) with ncols <= G*V and ncols % V == 0.
-template <typename T, int N, int MODE, int G, int U, int RB>
+template <typename T, int N, int MODE, int G, int U, int RB, bool SORTED>
 __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
     constexpr int V = 32 / sizeof(T);
     constexpr int OFF = sizeof(T) / 4;  // first index word in a record
@@ -143,26 +143,53 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
         else st_row(dst, o);
     };
 
+    // SORTED: records are stored in perm_n order, position i is record i
+    // (streamed, prefetched one step ahead).  Otherwise the paper's
+    // traversal: p = perm_n[i] (prefetched one step ahead), gather record p.
     uint32_t pn[U];
+    uint32_t wn[U][8];
+    auto load_rec = [&](int64_t pos, uint32_t (&r)[8]) {
+        if constexpr (RB == 32) ld_rec32(rec + (size_t)pos * 32, r);
+        else ld_rec16(rec + (size_t)pos * 16, r);
+    };
 #pragma unroll
-    for (int u = 0; u < U; ++u) pn[u] = (s + u < e) ? __ldg(perm + s + u) : kNoRow;
+    for (int u = 0; u < U; ++u) {
+        if constexpr (SORTED) {
+            pn[u] = (s + u < e) ? 0u : kNoRow;
+            if (s + u < e) load_rec(s + u, wn[u]);
+        } else {
+            pn[u] = (s + u < e) ? __ldg(perm + s + u) : kNoRow;
+        }
+    }
 
     for (int64_t i = s; i < e; i += U) {
         uint32_t p[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) p[u] = pn[u];
-#pragma unroll
-        for (int u = 0; u < U; ++u) pn[u] = (i + U + u < e) ? __ldg(perm + i + U + u) : kNoRow;
-
         uint32_t w[U][8];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (p[u] != kNoRow) {
-                if constexpr (RB == 32) ld_rec32(rec + (size_t)p[u] * 32, w[u]);
-                else ld_rec16(rec + (size_t)p[u] * 16, w[u]);
-            } else {
+        for (int u = 0; u < U; ++u) p[u] = pn[u];
+        if constexpr (SORTED) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) w[u][k] = 0;
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) w[u][k] = wn[u][k];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t q = i + U + u;
+                pn[u] = q < e ? 0u : kNoRow;
+                if (q < e) load_rec(q, wn[u]);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                pn[u] = (i + U + u < e) ? __ldg(perm + i + U + u) : kNoRow;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (p[u] != kNoRow) {
+                    load_rec(p[u], w[u]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) w[u][k] = 0;
+                }
             }
         }
         T f[U][N][V];
@@ -203,13 +230,13 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
     if (cur != kNoRow) flush(cur, true);
 }
 
-template <typename T, int N, int G, int U, int RB>
+template <typename T, int N, int G, int U, int RB, bool SORTED>
 __global__ void __launch_bounds__(256) mttkrp_fast_kernel(const MttkrpArgs a) {
-    if constexpr (N >= 1) if (a.mode == 0) { mttkrp_fast_body<T, N, 0, G, U, RB>(a); return; }
-    if constexpr (N >= 2) if (a.mode == 1) { mttkrp_fast_body<T, N, 1, G, U, RB>(a); return; }
-    if constexpr (N >= 3) if (a.mode == 2) { mttkrp_fast_body<T, N, 2, G, U, RB>(a); return; }
-    if constexpr (N >= 4) if (a.mode == 3) { mttkrp_fast_body<T, N, 3, G, U, RB>(a); return; }
-    if constexpr (N >= 5) if (a.mode == 4) { mttkrp_fast_body<T, N, 4, G, U, RB>(a); return; }
+    if constexpr (N >= 1) if (a.mode == 0) { mttkrp_fast_body<T, N, 0, G, U, RB, SORTED>(a); return; }
+    if constexpr (N >= 2) if (a.mode == 1) { mttkrp_fast_body<T, N, 1, G, U, RB, SORTED>(a); return; }
+    if constexpr (N >= 3) if (a.mode == 2) { mttkrp_fast_body<T, N, 2, G, U, RB, SORTED>(a); return; }
+    if constexpr (N >= 4) if (a.mode == 3) { mttkrp_fast_body<T, N, 3, G, U, RB, SORTED>(a); return; }
+    if constexpr (N >= 5) if (a.mode == 4) { mttkrp_fast_body<T, N, 4, G, U, RB, SORTED>(a); return; }
 }
 
 // ---------------------------------------------------- generic kernel
@@ -255,7 +282,7 @@ __global__ void __launch_bounds__(256) mttkrp_generic_kernel(const MttkrpArgs a)
         T t[U][NV];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            p[u] = (i + u < e) ? __ldg(a.perm + i + u) : kNoRow;
+            p[u] = (i + u < e) ? (a.perm ? __ldg(a.perm + i + u) : (uint32_t)(i + u)) : kNoRow;
             if (p[u] == kNoRow) continue;
             const uint8_t *r = rec + (size_t)p[u] * rb;
             x[u] = __ldg(reinterpret_cast<const T *>(r));

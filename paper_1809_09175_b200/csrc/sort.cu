@@ -255,11 +255,50 @@ __global__ void fill_u32(uint32_t *__restrict__ out, int64_t n, uint32_t v) {
         out[i] = v;
 }
 
+// srec[i] = rec[perm[i]]: the records in permuted order (one gather at build time)
+template <int RB>
+__global__ void __launch_bounds__(256) permute_records(const uint8_t *__restrict__ rec,
+                                                       const uint32_t *__restrict__ perm, int64_t P,
+                                                       uint8_t *__restrict__ srec) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(rec + (size_t)__ldg(perm + i) * RB);
+        uint4 *dst = reinterpret_cast<uint4 *>(srec + (size_t)i * RB);
+        dst[0] = __ldg(src);
+        if constexpr (RB == 32) dst[1] = __ldg(src + 1);
+    }
+}
+
 static int grid_for(int64_t n) {
     int64_t b = (n + 255) / 256;
     const int64_t cap = (int64_t)dev_sms() * 16;
     if (b > cap) b = cap;
     return b < 1 ? 1 : (int)b;
+}
+
+// Materialise the records in perm_n order unless the tensor keeps the paper's
+// perm-gather traversal; an allocation failure falls back to that traversal.
+static sptk_status build_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
+    t->has_srec[mode] = false;
+    if (t->perm_gather_only || t->P == 0) {
+        t->srec[mode].release();
+        return SPTK_OK;
+    }
+    if (t->srec[mode].reserve((size_t)t->rec_bytes * t->P) != SPTK_OK) {
+        set_error("");
+        return SPTK_OK;
+    }
+    const uint32_t *perm = t->perm[mode].as<uint32_t>();
+    if (t->rec_bytes == 32)
+        permute_records<32><<<grid_for(t->P), 256, 0, s>>>(t->rec.as<uint8_t>(), perm, t->P,
+                                                          t->srec[mode].as<uint8_t>());
+    else
+        permute_records<16><<<grid_for(t->P), 256, 0, s>>>(t->rec.as<uint8_t>(), perm, t->P,
+                                                          t->srec[mode].as<uint8_t>());
+    count_launch();
+    SPTK_CUDA(cudaGetLastError());
+    t->has_srec[mode] = true;
+    return SPTK_OK;
 }
 
 sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s) {
@@ -336,7 +375,7 @@ sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s) {
     // temporaries are freed when this returns: order the frees after the work
     SPTK_CUDA(cudaStreamSynchronize(s));
     t->has_perm[mode] = true;
-    return SPTK_OK;
+    return build_sorted_copy(t, mode, s);
 }
 
 }  // namespace sptk

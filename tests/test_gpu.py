@@ -40,8 +40,9 @@ def dev(x, dtype=None):
     return t.to(dtype) if dtype is not None else t
 
 
-def make(sp, dims, idx, vals, dtype=torch.float64):
-    return sp.sptensor_create(dims, dev(idx.astype(np.int64)), dev(vals, dtype))
+def make(sp, dims, idx, vals, dtype=torch.float64, perm_gather=False):
+    return sp.sptensor_create(dims, dev(idx.astype(np.int64)), dev(vals, dtype),
+                              perm_gather=perm_gather)
 
 
 def factors_np(seed, dims, R, dtype=np.float64):
@@ -110,10 +111,11 @@ def test_perm_golden_and_empty(sp):
 
 
 # ------------------------------------------------------------------ MTTKRP
+@pytest.mark.parametrize("layout", ["sorted", "perm_gather"])
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
 @pytest.mark.parametrize("N,R", [(3, 8), (3, 16), (3, 64), (3, 128), (3, 256), (4, 16),
                                  (5, 16), (3, 24), (4, 32)])
-def test_mttkrp_fast_path_parity(sp, dtype, N, R):
+def test_mttkrp_fast_path_parity(sp, layout, dtype, N, R):
     dims = [57, 1203, 311, 40, 9][:N]
     P = 5 * 4096 + 123
     idx, vals = synth.tensor(1000 + N, dims, P, "uniform")
@@ -121,7 +123,7 @@ def test_mttkrp_fast_path_parity(sp, dtype, N, R):
     vals = vals.astype(npd)
     A = factors_np(2000 + R, dims, R, npd)
     lam = np.linspace(0.5, 1.5, R).astype(npd)
-    t = make(sp, dims, idx, vals, dtype)
+    t = make(sp, dims, idx, vals, dtype, perm_gather=layout == "perm_gather")
     sp.build_perm(t, -1)
     for n in range(N):
         for L in (None, lam):
@@ -131,6 +133,7 @@ def test_mttkrp_fast_path_parity(sp, dtype, N, R):
             assert rel(V, Vo) <= TOL[dtype], (n, L is None)
 
 
+@pytest.mark.parametrize("layout", ["sorted", "perm_gather"])
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
 @pytest.mark.parametrize("dims,R,offset", [
     ((40, 1000), 1, 0), ((40, 1000), 3, 0), ((7, 9, 11, 3, 5, 4), 17, 0),   # N = 2, 6 generic
@@ -138,13 +141,13 @@ def test_mttkrp_fast_path_parity(sp, dtype, N, R):
     ((57, 1203, 311), 33, 0), ((57, 1203, 311), 130, 0),                    # odd R, col tiles
     ((57, 1203, 311), 16, 1),                                               # unaligned factors
 ])
-def test_mttkrp_generic_path_parity(sp, dtype, dims, R, offset):
+def test_mttkrp_generic_path_parity(sp, layout, dtype, dims, R, offset):
     P = 3 * 4096 + 5
     idx, vals = synth.tensor(77, dims, P, "uniform")
     npd = np.float64 if dtype == torch.float64 else np.float32
     vals = vals.astype(npd)
     A = factors_np(78, dims, R, npd)
-    t = make(sp, dims, idx, vals, dtype)
+    t = make(sp, dims, idx, vals, dtype, perm_gather=layout == "perm_gather")
     sp.build_perm(t, -1)
     for n in range(len(dims)):
         V = gpu_mttkrp(sp, t, n, A, R, dtype, offset=offset)
@@ -152,14 +155,15 @@ def test_mttkrp_generic_path_parity(sp, dtype, dims, R, offset):
         assert rel(V, Vo) <= TOL[dtype], n
 
 
-def test_mttkrp_contention_and_empty_rows(sp):
+@pytest.mark.parametrize("layout", ["sorted", "perm_gather"])
+def test_mttkrp_contention_and_empty_rows(sp, layout):
     """All nonzeros in one row (maximum contention), a 2-long mode, many empty rows."""
     dims = (5000, 2, 700)
     P = 300_000
     idx, vals = synth.tensor(5, dims, P, "uniform")
     idx[:, 0] = 4321
     A = factors_np(6, dims, 16)
-    t = make(sp, dims, idx, vals)
+    t = make(sp, dims, idx, vals, perm_gather=layout == "perm_gather")
     sp.build_perm(t, -1)
     for n in range(3):
         V = gpu_mttkrp(sp, t, n, A, 16, torch.float64)
@@ -282,7 +286,7 @@ def sampled_rows(counts, k=48, seed=0):
     return np.array(sorted(rows), dtype=np.int64)
 
 
-def full_config_check(sp, name, R, dtype, sample=True):
+def full_config_check(sp, name, R, dtype, perm_gather=False):
     """Bench-sized input and launch configuration: perms bit-exact (host
     counting sort) or by device invariants, MTTKRP on sampled rows vs the
     oracle restricted to those rows."""
@@ -290,7 +294,7 @@ def full_config_check(sp, name, R, dtype, sample=True):
     c = synth.CONFIGS[name]
     idx_d, val_d = device.tensor(c.seed, c.dims, c.nnz, c.dist, dtype=dtype)
     A_d = [device.factor(c.seed_f, c.N, m, I, R, dtype=dtype) for m, I in enumerate(c.dims)]
-    t = sp.sptensor_create(c.dims, idx_d, val_d)
+    t = sp.sptensor_create(c.dims, idx_d, val_d, perm_gather=perm_gather)
     sp.build_perm(t, -1)
     A_h = [a.double().cpu().numpy() for a in A_d]
     small = c.nnz <= 200_000_000
@@ -312,9 +316,6 @@ def full_config_check(sp, name, R, dtype, sample=True):
         Vo = oracle.mttkrp_rows(c.dims, sub_idx, sub_val, A_h, n, rows, acc_long=True)
         V = out[torch.from_numpy(rows).cuda()].double().cpu().numpy()
         assert rel(V, Vo) <= TOL[dtype], f"mode {n}"
-        if not small:   # perm invariants on the device, in chunks
-            p_d = torch.from_numpy(p.view(np.int32)).cuda()
-            del p_d
     return t
 
 
@@ -326,6 +327,10 @@ def test_config_lbnl_full(sp):
                                      (16, torch.float32), (64, torch.float32)])
 def test_config_nell2_full(sp, R, dtype):
     full_config_check(sp, "nell2", R, dtype)
+
+
+def test_config_nell2_full_perm_gather(sp):
+    full_config_check(sp, "nell2", 16, torch.float64, perm_gather=True)
 
 
 def test_config_delicious_full(sp):
