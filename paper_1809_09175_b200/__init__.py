@@ -54,6 +54,7 @@ _SIGS = [
     ("sptk_profile_enable", [_I], _I),
     ("sptk_profile_reset", [], _I),
     ("sptk_profile_read", [_P, _P, _P], _I),
+    ("sptk_set_tuning", [_I, _I64], _I),
 ]
 EXPORTS = [s[0] for s in _SIGS]
 
@@ -278,6 +279,10 @@ def partition_rows(rowptr, nranks: int) -> np.ndarray:
     _check(lib().sptk_partition_rows(rp.ctypes.data, rp.shape[0] - 1, nranks, bounds.ctypes.data),
            "partition_rows")
     return bounds
+
+
+def set_tuning(variant: int = -1, run: int = 0):
+    _check(lib().sptk_set_tuning(variant, run), "set_tuning")
 
 
 def profile_enable(on: bool = True):

@@ -4,15 +4,18 @@
 // readings Z11, Z12):
 //   per mode n:  V = MTTKRP(X, A, n)          (mttkrp.cuh, lambda = NULL)
 //                Gamma = Hadamard_{m!=n} G_m  (G_m = A_m^T A_m, cached)
-//                Gamma = L L^T                (one block; ridge retry)
-//                A_n = V Gamma^{-1}           (per-row triangular solves)
+//                Gamma = L L^T, Gamma^{-1} = L^{-T} L^{-1}  (one block; ridge retry)
+//                A_n = V Gamma^{-1}           (row-parallel product, fused with the
+//                                              column sums of squares for lambda)
 //                lambda_j = ||A_n(:,j)||_2, normalise (zero column -> e_1)
 //                G_n = A_n^T A_n
 //   per iteration: fit = 1 - sqrt(max(0, ||X||^2 + ||M||^2 - 2<X,M>)) / ||X||
 //                <X,M> = sum_j lambda_j sum_k A_{N-1}(k,j) V(k,j)
 //                ||M||^2 = lambda^T (Hadamard_m G_m) lambda
-// All reductions are fixed-order (per-block partials, then an in-order sum),
-// so a run is bit-reproducible; one 16-byte D2H (fit, status) per iteration.
+// All reductions are fixed-order (per-block partials, then a fixed shuffle
+// tree), so a run is bit-reproducible; one small D2H (fit, status) per
+// iteration.  The oracle solves with the Cholesky factor row by row; using
+// the explicit inverse differs only at rounding level.
 // Multi-GPU: each rank solves its own row range of every mode, the R column
 // sums of squares and <X,M> partials are all-reduced, the rows broadcast.
 #include <math.h>
@@ -83,147 +86,192 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-// out[e] = sum_b partial[b][e]  (fixed order)
-__global__ void reduce_partials_kernel(const double *__restrict__ partial, int nb, int ne,
-                                       double *__restrict__ out) {
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) {
+// out[e] = sum_b partial[b][e]: one warp per entry, lanes stride over the
+// blocks, fixed-order shuffle tree (deterministic).
+__global__ void __launch_bounds__(256)
+    reduce_partials_kernel(const double *__restrict__ partial, int nb, int ne,
+                           double *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < ne;
+         e += (gridDim.x * blockDim.x) >> 5) {
         double s = 0.0;
-        for (int b = 0; b < nb; ++b) s += partial[(int64_t)b * ne + e];
-        out[e] = s;
+        for (int b = lane; b < nb; b += 32) s += partial[(int64_t)b * ne + e];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) out[e] = s;
     }
 }
 
-// partial[b][j] = sum over rows of block b of X(k,j) * Y(k,j)
-template <typename T>
+// Gamma = Hadamard_{m != n} G_m; Cholesky Gamma = L L^T (one ridge retry with
+// 1e-12 tr(Gamma)/R, as the oracle); Gamma^{-1} = L^{-T} L^{-1} -> Ginv.
+// One block.  Shared memory: R x R (L in the lower triangle, L^{-1}
+// transposed in the strict upper triangle) + R (diagonal of L^{-1}).
 __global__ void __launch_bounds__(256)
-    coldot_partial_kernel(const T *__restrict__ X, const T *__restrict__ Y, int64_t r0,
-                          int64_t r1, int R, int64_t rows_per_block, double *__restrict__ partial) {
-    __shared__ double sh[256];
-    const int lanes = 256 / R;  // row lanes per column (R <= 256)
-    const int j = threadIdx.x % R, l = threadIdx.x / R;
-    const int64_t b0 = r0 + blockIdx.x * rows_per_block;
-    const int64_t b1 = min(r1, b0 + rows_per_block);
-    double s = 0.0;
-    if (l < lanes)
-        for (int64_t k = b0 + l; k < b1; k += lanes)
-            s += (double)X[k * R + j] * (double)Y[k * R + j];
-    sh[threadIdx.x] = s;
-    __syncthreads();
-    if (threadIdx.x < R) {
-        double t = 0.0;
-        for (int q = 0; q < lanes; ++q) t += sh[q * R + threadIdx.x];
-        partial[(int64_t)blockIdx.x * R + threadIdx.x] = t;
-    }
-}
-
-// Gamma = Hadamard_{m != n} G_m, then L L^T = Gamma (+ ridge retry), one block.
-__global__ void __launch_bounds__(256)
-    gamma_chol_kernel(const double *__restrict__ G, int N, int n, int R, double *__restrict__ Lout,
-                      int *__restrict__ status) {
-    extern __shared__ double L[];  // R x R
+    chol_inv_kernel(const double *__restrict__ G, int N, int n, int R,
+                    double *__restrict__ Ginv, int *__restrict__ status) {
+    extern __shared__ double sm[];
+    double *L = sm;             // R x R
+    double *dinv = sm + R * R;  // R
     __shared__ int bad;
     __shared__ double ridge;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     auto gamma = [&](int i, int j) {
         double h = 1.0;
         for (int m = 0; m < N; ++m)
             if (m != n) h *= G[(int64_t)m * R * R + i * R + j];
         return h;
     };
-    if (threadIdx.x == 0) ridge = 0.0;
+    if (tid == 0) {
+        ridge = 0.0;
+        bad = 0;
+    }
+    __syncthreads();
     for (int attempt = 0; attempt < 2; ++attempt) {
-        for (int x = threadIdx.x; x < R * R; x += blockDim.x) L[x] = 0.0;
-        if (threadIdx.x == 0) bad = 0;
+        for (int e = tid; e < R * R; e += blockDim.x) {
+            const int i = e / R, j = e % R;
+            if (j <= i) L[e] = gamma(i, j) + (i == j ? ridge : 0.0);
+        }
         __syncthreads();
-        for (int j = 0; j < R; ++j) {
-            if (threadIdx.x == 0) {
-                double d = gamma(j, j) + ridge;
-                for (int k = 0; k < j; ++k) d -= L[j * R + k] * L[j * R + k];
+        if (warp == 0) {  // left-looking in-place Cholesky by one warp
+            for (int j = 0; j < R; ++j) {
+                double d = 0.0;
+                for (int k = lane; k < j; k += 32) d += L[j * R + k] * L[j * R + k];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+                d = L[j * R + j] - d;
                 if (!(d > 0.0)) {
-                    bad = 1;
+                    if (lane == 0) bad = 1;
                     d = 1.0;
                 }
-                L[j * R + j] = sqrt(d);
+                const double ljj = sqrt(d);
+                __syncwarp();
+                if (lane == 0) L[j * R + j] = ljj;
+                for (int i = j + 1 + lane; i < R; i += 32) {
+                    double s2 = L[i * R + j];
+                    for (int k = 0; k < j; ++k) s2 -= L[i * R + k] * L[j * R + k];
+                    L[i * R + j] = s2 / ljj;
+                }
+                __syncwarp();
             }
-            __syncthreads();
-            const double ljj = L[j * R + j];
-            for (int i = j + 1 + threadIdx.x; i < R; i += blockDim.x) {
-                double s = gamma(i, j);
-                for (int k = 0; k < j; ++k) s -= L[i * R + k] * L[j * R + k];
-                L[i * R + j] = s / ljj;
-            }
-            __syncthreads();
-        }
-        if (!bad) break;
-        if (threadIdx.x == 0) {
-            double tr = 0.0;
-            for (int j = 0; j < R; ++j) tr += gamma(j, j);
-            ridge = 1e-12 * (tr / (double)R);
         }
         __syncthreads();
-        if (attempt == 1 && threadIdx.x == 0) atomicOr(status, 1);
+        const int failed = bad;
+        __syncthreads();
+        if (!failed) break;
+        if (attempt == 0) {
+            if (tid == 0) {
+                double tr = 0.0;
+                for (int j = 0; j < R; ++j) tr += gamma(j, j);
+                ridge = 1e-12 * (tr / (double)R);
+                bad = 0;
+            }
+            __syncthreads();
+        } else if (tid == 0) {
+            atomicOr(status, 1);
+        }
     }
-    for (int x = threadIdx.x; x < R * R; x += blockDim.x) Lout[x] = L[x];
-}
-
-// A(k,:) = V(k,:) Gamma^{-1}: forward then back substitution, one row per thread.
-template <typename T>
-__global__ void row_solve_kernel(const T *__restrict__ V, int64_t r0, int64_t r1, int R,
-                                 const double *__restrict__ Lg, T *__restrict__ A) {
-    extern __shared__ double sm[];
-    double *L = sm;             // R x R
-    double *x = sm + R * R;     // R x blockDim (column-major by thread)
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) L[e] = Lg[e];
+    // column j of L^{-1} (thread j): z_j = 1/L_jj, z_i = -sum_{k=j}^{i-1} L_ik z_k / L_ii;
+    // z_i (i > j) stored at L[j][i] (strict upper triangle), z_j in dinv[j].
+    for (int j = tid; j < R; j += blockDim.x) {
+        const double zj = 1.0 / L[j * R + j];
+        dinv[j] = zj;
+        for (int i = j + 1; i < R; ++i) {
+            double s2 = L[i * R + j] * zj;
+            for (int k = j + 1; k < i; ++k) s2 += L[i * R + k] * L[j * R + k];
+            L[j * R + i] = -s2 / L[i * R + i];
+        }
+    }
     __syncthreads();
-    const int64_t k = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k >= r1) return;
-    const int bd = blockDim.x, t = threadIdx.x;
-    for (int i = 0; i < R; ++i) {
-        double s = (double)V[k * R + i];
-        for (int q = 0; q < i; ++q) s -= L[i * R + q] * x[q * bd + t];
-        x[i * bd + t] = s / L[i * R + i];
+    // Ginv[a][b] = sum_{k >= max(a,b)} Linv[k][a] Linv[k][b]
+    for (int e = tid; e < R * R; e += blockDim.x) {
+        const int a = e / R, b = e % R;
+        const int k0 = a > b ? a : b;
+        double s2 = 0.0;
+        for (int k = k0; k < R; ++k) {
+            const double la = (k == a) ? dinv[a] : L[a * R + k];
+            const double lb = (k == b) ? dinv[b] : L[b * R + k];
+            s2 += la * lb;
+        }
+        Ginv[e] = s2;
     }
-    for (int i = R - 1; i >= 0; --i) {
-        double s = x[i * bd + t];
-        for (int q = i + 1; q < R; ++q) s -= L[q * R + i] * x[q * bd + t];
-        x[i * bd + t] = s / L[i * R + i];
-    }
-    for (int i = 0; i < R; ++i) A[k * R + i] = (T)x[i * bd + t];
 }
 
-// lambda_j = sqrt(colsq_j)
-__global__ void lambda_kernel(const double *__restrict__ colsq, int R, double *__restrict__ lam) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < R) lam[j] = sqrt(colsq[j]);
+// A_raw(k,:) = V(k,:) Gamma^{-1} for rows [r0, r1); per-block partial column
+// sums of squares of A_raw (-> lambda) and, for the fit, of A_raw(k,j) V(k,j).
+// Thread t: column j = t % R, row lane t / R (R <= 256).
+template <typename T>
+__global__ void __launch_bounds__(256)
+    apply_inv_kernel(const T *__restrict__ V, int64_t r0, int64_t r1, int R,
+                     int64_t rows_per_block, const double *__restrict__ Ginv, T *__restrict__ A,
+                     double *__restrict__ part_sq, double *__restrict__ part_dot) {
+    extern __shared__ double sm[];
+    double *Gi = sm;           // R x R
+    double *red = sm + R * R;  // 2 x 256
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) Gi[e] = Ginv[e];
+    __syncthreads();
+    const int lanes = 256 / R;
+    const int j = threadIdx.x % R, l = threadIdx.x / R;
+    const int64_t b0 = r0 + blockIdx.x * rows_per_block;
+    const int64_t b1 = min(r1, b0 + rows_per_block);
+    double sq = 0.0, dot = 0.0;
+    if (l < lanes) {
+        for (int64_t k = b0 + l; k < b1; k += lanes) {
+            const T *v = V + k * R;
+            double x = 0.0;
+            for (int i = 0; i < R; ++i) x += (double)v[i] * Gi[i * R + j];
+            const T xt = (T)x;
+            A[k * R + j] = xt;
+            sq += (double)xt * (double)xt;
+            dot += (double)xt * (double)v[j];
+        }
+    }
+    red[threadIdx.x] = sq;
+    red[256 + threadIdx.x] = dot;
+    __syncthreads();
+    if (threadIdx.x < R) {
+        double a = 0.0, d = 0.0;
+        for (int q = 0; q < lanes; ++q) {
+            a += red[q * R + threadIdx.x];
+            d += red[256 + q * R + threadIdx.x];
+        }
+        part_sq[(int64_t)blockIdx.x * R + threadIdx.x] = a;
+        if (part_dot) part_dot[(int64_t)blockIdx.x * R + threadIdx.x] = d;
+    }
 }
 
+// lambda_j = ||A_raw(:,j)||_2 from colsq; A(:,j) /= lambda_j; a zero column
+// becomes e_1 with lambda_j = 0.  Block 0 also writes lambda.
 template <typename T>
 __global__ void normalize_kernel(T *__restrict__ A, int64_t r0, int64_t r1, int R,
-                                 const double *__restrict__ lam) {
+                                 const double *__restrict__ colsq, double *__restrict__ lam) {
+    if (blockIdx.x == 0)
+        for (int j = threadIdx.x; j < R; j += blockDim.x) lam[j] = sqrt(colsq[j]);
     const int64_t n = (r1 - r0) * R;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = r0 + i / R;
         const int j = (int)(i % R);
-        const double l = lam[j];
+        const double l = sqrt(colsq[j]);
         T *a = A + k * R + j;
         if (l == 0.0) *a = (T)(k == 0 ? 1.0 : 0.0);
         else *a = (T)((double)*a / l);
     }
 }
 
-// fit from s_j = sum_k A_{N-1}(k,j) V(k,j), lambda, G_m  -> out[0]
+// fit from dot_j = sum_k A_raw(k,j) V(k,j) (= lambda_j sum_k A(k,j) V(k,j)),
+// lambda and the Gram matrices -> out[0] = fit, out[1] = <X,M>, out[2] = ||M||^2
 __global__ void __launch_bounds__(256)
-    fit_kernel(const double *__restrict__ s, const double *__restrict__ lam,
+    fit_kernel(const double *__restrict__ dot, const double *__restrict__ lam,
                const double *__restrict__ G, int N, int R, double normX2,
                double *__restrict__ out) {
     __shared__ double sh[256];
     double acc = 0.0;
-    for (int a = threadIdx.x; a < R; a += blockDim.x)
-        for (int b = 0; b < R; ++b) {
-            double h = 1.0;
-            for (int m = 0; m < N; ++m) h *= G[(int64_t)m * R * R + a * R + b];
-            acc += lam[a] * h * lam[b];
-        }
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+        const int a = e / R, b = e % R;
+        double h = 1.0;
+        for (int m = 0; m < N; ++m) h *= G[(int64_t)m * R * R + e];
+        acc += lam[a] * h * lam[b];
+    }
     sh[threadIdx.x] = acc;
     __syncthreads();
     for (int w = 128; w > 0; w >>= 1) {
@@ -233,7 +281,7 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) {
         const double normM2 = sh[0];
         double inner = 0.0;
-        for (int j = 0; j < R; ++j) inner += lam[j] * s[j];
+        for (int j = 0; j < R; ++j) inner += dot[j];
         double res2 = normX2 + normM2 - 2.0 * inner;
         if (res2 < 0.0) res2 = 0.0;
         out[0] = 1.0 - sqrt(res2) / sqrt(normX2);
@@ -278,29 +326,8 @@ static sptk_status gram(AlsCtx &c, int m) {
     const size_t sm = sizeof(double) * 32 * R;
     gram_partial_kernel<T><<<nb, 256, sm, c.s>>>(static_cast<const T *>(c.A[m]), I, R, rpb,
                                                  w.partial.as<double>());
-    reduce_partials_kernel<<<grid_for(R * R), 256, 0, c.s>>>(
+    reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(
         w.partial.as<double>(), nb, R * R, w.G.as<double>() + (int64_t)m * R * R);
-    count_launch(2);
-    SPTK_CUDA(cudaGetLastError());
-    return SPTK_OK;
-}
-
-// colsum_j = sum_{k in [r0,r1)} X(k,j) Y(k,j) -> out (device, R doubles)
-template <typename T>
-static sptk_status coldot(AlsCtx &c, const T *X, const T *Y, int64_t r0, int64_t r1,
-                          double *out) {
-    const int R = (int)c.R;
-    ALSWork &w = c.t->als;
-    const int64_t n = r1 - r0;
-    if (n <= 0) {
-        SPTK_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * R, c.s));
-        return SPTK_OK;
-    }
-    int nb = (int)std::min<int64_t>(c.nblocks, (n + 63) / 64);
-    const int64_t rpb = (n + nb - 1) / nb;
-    nb = (int)((n + rpb - 1) / rpb);
-    coldot_partial_kernel<T><<<nb, 256, 0, c.s>>>(X, Y, r0, r1, R, rpb, w.partial.as<double>());
-    reduce_partials_kernel<<<grid_for(R), 256, 0, c.s>>>(w.partial.as<double>(), nb, R, out);
     count_launch(2);
     SPTK_CUDA(cudaGetLastError());
     return SPTK_OK;
@@ -312,44 +339,52 @@ static sptk_status als_iteration(AlsCtx &c, double *fit_host, int *status_host) 
     ALSWork &w = t->als;
     const int N = t->N, R = (int)c.R;
     const bool multi = c.comm && c.comm->nranks > 1;
-    double *colsq = w.colsq.as<double>();
+    double *colsq = w.colsq.as<double>();  // [0,R): sum A_raw^2; [R,2R): sum A_raw V
     double *lam = w.lam.as<double>();
     double *scal = w.scal.as<double>();
     int *status = reinterpret_cast<int *>(scal + 8);
+    double *Ginv = w.L.as<double>();
     T *V = w.V.as<T>();
     for (int n = 0; n < N; ++n) {
+        const bool last = n == N - 1;
         const int64_t r0 = multi ? c.b[n][c.comm->rank] : 0;
         const int64_t r1 = multi ? c.b[n][c.comm->rank + 1] : t->dims[n];
         SPTK_TRY(mttkrp_launch(t, n, c.R, c.A.data(), nullptr, V, r0, r1, c.s));
-        gamma_chol_kernel<<<1, 256, sizeof(double) * R * R, c.s>>>(w.G.as<double>(), N, n, R,
-                                                                 w.L.as<double>(), status);
+        chol_inv_kernel<<<1, 256, sizeof(double) * (R * R + R), c.s>>>(w.G.as<double>(), N, n, R,
+                                                                     Ginv, status);
         count_launch();
         SPTK_CUDA(cudaGetLastError());
         T *An = static_cast<T *>(c.A[n]);
-        if (r1 > r0) {
-            const int bd = R <= 64 ? 128 : 32;
-            const size_t sm = sizeof(double) * ((size_t)R * R + (size_t)R * bd);
-            row_solve_kernel<T><<<(unsigned)((r1 - r0 + bd - 1) / bd), bd, sm, c.s>>>(
-                V, r0, r1, R, w.L.as<double>(), An);
-            count_launch();
+        const int64_t rows = r1 - r0;
+        if (rows > 0) {
+            const int lanes = 256 / R;
+            int nb = (int)std::min<int64_t>(c.nblocks, (rows + 4 * lanes - 1) / (4 * lanes));
+            if (nb < 1) nb = 1;
+            const int64_t rpb = (rows + nb - 1) / nb;
+            nb = (int)((rows + rpb - 1) / rpb);
+            double *pdot = w.partial.as<double>() + (size_t)c.nblocks * R;
+            apply_inv_kernel<T><<<nb, 256, sizeof(double) * (R * R + 512), c.s>>>(
+                V, r0, r1, R, rpb, Ginv, An, w.partial.as<double>(), last ? pdot : nullptr);
+            reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(w.partial.as<double>(), nb, R,
+                                                                colsq);
+            count_launch(2);
+            if (last) {
+                reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(pdot, nb, R, colsq + R);
+                count_launch();
+            }
             SPTK_CUDA(cudaGetLastError());
+        } else {
+            SPTK_CUDA(cudaMemsetAsync(colsq, 0, sizeof(double) * 2 * R, c.s));
         }
-        SPTK_TRY(coldot<T>(c, An, An, r0, r1, colsq));
-        if (multi) SPTK_TRY(comm_allreduce_f64(c.comm, colsq, R, c.s));
-        lambda_kernel<<<1, 128, 0, c.s>>>(colsq, R, lam);
-        if (r1 > r0) normalize_kernel<T><<<grid_for((r1 - r0) * R), 256, 0, c.s>>>(An, r0, r1, R, lam);
-        count_launch(2);
+        if (multi) SPTK_TRY(comm_allreduce_f64(c.comm, colsq, last ? 2 * R : R, c.s));
+        normalize_kernel<T><<<grid_for(std::max<int64_t>(rows, 1) * R), 256, 0, c.s>>>(
+            An, r0, r1, R, colsq, lam);
+        count_launch();
         SPTK_CUDA(cudaGetLastError());
         if (multi) SPTK_TRY(comm_bcast_rows(c.comm, An, c.R, t->dtype, c.b[n].data(), c.s));
         SPTK_TRY(gram<T>(c, n));
     }
-    // fit (last mode's V and A)
-    const int n = N - 1;
-    const int64_t r0 = multi ? c.b[n][c.comm->rank] : 0;
-    const int64_t r1 = multi ? c.b[n][c.comm->rank + 1] : t->dims[n];
-    SPTK_TRY(coldot<T>(c, static_cast<const T *>(c.A[n]), V, r0, r1, colsq));
-    if (multi) SPTK_TRY(comm_allreduce_f64(c.comm, colsq, R, c.s));
-    fit_kernel<<<1, 256, 0, c.s>>>(colsq, lam, w.G.as<double>(), N, R, t->normX2, scal);
+    fit_kernel<<<1, 256, 0, c.s>>>(colsq + R, lam, w.G.as<double>(), N, R, t->normX2, scal);
     count_launch();
     SPTK_CUDA(cudaGetLastError());
     double h[9];
@@ -383,9 +418,9 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     c.nblocks = dev_sms() * 2;
     SPTK_TRY(w.V.reserve(es * Imax * R));
     SPTK_TRY(w.G.reserve(sizeof(double) * N * R * R));
-    SPTK_TRY(w.L.reserve(sizeof(double) * R * R));
-    SPTK_TRY(w.partial.reserve(sizeof(double) * (size_t)c.nblocks * R * R));
-    SPTK_TRY(w.colsq.reserve(sizeof(double) * R));
+    SPTK_TRY(w.L.reserve(sizeof(double) * R * R));  // Gamma^{-1}
+    SPTK_TRY(w.partial.reserve(sizeof(double) * (size_t)c.nblocks * std::max<int64_t>(R * R, 2 * R)));
+    SPTK_TRY(w.colsq.reserve(sizeof(double) * 2 * R));
     SPTK_TRY(w.lam.reserve(sizeof(double) * R));
     SPTK_TRY(w.scal.reserve(sizeof(double) * 16));
     SPTK_TRY(w.lamT.reserve(es * R));
@@ -500,12 +535,12 @@ extern "C" sptk_status sptk_cp_als(sptk_tensor t, int64_t R, int max_iters, doub
         if (!factors_out[m]) return fail(SPTK_EINVAL, "factors_out[m] is NULL");
     if (!(t->normX2 > 0.0)) return fail(SPTK_EZERONORM, "||X|| = 0");
     cudaStream_t s = (cudaStream_t)stream;
-    // row_solve shared memory can exceed the 48 KB default for R > 64
+    // Gamma^{-1} staging can exceed the 48 KB default shared memory for R > 64
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(row_solve_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(row_solve_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(gamma_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(apply_inv_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(apply_inv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
     sptk_status st =

@@ -6,15 +6,45 @@
 
 namespace sptk {
 
-static int64_t run_length() {
-    static int64_t run = 0;
-    if (!run) {
+static int64_t g_run = -1;  // -1: unset, 0: adaptive, > 0: fixed
+static int g_variant = -1;
+
+// Nonzeros per worker (the paper's NZPTM block).  Adaptive by default:
+// long runs amortise the two boundary atomics, but the grid must still cover
+// every SM several times, so small tensors get short runs (>= 16).
+static int64_t run_length(int64_t npos, int G) {
+    if (g_run < 0) {
         const char *e = getenv("SPTK_RUN");
-        run = e ? atoll(e) : 256;
-        if (run < 2) run = 2;
-        run = (run + 1) / 2 * 2;  // multiple of the unroll (2)
+        g_run = e ? atoll(e) : 0;
+        if (g_run < 0) g_run = 0;
     }
-    return run;
+    if (g_run > 0) return g_run;
+    const int64_t workers_per_sm = 768 / G;  // ~3 resident 256-thread blocks
+    const int64_t target = (int64_t)dev_sms() * workers_per_sm * 4;
+    int64_t run = npos / (target > 0 ? target : 1);
+    if (run > 256) run = 256;
+    if (run < 16) run = 16;
+    return (run + 3) / 4 * 4;
+}
+
+static int variant() {
+    if (g_variant < 0) {
+        const char *e = getenv("SPTK_VARIANT");
+        g_variant = e ? atoi(e) : 0;
+        if (g_variant < 0 || g_variant >= kNumVariants) g_variant = 0;
+    }
+    return g_variant;
+}
+
+template <typename T>
+static sptk_status launch_fast(int N, int G, int rb, const MttkrpArgs &a, int64_t workers,
+                               cudaStream_t s) {
+    switch (N) {
+    case 3: return launch_fast_tn<T, 3>(G, rb, variant(), a, workers, s);
+    case 4: return launch_fast_tn<T, 4>(G, rb, variant(), a, workers, s);
+    case 5: return launch_fast_tn<T, 5>(G, rb, variant(), a, workers, s);
+    default: return fail(SPTK_EINVAL, "fast MTTKRP: N must be 3..5");
+    }
 }
 
 static int pow2ceil(int x) {
@@ -61,7 +91,6 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     }
     a.pos_begin = pb;
     a.pos_end = pe;
-    a.run = run_length();
     a.ld = R;
     a.mode = mode;
     a.N = t->N;
@@ -69,13 +98,15 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     for (int m = 0; m < t->N; ++m) a.A[m] = (m == mode) ? nullptr : factors[m];
     a.lambda = lambda;
     a.out = out;
-    const int64_t workers = (pe - pb + a.run - 1) / a.run;
 
     const int V = 32 / (int)es;
     bool fast = t->N >= 3 && t->N <= 5 && R % V == 0 && aligned32(out) &&
                 (!lambda || aligned32(lambda));
     for (int m = 0; m < t->N && fast; ++m)
         if (m != mode && !aligned32(factors[m])) fast = false;
+    const int G0 = fast ? pow2ceil((int)((R < 32 * V ? R : 32 * V) / V)) : (R <= 16 ? 4 : 32);
+    a.run = run_length(pe - pb, G0);
+    const int64_t workers = (pe - pb + a.run - 1) / a.run;
 
     cudaEvent_t ev;
     SPTK_TRY(mttkrp_span_begin(s, &ev));
@@ -105,6 +136,15 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
 }  // namespace sptk
 
 using namespace sptk;
+
+extern "C" sptk_status sptk_set_tuning(int variant, int64_t run) {
+    if (variant >= kNumVariants || variant < -1 || run < -2)
+        return fail(SPTK_EINVAL, "set_tuning: variant in [-1, 4], run >= -2");
+    if (variant >= 0) g_variant = variant;
+    if (run > 0) g_run = run < 4 ? 4 : (run + 3) / 4 * 4;
+    if (run == -2) g_run = 0;  // back to adaptive
+    return SPTK_OK;
+}
 
 extern "C" sptk_status sptk_mttkrp(sptk_tensor t, int mode, int64_t R,
                                    const void *const *factors, const void *lambda, void *out,

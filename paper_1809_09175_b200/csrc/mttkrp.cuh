@@ -230,8 +230,8 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
     if (cur != kNoRow) flush(cur, true);
 }
 
-template <typename T, int N, int G, int U, int RB, bool SORTED>
-__global__ void __launch_bounds__(256) mttkrp_fast_kernel(const MttkrpArgs a) {
+template <typename T, int N, int G, int U, int RB, bool SORTED, int MINB>
+__global__ void __launch_bounds__(256, MINB) mttkrp_fast_kernel(const MttkrpArgs a) {
     if constexpr (N >= 1) if (a.mode == 0) { mttkrp_fast_body<T, N, 0, G, U, RB, SORTED>(a); return; }
     if constexpr (N >= 2) if (a.mode == 1) { mttkrp_fast_body<T, N, 1, G, U, RB, SORTED>(a); return; }
     if constexpr (N >= 3) if (a.mode == 2) { mttkrp_fast_body<T, N, 2, G, U, RB, SORTED>(a); return; }
@@ -316,10 +316,57 @@ __global__ void __launch_bounds__(256) mttkrp_generic_kernel(const MttkrpArgs a)
     if (cur != kNoRow) flush(cur, true);
 }
 
-// launchers (instantiated per dtype in mttkrp_f64.cu / mttkrp_f32.cu)
-template <typename T>
-sptk_status launch_fast(int N, int G, int rb, const MttkrpArgs &a, int64_t workers,
-                        cudaStream_t s);
+// Launch-shape variants of the fast kernel: (U positions per step, min
+// resident 256-thread blocks per SM -> register cap).  Variant 0 is the
+// default; SPTK_VARIANT selects another one (tuning sweeps).
+constexpr int kNumVariants = 5;
+template <int V> struct Variant;
+template <> struct Variant<0> { static constexpr int U = 2, MINB = 3; };
+template <> struct Variant<1> { static constexpr int U = 2, MINB = 4; };
+template <> struct Variant<2> { static constexpr int U = 4, MINB = 2; };
+template <> struct Variant<3> { static constexpr int U = 4, MINB = 3; };
+template <> struct Variant<4> { static constexpr int U = 1, MINB = 5; };
+
+template <typename T, int N, int RB, bool SORTED, int VAR>
+inline sptk_status fast_launch_g(int G, const MttkrpArgs &a, int64_t workers, cudaStream_t s) {
+    constexpr int U = Variant<VAR>::U, MB = Variant<VAR>::MINB;
+    const int64_t threads = workers * G;
+    const unsigned blocks = (unsigned)((threads + 255) / 256);
+    switch (G) {
+    case 1: mttkrp_fast_kernel<T, N, 1, U, RB, SORTED, MB><<<blocks, 256, 0, s>>>(a); break;
+    case 2: mttkrp_fast_kernel<T, N, 2, U, RB, SORTED, MB><<<blocks, 256, 0, s>>>(a); break;
+    case 4: mttkrp_fast_kernel<T, N, 4, U, RB, SORTED, MB><<<blocks, 256, 0, s>>>(a); break;
+    case 8: mttkrp_fast_kernel<T, N, 8, U, RB, SORTED, MB><<<blocks, 256, 0, s>>>(a); break;
+    case 16: mttkrp_fast_kernel<T, N, 16, U, RB, SORTED, MB><<<blocks, 256, 0, s>>>(a); break;
+    case 32: mttkrp_fast_kernel<T, N, 32, U, RB, SORTED, MB><<<blocks, 256, 0, s>>>(a); break;
+    default: return fail(SPTK_EINVAL, "fast MTTKRP: bad lane count");
+    }
+    count_launch();
+    SPTK_CUDA(cudaGetLastError());
+    return SPTK_OK;
+}
+
+// Per-(T, N) launcher, explicitly instantiated in mttkrp_<t>_n<N>.cu.
+template <typename T, int N>
+sptk_status launch_fast_tn(int G, int rb, int variant, const MttkrpArgs &a, int64_t workers,
+                           cudaStream_t s);
+
+#define SPTK_INSTANTIATE_FAST(T, N)                                                          \
+    template <>                                                                              \
+    sptk_status launch_fast_tn<T, N>(int G, int rb, int variant, const MttkrpArgs &a,        \
+                                     int64_t workers, cudaStream_t s) {                      \
+        constexpr int RB = (sizeof(T) + 4 * N <= 16) ? 16 : 32;                              \
+        (void)rb;                                                                            \
+        if (a.perm) return fast_launch_g<T, N, RB, false, 0>(G, a, workers, s);              \
+        switch (variant) {                                                                   \
+        case 1: return fast_launch_g<T, N, RB, true, 1>(G, a, workers, s);                   \
+        case 2: return fast_launch_g<T, N, RB, true, 2>(G, a, workers, s);                   \
+        case 3: return fast_launch_g<T, N, RB, true, 3>(G, a, workers, s);                   \
+        case 4: return fast_launch_g<T, N, RB, true, 4>(G, a, workers, s);                   \
+        default: return fast_launch_g<T, N, RB, true, 0>(G, a, workers, s);                  \
+        }                                                                                    \
+    }
+
 template <typename T>
 sptk_status launch_generic(int G, const MttkrpArgs &a, int64_t workers, cudaStream_t s);
 
