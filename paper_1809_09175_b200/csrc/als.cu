@@ -12,9 +12,9 @@
 //   per iteration: fit = 1 - sqrt(max(0, ||X||^2 + ||M||^2 - 2<X,M>)) / ||X||
 //                <X,M> = sum_j lambda_j sum_k A_{N-1}(k,j) V(k,j)
 //                ||M||^2 = lambda^T (Hadamard_m G_m) lambda
-// All reductions are fixed-order (per-block partials, then a fixed shuffle
-// tree), so a run is bit-reproducible; one small D2H (fit, status) per
-// iteration.  The oracle solves with the Cholesky factor row by row; using
+// All glue reductions are fixed-order (per-block partials, then a fixed
+// shuffle tree); the MTTKRP's boundary-row atomics are not, so runs agree to
+// rounding, not bit for bit.  One small D2H (fit, status) per iteration.  The oracle solves with the Cholesky factor row by row; using
 // the explicit inverse differs only at rounding level.
 // Multi-GPU: each rank solves its own row range of every mode, the R column
 // sums of squares and <X,M> partials are all-reduced, the rows broadcast.

@@ -244,8 +244,10 @@ def test_cp_als_tiny_trajectory(sp):
     Ah = [np.empty((I, R)) for I in c.dims]
     lamh = np.empty(R)
     res2 = sp.cp_als(t, R, 10, Ah, seed=c.seed_f, lambda_out=lamh)
-    assert np.array_equal(res2["trace"], res["trace"])
-    assert all(np.array_equal(Ah[m], A[m].cpu().numpy()) for m in range(3))
+    # MTTKRP boundary rows use atomics (summation order varies run to run)
+    assert np.max(np.abs(res2["trace"] - res["trace"])) <= 1e-12
+    assert all(rel(Ah[m], A[m].cpu().numpy()) <= 1e-12 for m in range(3))
+    assert rel(lamh, lam.cpu().numpy()) <= 1e-12
 
 
 def test_cp_als_planted_recovery_and_f32(sp):
