@@ -268,6 +268,7 @@ def main():
     e2.record()
     torch.cuda.synchronize()
     del idx_d, val_d
+    torch.cuda.empty_cache()  # return the COO staging to the driver (perm copies need it)
     perm_ms, perm_first_ms = [], []
     for n in range(c.N):
         for rep in range(2):        # first call includes lazy module load + allocations
@@ -278,6 +279,7 @@ def main():
             torch.cuda.synchronize()
             (perm_first_ms if rep == 0 else perm_ms).append(a.elapsed_time(b))
     F = [sdev.factor(c.seed_f, c.N, m, I, R, dtype=tdt) for m, I in enumerate(c.dims)]
+    dev_bytes = sp.sptensor_device_bytes(t)
 
     # per-rank share of the work (row-range sharding) for the byte model
     bounds, pos = [], []
@@ -395,7 +397,8 @@ def main():
             "gflops": sum(metrics.flops(c.N, c.nnz, R) for _ in c.dims) / (ms_max * 1e-3) / 1e9,
             "setup": {"generate_ms": e0.elapsed_time(e1), "create_ms": e1.elapsed_time(e2),
                       "build_perm_ms": perm_ms, "build_perm_first_call_ms": perm_first_ms,
-                      "sort_to_iteration_ratio": sum(perm_ms) / ms_max},
+                      "sort_to_iteration_ratio": sum(perm_ms) / ms_max,
+                      "tensor_device_bytes": dev_bytes},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "mttkrp_fast_kernel (permuted traversal)",

@@ -223,7 +223,8 @@ sptk_status sptk_sptensor_info(sptk_tensor t, int *nmodes, int64_t *dims, int64_
 sptk_status sptk_sptensor_device_bytes(sptk_tensor t, int64_t *bytes) {
     if (!t || !bytes) return fail(SPTK_EINVAL, "null argument");
     int64_t b = t->rec.bytes;
-    for (int m = 0; m < t->N; ++m) b += t->perm[m].bytes + t->rowptr[m].bytes + t->srec[m].bytes;
+    for (int m = 0; m < t->N; ++m)
+        b += t->perm[m].bytes + t->rowptr[m].bytes + t->srec[m].bytes + t->wrow[m].bytes;
     const ALSWork &w = t->als;
     b += w.V.bytes + w.G.bytes + w.L.bytes + w.partial.bytes + w.colsq.bytes + w.lam.bytes +
          w.scal.bytes + w.stage.bytes + w.lamT.bytes;
@@ -235,8 +236,14 @@ sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream) {
     CHECK_HANDLE(t);
     if (mode < -1 || mode >= t->N) return fail(SPTK_EINVAL, "mode out of range");
     cudaStream_t s = (cudaStream_t)stream;
-    for (int m = (mode < 0 ? 0 : mode); m < (mode < 0 ? t->N : mode + 1); ++m) {
+    const int m0 = mode < 0 ? 0 : mode, m1 = mode < 0 ? t->N : mode + 1;
+    for (int m = m0; m < m1; ++m) {  // all sorts first: their temporaries are the peak
         sptk_status st = build_perm_mode(t, m, s);
+        if (st == SPTK_ECUDA) t->poisoned = true;
+        if (st != SPTK_OK) return st;
+    }
+    for (int m = m0; m < m1; ++m) {  // then the permuted copies, while memory allows
+        sptk_status st = ensure_sorted_copy(t, m, s);
         if (st == SPTK_ECUDA) t->poisoned = true;
         if (st != SPTK_OK) return st;
     }

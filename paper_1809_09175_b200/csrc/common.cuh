@@ -92,8 +92,10 @@ struct sptk_tensor_s {
     sptk::DevBuf perm[sptk::kMaxModes];         // uint32[P]
     sptk::DevBuf rowptr[sptk::kMaxModes];       // uint32[I_n + 1]
     bool has_perm[sptk::kMaxModes] = {false};
-    sptk::DevBuf srec[sptk::kMaxModes];         // records in perm_n order (optional)
+    sptk::DevBuf srec[sptk::kMaxModes];         // compact records in perm_n order (optional)
     bool has_srec[sptk::kMaxModes] = {false};
+    sptk::DevBuf wrow[sptk::kMaxModes];         // worker start rows for the copy (cached)
+    int64_t wrow_key[sptk::kMaxModes][3] = {{-1, -1, -1}};  // (pos_begin, pos_end, run)
     bool perm_gather_only = false;              // SPTK_CREATE_PERM_GATHER
     std::vector<uint32_t> host_rowptr[sptk::kMaxModes];  // for partitioning (lazy)
     double normX2 = 0.0;
@@ -116,11 +118,17 @@ inline int record_bytes(sptk_dtype dt, int N) {
     return (vb + 4 * N <= 16) ? 16 : 32;
 }
 inline int dtype_bytes(sptk_dtype dt) { return dt == SPTK_F64 ? 8 : 4; }
+// compact permuted copy of mode n: value, then the N-1 other indices
+inline int compact_bytes(sptk_dtype dt, int N) {
+    const int vb = dt == SPTK_F64 ? 8 : 4;
+    return (vb + 4 * (N - 1) <= 16) ? 16 : 32;
+}
 
 // --- kernels implemented in the .cu files (host launchers) ---
 sptk_status launch_pack(sptk_tensor t, const void *idx, sptk_idx_type itype, const void *vals,
                         int *d_flag, double *d_normsq, cudaStream_t s);
 sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s);
+sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s);
 sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const *factors,
                           const void *lambda, void *out, int64_t row_begin, int64_t row_end,
                           cudaStream_t s);

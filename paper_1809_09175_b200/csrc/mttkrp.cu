@@ -65,6 +65,40 @@ sptk_status host_rowptr(sptk_tensor t, int mode, cudaStream_t s) {
     return SPTK_OK;
 }
 
+// start row of every worker: the largest r with rowptr[r] <= s (binary search)
+__global__ void worker_rows_kernel(const uint32_t *__restrict__ rowptr, int64_t In, int64_t pb,
+                                   int64_t run, int64_t nworkers, uint32_t *__restrict__ wrow) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nworkers;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = pb + w * run;
+        int64_t lo = 0, hi = In - 1;  // invariant: rowptr[lo] <= s
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if ((int64_t)__ldg(rowptr + mid) <= s) lo = mid;
+            else hi = mid - 1;
+        }
+        wrow[w] = (uint32_t)lo;
+    }
+}
+
+static sptk_status worker_rows(sptk_tensor t, int mode, int64_t pb, int64_t pe, int64_t run,
+                               int64_t workers, cudaStream_t s) {
+    int64_t *key = t->wrow_key[mode];
+    if (key[0] == pb && key[1] == pe && key[2] == run && t->wrow[mode].p) return SPTK_OK;
+    SPTK_TRY(t->wrow[mode].reserve(sizeof(uint32_t) * workers));
+    int64_t blocks = (workers + 255) / 256;
+    if (blocks > (int64_t)dev_sms() * 16) blocks = (int64_t)dev_sms() * 16;
+    worker_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(t->rowptr[mode].as<uint32_t>(),
+                                                        t->dims[mode], pb, run, workers,
+                                                        t->wrow[mode].as<uint32_t>());
+    count_launch();
+    SPTK_CUDA(cudaGetLastError());
+    key[0] = pb;
+    key[1] = pe;
+    key[2] = run;
+    return SPTK_OK;
+}
+
 sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const *factors,
                           const void *lambda, void *out, int64_t row_begin, int64_t row_end,
                           cudaStream_t s) {
@@ -81,14 +115,10 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     }
     if (pe <= pb) return SPTK_OK;
 
+    SPTK_TRY(ensure_sorted_copy(t, mode, s));
     MttkrpArgs a{};
-    if (t->has_srec[mode]) {  // records materialised in perm_n order: stream them
-        a.rec = t->srec[mode].as<uint8_t>();
-        a.perm = nullptr;
-    } else {                  // the paper's traversal: gather through perm_n
-        a.rec = t->rec.as<uint8_t>();
-        a.perm = t->perm[mode].as<uint32_t>();
-    }
+    a.rec = t->rec.as<uint8_t>();  // the paper's traversal: gather through perm_n
+    a.perm = t->perm[mode].as<uint32_t>();
     a.pos_begin = pb;
     a.pos_end = pe;
     a.ld = R;
@@ -107,6 +137,13 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     const int G0 = fast ? pow2ceil((int)((R < 32 * V ? R : 32 * V) / V)) : (R <= 16 ? 4 : 32);
     a.run = run_length(pe - pb, G0);
     const int64_t workers = (pe - pb + a.run - 1) / a.run;
+    if (fast && t->has_srec[mode]) {  // stream the compact permuted copy instead
+        SPTK_TRY(worker_rows(t, mode, pb, pe, a.run, workers, s));
+        a.rec = t->srec[mode].as<uint8_t>();
+        a.perm = nullptr;
+        a.rowptr = t->rowptr[mode].as<uint32_t>();
+        a.wrow = t->wrow[mode].as<uint32_t>();
+    }
 
     cudaEvent_t ev;
     SPTK_TRY(mttkrp_span_begin(s, &ev));

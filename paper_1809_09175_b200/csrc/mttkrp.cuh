@@ -26,8 +26,8 @@
 //   * lambda (NULL = ones) is applied once per flush (Z1);
 //   * U positions are processed per step with the perm entries for the next
 //     step prefetched, so several records and 2U factor rows are in flight.
-// The generic kernel (any N <= 6, any R) uses scalar loads with runtime
-// record offsets and column tiles; same write discipline.
+// The generic kernel (any N <= 6, any R) gathers through perm_n with scalar
+// loads, runtime record offsets and column tiles; same write discipline.
 #pragma once
 #include "common.cuh"
 
@@ -37,7 +37,9 @@ constexpr uint32_t kNoRow = 0xffffffffu;
 
 struct MttkrpArgs {
     const uint8_t *rec;
-    const uint32_t *perm;        // NULL: `rec` is already in perm_n order
+    const uint32_t *perm;        // NULL: `rec` is the compact permuted copy of `mode`
+    const uint32_t *rowptr;      // rowptr_n (permuted copy only)
+    const uint32_t *wrow;        // start row of every worker (permuted copy only)
     int64_t pos_begin, pos_end;  // permuted positions handled by this launch
     int64_t run;                 // positions per worker
     int64_t ld;                  // row stride of factors and out (= R)
@@ -107,6 +109,12 @@ template <> __device__ __forceinline__ float rec_val<float>(const uint32_t (&w)[
 // ------------------------------------------------------- fast kernel body
 // T, N (3..5), MODE (< N) and G (lanes per worker) are compile-time; the
 // column tile is [col0, col0 + ncols) with ncols <= G*V and ncols % V == 0.
+// SORTED: `rec` is the compact permuted copy of mode MODE ({x, l_m for
+// m != MODE}, RB bytes, position i = record i, streamed and prefetched one
+// step ahead); the mode-n row of position i is tracked with rowptr_n from
+// the worker's start row `wrow` (rows only grow along the permutation).
+// Otherwise the paper's traversal: p = perm_n[i] (prefetched one step ahead),
+// gather the full record p and read l_pn from it.
 template <typename T, int N, int MODE, int G, int U, int RB, bool SORTED>
 __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
     constexpr int V = 32 / sizeof(T);
@@ -114,19 +122,15 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
     const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t worker = gtid / G;
     const int q = (int)(gtid % G);
-    const int64_t s = a.pos_begin + worker * a.run;
-    if (s >= a.pos_end) return;
-    const int64_t e = min(s + a.run, a.pos_end);
+    if (a.pos_begin + worker * a.run >= a.pos_end) return;
+    // positions fit in 32 bits (P < 2^32): keeps the loop state small
+    const uint32_t s = (uint32_t)(a.pos_begin + worker * a.run);
+    const uint32_t e = (uint32_t)min(a.pos_begin + worker * a.run + a.run, a.pos_end);
     const bool lane_on = q * V < a.ncols;
     const int c = a.col0 + q * V;
     const uint8_t *__restrict__ rec = a.rec;
     const uint32_t *__restrict__ perm = a.perm;
     T *__restrict__ out = static_cast<T *>(a.out);
-
-    T lam[V];
-#pragma unroll
-    for (int v = 0; v < V; ++v) lam[v] = T(1);
-    if (a.lambda && lane_on) ld_row(static_cast<const T *>(a.lambda) + c, lam);
 
     T acc[V];
 #pragma unroll
@@ -137,21 +141,30 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
         if (!lane_on) return;
         T o[V];
 #pragma unroll
-        for (int v = 0; v < V; ++v) o[v] = acc[v] * lam[v];
+        for (int v = 0; v < V; ++v) o[v] = acc[v];
+        if (a.lambda) {  // lambda applied once per flushed row (Z1)
+            T lam[V];
+            ld_row(static_cast<const T *>(a.lambda) + c, lam);
+#pragma unroll
+            for (int v = 0; v < V; ++v) o[v] *= lam[v];
+        }
         T *dst = out + (int64_t)row * a.ld + c;
         if (atomic) red_row(dst, o);
         else st_row(dst, o);
     };
-
-    // SORTED: records are stored in perm_n order, position i is record i
-    // (streamed, prefetched one step ahead).  Otherwise the paper's
-    // traversal: p = perm_n[i] (prefetched one step ahead), gather record p.
-    uint32_t pn[U];
-    uint32_t wn[U][8];
-    auto load_rec = [&](int64_t pos, uint32_t (&r)[8]) {
+    auto load_rec = [&](uint32_t pos, uint32_t (&r)[8]) {
         if constexpr (RB == 32) ld_rec32(rec + (size_t)pos * 32, r);
         else ld_rec16(rec + (size_t)pos * 16, r);
     };
+
+    uint32_t row = 0;   // SORTED: row of the current position
+    uint32_t nxt = 0;   // SORTED: first position of row + 1
+    if constexpr (SORTED) {
+        row = __ldg(a.wrow + worker);
+        nxt = __ldg(a.rowptr + row + 1);
+    }
+    uint32_t pn[U];
+    uint32_t wn[U][8];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         if constexpr (SORTED) {
@@ -162,7 +175,7 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
         }
     }
 
-    for (int64_t i = s; i < e; i += U) {
+    for (uint32_t i = s; i < e; i += U) {
         uint32_t p[U];
         uint32_t w[U][8];
 #pragma unroll
@@ -174,9 +187,9 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
                 for (int k = 0; k < 8; ++k) w[u][k] = wn[u][k];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int64_t q = i + U + u;
-                pn[u] = q < e ? 0u : kNoRow;
-                if (q < e) load_rec(q, wn[u]);
+                const uint32_t qq = i + U + u;
+                pn[u] = qq < e ? 0u : kNoRow;
+                if (qq < e) load_rec(qq, wn[u]);
             }
         } else {
 #pragma unroll
@@ -198,8 +211,9 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
 #pragma unroll
             for (int m = 0; m < N; ++m)
                 if (m != MODE) {
+                    const int word = SORTED ? OFF + (m < MODE ? m : m - 1) : OFF + m;
                     if (p[u] != kNoRow && lane_on)
-                        ld_row(static_cast<const T *>(a.A[m]) + (int64_t)w[u][OFF + m] * a.ld + c,
+                        ld_row(static_cast<const T *>(a.A[m]) + (int64_t)w[u][word] * a.ld + c,
                                f[u][m]);
                     else
 #pragma unroll
@@ -208,13 +222,23 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (p[u] == kNoRow) continue;
-            const uint32_t row = w[u][OFF + MODE];
-            if (row != cur) {
+            uint32_t r;
+            if constexpr (SORTED) {
+                const uint32_t pos = i + u;
+                while (pos >= nxt) {
+                    ++row;
+                    nxt = __ldg(a.rowptr + row + 1);
+                }
+                r = row;
+            } else {
+                r = w[u][OFF + MODE];
+            }
+            if (r != cur) {
                 if (cur != kNoRow) flush(cur, cur == first);
 #pragma unroll
                 for (int v = 0; v < V; ++v) acc[v] = T(0);
-                if (first == kNoRow) first = row;
-                cur = row;
+                if (first == kNoRow) first = r;
+                cur = r;
             }
             const T x = rec_val<T>(w[u]);
 #pragma unroll
@@ -282,7 +306,7 @@ __global__ void __launch_bounds__(256) mttkrp_generic_kernel(const MttkrpArgs a)
         T t[U][NV];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            p[u] = (i + u < e) ? (a.perm ? __ldg(a.perm + i + u) : (uint32_t)(i + u)) : kNoRow;
+            p[u] = (i + u < e) ? __ldg(a.perm + i + u) : kNoRow;
             if (p[u] == kNoRow) continue;
             const uint8_t *r = rec + (size_t)p[u] * rb;
             x[u] = __ldg(reinterpret_cast<const T *>(r));
@@ -355,15 +379,16 @@ sptk_status launch_fast_tn(int G, int rb, int variant, const MttkrpArgs &a, int6
     template <>                                                                              \
     sptk_status launch_fast_tn<T, N>(int G, int rb, int variant, const MttkrpArgs &a,        \
                                      int64_t workers, cudaStream_t s) {                      \
-        constexpr int RB = (sizeof(T) + 4 * N <= 16) ? 16 : 32;                              \
+        constexpr int RB = (sizeof(T) + 4 * N <= 16) ? 16 : 32;        /* full record */      \
+        constexpr int RC = (sizeof(T) + 4 * (N - 1) <= 16) ? 16 : 32;  /* compact copy */     \
         (void)rb;                                                                            \
         if (a.perm) return fast_launch_g<T, N, RB, false, 0>(G, a, workers, s);              \
         switch (variant) {                                                                   \
-        case 1: return fast_launch_g<T, N, RB, true, 1>(G, a, workers, s);                   \
-        case 2: return fast_launch_g<T, N, RB, true, 2>(G, a, workers, s);                   \
-        case 3: return fast_launch_g<T, N, RB, true, 3>(G, a, workers, s);                   \
-        case 4: return fast_launch_g<T, N, RB, true, 4>(G, a, workers, s);                   \
-        default: return fast_launch_g<T, N, RB, true, 0>(G, a, workers, s);                  \
+        case 1: return fast_launch_g<T, N, RC, true, 1>(G, a, workers, s);                   \
+        case 2: return fast_launch_g<T, N, RC, true, 2>(G, a, workers, s);                   \
+        case 3: return fast_launch_g<T, N, RC, true, 3>(G, a, workers, s);                   \
+        case 4: return fast_launch_g<T, N, RC, true, 4>(G, a, workers, s);                   \
+        default: return fast_launch_g<T, N, RC, true, 0>(G, a, workers, s);                  \
         }                                                                                    \
     }
 

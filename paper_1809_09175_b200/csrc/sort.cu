@@ -11,6 +11,8 @@
 //              [w*512, w*512+512) and ranks equal digits with __match_any_sync
 //              in rounds of 32, so equal keys keep their storage order.
 // Then rowptr_n[r] = first sorted position with key >= r (boundary kernel).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace sptk {
@@ -255,17 +257,35 @@ __global__ void fill_u32(uint32_t *__restrict__ out, int64_t n, uint32_t v) {
         out[i] = v;
 }
 
-// srec[i] = rec[perm[i]]: the records in permuted order (one gather at build time)
-template <int RB>
-__global__ void __launch_bounds__(256) permute_records(const uint8_t *__restrict__ rec,
-                                                       const uint32_t *__restrict__ perm, int64_t P,
-                                                       uint8_t *__restrict__ srec) {
+// srec[i] = compact(rec[perm[i]]): the records in permuted order with the
+// mode-n index dropped (it is implied by rowptr_n): {x, l_m for m != mode}.
+template <int RB, int RC>
+__global__ void __launch_bounds__(256)
+    permute_records(const uint8_t *__restrict__ rec, const uint32_t *__restrict__ perm, int64_t P,
+                    int vw, int N, int mode, uint8_t *__restrict__ srec) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint4 *src = reinterpret_cast<const uint4 *>(rec + (size_t)__ldg(perm + i) * RB);
-        uint4 *dst = reinterpret_cast<uint4 *>(srec + (size_t)i * RB);
-        dst[0] = __ldg(src);
-        if constexpr (RB == 32) dst[1] = __ldg(src + 1);
+        uint32_t w[8];
+        const uint4 a = __ldg(src);
+        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+        if constexpr (RB == 32) {
+            const uint4 b = __ldg(src + 1);
+            w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+        } else {
+            w[4] = w[5] = w[6] = w[7] = 0;
+        }
+        uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k < vw) o[k] = w[k];
+        int d = vw;
+#pragma unroll
+        for (int m = 0; m < kMaxModes; ++m)
+            if (m < N && m != mode && vw + m < 8 && d < 8) o[d++] = w[vw + m];
+        uint4 *dst = reinterpret_cast<uint4 *>(srec + (size_t)i * RC);
+        dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+        if constexpr (RC == 32) dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
     }
 }
 
@@ -276,29 +296,50 @@ static int grid_for(int64_t n) {
     return b < 1 ? 1 : (int)b;
 }
 
-// Materialise the records in perm_n order unless the tensor keeps the paper's
-// perm-gather traversal; an allocation failure falls back to that traversal.
-static sptk_status build_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
-    t->has_srec[mode] = false;
-    if (t->perm_gather_only || t->P == 0) {
-        t->srec[mode].release();
+// Materialise the compact permuted copy of `mode` unless the tensor keeps the
+// paper's perm-gather traversal or the copy would leave less than the reserve
+// free (then that mode keeps gathering through perm_n).  Copies are caches:
+// build_perm releases them if a sort needs their memory.
+sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
+    if (t->has_srec[mode] || t->perm_gather_only || t->P == 0 || !t->has_perm[mode])
+        return SPTK_OK;
+    const int rc = compact_bytes(t->dtype, t->N);
+    const size_t need = (size_t)rc * t->P;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        cudaGetLastError();
         return SPTK_OK;
     }
-    if (t->srec[mode].reserve((size_t)t->rec_bytes * t->P) != SPTK_OK) {
+    const size_t reserve = std::max<size_t>(total_b / 32, (size_t)4 << 30);
+    if (free_b < need + reserve) return SPTK_OK;
+    if (t->srec[mode].reserve(need) != SPTK_OK) {
         set_error("");
         return SPTK_OK;
     }
     const uint32_t *perm = t->perm[mode].as<uint32_t>();
-    if (t->rec_bytes == 32)
-        permute_records<32><<<grid_for(t->P), 256, 0, s>>>(t->rec.as<uint8_t>(), perm, t->P,
-                                                          t->srec[mode].as<uint8_t>());
+    const int vw = dtype_bytes(t->dtype) / 4;
+    const unsigned g = (unsigned)grid_for(t->P);
+    uint8_t *dst = t->srec[mode].as<uint8_t>();
+    const uint8_t *src = t->rec.as<uint8_t>();
+    if (t->rec_bytes == 32 && rc == 32)
+        permute_records<32, 32><<<g, 256, 0, s>>>(src, perm, t->P, vw, t->N, mode, dst);
+    else if (t->rec_bytes == 32)
+        permute_records<32, 16><<<g, 256, 0, s>>>(src, perm, t->P, vw, t->N, mode, dst);
     else
-        permute_records<16><<<grid_for(t->P), 256, 0, s>>>(t->rec.as<uint8_t>(), perm, t->P,
-                                                          t->srec[mode].as<uint8_t>());
+        permute_records<16, 16><<<g, 256, 0, s>>>(src, perm, t->P, vw, t->N, mode, dst);
     count_launch();
     SPTK_CUDA(cudaGetLastError());
     t->has_srec[mode] = true;
     return SPTK_OK;
+}
+
+static void drop_copies(sptk_tensor t) {
+    for (int m = 0; m < t->N; ++m) {
+        t->srec[m].release();
+        t->has_srec[m] = false;
+        t->wrow[m].release();
+        t->wrow_key[m][0] = -1;
+    }
 }
 
 sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s) {
@@ -308,6 +349,7 @@ sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s) {
     uint32_t *perm = t->perm[mode].as<uint32_t>();
     uint32_t *rowptr = t->rowptr[mode].as<uint32_t>();
     t->host_rowptr[mode].clear();
+    t->wrow_key[mode][0] = -1;
     if (P == 0) {
         SPTK_CUDA(cudaMemsetAsync(rowptr, 0, sizeof(uint32_t) * (In + 1), s));
         t->has_perm[mode] = true;
@@ -328,10 +370,17 @@ sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s) {
     const int dbits = (bits + npass - 1) / npass;
     const int64_t ntiles = (P + kSortTile - 1) / kSortTile;
     DevBuf kA, kB, vA, counts, tmp;
-    SPTK_TRY(kA.reserve(sizeof(uint32_t) * P));
-    SPTK_TRY(kB.reserve(sizeof(uint32_t) * P));
-    SPTK_TRY(vA.reserve(sizeof(uint32_t) * P));
-    SPTK_TRY(counts.reserve(sizeof(uint32_t) * ntiles * (1 << dbits)));
+    auto alloc_temps = [&]() -> sptk_status {
+        SPTK_TRY(kA.reserve(sizeof(uint32_t) * P));
+        SPTK_TRY(kB.reserve(sizeof(uint32_t) * P));
+        SPTK_TRY(vA.reserve(sizeof(uint32_t) * P));
+        SPTK_TRY(counts.reserve(sizeof(uint32_t) * ntiles * (1 << dbits)));
+        return SPTK_OK;
+    };
+    if (alloc_temps() != SPTK_OK) {  // permuted copies are caches: free them and retry
+        drop_copies(t);
+        SPTK_TRY(alloc_temps());
+    }
     // ping-pong: vals end in `perm` after the last pass
     uint32_t *kin = nullptr, *vin = nullptr;
     uint32_t *kbuf[2] = {kA.as<uint32_t>(), kB.as<uint32_t>()};
@@ -375,7 +424,7 @@ sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s) {
     // temporaries are freed when this returns: order the frees after the work
     SPTK_CUDA(cudaStreamSynchronize(s));
     t->has_perm[mode] = true;
-    return build_sorted_copy(t, mode, s);
+    return SPTK_OK;
 }
 
 }  // namespace sptk

@@ -115,6 +115,70 @@ __global__ void __launch_bounds__(256) row_gather(const double *A, int64_t rows,
     if (acc == 1.2345) out[0] = acc;
 }
 
+// MTTKRP-shaped access without the arithmetic: stream 32 B records (val,
+// i0, i1, i2), gather two 128 B rows per record (4 lanes x 32 B) from
+// L2-resident tables.  COOP=false: each 4-lane group walks its own
+// contiguous run (as mttkrp_fast_kernel); COOP=true: the 8 groups of a warp
+// take 8 consecutive records per step (one 256 B coalesced record load).
+template <bool COOP>
+__global__ void __launch_bounds__(256, 3) stream_gather(const uint8_t *rec, int64_t n,
+                                                        const double *A1, const double *A2,
+                                                        int64_t run, double *out) {
+    const int q = threadIdx.x & 3;
+    const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t s, e, stride;
+    if (COOP) {
+        const int64_t warp = gtid >> 5;
+        const int g = (threadIdx.x & 31) >> 2;
+        s = warp * run * 8 + g;
+        e = min(warp * run * 8 + run * 8, n);
+        stride = 8;
+    } else {
+        const int64_t grp = gtid >> 2;
+        s = grp * run;
+        e = min(s + run, n);
+        stride = 1;
+    }
+    double acc[4] = {0, 0, 0, 0};
+    for (int64_t i = s; i < e; i += 2 * stride) {
+        uint32_t r[2][8];
+        double f[2][2][4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int64_t p = i + u * stride;
+            if (p < e) load32<1>(rec + p * 32, r[u]);
+            else r[u][3] = r[u][4] = 0, r[u][0] = r[u][1] = 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                         : "=d"(f[u][0][0]), "=d"(f[u][0][1]), "=d"(f[u][0][2]), "=d"(f[u][0][3])
+                         : "l"(A1 + (uint64_t)(r[u][3] % 9200u) * 16 + q * 4));
+            asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                         : "=d"(f[u][1][0]), "=d"(f[u][1][1]), "=d"(f[u][1][2]), "=d"(f[u][1][3])
+                         : "l"(A2 + (uint64_t)(r[u][4] % 28800u) * 16 + q * 4));
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[v] += __uint_as_float(r[u][0]) * f[u][0][v] * f[u][1][v];
+    }
+    if (acc[0] + acc[1] + acc[2] + acc[3] == 1.2345) out[0] = acc[0];
+}
+
+__global__ void fill_rec(uint8_t *rec, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t *w = reinterpret_cast<uint32_t *>(rec + i * 32);
+        const uint64_t h = mix((uint64_t)i);
+        w[0] = 0x3f800000u;
+        w[1] = 0;
+        w[2] = (uint32_t)(i / 6400);
+        w[3] = (uint32_t)(h & 0xffffffffu);
+        w[4] = (uint32_t)(h >> 32);
+    }
+}
+
 int main() {
     const int64_t n = 77000000;  // NELL-2 nonzeros
     uint8_t *rec;
@@ -155,6 +219,23 @@ int main() {
     time_it([&] { rec_gather<4, true><<<grid, 256>>>(rec, n, out); }, "rec32 random  ld.global.cs.v8 (evict-first)", rb);
     time_it([&] { rec_gather<5, true><<<grid, 256>>>(rec, n, out); }, "rec16 random  ld.nc.v4 (half record)", rb / 2);
     time_it([&] { rec_gather<0, false><<<grid, 256>>>(rec, n, out); }, "rec32 stream  ld.nc.v8", rb);
+    fill_rec<<<sms * 8, 256>>>(rec, n);
+    CK(cudaDeviceSynchronize());
+    double *T1, *T2;
+    CK(cudaMalloc(&T1, 9200 * 128));
+    CK(cudaMalloc(&T2, 28800 * 128));
+    CK(cudaMemset(T1, 0, 9200 * 128));
+    CK(cudaMemset(T2, 0, 28800 * 128));
+    const double mb = (double)n * (32 + 256);
+    for (int64_t run : {64, 256}) {
+        const int64_t groups = (n + run - 1) / run;
+        char name[128];
+        snprintf(name, sizeof name, "mttkrp-shaped: per-group runs (run=%ld)", (long)run);
+        time_it([&] { stream_gather<false><<<(unsigned)((groups * 4 + 255) / 256), 256>>>(rec, n, T1, T2, run, (double *)out); }, name, mb);
+        const int64_t warps = (n + run * 8 - 1) / (run * 8);
+        snprintf(name, sizeof name, "mttkrp-shaped: warp-cooperative (run=%ld/group)", (long)run);
+        time_it([&] { stream_gather<true><<<(unsigned)((warps * 32 + 255) / 256), 256>>>(rec, n, T1, T2, run, (double *)out); }, name, mb);
+    }
     const int64_t ng = 154000000;  // 77M nnz x 2 gathered rows
     const double gb = (double)ng * 128;
     time_it([&] { row_gather<<<grid, 256>>>(A, 50000, ng, (double *)out); }, "row128 random from 6.4 MB (L2-resident)", gb);
