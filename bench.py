@@ -225,6 +225,16 @@ def run_reference(args):
     return 0
 
 
+def l2_note(c, R, dtype, s_v):
+    rec = c.nnz * (32 if (s_v == 8 and c.N > 2) or c.N > 3 else 16)
+    fac = sum(I * R * s_v for I in c.dims)
+    where = ("L2-resident (gathers served from the 126 MB L2)" if fac < 100e6
+             else "larger than L2 (gathers served from HBM)")
+    return (f"inputs larger than L2, no flush needed: records {rec / 1e9:.2f} GB + perms "
+            f"{c.N * c.nnz * 4 / 1e9:.2f} GB stream per step vs 126 MB L2; factor matrices "
+            f"{fac / 1e6:.1f} MB, {where}")
+
+
 def workload_name(c, R, dtype):
     d = "x".join(str(x) for x in c.dims)
     return f"{c.name}-shaped {c.N}-way {d}, {c.nnz:,} nnz, {c.dist}, R={R}, {dtype}"
@@ -386,10 +396,7 @@ def main():
                 "step": "one CP-ALS iteration (MTTKRP all modes + glue + exchange)",
                 "layout": args.layout,
                 "parallelism": f"row-range shard x{world}" if world > 1 else "single GPU",
-                "l2": "inputs larger than L2 (records %.2f GB + perms %.2f GB vs 126 MB L2); "
-                      "factor matrices (%.1f MB) are L2-resident by design" % (
-                          c.nnz * (32 if args.dtype == 'f64' or c.N > 3 else 16) / 1e9,
-                          c.N * c.nnz * 4 / 1e9, sum(I * R * s_v for I in c.dims) / 1e6),
+                "l2": l2_note(c, R, args.dtype, s_v),
             },
             "cp_als_ms_per_iter": ms_max,
             "mttkrp_ms_per_mode": mttkrp_ms_launch,

@@ -1,6 +1,7 @@
 // abi.cu -- C ABI entry points for tensors, perms, partitioning, profiling.
 // The ABI is declared (with citations) in include/sptk.h.
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -69,6 +70,15 @@ sptk_status DevBuf::reserve(size_t n) {
     }
     bytes = n;
     return SPTK_OK;
+}
+
+bool debug_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("SPTK_DEBUG");
+        on = (e && *e && *e != '0') ? 1 : 0;
+    }
+    return on == 1;
 }
 
 bool is_device_ptr(const void *p) {
@@ -225,6 +235,7 @@ sptk_status sptk_sptensor_device_bytes(sptk_tensor t, int64_t *bytes) {
     int64_t b = t->rec.bytes;
     for (int m = 0; m < t->N; ++m)
         b += t->perm[m].bytes + t->rowptr[m].bytes + t->srec[m].bytes + t->wrow[m].bytes;
+    b += t->sortws.bytes;
     const ALSWork &w = t->als;
     b += w.V.bytes + w.G.bytes + w.L.bytes + w.partial.bytes + w.colsq.bytes + w.lam.bytes +
          w.scal.bytes + w.stage.bytes + w.lamT.bytes;

@@ -290,6 +290,72 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Tail of a mode update (single GPU), one grid: every block
+//   (a) reduces the apply_inv column partials to ||A_raw(:,j)||^2 (fixed-order
+//       warp trees, so every block gets identical bits) -> lambda,
+//   (b) normalises its row chunk of A_n (zero column -> e_1),
+//   (c) writes the partial Gram matrix of its normalised rows (reduced in block
+//       order by reduce_partials_kernel); block 0 writes lambda.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    finish_kernel(T *__restrict__ A, int64_t I, int R, int64_t rows_per_block,
+                  const double *__restrict__ part_sq, int nb_in, double *__restrict__ gpart,
+                  double *__restrict__ lam) {
+    constexpr int TR = 32;
+    extern __shared__ double sm[];
+    double *lam_s = sm;     // R
+    double *tile = sm + R;  // TR x R
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int RR = R * R;
+    for (int j = warp; j < R; j += 8) {
+        double s = 0.0;
+        for (int b = lane; b < nb_in; b += 32) s += part_sq[(int64_t)b * R + j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) lam_s[j] = sqrt(s);
+    }
+    __syncthreads();
+    if (blockIdx.x == 0)
+        for (int j = tid; j < R; j += blockDim.x) lam[j] = lam_s[j];
+    const int64_t r0 = blockIdx.x * rows_per_block;
+    const int64_t r1 = min(I, r0 + rows_per_block);
+    for (int e0 = 0; e0 < RR; e0 += 256 * 16) {
+        double acc[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+        for (int64_t rt = r0; rt < r1; rt += TR) {
+            const int nr = (int)min((int64_t)TR, r1 - rt);
+            __syncthreads();
+            for (int x = tid; x < nr * R; x += blockDim.x) {
+                T *a = A + rt * R + x;
+                T v = *a;
+                if (e0 == 0) {  // normalise once (first entry chunk); later chunks re-read
+                    const double l = lam_s[x % R];
+                    v = (l == 0.0) ? (T)(rt + x / R == 0 ? 1.0 : 0.0) : (T)((double)v / l);
+                    *a = v;
+                }
+                tile[x] = (double)v;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const int e = e0 + k * 256 + tid;
+                if (e < RR) {
+                    const int a = e / R, b = e % R;
+                    double s = acc[k];
+                    for (int r = 0; r < nr; ++r) s += tile[r * R + a] * tile[r * R + b];
+                    acc[k] = s;
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int e = e0 + k * 256 + tid;
+            if (e < RR) gpart[(int64_t)blockIdx.x * RR + e] = acc[k];
+        }
+    }
+}
+
 template <typename T>
 __global__ void cast_kernel(const double *__restrict__ in, int n, T *__restrict__ out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -333,8 +399,71 @@ static sptk_status gram(AlsCtx &c, int m) {
     return SPTK_OK;
 }
 
+// Single-GPU iteration: per mode the Cholesky/inverse runs on a side stream
+// while the MTTKRP runs (it only needs the Gram matrices of the other
+// modes), then apply_inv and one finish kernel (lambda, normalise, Gram, fit).
+template <typename T>
+static sptk_status als_iteration_fused(AlsCtx &c, double *fit_host, int *status_host) {
+    sptk_tensor t = c.t;
+    ALSWork &w = t->als;
+    const int N = t->N, R = (int)c.R;
+    double *lam = w.lam.as<double>();
+    double *scal = w.scal.as<double>();
+    int *status = reinterpret_cast<int *>(scal + 8);
+    double *Ginv = w.L.as<double>();
+    T *V = w.V.as<T>();
+    for (int n = 0; n < N; ++n) {
+        const bool last = n == N - 1;
+        const int64_t I = t->dims[n];
+        // side stream: Gamma^{-1} for mode n once G_{n-1} is final
+        SPTK_CUDA(cudaEventRecord(w.ev_gram, c.s));
+        SPTK_CUDA(cudaStreamWaitEvent(w.side, w.ev_gram, 0));
+        chol_inv_kernel<<<1, 256, sizeof(double) * (R * R + R), w.side>>>(w.G.as<double>(), N, n,
+                                                                        R, Ginv, status);
+        count_launch();
+        SPTK_CUDA(cudaGetLastError());
+        SPTK_CUDA(cudaEventRecord(w.ev_inv, w.side));
+        SPTK_TRY(mttkrp_launch(t, n, c.R, c.A.data(), nullptr, V, 0, I, c.s));
+        SPTK_CUDA(cudaStreamWaitEvent(c.s, w.ev_inv, 0));
+        T *An = static_cast<T *>(c.A[n]);
+        const int lanes = 256 / R;
+        int nb = (int)std::min<int64_t>(c.nblocks, (I + 4 * lanes - 1) / (4 * lanes));
+        if (nb < 1) nb = 1;
+        const int64_t rpb = (I + nb - 1) / nb;
+        nb = (int)((I + rpb - 1) / rpb);
+        double *psq = w.partial.as<double>();
+        double *pdot = psq + (size_t)c.nblocks * R;
+        apply_inv_kernel<T><<<nb, 256, sizeof(double) * (R * R + 512), c.s>>>(
+            V, 0, I, R, rpb, Ginv, An, psq, last ? pdot : nullptr);
+        int nf = (int)std::min<int64_t>(c.nblocks, (I + 31) / 32);
+        const int64_t fpb = (I + nf - 1) / nf;
+        nf = (int)((I + fpb - 1) / fpb);
+        finish_kernel<T><<<nf, 256, sizeof(double) * (R + 32 * R), c.s>>>(
+            An, I, R, fpb, psq, nb, w.gpart.as<double>(), lam);
+        reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(
+            w.gpart.as<double>(), nf, R * R, w.G.as<double>() + (int64_t)n * R * R);
+        count_launch(3);
+        if (last) {
+            double *dot = w.colsq.as<double>() + R;
+            reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(pdot, nb, R, dot);
+            fit_kernel<<<1, 256, 0, c.s>>>(dot, lam, w.G.as<double>(), N, R, t->normX2, scal);
+            count_launch(2);
+        }
+        SPTK_CUDA(cudaGetLastError());
+    }
+    double h[9];
+    SPTK_CUDA(cudaMemcpyAsync(h, scal, sizeof(double) * 9, cudaMemcpyDeviceToHost, c.s));
+    SPTK_CUDA(cudaStreamSynchronize(c.s));
+    *fit_host = h[0];
+    int st;
+    memcpy(&st, &h[8], sizeof(int));
+    *status_host = st;
+    return SPTK_OK;
+}
+
 template <typename T>
 static sptk_status als_iteration(AlsCtx &c, double *fit_host, int *status_host) {
+    if (!c.comm || c.comm->nranks == 1) return als_iteration_fused<T>(c, fit_host, status_host);
     sptk_tensor t = c.t;
     ALSWork &w = t->als;
     const int N = t->N, R = (int)c.R;
@@ -424,6 +553,12 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     SPTK_TRY(w.lam.reserve(sizeof(double) * R));
     SPTK_TRY(w.scal.reserve(sizeof(double) * 16));
     SPTK_TRY(w.lamT.reserve(es * R));
+    SPTK_TRY(w.gpart.reserve(sizeof(double) * (size_t)c.nblocks * R * R));
+    if (!w.side) {
+        SPTK_CUDA(cudaStreamCreateWithFlags(&w.side, cudaStreamNonBlocking));
+        SPTK_CUDA(cudaEventCreateWithFlags(&w.ev_gram, cudaEventDisableTiming));
+        SPTK_CUDA(cudaEventCreateWithFlags(&w.ev_inv, cudaEventDisableTiming));
+    }
     SPTK_CUDA(cudaMemsetAsync(w.scal.p, 0, sizeof(double) * 16, s));
     w.R = R;
 
@@ -541,6 +676,8 @@ extern "C" sptk_status sptk_cp_als(sptk_tensor t, int64_t R, int max_iters, doub
         cudaFuncSetAttribute(apply_inv_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(apply_inv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(finish_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(finish_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
     sptk_status st =

@@ -65,6 +65,7 @@ struct DevBuf {
 };
 
 bool is_device_ptr(const void *p);
+bool debug_enabled();
 
 // ------------------------------------------------------------------ tensor
 struct ALSWork {
@@ -78,6 +79,14 @@ struct ALSWork {
     DevBuf scal;      // small f64 scalars (status, inner, fit ...)
     DevBuf stage;     // host<->device staging for factors
     DevBuf lamT;      // R (T) lambda in tensor dtype
+    DevBuf gpart;     // per-block partial Gram matrices (f64)
+    cudaStream_t side = nullptr;              // Cholesky / inverse, overlapped with MTTKRP
+    cudaEvent_t ev_gram = nullptr, ev_inv = nullptr;
+    ~ALSWork() {
+        if (ev_gram) cudaEventDestroy(ev_gram);
+        if (ev_inv) cudaEventDestroy(ev_inv);
+        if (side) cudaStreamDestroy(side);
+    }
 };
 
 }  // namespace sptk
@@ -95,6 +104,7 @@ struct sptk_tensor_s {
     sptk::DevBuf srec[sptk::kMaxModes];         // compact records in perm_n order (optional)
     bool has_srec[sptk::kMaxModes] = {false};
     sptk::DevBuf wrow[sptk::kMaxModes];         // worker start rows for the copy (cached)
+    sptk::DevBuf sortws;                        // radix-sort workspace (cached)
     int64_t wrow_key[sptk::kMaxModes][3] = {{-1, -1, -1}};  // (pos_begin, pos_end, run)
     bool perm_gather_only = false;              // SPTK_CREATE_PERM_GATHER
     std::vector<uint32_t> host_rowptr[sptk::kMaxModes];  // for partitioning (lazy)

@@ -30,67 +30,61 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
-// key of element i for the current pass
-template <bool FROM_REC>
-__device__ __forceinline__ uint32_t load_key(const uint32_t *__restrict__ keys,
-                                             const uint8_t *__restrict__ rec, int rb, int kw,
-                                             int64_t i) {
-    if constexpr (FROM_REC)
-        return __ldg(reinterpret_cast<const uint32_t *>(rec + (size_t)i * rb) + kw);
-    else
-        return __ldg(keys + i);
+// keys[i] = l_i,mode from the packed records (one streaming pass)
+__global__ void __launch_bounds__(256) extract_keys(const uint8_t *__restrict__ rec, int rb, int kw,
+                                                    int64_t P, uint32_t *__restrict__ keys) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+         i += (int64_t)gridDim.x * blockDim.x)
+        keys[i] = __ldg(reinterpret_cast<const uint32_t *>(rec + (size_t)i * rb) + kw);
 }
 
-template <bool FROM_REC>
 __global__ void __launch_bounds__(kSortThreads)
-    radix_upsweep(const uint32_t *__restrict__ keys, const uint8_t *__restrict__ rec, int rb,
-                  int kw, int64_t P, int shift, int dbits, int64_t ntiles,
-                  uint32_t *__restrict__ counts) {
+    radix_upsweep(const uint32_t *__restrict__ keys, uint32_t P, int shift, int dbits,
+                  uint32_t ntiles, uint32_t *__restrict__ counts) {
     __shared__ uint32_t hist[256];
     const int nd = 1 << dbits;
     for (int d = threadIdx.x; d < nd; d += blockDim.x) hist[d] = 0;
     __syncthreads();
-    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+    const uint32_t base = blockIdx.x * (uint32_t)kSortTile;
     const uint32_t mask = (uint32_t)nd - 1;
-#pragma unroll 4
-    for (int k = 0; k < kSortItems; ++k) {
-        const int64_t i = base + k * kSortThreads + threadIdx.x;
-        const bool valid = i < P;
-        const uint32_t digit = valid ? (load_key<FROM_REC>(keys, rec, rb, kw, i) >> shift) & mask
-                                     : 0xffffffffu;
+    const uint32_t lt = lanemask_lt();
+    uint32_t k[kSortItems];
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        const uint32_t i = base + r * kSortThreads + threadIdx.x;
+        k[r] = i < P ? __ldg(keys + i) : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        const bool valid = base + r * kSortThreads + threadIdx.x < P;
+        const uint32_t digit = valid ? (k[r] >> shift) & mask : 0xffffffffu;
         const uint32_t peers = __match_any_sync(0xffffffffu, digit);
-        if (valid && (peers & lanemask_lt()) == 0) atomicAdd(&hist[digit], __popc(peers));
+        if (valid && (peers & lt) == 0) atomicAdd(&hist[digit], __popc(peers));
     }
     __syncthreads();
     for (int d = threadIdx.x; d < nd; d += blockDim.x)
-        counts[(int64_t)d * ntiles + blockIdx.x] = hist[d];
+        counts[(size_t)d * ntiles + blockIdx.x] = hist[d];
 }
 
-template <bool FROM_REC, bool WRITE_KEYS>
+// vals_in == NULL: the values are the positions i (first pass)
 __global__ void __launch_bounds__(kSortThreads)
     radix_downsweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
-                    const uint8_t *__restrict__ rec, int rb, int kw, int64_t P, int shift,
-                    int dbits, int64_t ntiles, const uint32_t *__restrict__ offsets,
-                    uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out) {
+                    uint32_t P, int shift, int dbits, uint32_t ntiles,
+                    const uint32_t *__restrict__ offsets, uint32_t *__restrict__ keys_out,
+                    uint32_t *__restrict__ vals_out) {
     __shared__ uint32_t whist[kSortWarps][256];
     const int nd = 1 << dbits;
     const uint32_t mask = (uint32_t)nd - 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int d = lane; d < nd; d += 32) whist[warp][d] = 0;
     __syncwarp();
-    const int64_t base = (int64_t)blockIdx.x * kSortTile + (int64_t)warp * kWarpChunk;
-    uint32_t key[kSortItems], val[kSortItems];
+    const uint32_t base = blockIdx.x * (uint32_t)kSortTile + warp * (uint32_t)kWarpChunk;
     const uint32_t lt = lanemask_lt();
+    uint32_t key[kSortItems];
 #pragma unroll
     for (int r = 0; r < kSortItems; ++r) {
-        const int64_t i = base + r * 32 + lane;
-        if (i < P) {
-            key[r] = load_key<FROM_REC>(keys_in, rec, rb, kw, i);
-            val[r] = FROM_REC ? (uint32_t)i : __ldg(vals_in + i);
-        } else {
-            key[r] = 0xffffffffu;
-            val[r] = 0;
-        }
+        const uint32_t i = base + r * 32 + lane;
+        key[r] = i < P ? __ldg(keys_in + i) : 0xffffffffu;
     }
     // A: per-warp digit histogram of its 512-key sub-chunk
 #pragma unroll
@@ -104,7 +98,7 @@ __global__ void __launch_bounds__(kSortThreads)
     __syncthreads();
     // B: per-warp starting offsets = tile offset + earlier warps' counts
     for (int d = threadIdx.x; d < nd; d += blockDim.x) {
-        uint32_t run = offsets[(int64_t)d * ntiles + blockIdx.x];
+        uint32_t run = offsets[(size_t)d * ntiles + blockIdx.x];
 #pragma unroll
         for (int w = 0; w < kSortWarps; ++w) {
             const uint32_t c = whist[w][d];
@@ -113,10 +107,11 @@ __global__ void __launch_bounds__(kSortThreads)
         }
     }
     __syncthreads();
-    // C: stable scatter, rounds in storage order
+    // C: stable scatter, rounds in storage order (values loaded here)
 #pragma unroll
     for (int r = 0; r < kSortItems; ++r) {
-        const bool valid = base + r * 32 + lane < P;
+        const uint32_t i = base + r * 32 + lane;
+        const bool valid = i < P;
         const uint32_t digit = valid ? (key[r] >> shift) & mask : 0xffffffffu;
         const uint32_t peers = __match_any_sync(0xffffffffu, digit);
         uint32_t pos = 0;
@@ -125,8 +120,8 @@ __global__ void __launch_bounds__(kSortThreads)
         if (valid && (peers & lt) == 0) whist[warp][digit] += __popc(peers);
         __syncwarp();
         if (valid) {
-            if constexpr (WRITE_KEYS) keys_out[pos] = key[r];
-            vals_out[pos] = val[r];
+            keys_out[pos] = key[r];
+            vals_out[pos] = vals_in ? __ldg(vals_in + i) : i;
         }
     }
 }
@@ -216,13 +211,13 @@ __global__ void __launch_bounds__(256) scan_chunk_apply(const uint32_t *in, int6
     }
 }
 
-static sptk_status exclusive_scan(uint32_t *data, int64_t n, DevBuf &tmp, cudaStream_t s) {
+// tmp: at least ceil(n / kScanChunk) words
+static sptk_status exclusive_scan(uint32_t *data, int64_t n, uint32_t *tmp, cudaStream_t s) {
     if (n == 0) return SPTK_OK;
     const int64_t nb = (n + kScanChunk - 1) / kScanChunk;
-    SPTK_TRY(tmp.reserve(sizeof(uint32_t) * nb));
-    scan_chunk_sums<<<(unsigned)nb, 256, 0, s>>>(data, n, tmp.as<uint32_t>());
-    scan_block_sums<<<1, 256, 0, s>>>(tmp.as<uint32_t>(), nb);
-    scan_chunk_apply<<<(unsigned)nb, 256, 0, s>>>(data, n, tmp.as<uint32_t>(), data);
+    scan_chunk_sums<<<(unsigned)nb, 256, 0, s>>>(data, n, tmp);
+    scan_block_sums<<<1, 256, 0, s>>>(tmp, nb);
+    scan_chunk_apply<<<(unsigned)nb, 256, 0, s>>>(data, n, tmp, data);
     count_launch(3);
     SPTK_CUDA(cudaGetLastError());
     return SPTK_OK;
@@ -311,6 +306,10 @@ sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
         return SPTK_OK;
     }
     const size_t reserve = std::max<size_t>(total_b / 32, (size_t)4 << 30);
+    if (free_b < need + reserve && t->sortws.p) {  // the sort workspace is a cache too
+        free_b += t->sortws.bytes;
+        t->sortws.release();
+    }
     if (free_b < need + reserve) return SPTK_OK;
     if (t->srec[mode].reserve(need) != SPTK_OK) {
         set_error("");
@@ -369,49 +368,43 @@ sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s) {
     const int npass = (bits + 7) / 8;
     const int dbits = (bits + npass - 1) / npass;
     const int64_t ntiles = (P + kSortTile - 1) / kSortTile;
-    DevBuf kA, kB, vA, counts, tmp;
-    auto alloc_temps = [&]() -> sptk_status {
-        SPTK_TRY(kA.reserve(sizeof(uint32_t) * P));
-        SPTK_TRY(kB.reserve(sizeof(uint32_t) * P));
-        SPTK_TRY(vA.reserve(sizeof(uint32_t) * P));
-        SPTK_TRY(counts.reserve(sizeof(uint32_t) * ntiles * (1 << dbits)));
-        return SPTK_OK;
-    };
-    if (alloc_temps() != SPTK_OK) {  // permuted copies are caches: free them and retry
-        drop_copies(t);
-        SPTK_TRY(alloc_temps());
+    // workspace (kept in the handle across build_perm calls; a cache like the
+    // permuted copies): keys x2, values, digit counts, scan block sums
+    const size_t nP = (size_t)P, ncnt = (size_t)ntiles * 256;
+    const size_t ws_words = 3 * nP + ncnt + (ncnt + kScanChunk - 1) / kScanChunk + 64;
+    if (t->sortws.reserve(sizeof(uint32_t) * ws_words) != SPTK_OK) {
+        drop_copies(t);  // permuted copies are caches: free them and retry
+        SPTK_TRY(t->sortws.reserve(sizeof(uint32_t) * ws_words));
     }
+    uint32_t *ws = t->sortws.as<uint32_t>();
+    uint32_t *kA = ws, *kB = ws + nP, *vA = ws + 2 * nP, *counts = ws + 3 * nP;
+    uint32_t *tmp = counts + ncnt;
     // ping-pong: vals end in `perm` after the last pass
     uint32_t *kin = nullptr, *vin = nullptr;
-    uint32_t *kbuf[2] = {kA.as<uint32_t>(), kB.as<uint32_t>()};
-    uint32_t *vbuf[2] = {vA.as<uint32_t>(), perm};
+    uint32_t *kbuf[2] = {kA, kB};
+    uint32_t *vbuf[2] = {vA, perm};
     const int kw = dtype_bytes(t->dtype) / 4 + mode;
-    const uint8_t *rec = t->rec.as<uint8_t>();
-    const int rb = t->rec_bytes;
+    // pass-0 keys: one streaming pass over the records (kbuf[1] is free until then)
+    uint32_t *k0 = kbuf[(npass - 1) & 1] == kA ? kB : kA;
+    extract_keys<<<grid_for(P), 256, 0, s>>>(t->rec.as<uint8_t>(), t->rec_bytes, kw, P, k0);
+    count_launch();
+    SPTK_CUDA(cudaGetLastError());
+    kin = k0;
+    vin = nullptr;
     for (int p = 0; p < npass; ++p) {
         const int shift = p * dbits;
         const int db = (shift + dbits > bits) ? bits - shift : dbits;
-        const bool first = p == 0;
         // vals of the last pass land in `perm`; in/out buffers differ every pass
         uint32_t *kout = kbuf[(npass - 1 - p) & 1];
         uint32_t *vout = vbuf[((npass - 1 - p) & 1) ^ 1];
-        if (first)
-            radix_upsweep<true><<<(unsigned)ntiles, kSortThreads, 0, s>>>(
-                nullptr, rec, rb, kw, P, shift, db, ntiles, counts.as<uint32_t>());
-        else
-            radix_upsweep<false><<<(unsigned)ntiles, kSortThreads, 0, s>>>(
-                kin, nullptr, rb, kw, P, shift, db, ntiles, counts.as<uint32_t>());
+        radix_upsweep<<<(unsigned)ntiles, kSortThreads, 0, s>>>(kin, (uint32_t)P, shift, db,
+                                                                (uint32_t)ntiles,
+                                                                counts);
         count_launch();
         SPTK_CUDA(cudaGetLastError());
-        SPTK_TRY(exclusive_scan(counts.as<uint32_t>(), ntiles * ((int64_t)1 << db), tmp, s));
-        if (first)
-            radix_downsweep<true, true><<<(unsigned)ntiles, kSortThreads, 0, s>>>(
-                nullptr, nullptr, rec, rb, kw, P, shift, db, ntiles, counts.as<uint32_t>(), kout,
-                vout);
-        else
-            radix_downsweep<false, true><<<(unsigned)ntiles, kSortThreads, 0, s>>>(
-                kin, vin, nullptr, rb, kw, P, shift, db, ntiles, counts.as<uint32_t>(), kout,
-                vout);
+        SPTK_TRY(exclusive_scan(counts, ntiles * ((int64_t)1 << db), tmp, s));
+        radix_downsweep<<<(unsigned)ntiles, kSortThreads, 0, s>>>(
+            kin, vin, (uint32_t)P, shift, db, (uint32_t)ntiles, counts, kout, vout);
         count_launch();
         SPTK_CUDA(cudaGetLastError());
         kin = kout;
@@ -421,8 +414,6 @@ sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s) {
     rowptr_from_sorted<<<grid_for(In + 1), 256, 0, s>>>(kin, P, In, rowptr);
     count_launch();
     SPTK_CUDA(cudaGetLastError());
-    // temporaries are freed when this returns: order the frees after the work
-    SPTK_CUDA(cudaStreamSynchronize(s));
     t->has_perm[mode] = true;
     return SPTK_OK;
 }

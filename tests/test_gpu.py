@@ -258,11 +258,14 @@ def test_cp_als_planted_recovery_and_f32(sp):
     res = sp.cp_als(t, 5, 60, A, seed=23)
     assert res["fit"] > 0.999
     ref = oracle.cp_als(dims, idx, vals, factors_np(23, dims, 5), 60)
-    assert abs(res["fit"] - ref["fit"]) <= 1e-9
+    # near a perfect fit, fit = 1 - sqrt(res2)/||X|| with res2 a difference of
+    # O(||X||^2) terms: |d fit| <= sqrt(c u) ~ 3e-8
+    assert abs(res["fit"] - ref["fit"]) <= 1e-7
     t32 = make(sp, dims, idx, vals.astype(np.float32), torch.float32)
     A32 = [torch.empty(I, 5, dtype=torch.float32, device="cuda") for I in dims]
     res32 = sp.cp_als(t32, 5, 60, A32, seed=23)
-    assert abs(res32["fit"] - ref["fit"]) <= 1e-4
+    # same cancellation in fp32: |d fit| <= sqrt(c u32) ~ 5e-4
+    assert res32["fit"] > 0.999 and abs(res32["fit"] - ref["fit"]) <= 1e-3
 
 
 def test_cp_als_tol_and_errors(sp):
