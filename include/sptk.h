@@ -208,8 +208,11 @@ sptk_status sptk_profile_read(double *mttkrp_ms, int64_t *mttkrp_launches,
                               int64_t *kernel_launches);
 
 /* Tuning knobs of the MTTKRP launch (process-wide; for sweeps): `variant`
- * selects a compiled launch shape of the fast kernel (0 = default, 0..4;
- * -1 = keep), `run` the nonzeros per worker (the paper's NZPTM, P:220;
+ * selects the fast kernel's worker shape on the permuted copy (0 = per-group
+ * runs, 1 = warp-cooperative steps; -1 = keep; -2 = automatic, the default:
+ * warp-cooperative when rows average >= 64 nonzeros and a warp holds >= 4
+ * groups), `run` the nonzeros per
+ * worker group (the paper's NZPTM, P:220;
  * rounded up to a multiple of 4; 0 = keep; -2 = adaptive, the default:
  * clamp(positions / (4 waves of workers), 16, 256)).  Initial values come
  * from SPTK_VARIANT / SPTK_RUN. */

@@ -282,6 +282,7 @@ def partition_rows(rowptr, nranks: int) -> np.ndarray:
 
 
 def set_tuning(variant: int = -1, run: int = 0):
+    """variant: 0 per-group, 1 warp-cooperative, -1 keep, -2 automatic; run: 0 keep, -2 adaptive."""
     _check(lib().sptk_set_tuning(variant, run), "set_tuning")
 
 

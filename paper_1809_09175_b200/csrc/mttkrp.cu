@@ -7,7 +7,7 @@
 namespace sptk {
 
 static int64_t g_run = -1;  // -1: unset, 0: adaptive, > 0: fixed
-static int g_variant = -1;
+static int g_variant = -2;
 
 // Nonzeros per worker (the paper's NZPTM block).  Adaptive by default:
 // long runs amortise the two boundary atomics, but the grid must still cover
@@ -27,22 +27,23 @@ static int64_t run_length(int64_t npos, int G) {
     return (run + 3) / 4 * 4;
 }
 
-static int variant() {
-    if (g_variant < 0) {
+// -2: not read yet; -1: automatic (warp-cooperative for long rows); 0/1: forced
+static int variant_setting() {
+    if (g_variant == -2) {
         const char *e = getenv("SPTK_VARIANT");
-        g_variant = e ? atoi(e) : 0;
-        if (g_variant < 0 || g_variant >= kNumVariants) g_variant = 0;
+        g_variant = e ? atoi(e) : -1;
+        if (g_variant < -1 || g_variant >= kNumVariants) g_variant = -1;
     }
     return g_variant;
 }
 
 template <typename T>
-static sptk_status launch_fast(int N, int G, int rb, const MttkrpArgs &a, int64_t workers,
+static sptk_status launch_fast(int N, int G, int variant, const MttkrpArgs &a, int64_t workers,
                                cudaStream_t s) {
     switch (N) {
-    case 3: return launch_fast_tn<T, 3>(G, rb, variant(), a, workers, s);
-    case 4: return launch_fast_tn<T, 4>(G, rb, variant(), a, workers, s);
-    case 5: return launch_fast_tn<T, 5>(G, rb, variant(), a, workers, s);
+    case 3: return launch_fast_tn<T, 3>(G, variant, a, workers, s);
+    case 4: return launch_fast_tn<T, 4>(G, variant, a, workers, s);
+    case 5: return launch_fast_tn<T, 5>(G, variant, a, workers, s);
     default: return fail(SPTK_EINVAL, "fast MTTKRP: N must be 3..5");
     }
 }
@@ -136,9 +137,19 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
         if (m != mode && !aligned32(factors[m])) fast = false;
     const int G0 = fast ? pow2ceil((int)((R < 32 * V ? R : 32 * V) / V)) : (R <= 16 ? 4 : 32);
     a.run = run_length(pe - pb, G0);
-    const int64_t workers = (pe - pb + a.run - 1) / a.run;
+    // warp-cooperative steps pay off when rows are long (few boundary steps)
+    const int64_t rows = row_end - row_begin;
+    int var = 0;
+    if (fast && t->has_srec[mode] && G0 < 32) {
+        var = variant_setting();
+        // measured (profiles/r01/sweep_*.log): a win for >= 4 groups per warp on
+        // rows averaging >= 64 nonzeros, a loss on short rows and for 2 groups
+        if (var < 0) var = ((pe - pb) >= 64 * rows && G0 <= 8) ? 1 : 0;
+    }
+    const int64_t chunk = var == 1 ? a.run * (32 / G0) : a.run;
+    const int64_t workers = (pe - pb + chunk - 1) / chunk;
     if (fast && t->has_srec[mode]) {  // stream the compact permuted copy instead
-        SPTK_TRY(worker_rows(t, mode, pb, pe, a.run, workers, s));
+        SPTK_TRY(worker_rows(t, mode, pb, pe, chunk, workers, s));
         a.rec = t->srec[mode].as<uint8_t>();
         a.perm = nullptr;
         a.rowptr = t->rowptr[mode].as<uint32_t>();
@@ -153,8 +164,8 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
             a.col0 = (int)c0;
             a.ncols = (int)((R - c0) < tile ? (R - c0) : tile);
             const int G = pow2ceil(a.ncols / V);
-            if (t->dtype == SPTK_F64) SPTK_TRY(launch_fast<double>(t->N, G, t->rec_bytes, a, workers, s));
-            else SPTK_TRY(launch_fast<float>(t->N, G, t->rec_bytes, a, workers, s));
+            if (t->dtype == SPTK_F64) SPTK_TRY(launch_fast<double>(t->N, G, var, a, workers, s));
+            else SPTK_TRY(launch_fast<float>(t->N, G, var, a, workers, s));
         }
     } else {
         const int G = R <= 16 ? 4 : 32;
@@ -175,9 +186,10 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
 using namespace sptk;
 
 extern "C" sptk_status sptk_set_tuning(int variant, int64_t run) {
-    if (variant >= kNumVariants || variant < -1 || run < -2)
-        return fail(SPTK_EINVAL, "set_tuning: variant in [-1, 4], run >= -2");
+    if (variant >= kNumVariants || variant < -2 || run < -2)
+        return fail(SPTK_EINVAL, "set_tuning: variant in [-2, 1], run >= -2");
     if (variant >= 0) g_variant = variant;
+    if (variant == -2) g_variant = -1;  // back to automatic
     if (run > 0) g_run = run < 4 ? 4 : (run + 3) / 4 * 4;
     if (run == -2) g_run = 0;  // back to adaptive
     return SPTK_OK;

@@ -263,6 +263,169 @@ __global__ void __launch_bounds__(256, MINB) mttkrp_fast_kernel(const MttkrpArgs
     if constexpr (N >= 5) if (a.mode == 4) { mttkrp_fast_body<T, N, 4, G, U, RB, SORTED>(a); return; }
 }
 
+// ------------------------------------------------- warp-cooperative body
+// Permuted copy only, for modes with long rows.  A worker is a whole warp
+// owning `run * NG` consecutive positions (NG = 32 / G lane groups); each
+// step the NG groups take NG consecutive positions (u = 0..U-1), so one
+// warp-wide load covers NG consecutive compact records (NG*RB contiguous
+// bytes) instead of NG scattered ones.  While every position of a step lies
+// in the current row (warp-uniform test against rowptr_n) each group just
+// accumulates its own products.  A step that crosses a row boundary (or the
+// chunk's tail) is resolved serially: the group accumulators are summed with
+// shuffles, then the step's products are taken in position order (broadcast
+// from the owning group) and every completed row is flushed -- atomically if
+// it is the chunk's first row, otherwise with a plain store; the last row of
+// the chunk is flushed atomically at the end (P:521-523 with worker = warp).
+template <typename T, int N, int MODE, int G, int U, int RB>
+__device__ __forceinline__ void mttkrp_coop_body(const MttkrpArgs &a) {
+    constexpr int V = 32 / sizeof(T);
+    constexpr int OFF = sizeof(T) / 4;
+    constexpr int NG = 32 / G;
+    const int64_t warp_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int g = lane / G, q = lane % G;
+    const int64_t chunk = a.run * NG;
+    if (a.pos_begin + warp_id * chunk >= a.pos_end) return;
+    const uint32_t s = (uint32_t)(a.pos_begin + warp_id * chunk);
+    const uint32_t e = (uint32_t)min(a.pos_begin + warp_id * chunk + chunk, a.pos_end);
+    const bool lane_on = q * V < a.ncols;
+    const int c = a.col0 + q * V;
+    const uint8_t *__restrict__ rec = a.rec;
+    T *__restrict__ out = static_cast<T *>(a.out);
+
+    auto flush = [&](uint32_t row, const T (&val)[V], bool atomic) {
+        if (g != 0 || !lane_on) return;
+        T o[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) o[v] = val[v];
+        if (a.lambda) {
+            T lam[V];
+            ld_row(static_cast<const T *>(a.lambda) + c, lam);
+#pragma unroll
+            for (int v = 0; v < V; ++v) o[v] *= lam[v];
+        }
+        T *dst = out + (int64_t)row * a.ld + c;
+        if (atomic) red_row(dst, o);
+        else st_row(dst, o);
+    };
+    auto load_rec = [&](uint32_t pos, uint32_t (&r)[8]) {
+        if constexpr (RB == 32) ld_rec32(rec + (size_t)pos * 32, r);
+        else ld_rec16(rec + (size_t)pos * 16, r);
+    };
+
+    uint32_t row = __ldg(a.wrow + warp_id);
+    uint32_t nxt = __ldg(a.rowptr + row + 1);
+    const uint32_t first = row;
+    T acc[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = T(0);
+
+    uint32_t wn[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const uint32_t pos = s + u * NG + g;
+        if (pos < e) load_rec(pos, wn[u]);
+    }
+    for (uint32_t base = s; base < e; base += U * NG) {
+        uint32_t w[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) w[u][k] = wn[u][k];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t pos = base + U * NG + u * NG + g;
+            if (pos < e) load_rec(pos, wn[u]);
+        }
+        T t[U][V];
+        {
+            T f[U][N][V];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int m = 0; m < N; ++m)
+                    if (m != MODE) {
+                        const int word = OFF + (m < MODE ? m : m - 1);
+                        if (base + u * NG + g < e && lane_on)
+                            ld_row(static_cast<const T *>(a.A[m]) + (int64_t)w[u][word] * a.ld + c,
+                                   f[u][m]);
+                        else
+#pragma unroll
+                            for (int v = 0; v < V; ++v) f[u][m][v] = T(0);
+                    }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const T x = (base + u * NG + g < e) ? rec_val<T>(w[u]) : T(0);
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    T p = x;
+#pragma unroll
+                    for (int m = 0; m < N; ++m)
+                        if (m != MODE) p *= f[u][m][v];
+                    t[u][v] = p;
+                }
+            }
+        }
+        const uint32_t last = base + U * NG - 1;
+        if (last < nxt && last < e) {  // whole step inside the current row
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[v] += t[u][v];
+            continue;
+        }
+        // serial resolution of the step: tot = sum of the group accumulators
+        T tot[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            T x = acc[v];
+#pragma unroll
+            for (int o = G; o < 32; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            tot[v] = x;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            for (int gg = 0; gg < NG; ++gg) {
+                const uint32_t pos = base + u * NG + gg;
+                if (pos >= e) break;
+                if (pos >= nxt) {
+                    flush(row, tot, row == first);
+#pragma unroll
+                    for (int v = 0; v < V; ++v) tot[v] = T(0);
+                    do {
+                        ++row;
+                        nxt = __ldg(a.rowptr + row + 1);
+                    } while (pos >= nxt);
+                }
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                    tot[v] += __shfl_sync(0xffffffffu, t[u][v], gg * G + q);
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[v] = (g == 0) ? tot[v] : T(0);
+    }
+    // the chunk's last row (possibly also its first): atomic
+    T tot[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        T x = acc[v];
+#pragma unroll
+        for (int o = G; o < 32; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        tot[v] = x;
+    }
+    flush(row, tot, true);
+}
+
+template <typename T, int N, int G, int U, int RB, int MINB>
+__global__ void __launch_bounds__(256, MINB) mttkrp_coop_kernel(const MttkrpArgs a) {
+    if constexpr (N >= 1) if (a.mode == 0) { mttkrp_coop_body<T, N, 0, G, U, RB>(a); return; }
+    if constexpr (N >= 2) if (a.mode == 1) { mttkrp_coop_body<T, N, 1, G, U, RB>(a); return; }
+    if constexpr (N >= 3) if (a.mode == 2) { mttkrp_coop_body<T, N, 2, G, U, RB>(a); return; }
+    if constexpr (N >= 4) if (a.mode == 3) { mttkrp_coop_body<T, N, 3, G, U, RB>(a); return; }
+    if constexpr (N >= 5) if (a.mode == 4) { mttkrp_coop_body<T, N, 4, G, U, RB>(a); return; }
+}
+
 // ---------------------------------------------------- generic kernel
 // Any N <= 6, any mode, any column tile: lane q of a G-lane worker owns
 // columns col0 + q + G*k (k < NV), scalar loads, runtime record offsets.
@@ -340,56 +503,52 @@ __global__ void __launch_bounds__(256) mttkrp_generic_kernel(const MttkrpArgs a)
     if (cur != kNoRow) flush(cur, true);
 }
 
-// Launch-shape variants of the fast kernel: (U positions per step, min
-// resident 256-thread blocks per SM -> register cap).  Variant 0 is the
-// default; SPTK_VARIANT selects another one (tuning sweeps).
-constexpr int kNumVariants = 5;
-template <int V> struct Variant;
-template <> struct Variant<0> { static constexpr int U = 2, MINB = 3; };
-template <> struct Variant<1> { static constexpr int U = 2, MINB = 4; };
-template <> struct Variant<2> { static constexpr int U = 4, MINB = 2; };
-template <> struct Variant<3> { static constexpr int U = 4, MINB = 3; };
-template <> struct Variant<4> { static constexpr int U = 1, MINB = 5; };
+// Launch shapes: U positions per step per group, >= 3 resident 256-thread
+// blocks per SM (register cap 85).  Variant 0: per-group runs
+// (mttkrp_fast_kernel); variant 1: warp-cooperative steps
+// (mttkrp_coop_kernel, permuted copy only).
+constexpr int kNumVariants = 2;
+constexpr int kU = 2, kMinBlocks = 3;
 
-template <typename T, int N, int RB, bool SORTED, int VAR>
+template <typename T, int N, int RB, bool SORTED, bool COOP>
 inline sptk_status fast_launch_g(int G, const MttkrpArgs &a, int64_t workers, cudaStream_t s) {
-    constexpr int U = Variant<VAR>::U, MB = Variant<VAR>::MINB;
-    const int64_t threads = workers * G;
+    const int64_t threads = COOP ? workers * 32 : workers * G;
     const unsigned blocks = (unsigned)((threads + 255) / 256);
+#define SPTK_LAUNCH_G(GG)                                                                     \
+    if constexpr (COOP)                                                                       \
+        mttkrp_coop_kernel<T, N, GG, kU, RB, kMinBlocks><<<blocks, 256, 0, s>>>(a);           \
+    else                                                                                      \
+        mttkrp_fast_kernel<T, N, GG, kU, RB, SORTED, kMinBlocks><<<blocks, 256, 0, s>>>(a);
     switch (G) {
-    case 1: mttkrp_fast_kernel<T, N, 1, U, RB, SORTED, MB><<<blocks, 256, 0, s>>>(a); break;
-    case 2: mttkrp_fast_kernel<T, N, 2, U, RB, SORTED, MB><<<blocks, 256, 0, s>>>(a); break;
-    case 4: mttkrp_fast_kernel<T, N, 4, U, RB, SORTED, MB><<<blocks, 256, 0, s>>>(a); break;
-    case 8: mttkrp_fast_kernel<T, N, 8, U, RB, SORTED, MB><<<blocks, 256, 0, s>>>(a); break;
-    case 16: mttkrp_fast_kernel<T, N, 16, U, RB, SORTED, MB><<<blocks, 256, 0, s>>>(a); break;
-    case 32: mttkrp_fast_kernel<T, N, 32, U, RB, SORTED, MB><<<blocks, 256, 0, s>>>(a); break;
+    case 1: SPTK_LAUNCH_G(1) break;
+    case 2: SPTK_LAUNCH_G(2) break;
+    case 4: SPTK_LAUNCH_G(4) break;
+    case 8: SPTK_LAUNCH_G(8) break;
+    case 16: SPTK_LAUNCH_G(16) break;
+    case 32: SPTK_LAUNCH_G(32) break;
     default: return fail(SPTK_EINVAL, "fast MTTKRP: bad lane count");
     }
+#undef SPTK_LAUNCH_G
     count_launch();
     SPTK_CUDA(cudaGetLastError());
     return SPTK_OK;
 }
 
 // Per-(T, N) launcher, explicitly instantiated in mttkrp_<t>_n<N>.cu.
+// `workers` counts groups (variant 0) or warps (variant 1).
 template <typename T, int N>
-sptk_status launch_fast_tn(int G, int rb, int variant, const MttkrpArgs &a, int64_t workers,
+sptk_status launch_fast_tn(int G, int variant, const MttkrpArgs &a, int64_t workers,
                            cudaStream_t s);
 
 #define SPTK_INSTANTIATE_FAST(T, N)                                                          \
     template <>                                                                              \
-    sptk_status launch_fast_tn<T, N>(int G, int rb, int variant, const MttkrpArgs &a,        \
+    sptk_status launch_fast_tn<T, N>(int G, int variant, const MttkrpArgs &a,                \
                                      int64_t workers, cudaStream_t s) {                      \
         constexpr int RB = (sizeof(T) + 4 * N <= 16) ? 16 : 32;        /* full record */      \
         constexpr int RC = (sizeof(T) + 4 * (N - 1) <= 16) ? 16 : 32;  /* compact copy */     \
-        (void)rb;                                                                            \
-        if (a.perm) return fast_launch_g<T, N, RB, false, 0>(G, a, workers, s);              \
-        switch (variant) {                                                                   \
-        case 1: return fast_launch_g<T, N, RC, true, 1>(G, a, workers, s);                   \
-        case 2: return fast_launch_g<T, N, RC, true, 2>(G, a, workers, s);                   \
-        case 3: return fast_launch_g<T, N, RC, true, 3>(G, a, workers, s);                   \
-        case 4: return fast_launch_g<T, N, RC, true, 4>(G, a, workers, s);                   \
-        default: return fast_launch_g<T, N, RC, true, 0>(G, a, workers, s);                  \
-        }                                                                                    \
+        if (a.perm) return fast_launch_g<T, N, RB, false, false>(G, a, workers, s);          \
+        if (variant == 1) return fast_launch_g<T, N, RC, true, true>(G, a, workers, s);      \
+        return fast_launch_g<T, N, RC, true, false>(G, a, workers, s);                       \
     }
 
 template <typename T>

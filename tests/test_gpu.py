@@ -340,3 +340,23 @@ def test_config_nell2_full_perm_gather(sp):
 
 def test_config_delicious_full(sp):
     full_config_check(sp, "delicious", 16, torch.float64)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("run", [4, 16, 256])
+def test_mttkrp_worker_shapes(sp, variant, run):
+    """Both worker shapes on the permuted copy (per-group runs / warp-
+    cooperative steps) and several block lengths, incl. rows shorter and
+    longer than a step, against the oracle."""
+    dims = (300, 40, 7)
+    idx, vals = synth.tensor(91, dims, 4 * 4096 + 77, "powerlaw")
+    A = factors_np(92, dims, 16)
+    t = make(sp, dims, idx, vals)
+    sp.build_perm(t, -1)
+    try:
+        sp.set_tuning(variant, run)
+        for n in range(3):
+            V = gpu_mttkrp(sp, t, n, A, 16, torch.float64)
+            assert rel(V, oracle.mttkrp(dims, idx, vals, A, n)) <= 1e-12, n
+    finally:
+        sp.set_tuning(-2, -2)

@@ -19,7 +19,7 @@ def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "nell2"
     R = int(sys.argv[2]) if len(sys.argv) > 2 else 16
     dt = torch.float64 if (len(sys.argv) < 4 or sys.argv[3] == "f64") else torch.float32
-    variants = [int(v) for v in os.environ.get("VARIANTS", "0,1,2,3,4").split(",")]
+    variants = [int(v) for v in os.environ.get("VARIANTS", "0,1").split(",")]
     runs = [int(r) for r in os.environ.get("RUNS", "128,256,512,1024").split(",")]
     layouts = os.environ.get("LAYOUTS", "sorted").split(",")
     c = synth.CONFIGS[name]
