@@ -258,6 +258,13 @@ sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream) {
         if (st == SPTK_ECUDA) t->poisoned = true;
         if (st != SPTK_OK) return st;
     }
+    // keep the sort workspace for the next build_perm only while memory is plentiful
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+        if (free_b < total_b / 4) t->sortws.release();
+    } else {
+        cudaGetLastError();
+    }
     return SPTK_OK;
 }
 

@@ -24,6 +24,8 @@ def lib():
         L.synth_coords.argtypes = [u64, i, i, C.c_uint32, u64, i64, i, d, u64, u64, p, p, p]
         L.synth_values.argtypes = [u64, i, u64, i64, i, p, p]
         L.synth_factor.argtypes = [u64, i, i, i64, i64, i, p, p]
+        L.synth_coords_at.argtypes = [u64, i, C.c_uint32, p, i64, i, d, u64, u64, p, p, p]
+        L.synth_values_at.argtypes = [u64, i, p, i64, p, p]
         _lib = L
     return _lib
 
@@ -66,4 +68,28 @@ def factor(seed_f: int, N: int, m: int, I: int, R: int, dtype=None, device="cuda
                             _stream())
     if st:
         raise RuntimeError(f"synth_factor failed: cuda error {st}")
+    return out
+
+
+def coords_at(seed: int, mode: int, I: int, ids, dist: str = "uniform"):
+    """Mode-`mode` coordinates of the nonzeros with generation counters `ids`
+    (a CUDA int32 tensor holding uint32 counters) -> CUDA int32 tensor."""
+    import torch
+    out = torch.empty_like(ids)
+    pl = PowerLawParams.for_dim(int(I)) if dist == "powerlaw" else PowerLawParams(0.0, 0, 0)
+    st = lib().synth_coords_at(seed, mode, int(I), ids.data_ptr(), ids.numel(),
+                               1 if dist == "powerlaw" else 0, pl.L, pl.a, pl.b,
+                               _COEFFS.ctypes.data, out.data_ptr(), _stream())
+    if st:
+        raise RuntimeError(f"synth_coords_at failed: cuda error {st}")
+    return out
+
+
+def values_at(seed: int, N: int, ids):
+    """fp64 values of the nonzeros with generation counters `ids`."""
+    import torch
+    out = torch.empty(ids.numel(), dtype=torch.float64, device=ids.device)
+    st = lib().synth_values_at(seed, N, ids.data_ptr(), ids.numel(), out.data_ptr(), _stream())
+    if st:
+        raise RuntimeError(f"synth_values_at failed: cuda error {st}")
     return out

@@ -52,6 +52,40 @@ __global__ void coords_kernel(uint64_t seed, int mode, int nmodes, uint32_t I, u
     }
 }
 
+// same draws at arbitrary counters ids[k] (instead of i0 + k), out[k]
+__global__ void coords_at_kernel(uint64_t seed, int mode, uint32_t I, const uint32_t *__restrict__ ids,
+                                 int64_t count, int dist, double L, uint64_t a, uint64_t b,
+                                 PowCoeffs pc, uint32_t *__restrict__ out) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t d = draw(seed, (uint64_t)mode, (uint64_t)ids[k]);
+        uint32_t l;
+        if (dist == 0) {
+            l = (uint32_t)(((d >> 32) * (uint64_t)I) >> 32);
+        } else {
+            const double t = __dmul_rn(unit(d), L);
+            const double e = floor(t);
+            const double f = __dadd_rn(t, -e);
+            double y = pc.c[16];
+#pragma unroll
+            for (int j = 15; j >= 0; --j) y = __dadd_rn(__dmul_rn(y, f), pc.c[j]);
+            y = ldexp(y, (int)e);
+            int64_t r = (int64_t)floor(y) - 1;
+            if (r < 0) r = 0;
+            if (r > (int64_t)I - 1) r = (int64_t)I - 1;
+            l = (uint32_t)((a * (uint64_t)r + b) % (uint64_t)I);
+        }
+        out[k] = l;
+    }
+}
+
+__global__ void values_at_kernel(uint64_t seed, int nmodes, const uint32_t *__restrict__ ids,
+                                 int64_t count, double *__restrict__ out) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count;
+         k += (int64_t)gridDim.x * blockDim.x)
+        out[k] = 1.0 - unit(draw(seed, (uint64_t)nmodes, (uint64_t)ids[k]));
+}
+
 __global__ void values_kernel(uint64_t seed, int nmodes, uint64_t i0, int64_t count, int f32,
                               void *__restrict__ out) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count;
@@ -91,6 +125,23 @@ int synth_coords(uint64_t seed, int mode, int nmodes, uint32_t I, uint64_t i0, i
     for (int j = 0; j < 17; ++j) pc.c[j] = coeffs ? coeffs[j] : 0.0;
     coords_kernel<<<grid(count), 256, 0, (cudaStream_t)stream>>>(seed, mode, nmodes, I, i0, count,
                                                                 dist, L, a, b, pc, out);
+    return (int)cudaGetLastError();
+}
+
+int synth_coords_at(uint64_t seed, int mode, uint32_t I, const uint32_t *ids, int64_t count,
+                    int dist, double L, uint64_t a, uint64_t b, const double *coeffs, uint32_t *out,
+                    void *stream) {
+    PowCoeffs pc;
+    for (int j = 0; j < 17; ++j) pc.c[j] = coeffs ? coeffs[j] : 0.0;
+    coords_at_kernel<<<grid(count), 256, 0, (cudaStream_t)stream>>>(seed, mode, I, ids, count, dist,
+                                                                   L, a, b, pc, out);
+    return (int)cudaGetLastError();
+}
+
+// fp64 values 1 - u at counters ids[k]
+int synth_values_at(uint64_t seed, int nmodes, const uint32_t *ids, int64_t count, double *out,
+                    void *stream) {
+    values_at_kernel<<<grid(count), 256, 0, (cudaStream_t)stream>>>(seed, nmodes, ids, count, out);
     return (int)cudaGetLastError();
 }
 

@@ -360,3 +360,84 @@ def test_mttkrp_worker_shapes(sp, variant, run):
             assert rel(V, oracle.mttkrp(dims, idx, vals, A, n)) <= 1e-12, n
     finally:
         sp.set_tuning(-2, -2)
+
+
+def test_device_generator_at_arbitrary_counters():
+    from synth import device
+    ids = np.array([0, 5, 1_699_999_999, 123456789, 77], dtype=np.uint32)
+    ids_d = torch.from_numpy(ids.view(np.int32)).cuda()
+    for dist, I in (("uniform", 4_800_000), ("powerlaw", 2_500_000)):
+        got = device.coords_at(1814, 1, I, ids_d, dist).cpu().numpy().view(np.uint32)
+        ref = np.array([synth.coords(1814, 1, I, int(i), 1, dist)[0] for i in ids])
+        assert np.array_equal(got, ref)
+    v = device.values_at(1814, 3, ids_d).cpu().numpy()
+    assert np.array_equal(v, np.array([synth.values(1814, 3, int(i), 1)[0] for i in ids]))
+
+
+def test_config_amazon_full(sp):
+    """C5 at full size (1.7B nonzeros) in the bench's launch configuration.
+    Host memory cannot hold the oracle's copy, so: the permutation is checked
+    on the device against the generator (bijection, non-decreasing keys,
+    increasing ids within ties, rowptr = key histogram), and the MTTKRP on
+    sampled rows against oracle_mttkrp_rows on exactly those rows' nonzeros
+    (selected through the verified perm/rowptr, coordinates and values
+    regenerated from their counters)."""
+    from synth import device
+    c = synth.CONFIGS["amazon"]
+    R = 16
+    free, total = torch.cuda.mem_get_info()
+    if free < 170e9:
+        pytest.skip(f"needs ~170 GB free device memory, have {free / 1e9:.0f} GB")
+    idx_d, val_d = device.tensor(c.seed, c.dims, c.nnz, c.dist)
+    t = sp.sptensor_create(c.dims, idx_d, val_d)
+    del idx_d, val_d
+    torch.cuda.empty_cache()
+    sp.build_perm(t, -1)
+    A_d = [device.factor(c.seed_f, c.N, m, I, R) for m, I in enumerate(c.dims)]
+    A_h = [a.cpu().numpy() for a in A_d]
+    P = c.nnz
+    chunk = 200_000_000
+    for n in range(c.N):
+        out = torch.empty((c.dims[n], R), dtype=torch.float64, device="cuda")
+        sp.mttkrp(t, n, A_d, out)
+        V_rows = out  # kept until the sampled check
+        perm = torch.empty(P, dtype=torch.int32, device="cuda")
+        sp.get_perm(t, n, perm)
+        rp = torch.empty(c.dims[n] + 1, dtype=torch.int32, device="cuda")
+        sp.get_rowptr(t, n, rp)
+        # bijection
+        seen = torch.zeros(P, dtype=torch.bool, device="cuda")
+        for s0 in range(0, P, chunk):
+            seen[perm[s0:s0 + chunk].long()] = True
+        assert bool(seen.all()), f"perm mode {n} is not a bijection"
+        del seen
+        counts = torch.zeros(c.dims[n], dtype=torch.int64, device="cuda")
+        prev_key = prev_id = None
+        for s0 in range(0, P, chunk):
+            ids = perm[s0:s0 + chunk]
+            keys = device.coords_at(c.seed, n, c.dims[n], ids, c.dist).long()
+            idl = ids.long() & 0xFFFFFFFF
+            if prev_key is not None:
+                keys = torch.cat([prev_key, keys])
+                idl = torch.cat([prev_id, idl])
+            dk = keys[1:] - keys[:-1]
+            assert bool((dk >= 0).all()), f"keys decrease in mode {n}"
+            assert bool((idl[1:][dk == 0] > idl[:-1][dk == 0]).all()), f"unstable ties, mode {n}"
+            counts += torch.bincount(keys[1:] if prev_key is not None else keys,
+                                     minlength=c.dims[n])
+            prev_key, prev_id = keys[-1:], idl[-1:]
+        rph = rp.long()
+        assert int(rph[0]) == 0 and int(rph[-1]) == P
+        assert torch.equal(rph[1:] - rph[:-1], counts), f"rowptr mode {n}"
+        # sampled rows
+        rows = sampled_rows(counts.cpu().numpy(), k=24, seed=n)
+        sel = torch.cat([perm[int(rph[r]):int(rph[r + 1])] for r in rows])
+        sub_idx = np.stack([device.coords_at(c.seed, m, c.dims[m], sel, c.dist).cpu().numpy()
+                            .view(np.uint32) for m in range(c.N)], axis=1)
+        sub_val = device.values_at(c.seed, c.N, sel).cpu().numpy()
+        Vo = oracle.mttkrp_rows(c.dims, sub_idx, sub_val, A_h, n, rows, acc_long=True)
+        V = V_rows[torch.from_numpy(rows).cuda()].cpu().numpy()
+        assert rel(V, Vo) <= 1e-12, f"mode {n}"
+        del perm, V_rows, out
+        torch.cuda.empty_cache()
+    t.close()
