@@ -149,6 +149,16 @@ sptk_status sptk_get_rowptr(sptk_tensor t, int mode, uint32_t *out, void *stream
 sptk_status sptk_mttkrp(sptk_tensor t, int mode, int64_t R, const void *const *factors,
                         const void *lambda, void *out, sptk_comm comm, void *stream);
 
+/* The per-shard unit of the multi-GPU path: the same computation restricted
+ * to output rows [row_begin, row_end) of mode n, i.e. to the permuted
+ * positions [rowptr_n[row_begin], rowptr_n[row_end]).  Rows
+ * outside the range are not touched; rows inside are overwritten.  Several
+ * calls over a partition of [0, I_n) (e.g. sptk_partition_rows) reproduce
+ * sptk_mttkrp. */
+sptk_status sptk_mttkrp_rows(sptk_tensor t, int mode, int64_t R, const void *const *factors,
+                             const void *lambda, void *out, int64_t row_begin, int64_t row_end,
+                             void *stream);
+
 /* ---------------------------------------------------------------- CP-ALS */
 
 /* CP-ALS (the paper omits the algorithm and defers to Kolda &

@@ -46,6 +46,7 @@ _SIGS = [
     ("sptk_get_perm", [_P, _I, _P, _P], _I),
     ("sptk_get_rowptr", [_P, _I, _P, _P], _I),
     ("sptk_mttkrp", [_P, _I, _I64, _P, _P, _P, _P, _P], _I),
+    ("sptk_mttkrp_rows", [_P, _I, _I64, _P, _P, _P, _I64, _I64, _P], _I),
     ("sptk_cp_als", [_P, _I64, _I, _D, _U64, _P, _P, _P, _P, _P, _P, _P, _P], _I),
     ("sptk_comm_unique_id", [_P], _I),
     ("sptk_comm_create", [_P, _I, _I, _P], _I),
@@ -214,6 +215,15 @@ def mttkrp(t: SpTensor, mode: int, factors, out, lam=None, comm=None, stream=Non
     _check(lib().sptk_mttkrp(t.handle, mode, R, table, _ptr(lam), _ptr(out),
                              comm.handle if comm is not None else None, _stream(stream)),
            "mttkrp")
+    return out
+
+
+def mttkrp_rows(t: SpTensor, mode: int, factors, out, row_begin: int, row_end: int, lam=None,
+                stream=None):
+    """out[row_begin:row_end] <- those rows of MTTKRP(X, factors, mode)."""
+    R = int(out.shape[1])
+    _check(lib().sptk_mttkrp_rows(t.handle, mode, R, _ptr_table(factors), _ptr(lam), _ptr(out),
+                                  row_begin, row_end, _stream(stream)), "mttkrp_rows")
     return out
 
 

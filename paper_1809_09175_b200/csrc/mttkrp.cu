@@ -224,3 +224,23 @@ extern "C" sptk_status sptk_mttkrp(sptk_tensor t, int mode, int64_t R,
     if (st == SPTK_ECUDA) t->poisoned = true;
     return st;
 }
+
+extern "C" sptk_status sptk_mttkrp_rows(sptk_tensor t, int mode, int64_t R,
+                                        const void *const *factors, const void *lambda,
+                                        void *out, int64_t row_begin, int64_t row_end,
+                                        void *stream) {
+    if (!t) return fail(SPTK_EINVAL, "null tensor handle");
+    if (t->poisoned) return fail(SPTK_ECUDA, "tensor handle poisoned by an earlier CUDA error");
+    if (mode < 0 || mode >= t->N) return fail(SPTK_EINVAL, "mode out of range");
+    if (R < 1 || R > (int64_t(1) << 20)) return fail(SPTK_EINVAL, "R must be in [1, 2^20]");
+    if (!factors || !out) return fail(SPTK_EINVAL, "factors/out is NULL");
+    for (int m = 0; m < t->N; ++m)
+        if (m != mode && !factors[m]) return fail(SPTK_EINVAL, "factors[m] is NULL");
+    if (row_begin < 0 || row_end > t->dims[mode] || row_begin > row_end)
+        return fail(SPTK_EINVAL, "row range outside [0, I_n]");
+    if (!t->has_perm[mode]) return fail(SPTK_ENOPERM, "build_perm(mode) has not run");
+    sptk_status st = mttkrp_launch(t, mode, R, factors, lambda, out, row_begin, row_end,
+                                   (cudaStream_t)stream);
+    if (st == SPTK_ECUDA) t->poisoned = true;
+    return st;
+}

@@ -383,8 +383,11 @@ def test_config_amazon_full(sp):
     (selected through the verified perm/rowptr, coordinates and values
     regenerated from their counters)."""
     from synth import device
+    import gc
     c = synth.CONFIGS["amazon"]
     R = 16
+    gc.collect()                  # earlier tests' tensors and handles
+    torch.cuda.empty_cache()
     free, total = torch.cuda.mem_get_info()
     if free < 170e9:
         pytest.skip(f"needs ~170 GB free device memory, have {free / 1e9:.0f} GB")
@@ -441,3 +444,24 @@ def test_config_amazon_full(sp):
         del perm, V_rows, out
         torch.cuda.empty_cache()
     t.close()
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_simulated_row_shards(sp, G):
+    """The multi-GPU work split on one device: each 'rank' computes its row
+    range (sptk_partition_rows over rowptr_n) with sptk_mttkrp_rows into one
+    buffer; the assembly equals the oracle (range edges use atomics)."""
+    dims = (500, 9000, 64)
+    idx, vals = synth.tensor(55, dims, 9 * 4096 + 3, "powerlaw")
+    A = factors_np(56, dims, 16)
+    t = make(sp, dims, idx, vals)
+    sp.build_perm(t, -1)
+    A_d = [dev(a) for a in A]
+    for n in range(3):
+        rp = gpu_perm(sp, t, n)[1]
+        b = sp.partition_rows(rp, G)
+        out = torch.full((dims[n], 16), float("nan"), dtype=torch.float64, device="cuda")
+        for g in range(G):
+            sp.mttkrp_rows(t, n, A_d, out, int(b[g]), int(b[g + 1]))
+        torch.cuda.synchronize()
+        assert rel(out.cpu().numpy(), oracle.mttkrp(dims, idx, vals, A, n)) <= 1e-12, n
