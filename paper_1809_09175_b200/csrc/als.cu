@@ -377,7 +377,8 @@ struct AlsCtx {
     sptk_comm comm;
     std::vector<void *> A;                 // device factor pointers
     std::vector<std::vector<int64_t>> b;   // per-mode row bounds (comm)
-    int nblocks;                           // partial-sum blocks
+    int nblocks;                           // blocks of the R x R partial-sum kernels
+    int nb_row;                            // blocks of the R-vector partial-sum kernels
 };
 
 template <typename T>
@@ -427,12 +428,12 @@ static sptk_status als_iteration_fused(AlsCtx &c, double *fit_host, int *status_
         SPTK_CUDA(cudaStreamWaitEvent(c.s, w.ev_inv, 0));
         T *An = static_cast<T *>(c.A[n]);
         const int lanes = 256 / R;
-        int nb = (int)std::min<int64_t>(c.nblocks, (I + 4 * lanes - 1) / (4 * lanes));
+        int nb = (int)std::min<int64_t>(c.nb_row, (I + 4 * lanes - 1) / (4 * lanes));
         if (nb < 1) nb = 1;
         const int64_t rpb = (I + nb - 1) / nb;
         nb = (int)((I + rpb - 1) / rpb);
         double *psq = w.partial.as<double>();
-        double *pdot = psq + (size_t)c.nblocks * R;
+        double *pdot = psq + (size_t)c.nb_row * R;
         apply_inv_kernel<T><<<nb, 256, sizeof(double) * (R * R + 512), c.s>>>(
             V, 0, I, R, rpb, Ginv, An, psq, last ? pdot : nullptr);
         int nf = (int)std::min<int64_t>(c.nblocks, (I + 31) / 32);
@@ -487,11 +488,11 @@ static sptk_status als_iteration(AlsCtx &c, double *fit_host, int *status_host) 
         const int64_t rows = r1 - r0;
         if (rows > 0) {
             const int lanes = 256 / R;
-            int nb = (int)std::min<int64_t>(c.nblocks, (rows + 4 * lanes - 1) / (4 * lanes));
+            int nb = (int)std::min<int64_t>(c.nb_row, (rows + 4 * lanes - 1) / (4 * lanes));
             if (nb < 1) nb = 1;
             const int64_t rpb = (rows + nb - 1) / nb;
             nb = (int)((rows + rpb - 1) / rpb);
-            double *pdot = w.partial.as<double>() + (size_t)c.nblocks * R;
+            double *pdot = w.partial.as<double>() + (size_t)c.nb_row * R;
             apply_inv_kernel<T><<<nb, 256, sizeof(double) * (R * R + 512), c.s>>>(
                 V, r0, r1, R, rpb, Ginv, An, w.partial.as<double>(), last ? pdot : nullptr);
             reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(w.partial.as<double>(), nb, R,
@@ -544,11 +545,15 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     c.R = R;
     c.s = s;
     c.comm = comm;
-    c.nblocks = dev_sms() * 2;
+    // enough blocks to cover tall factors (LBNL's 868K-row mode) in one wave
+    // set; R x R partials are capped harder at large R
+    c.nblocks = dev_sms() * (R <= 32 ? 8 : 2);
+    c.nb_row = dev_sms() * 8;
     SPTK_TRY(w.V.reserve(es * Imax * R));
     SPTK_TRY(w.G.reserve(sizeof(double) * N * R * R));
     SPTK_TRY(w.L.reserve(sizeof(double) * R * R));  // Gamma^{-1}
-    SPTK_TRY(w.partial.reserve(sizeof(double) * (size_t)c.nblocks * std::max<int64_t>(R * R, 2 * R)));
+    SPTK_TRY(w.partial.reserve(sizeof(double) * std::max<size_t>((size_t)c.nblocks * R * R,
+                                                                (size_t)c.nb_row * 2 * R)));
     SPTK_TRY(w.colsq.reserve(sizeof(double) * 2 * R));
     SPTK_TRY(w.lam.reserve(sizeof(double) * R));
     SPTK_TRY(w.scal.reserve(sizeof(double) * 16));
