@@ -193,7 +193,10 @@ sptk_status sptk_cp_als(sptk_tensor t, int64_t R, int max_iters, double tol, uin
 sptk_status sptk_comm_unique_id(void *id128);
 
 /* Create / destroy a communicator over `nranks` processes (one GPU each;
- * the current CUDA device is used).  Collective: every rank must call it. */
+ * the current CUDA device is used).  Collective: every rank must call it.
+ * With SPTK_FORCE_SHARDED=1 in the environment a 1-rank communicator still
+ * takes the sharded code path (partition, per-rank kernels, NCCL exchange) --
+ * used to test that path on a single GPU. */
 sptk_status sptk_comm_create(const void *id128, int nranks, int rank, sptk_comm *out);
 sptk_status sptk_comm_destroy(sptk_comm c);
 

@@ -464,11 +464,11 @@ static sptk_status als_iteration_fused(AlsCtx &c, double *fit_host, int *status_
 
 template <typename T>
 static sptk_status als_iteration(AlsCtx &c, double *fit_host, int *status_host) {
-    if (!c.comm || c.comm->nranks == 1) return als_iteration_fused<T>(c, fit_host, status_host);
+    if (!sharded(c.comm)) return als_iteration_fused<T>(c, fit_host, status_host);
     sptk_tensor t = c.t;
     ALSWork &w = t->als;
     const int N = t->N, R = (int)c.R;
-    const bool multi = c.comm && c.comm->nranks > 1;
+    const bool multi = sharded(c.comm);
     double *colsq = w.colsq.as<double>();  // [0,R): sum A_raw^2; [R,2R): sum A_raw V
     double *lam = w.lam.as<double>();
     double *scal = w.scal.as<double>();
@@ -600,7 +600,7 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     }
     for (int m = 0; m < N; ++m)
         if (!t->has_perm[m]) SPTK_TRY(build_perm_mode(t, m, s));
-    const bool multi = comm && comm->nranks > 1;
+    const bool multi = sharded(comm);
     if (multi) {
         c.b.assign(N, std::vector<int64_t>(comm->nranks + 1));
         for (int m = 0; m < N; ++m) {

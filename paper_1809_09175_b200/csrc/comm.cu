@@ -7,6 +7,8 @@
 // the library loads (and its single-GPU path runs) without it; the same
 // libnccl.so.2 torch.distributed already loaded in-process is reused.
 #include <dlfcn.h>
+#include <stdlib.h>
+#include <string.h>
 #include <nccl.h>
 
 #include <mutex>
@@ -130,6 +132,8 @@ sptk_status sptk_comm_create(const void *id128, int nranks, int rank, sptk_comm 
     c->nccl = comm;
     c->nranks = nranks;
     c->rank = rank;
+    const char *f = getenv("SPTK_FORCE_SHARDED");
+    c->force_sharded = f && *f && *f != '0';
     *out = c;
     return SPTK_OK;
 }

@@ -118,7 +118,13 @@ struct sptk_comm_s {
     void *nccl = nullptr;  // ncclComm_t
     int nranks = 1;
     int rank = 0;
+    bool force_sharded = false;  // SPTK_FORCE_SHARDED=1: take the N>1 code path at N=1
 };
+
+namespace sptk {
+// true when the row-sharded path (partition + NCCL exchange) must be taken
+inline bool sharded(const sptk_comm_s *c) { return c && (c->nranks > 1 || c->force_sharded); }
+}  // namespace sptk
 
 namespace sptk {
 

@@ -208,7 +208,7 @@ extern "C" sptk_status sptk_mttkrp(sptk_tensor t, int mode, int64_t R,
     if (!t->has_perm[mode]) return fail(SPTK_ENOPERM, "build_perm(mode) has not run");
     cudaStream_t s = (cudaStream_t)stream;
     sptk_status st;
-    if (!comm || comm->nranks == 1) {
+    if (!sharded(comm)) {
         st = mttkrp_launch(t, mode, R, factors, lambda, out, 0, t->dims[mode], s);
     } else {
         st = host_rowptr(t, mode, s);

@@ -465,3 +465,33 @@ def test_simulated_row_shards(sp, G):
             sp.mttkrp_rows(t, n, A_d, out, int(b[g]), int(b[g + 1]))
         torch.cuda.synchronize()
         assert rel(out.cpu().numpy(), oracle.mttkrp(dims, idx, vals, A, n)) <= 1e-12, n
+
+
+def test_sharded_code_path_one_rank(sp, monkeypatch):
+    """The N>1 code path (partition, per-rank launches, NCCL all-reduce and
+    grouped broadcasts) driven through a real 1-rank NCCL communicator with
+    SPTK_FORCE_SHARDED=1; results must match the oracle."""
+    monkeypatch.setenv("SPTK_FORCE_SHARDED", "1")
+    try:
+        comm = sp.comm_create(sp.comm_unique_id(), 1, 0)
+    except sp.SptkError as e:
+        pytest.skip(f"NCCL unavailable: {e}")
+    c = synth.CONFIGS["tiny"]
+    idx, vals = synth.unique_tensor(c.seed, c.dims, c.nnz)
+    R = 8
+    t = make(sp, c.dims, idx, vals)
+    sp.build_perm(t, -1)
+    A = factors_np(c.seed_f, c.dims, R)
+    A_d = [dev(a) for a in A]
+    for n in range(3):
+        out = torch.full((c.dims[n], R), float("nan"), dtype=torch.float64, device="cuda")
+        sp.mttkrp(t, n, A_d, out, comm=comm)
+        torch.cuda.synchronize()
+        assert rel(out.cpu().numpy(), oracle.mttkrp(c.dims, idx, vals, A, n)) <= 1e-12
+    F = [torch.empty(I, R, dtype=torch.float64, device="cuda") for I in c.dims]
+    res = sp.cp_als(t, R, 10, F, seed=c.seed_f, comm=comm)
+    ref = oracle.cp_als(c.dims, idx, vals, A, 10)
+    assert np.max(np.abs(res["trace"] - ref["trace"])) <= 1e-9
+    for m in range(3):
+        assert rel(F[m].cpu().numpy(), ref["A"][m]) <= 1e-8
+    comm.close()
