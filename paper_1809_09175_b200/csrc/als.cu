@@ -404,7 +404,7 @@ static sptk_status gram(AlsCtx &c, int m) {
 // while the MTTKRP runs (it only needs the Gram matrices of the other
 // modes), then apply_inv and one finish kernel (lambda, normalise, Gram, fit).
 template <typename T>
-static sptk_status als_iteration_fused(AlsCtx &c, double *fit_host, int *status_host) {
+static sptk_status enqueue_iteration_fused(AlsCtx &c) {
     sptk_tensor t = c.t;
     ALSWork &w = t->als;
     const int N = t->N, R = (int)c.R;
@@ -452,9 +452,15 @@ static sptk_status als_iteration_fused(AlsCtx &c, double *fit_host, int *status_
         }
         SPTK_CUDA(cudaGetLastError());
     }
-    double h[9];
-    SPTK_CUDA(cudaMemcpyAsync(h, scal, sizeof(double) * 9, cudaMemcpyDeviceToHost, c.s));
+    // fit and status to pinned host memory (a graph-capturable copy)
+    SPTK_CUDA(cudaMemcpyAsync(w.hres, scal, sizeof(double) * 9, cudaMemcpyDeviceToHost, c.s));
+    return SPTK_OK;
+}
+
+// wait for the iteration and read (fit, status) from the pinned buffer
+static sptk_status complete_iteration(AlsCtx &c, double *fit_host, int *status_host) {
     SPTK_CUDA(cudaStreamSynchronize(c.s));
+    const double *h = c.t->als.hres;
     *fit_host = h[0];
     int st;
     memcpy(&st, &h[8], sizeof(int));
@@ -464,7 +470,10 @@ static sptk_status als_iteration_fused(AlsCtx &c, double *fit_host, int *status_
 
 template <typename T>
 static sptk_status als_iteration(AlsCtx &c, double *fit_host, int *status_host) {
-    if (!sharded(c.comm)) return als_iteration_fused<T>(c, fit_host, status_host);
+    if (!sharded(c.comm)) {
+        SPTK_TRY(enqueue_iteration_fused<T>(c));
+        return complete_iteration(c, fit_host, status_host);
+    }
     sptk_tensor t = c.t;
     ALSWork &w = t->als;
     const int N = t->N, R = (int)c.R;
@@ -559,6 +568,7 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     SPTK_TRY(w.scal.reserve(sizeof(double) * 16));
     SPTK_TRY(w.lamT.reserve(es * R));
     SPTK_TRY(w.gpart.reserve(sizeof(double) * (size_t)c.nblocks * R * R));
+    if (!w.hres) SPTK_CUDA(cudaMallocHost(&w.hres, sizeof(double) * 16));
     if (!w.side) {
         SPTK_CUDA(cudaStreamCreateWithFlags(&w.side, cudaStreamNonBlocking));
         SPTK_CUDA(cudaEventCreateWithFlags(&w.ev_gram, cudaEventDisableTiming));
@@ -614,10 +624,53 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     double fit = 0.0, fit_prev = 0.0;
     int it = 0;
     sptk_status st = SPTK_OK;
+    // Single GPU: after one eager iteration (which builds every cache the
+    // launches read), capture one iteration -- both streams, ~4N+2 kernels and
+    // the fit copy -- into a CUDA graph and replay it.  Not while profiling
+    // (kernel-span events cannot be timed inside graphs) or for < 4 iterations.
+    const char *ng = getenv("SPTK_NO_GRAPH");
+    bool use_graph = !multi && !profile().on && max_iters >= 4 && !(ng && *ng && *ng != '0');
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches_per_iter = 0;
     for (it = 0; it < max_iters; ++it) {
         int bad = 0;
-        st = als_iteration<T>(c, &fit, &bad);
+        if (use_graph && it >= 1) {
+            if (!exec) {
+                const int64_t l0 = profile().launches;
+                bool ok = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+                sptk_status est = ok ? enqueue_iteration_fused<T>(c) : SPTK_ECUDA;
+                cudaGraph_t g = nullptr;
+                const bool ended = cudaStreamEndCapture(s, &g) == cudaSuccess;
+                ok = ok && est == SPTK_OK && ended && g &&
+                     cudaGraphInstantiate(&exec, g, 0) == cudaSuccess;
+                graph = g;
+                launches_per_iter = profile().launches - l0;
+                if (!ok) {  // fall back to eager launches for the rest of the call
+                    cudaGetLastError();
+                    set_error("");
+                    if (exec) cudaGraphExecDestroy(exec);
+                    exec = nullptr;
+                    use_graph = false;
+                    profile().launches = l0;
+                    st = enqueue_iteration_fused<T>(c);
+                    if (st == SPTK_OK) st = complete_iteration(c, &fit, &bad);
+                    if (st != SPTK_OK) break;
+                    goto have_fit;
+                }
+            } else {
+                profile().launches += launches_per_iter;
+            }
+            if (cudaGraphLaunch(exec, s) != cudaSuccess) {
+                st = cuda_fail(cudaGetLastError(), "cudaGraphLaunch(ALS iteration)");
+                break;
+            }
+            st = complete_iteration(c, &fit, &bad);
+        } else {
+            st = als_iteration<T>(c, &fit, &bad);
+        }
         if (st != SPTK_OK) break;
+    have_fit:
         if (bad) {
             st = fail(SPTK_ESINGULAR, "Gamma is singular after the ridge retry");
             break;
@@ -629,6 +682,8 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
         }
         fit_prev = fit;
     }
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
     if (fit_out) *fit_out = fit;
     if (iters_out) *iters_out = it;
     if (st != SPTK_OK) return st;

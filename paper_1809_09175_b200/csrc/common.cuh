@@ -82,7 +82,9 @@ struct ALSWork {
     DevBuf gpart;     // per-block partial Gram matrices (f64)
     cudaStream_t side = nullptr;              // Cholesky / inverse, overlapped with MTTKRP
     cudaEvent_t ev_gram = nullptr, ev_inv = nullptr;
+    double *hres = nullptr;                   // pinned: fit, inner, ||M||^2, ..., status
     ~ALSWork() {
+        if (hres) cudaFreeHost(hres);
         if (ev_gram) cudaEventDestroy(ev_gram);
         if (ev_inv) cudaEventDestroy(ev_inv);
         if (side) cudaStreamDestroy(side);
