@@ -149,6 +149,14 @@ sptk_status sptk_get_rowptr(sptk_tensor t, int mode, uint32_t *out, void *stream
 sptk_status sptk_mttkrp(sptk_tensor t, int mode, int64_t R, const void *const *factors,
                         const void *lambda, void *out, sptk_comm comm, void *stream);
 
+/* The paper's atomic-per-nonzero MTTKRP (VerA/VerB, Figs. mttkrp_alg and
+ * mttkrp_array): nonzeros in storage order, every
+ * contribution added to `out` with atomics.  Same arguments and result as
+ * sptk_mttkrp (up to summation order); needs no permutation.
+ * Provided for the paper's VerB-vs-VerC comparison. */
+sptk_status sptk_mttkrp_atomic(sptk_tensor t, int mode, int64_t R, const void *const *factors,
+                               const void *lambda, void *out, void *stream);
+
 /* The per-shard unit of the multi-GPU path: the same computation restricted
  * to output rows [row_begin, row_end) of mode n, i.e. to the permuted
  * positions [rowptr_n[row_begin], rowptr_n[row_end]).  Rows

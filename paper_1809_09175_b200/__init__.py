@@ -47,6 +47,7 @@ _SIGS = [
     ("sptk_get_rowptr", [_P, _I, _P, _P], _I),
     ("sptk_mttkrp", [_P, _I, _I64, _P, _P, _P, _P, _P], _I),
     ("sptk_mttkrp_rows", [_P, _I, _I64, _P, _P, _P, _I64, _I64, _P], _I),
+    ("sptk_mttkrp_atomic", [_P, _I, _I64, _P, _P, _P, _P], _I),
     ("sptk_cp_als", [_P, _I64, _I, _D, _U64, _P, _P, _P, _P, _P, _P, _P, _P], _I),
     ("sptk_comm_unique_id", [_P], _I),
     ("sptk_comm_create", [_P, _I, _I, _P], _I),
@@ -215,6 +216,14 @@ def mttkrp(t: SpTensor, mode: int, factors, out, lam=None, comm=None, stream=Non
     _check(lib().sptk_mttkrp(t.handle, mode, R, table, _ptr(lam), _ptr(out),
                              comm.handle if comm is not None else None, _stream(stream)),
            "mttkrp")
+    return out
+
+
+def mttkrp_atomic(t: SpTensor, mode: int, factors, out, lam=None, stream=None):
+    """The paper's atomic-per-nonzero MTTKRP (VerA/VerB): storage order, no perm."""
+    R = int(out.shape[1])
+    _check(lib().sptk_mttkrp_atomic(t.handle, mode, R, _ptr_table(factors), _ptr(lam), _ptr(out),
+                                    _stream(stream)), "mttkrp_atomic")
     return out
 
 

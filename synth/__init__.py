@@ -259,4 +259,7 @@ CONFIGS = {
                         (16,), ("f64",), dist="powerlaw"),
     "amazon": Config(5, "amazon", (4_800_000, 1_800_000, 1_800_000), 1_700_000_000,
                      (16,), ("f64",)),
+    # the paper's own synthetic CP-ALS / bandwidth-vs-R workload:
+    # "30K x 40K x 50K with 10M nonzeros placed randomly", R = 128 and R in [8, 256]
+    "paper_synth": Config(6, "paper_synth", (30000, 40000, 50000), 10_000_000, (128,), ("f64",)),
 }

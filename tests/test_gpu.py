@@ -495,3 +495,29 @@ def test_sharded_code_path_one_rank(sp, monkeypatch):
     for m in range(3):
         assert rel(F[m].cpu().numpy(), ref["A"][m]) <= 1e-8
     comm.close()
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("dims,R,offset", [((57, 1203, 311), 16, 0), ((57, 1203, 311), 64, 0),
+                                           ((40, 30, 20, 10), 17, 0), ((57, 1203, 311), 16, 1),
+                                           ((500, 7), 300, 0)])
+def test_mttkrp_atomic_variant(sp, dtype, dims, R, offset):
+    """The paper's VerA/VerB traversal (storage order, atomics): no perm needed."""
+    P = 3 * 4096 + 11
+    idx, vals = synth.tensor(13, dims, P, "powerlaw")
+    npd = np.float64 if dtype == torch.float64 else np.float32
+    vals = vals.astype(npd)
+    A = factors_np(14, dims, R, npd)
+    lam = np.linspace(0.5, 1.5, R).astype(npd)
+    t = make(sp, dims, idx, vals, dtype)
+    for n in range(len(dims)):
+        A_dev = []
+        for a in A:
+            buf = torch.zeros(a.size + offset, dtype=dtype, device="cuda")
+            buf[offset:] = dev(a.reshape(-1), dtype)
+            A_dev.append(buf[offset:].view(a.shape))
+        out = torch.full((dims[n], R), float("nan"), dtype=dtype, device="cuda")
+        sp.mttkrp_atomic(t, n, A_dev, out, lam=dev(lam, dtype))
+        Vo = oracle.mttkrp(dims, idx, vals.astype(np.float64), [a.astype(np.float64) for a in A], n,
+                           lam=lam.astype(np.float64))
+        assert rel(out.double().cpu().numpy(), Vo) <= TOL[dtype], n

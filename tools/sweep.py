@@ -1,5 +1,7 @@
-"""Launch-shape sweep of the MTTKRP fast kernel on a BASELINE config
-(device-generated inputs).  Usage: python tools/sweep.py [config] [R] [f64|f32]
+"""MTTKRP sweep on a BASELINE config (device-generated inputs): layouts
+(LAYOUTS=sorted,perm_gather,atomic -- atomic is the paper's VerA/VerB
+storage-order traversal), worker shapes (VARIANTS) and block lengths (RUNS).
+Usage: python tools/sweep.py [config] [R] [f64|f32]
 Prints ms per mode (mean of 20 launches after warm-up, CUDA events)."""
 import os
 import sys
@@ -29,18 +31,20 @@ def main():
     s_v = 8 if dt == torch.float64 else 4
     for layout in layouts:
         t = sp.sptensor_create(c.dims, idx, val, perm_gather=layout == "perm_gather")
-        sp.build_perm(t, -1)
-        for v in variants:
-            for run in runs:
+        if layout != "atomic":
+            sp.build_perm(t, -1)
+        call = sp.mttkrp_atomic if layout == "atomic" else sp.mttkrp
+        for v in (variants if layout == "sorted" else [-1]):
+            for run in (runs if layout != "atomic" else [0]):
                 sp.set_tuning(v, run)
                 ms = []
                 for n in range(c.N):
                     for _ in range(3):
-                        sp.mttkrp(t, n, A, outs[n])
+                        call(t, n, A, outs[n])
                     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     a.record()
                     for _ in range(20):
-                        sp.mttkrp(t, n, A, outs[n])
+                        call(t, n, A, outs[n])
                     b.record()
                     torch.cuda.synchronize()
                     ms.append(a.elapsed_time(b) / 20)
@@ -49,6 +53,7 @@ def main():
                       f"ms/mode={' '.join(f'{x:.3f}' for x in ms)}  sum={sum(ms):.3f}  "
                       f"B_model GB/s={bm / sum(ms) / 1e6:.0f}", flush=True)
         t.close()
+        sp.set_tuning(-2, -2)
 
 
 if __name__ == "__main__":
