@@ -356,6 +356,147 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// ---------------------------------------------------------- tiled glue (R > 32)
+// Register-blocked fp64 tiles for the two dense products of the glue when R
+// is large (the paper's R = 128 CP-ALS workload): A_raw = V Gamma^{-1} and the
+// Gram matrix A^T A.  64 x 64 output tiles, 256 threads x (4 x 4) outputs,
+// k-chunks of 32 staged in shared memory.
+constexpr int kTB = 64, kTK = 32;
+
+// A_raw(k,:) = V(k,:) Ginv for rows [r0, r1); grid (row tiles, col tiles).
+// part_sq / part_dot: [row tile][R] column partials of A_raw^2 and A_raw .* V.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    apply_inv_tiled_kernel(const T *__restrict__ V, int64_t r0, int64_t r1, int R,
+                           const double *__restrict__ Ginv, T *__restrict__ A,
+                           double *__restrict__ part_sq, double *__restrict__ part_dot) {
+    __shared__ double sV[kTB][kTK + 1];             // [row][k] (padded: conflict-free)
+    __shared__ __align__(16) double sG[kTK][kTB];   // [k][col] (vector reads)
+    // after the main loop sV is reused for the column partials: red[2][16][kTB]
+    double(*red)[16][kTB] = reinterpret_cast<double(*)[16][kTB]>(&sV[0][0]);
+    static_assert(2 * 16 * kTB <= kTB * (kTK + 1), "partials must fit in sV");
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t row0 = r0 + (int64_t)blockIdx.x * kTB;
+    const int col0 = blockIdx.y * kTB;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int k0 = 0; k0 < R; k0 += kTK) {
+        for (int x = threadIdx.x; x < kTB * kTK; x += 256) {
+            const int r = x / kTK, k = x % kTK;  // V tile: coalesced along k
+            const int64_t row = row0 + r;
+            sV[r][k] = (row < r1 && k0 + k < R) ? (double)V[row * R + k0 + k] : 0.0;
+            const int kk = x / kTB, c = x % kTB;  // Ginv tile: coalesced along cols
+            sG[kk][c] = (k0 + kk < R && col0 + c < R) ? Ginv[(int64_t)(k0 + kk) * R + col0 + c] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int k = 0; k < kTK; ++k) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = sV[ty * 4 + i][k];
+            const double2 g01 = *reinterpret_cast<const double2 *>(&sG[k][tx * 4]);
+            const double2 g23 = *reinterpret_cast<const double2 *>(&sG[k][tx * 4 + 2]);
+            b[0] = g01.x; b[1] = g01.y; b[2] = g23.x; b[3] = g23.y;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
+        }
+        __syncthreads();
+    }
+    double sq[4] = {0, 0, 0, 0}, dt[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t row = row0 + ty * 4 + i;
+        if (row >= r1) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int col = col0 + tx * 4 + j;
+            if (col >= R) continue;
+            const T v = (T)acc[i][j];
+            A[row * R + col] = v;
+            sq[j] += (double)v * (double)v;
+            dt[j] += (double)v * (double)V[row * R + col];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        red[0][ty][tx * 4 + j] = sq[j];
+        red[1][ty][tx * 4 + j] = dt[j];
+    }
+    __syncthreads();
+    if (threadIdx.x < kTB) {
+        const int col = col0 + threadIdx.x;
+        if (col < R) {
+            double a = 0.0, d = 0.0;
+            for (int q = 0; q < 16; ++q) {
+                a += red[0][q][threadIdx.x];
+                d += red[1][q][threadIdx.x];
+            }
+            part_sq[(int64_t)blockIdx.x * R + col] = a;
+            if (part_dot) part_dot[(int64_t)blockIdx.x * R + col] = d;
+        }
+    }
+}
+
+// partial[b][a*R + c] = sum over rows of block b of A(k,a) A(k,c);
+// grid (row chunks, (R/64)^2 output tiles)
+template <typename T>
+__global__ void __launch_bounds__(256)
+    gram_tiled_kernel(const T *__restrict__ A, int64_t I, int R, int64_t rows_per_block,
+                      double *__restrict__ partial) {
+    __shared__ __align__(16) double sa[kTK][kTB];
+    __shared__ __align__(16) double sb[kTK][kTB];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int nt = (R + kTB - 1) / kTB;
+    const int ta = blockIdx.y / nt, tb = blockIdx.y % nt;
+    const int64_t b0 = (int64_t)blockIdx.x * rows_per_block;
+    const int64_t b1 = min(I, b0 + rows_per_block);
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int64_t k0 = b0; k0 < b1; k0 += kTK) {
+        for (int x = threadIdx.x; x < kTB * kTK; x += 256) {
+            const int k = x / kTB, c = x % kTB;
+            const int64_t row = k0 + k;
+            const int ca = ta * kTB + c, cb = tb * kTB + c;
+            sa[k][c] = (row < b1 && ca < R) ? (double)A[row * R + ca] : 0.0;
+            sb[k][c] = (row < b1 && cb < R) ? (double)A[row * R + cb] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int k = 0; k < kTK; ++k) {
+            double a[4], b[4];
+            const double2 a01 = *reinterpret_cast<const double2 *>(&sa[k][ty * 4]);
+            const double2 a23 = *reinterpret_cast<const double2 *>(&sa[k][ty * 4 + 2]);
+            const double2 b01 = *reinterpret_cast<const double2 *>(&sb[k][tx * 4]);
+            const double2 b23 = *reinterpret_cast<const double2 *>(&sb[k][tx * 4 + 2]);
+            a[0] = a01.x; a[1] = a01.y; a[2] = a23.x; a[3] = a23.y;
+            b[0] = b01.x; b[1] = b01.y; b[2] = b23.x; b[3] = b23.y;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int ra = ta * kTB + ty * 4 + i;
+        if (ra >= R) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int cb = tb * kTB + tx * 4 + j;
+            if (cb < R) partial[(int64_t)blockIdx.x * R * R + (int64_t)ra * R + cb] = acc[i][j];
+        }
+    }
+}
+
 template <typename T>
 __global__ void cast_kernel(const double *__restrict__ in, int n, T *__restrict__ out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -379,10 +520,14 @@ struct AlsCtx {
     std::vector<std::vector<int64_t>> b;   // per-mode row bounds (comm)
     int nblocks;                           // blocks of the R x R partial-sum kernels
     int nb_row;                            // blocks of the R-vector partial-sum kernels
+    size_t part_stride;                    // doubles between the psq and pdot partials
 };
 
+// G_m = A_m^T A_m (fixed-order reduction of per-block partials in `part`,
+// default w.partial; the fused path passes w.gpart so w.partial keeps the
+// fit's column partials)
 template <typename T>
-static sptk_status gram(AlsCtx &c, int m) {
+static sptk_status gram(AlsCtx &c, int m, double *part = nullptr) {
     sptk_tensor t = c.t;
     ALSWork &w = t->als;
     const int R = (int)c.R;
@@ -390,12 +535,48 @@ static sptk_status gram(AlsCtx &c, int m) {
     int nb = (int)std::min<int64_t>(c.nblocks, (I + 31) / 32);
     const int64_t rpb = (I + nb - 1) / nb;
     nb = (int)((I + rpb - 1) / rpb);
-    const size_t sm = sizeof(double) * 32 * R;
-    gram_partial_kernel<T><<<nb, 256, sm, c.s>>>(static_cast<const T *>(c.A[m]), I, R, rpb,
-                                                 w.partial.as<double>());
+    if (!part) part = w.partial.as<double>();
+    if (R > 32) {
+        const int nt = (R + kTB - 1) / kTB;
+        gram_tiled_kernel<T><<<dim3((unsigned)nb, (unsigned)(nt * nt)), 256, 0, c.s>>>(
+            static_cast<const T *>(c.A[m]), I, R, rpb, part);
+    } else {
+        const size_t sm = sizeof(double) * 32 * R;
+        gram_partial_kernel<T><<<nb, 256, sm, c.s>>>(static_cast<const T *>(c.A[m]), I, R, rpb,
+                                                     part);
+    }
     reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(
-        w.partial.as<double>(), nb, R * R, w.G.as<double>() + (int64_t)m * R * R);
+        part, nb, R * R, w.G.as<double>() + (int64_t)m * R * R);
     count_launch(2);
+    SPTK_CUDA(cudaGetLastError());
+    return SPTK_OK;
+}
+
+// A_raw = V Gamma^{-1} on rows [r0, r1) with per-partition column partials
+// of A_raw^2 (psq) and A_raw .* V (pdot, may be NULL); returns the number of
+// partials.  R <= 32: row-parallel kernel; R > 32: register-blocked tiles.
+template <typename T>
+static sptk_status apply_inverse(AlsCtx &c, const T *V, int64_t r0, int64_t r1, T *An,
+                                 double *psq, double *pdot, int *nparts) {
+    const int R = (int)c.R;
+    const double *Ginv = c.t->als.L.as<double>();
+    const int64_t rows = r1 - r0;
+    if (R > 32) {
+        const int nrt = (int)((rows + kTB - 1) / kTB);
+        const dim3 grid((unsigned)nrt, (unsigned)((R + kTB - 1) / kTB));
+        apply_inv_tiled_kernel<T><<<grid, 256, 0, c.s>>>(V, r0, r1, R, Ginv, An, psq, pdot);
+        *nparts = nrt;
+    } else {
+        const int lanes = 256 / R;
+        int nb = (int)std::min<int64_t>(c.nb_row, (rows + 4 * lanes - 1) / (4 * lanes));
+        if (nb < 1) nb = 1;
+        const int64_t rpb = (rows + nb - 1) / nb;
+        nb = (int)((rows + rpb - 1) / rpb);
+        apply_inv_kernel<T><<<nb, 256, sizeof(double) * (R * R + 512), c.s>>>(
+            V, r0, r1, R, rpb, Ginv, An, psq, pdot);
+        *nparts = nb;
+    }
+    count_launch();
     SPTK_CUDA(cudaGetLastError());
     return SPTK_OK;
 }
@@ -427,23 +608,28 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
         SPTK_TRY(mttkrp_launch(t, n, c.R, c.A.data(), nullptr, V, 0, I, c.s));
         SPTK_CUDA(cudaStreamWaitEvent(c.s, w.ev_inv, 0));
         T *An = static_cast<T *>(c.A[n]);
-        const int lanes = 256 / R;
-        int nb = (int)std::min<int64_t>(c.nb_row, (I + 4 * lanes - 1) / (4 * lanes));
-        if (nb < 1) nb = 1;
-        const int64_t rpb = (I + nb - 1) / nb;
-        nb = (int)((I + rpb - 1) / rpb);
         double *psq = w.partial.as<double>();
-        double *pdot = psq + (size_t)c.nb_row * R;
-        apply_inv_kernel<T><<<nb, 256, sizeof(double) * (R * R + 512), c.s>>>(
-            V, 0, I, R, rpb, Ginv, An, psq, last ? pdot : nullptr);
-        int nf = (int)std::min<int64_t>(c.nblocks, (I + 31) / 32);
-        const int64_t fpb = (I + nf - 1) / nf;
-        nf = (int)((I + fpb - 1) / fpb);
-        finish_kernel<T><<<nf, 256, sizeof(double) * (R + 32 * R), c.s>>>(
-            An, I, R, fpb, psq, nb, w.gpart.as<double>(), lam);
-        reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(
-            w.gpart.as<double>(), nf, R * R, w.G.as<double>() + (int64_t)n * R * R);
-        count_launch(3);
+        double *pdot = psq + c.part_stride;
+        int nb = 0;
+        SPTK_TRY(apply_inverse<T>(c, V, 0, I, An, psq, last ? pdot : nullptr, &nb));
+        if (R <= 32) {  // one fused tail: lambda, normalise, Gram partials
+            int nf = (int)std::min<int64_t>(c.nblocks, (I + 31) / 32);
+            const int64_t fpb = (I + nf - 1) / nf;
+            nf = (int)((I + fpb - 1) / fpb);
+            finish_kernel<T><<<nf, 256, sizeof(double) * (R + 32 * R), c.s>>>(
+                An, I, R, fpb, psq, nb, w.gpart.as<double>(), lam);
+            reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(
+                w.gpart.as<double>(), nf, R * R, w.G.as<double>() + (int64_t)n * R * R);
+            count_launch(2);
+        } else {        // large R: reduce, normalise, tiled Gram
+            double *colsq = w.colsq.as<double>();
+            reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(psq, nb, R, colsq);
+            normalize_kernel<T><<<grid_for(std::max<int64_t>(I, 1) * R), 256, 0, c.s>>>(
+                An, 0, I, R, colsq, lam);
+            count_launch(2);
+            SPTK_CUDA(cudaGetLastError());
+            SPTK_TRY(gram<T>(c, n, w.gpart.as<double>()));
+        }
         if (last) {
             double *dot = w.colsq.as<double>() + R;
             reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(pdot, nb, R, dot);
@@ -496,17 +682,13 @@ static sptk_status als_iteration(AlsCtx &c, double *fit_host, int *status_host) 
         T *An = static_cast<T *>(c.A[n]);
         const int64_t rows = r1 - r0;
         if (rows > 0) {
-            const int lanes = 256 / R;
-            int nb = (int)std::min<int64_t>(c.nb_row, (rows + 4 * lanes - 1) / (4 * lanes));
-            if (nb < 1) nb = 1;
-            const int64_t rpb = (rows + nb - 1) / nb;
-            nb = (int)((rows + rpb - 1) / rpb);
-            double *pdot = w.partial.as<double>() + (size_t)c.nb_row * R;
-            apply_inv_kernel<T><<<nb, 256, sizeof(double) * (R * R + 512), c.s>>>(
-                V, r0, r1, R, rpb, Ginv, An, w.partial.as<double>(), last ? pdot : nullptr);
+            double *pdot = w.partial.as<double>() + c.part_stride;
+            int nb = 0;
+            SPTK_TRY(apply_inverse<T>(c, V, r0, r1, An, w.partial.as<double>(),
+                                      last ? pdot : nullptr, &nb));
             reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(w.partial.as<double>(), nb, R,
                                                                 colsq);
-            count_launch(2);
+            count_launch();
             if (last) {
                 reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(pdot, nb, R, colsq + R);
                 count_launch();
@@ -561,8 +743,12 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     SPTK_TRY(w.V.reserve(es * Imax * R));
     SPTK_TRY(w.G.reserve(sizeof(double) * N * R * R));
     SPTK_TRY(w.L.reserve(sizeof(double) * R * R));  // Gamma^{-1}
+    // R-vector partials: one per block (R <= 32) or per 64-row tile (R > 32)
+    const int64_t nparts_max =
+        R > 32 ? (Imax + kTB - 1) / kTB : std::max<int64_t>(c.nb_row, 1);
+    c.part_stride = (size_t)nparts_max * R;
     SPTK_TRY(w.partial.reserve(sizeof(double) * std::max<size_t>((size_t)c.nblocks * R * R,
-                                                                (size_t)c.nb_row * 2 * R)));
+                                                                2 * c.part_stride)));
     SPTK_TRY(w.colsq.reserve(sizeof(double) * 2 * R));
     SPTK_TRY(w.lam.reserve(sizeof(double) * R));
     SPTK_TRY(w.scal.reserve(sizeof(double) * 16));

@@ -521,3 +521,36 @@ def test_mttkrp_atomic_variant(sp, dtype, dims, R, offset):
         Vo = oracle.mttkrp(dims, idx, vals.astype(np.float64), [a.astype(np.float64) for a in A], n,
                            lam=lam.astype(np.float64))
         assert rel(out.double().cpu().numpy(), Vo) <= TOL[dtype], n
+
+
+@pytest.mark.parametrize("R", [40, 100])
+def test_cp_als_large_rank_tiled_glue(sp, R):
+    """R > 32 takes the register-blocked glue (tiled V Gamma^{-1} and Gram)."""
+    dims = (120, 130, 140)
+    idx, vals = synth.unique_tensor(33, dims, 30000)
+    t = make(sp, dims, idx, vals)
+    F = [torch.empty(I, R, dtype=torch.float64, device="cuda") for I in dims]
+    res = sp.cp_als(t, R, 6, F, seed=34)
+    ref = oracle.cp_als(dims, idx, vals, factors_np(34, dims, R), 6)
+    assert np.max(np.abs(res["trace"] - ref["trace"])) <= 1e-8
+    for m in range(3):
+        assert rel(F[m].cpu().numpy(), ref["A"][m]) <= 1e-6
+
+
+def test_cp_als_large_rank_sharded_path(sp, monkeypatch):
+    """R > 32 through the sharded (N>1) code path on one rank."""
+    monkeypatch.setenv("SPTK_FORCE_SHARDED", "1")
+    try:
+        comm = sp.comm_create(sp.comm_unique_id(), 1, 0)
+    except sp.SptkError as e:
+        pytest.skip(f"NCCL unavailable: {e}")
+    dims, R = (120, 130, 140), 40
+    idx, vals = synth.unique_tensor(33, dims, 30000)
+    t = make(sp, dims, idx, vals)
+    F = [torch.empty(I, R, dtype=torch.float64, device="cuda") for I in dims]
+    res = sp.cp_als(t, R, 6, F, seed=34, comm=comm)
+    ref = oracle.cp_als(dims, idx, vals, factors_np(34, dims, R), 6)
+    assert np.max(np.abs(res["trace"] - ref["trace"])) <= 1e-8
+    for m in range(3):
+        assert rel(F[m].cpu().numpy(), ref["A"][m]) <= 1e-6
+    comm.close()
