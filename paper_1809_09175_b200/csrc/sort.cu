@@ -66,19 +66,30 @@ __global__ void __launch_bounds__(kSortThreads)
         counts[(size_t)d * ntiles + blockIdx.x] = hist[d];
 }
 
-// vals_in == NULL: the values are the positions i (first pass)
+// vals_in == NULL: the values are the positions i (first pass).
+// Stable tile-local ranking (warp w owns keys [w*512, w*512+512) of the 4096-
+// key tile; __match_any_sync ranks equal digits within each round of 32, in
+// storage order), then the tile is reordered by digit in shared memory and
+// written out so that consecutive threads write consecutive positions of each
+// digit's run (coalesced), global run start = scanned count of (digit, tile).
 __global__ void __launch_bounds__(kSortThreads)
     radix_downsweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
                     uint32_t P, int shift, int dbits, uint32_t ntiles,
                     const uint32_t *__restrict__ offsets, uint32_t *__restrict__ keys_out,
                     uint32_t *__restrict__ vals_out) {
     __shared__ uint32_t whist[kSortWarps][256];
+    __shared__ uint32_t lstart[256];   // tile-local start of each digit
+    __shared__ uint32_t gstart[256];   // global start of each digit's run of this tile
+    __shared__ uint32_t skey[kSortTile];
+    __shared__ uint32_t sval[kSortTile];
     const int nd = 1 << dbits;
     const uint32_t mask = (uint32_t)nd - 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int d = lane; d < nd; d += 32) whist[warp][d] = 0;
     __syncwarp();
-    const uint32_t base = blockIdx.x * (uint32_t)kSortTile + warp * (uint32_t)kWarpChunk;
+    const uint32_t tile0 = blockIdx.x * (uint32_t)kSortTile;
+    const uint32_t tile_n = min((uint32_t)kSortTile, P - tile0);
+    const uint32_t base = tile0 + warp * (uint32_t)kWarpChunk;
     const uint32_t lt = lanemask_lt();
     uint32_t key[kSortItems];
 #pragma unroll
@@ -96,18 +107,38 @@ __global__ void __launch_bounds__(kSortThreads)
         __syncwarp();
     }
     __syncthreads();
-    // B: per-warp starting offsets = tile offset + earlier warps' counts
-    for (int d = threadIdx.x; d < nd; d += blockDim.x) {
-        uint32_t run = offsets[(size_t)d * ntiles + blockIdx.x];
+    // B: tile-local digit starts (exclusive scan over digits of the tile counts)
+    //    and per-warp starts within each digit
+    {
+        const int d = threadIdx.x;  // kSortThreads == 256 >= nd
+        uint32_t tot = 0;
+        if (d < nd) {
+            uint32_t run = 0;
 #pragma unroll
-        for (int w = 0; w < kSortWarps; ++w) {
-            const uint32_t c = whist[w][d];
-            whist[w][d] = run;
-            run += c;
+            for (int w = 0; w < kSortWarps; ++w) {
+                const uint32_t c = whist[w][d];
+                whist[w][d] = run;  // offset of warp w within digit d
+                run += c;
+            }
+            tot = run;
+            gstart[d] = offsets[(size_t)d * ntiles + blockIdx.x];
         }
+        // exclusive scan of tot over d (block-wide, 256 threads)
+        uint32_t inc = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        __shared__ uint32_t wsum[kSortWarps];
+        if (lane == 31) wsum[warp] = inc;
+        __syncthreads();
+        uint32_t wpre = 0;
+        for (int w = 0; w < warp; ++w) wpre += wsum[w];
+        if (d < nd) lstart[d] = wpre + inc - tot;
     }
     __syncthreads();
-    // C: stable scatter, rounds in storage order (values loaded here)
+    // C: stable local positions, scatter into shared memory (rounds in storage order)
 #pragma unroll
     for (int r = 0; r < kSortItems; ++r) {
         const uint32_t i = base + r * 32 + lane;
@@ -115,14 +146,23 @@ __global__ void __launch_bounds__(kSortThreads)
         const uint32_t digit = valid ? (key[r] >> shift) & mask : 0xffffffffu;
         const uint32_t peers = __match_any_sync(0xffffffffu, digit);
         uint32_t pos = 0;
-        if (valid) pos = whist[warp][digit] + __popc(peers & lt);
+        if (valid) pos = lstart[digit] + whist[warp][digit] + __popc(peers & lt);
         __syncwarp();
         if (valid && (peers & lt) == 0) whist[warp][digit] += __popc(peers);
         __syncwarp();
         if (valid) {
-            keys_out[pos] = key[r];
-            vals_out[pos] = vals_in ? __ldg(vals_in + i) : i;
+            skey[pos] = key[r];
+            sval[pos] = vals_in ? __ldg(vals_in + i) : i;
         }
+    }
+    __syncthreads();
+    // D: coalesced write-out of the digit runs
+    for (uint32_t j = threadIdx.x; j < tile_n; j += kSortThreads) {
+        const uint32_t k = skey[j];
+        const uint32_t d = (k >> shift) & mask;
+        const uint32_t g = gstart[d] + (j - lstart[d]);
+        keys_out[g] = k;
+        vals_out[g] = sval[j];
     }
 }
 
