@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(256) row_gather(const double *A, int64_t rows,
 // L2-resident tables.  COOP=false: each 4-lane group walks its own
 // contiguous run (as mttkrp_fast_kernel); COOP=true: the 8 groups of a warp
 // take 8 consecutive records per step (one 256 B coalesced record load).
-template <bool COOP>
+template <bool COOP, int WINDOW = 0>
 __global__ void __launch_bounds__(256, 3) stream_gather(const uint8_t *rec, int64_t n,
                                                         const double *A1, const double *A2,
                                                         int64_t run, double *out) {
@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(256, 3) stream_gather(const uint8_t *rec, int6
                          : "l"(A1 + (uint64_t)(r[u][3] % 9200u) * 16 + q * 4));
             asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
                          : "=d"(f[u][1][0]), "=d"(f[u][1][1]), "=d"(f[u][1][2]), "=d"(f[u][1][3])
-                         : "l"(A2 + (uint64_t)(r[u][4] % 28800u) * 16 + q * 4));
+                         : "l"(A2 + (WINDOW ? (uint64_t)((blockIdx.x % 148) * WINDOW + r[u][4] % WINDOW)
+                                            : (uint64_t)(r[u][4] % 28800u)) * 16 + q * 4));
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u)
@@ -235,6 +236,10 @@ int main() {
         const int64_t warps = (n + run * 8 - 1) / (run * 8);
         snprintf(name, sizeof name, "mttkrp-shaped: warp-cooperative (run=%ld/group)", (long)run);
         time_it([&] { stream_gather<true><<<(unsigned)((warps * 32 + 255) / 256), 256>>>(rec, n, T1, T2, run, (double *)out); }, name, mb);
+        snprintf(name, sizeof name, "  ... A2 rows from a 195-row window per block (run=%ld)", (long)run);
+        time_it([&] { stream_gather<true, 195><<<(unsigned)((warps * 32 + 255) / 256), 256>>>(rec, n, T1, T2, run, (double *)out); }, name, mb);
+        snprintf(name, sizeof name, "  ... A2 rows from a 32-row window per block (run=%ld)", (long)run);
+        time_it([&] { stream_gather<true, 32><<<(unsigned)((warps * 32 + 255) / 256), 256>>>(rec, n, T1, T2, run, (double *)out); }, name, mb);
     }
     const int64_t ng = 154000000;  // 77M nnz x 2 gathered rows
     const double gb = (double)ng * 128;
