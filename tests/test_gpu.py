@@ -554,3 +554,32 @@ def test_cp_als_large_rank_sharded_path(sp, monkeypatch):
     for m in range(3):
         assert rel(F[m].cpu().numpy(), ref["A"][m]) <= 1e-6
     comm.close()
+
+
+def test_mttkrp_property_random_shapes(sp):
+    """Property sweep: random N in 1..6, dims (incl. length-1 and
+    -2 modes), P in {0, 1, 2, ragged}, R in 1..70, dtype, distribution, layout
+    -- every mode against the oracle."""
+    hyp = pytest.importorskip("hypothesis")
+    from hypothesis import given, settings, strategies as st
+
+    @settings(max_examples=40, deadline=None, derandomize=True)
+    @given(st.integers(1, 6), st.integers(0, 2**31 - 1), st.sampled_from([0, 1, 2, 37, 4096 + 5, 9000]),
+           st.integers(1, 70), st.booleans(), st.booleans(), st.booleans())
+    def run(N, seed, P, R, f32, powerlaw, pg):
+        rng = np.random.default_rng(seed)
+        dims = tuple(int(x) for x in rng.choice([1, 2, 3, 17, 64, 300, 5000], size=N))
+        idx, vals = synth.tensor(seed % 10007, dims, P, "powerlaw" if powerlaw else "uniform")
+        dtype = torch.float32 if f32 else torch.float64
+        npd = np.float32 if f32 else np.float64
+        vals = vals.astype(npd)
+        A = factors_np(seed % 977, dims, R, npd)
+        t = make(sp, dims, idx, vals, dtype, perm_gather=pg)
+        sp.build_perm(t, -1)
+        for n in range(N):
+            V = gpu_mttkrp(sp, t, n, A, R, dtype)
+            Vo = oracle.mttkrp(dims, idx, vals.astype(np.float64),
+                               [a.astype(np.float64) for a in A], n)
+            assert rel(V, Vo) <= TOL[dtype], (dims, P, R, n)
+
+    run()

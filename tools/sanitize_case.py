@@ -1,0 +1,35 @@
+"""Small end-to-end case for compute-sanitizer (one tool per run): create,
+build_perm, every MTTKRP path (permuted copy per-group / warp-cooperative,
+perm-gather, generic, atomic, row shards) and CP-ALS (R=8 and R=40)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1809_09175_b200 as sp  # noqa: E402
+import synth  # noqa: E402
+
+dims = (300, 40, 7)
+idx, vals = synth.tensor(91, dims, 3 * 4096 + 77, "powerlaw")
+for pg in (False, True):
+    t = sp.sptensor_create(dims, torch.from_numpy(idx.astype(np.int64)).cuda(),
+                           torch.from_numpy(vals).cuda(), perm_gather=pg)
+    sp.build_perm(t, -1)
+    for R in (8, 16, 17, 40):
+        A = [torch.rand(I, R, dtype=torch.float64, device="cuda") for I in dims]
+        for n in range(3):
+            out = torch.empty(dims[n], R, dtype=torch.float64, device="cuda")
+            for v in (0, 1):
+                sp.set_tuning(v, 0)
+                sp.mttkrp(t, n, A, out)
+            sp.set_tuning(-2, -2)
+            sp.mttkrp_atomic(t, n, A, out)
+            sp.mttkrp_rows(t, n, A, out, 0, dims[n] // 2)
+            sp.mttkrp_rows(t, n, A, out, dims[n] // 2, dims[n])
+    for R in (8, 40):
+        F = [torch.empty(I, R, dtype=torch.float64, device="cuda") for I in dims]
+        sp.cp_als(t, R, 5, F, seed=1)
+    torch.cuda.synchronize()
+print("sanitize case done")
