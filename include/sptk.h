@@ -48,7 +48,14 @@ enum {
      * discipline, same result; DESIGN.md §4 gives the measured reason (a
      * random 32 B record read costs a 128 B HBM line on B200).  If the copy
      * cannot be allocated the mode silently uses the perm-gather traversal. */
-    SPTK_CREATE_PERM_GATHER = 2
+    SPTK_CREATE_PERM_GATHER = 2,
+    /* Bit-reproducible MTTKRP (and hence CP-ALS): the rows a worker shares
+     * with its neighbours are not flushed with atomics but written to a
+     * scratch slot and summed in worker order by a fix-up kernel (SURVEY
+     * §8(f) NEXT-3).  Supported on the permuted-copy fast path (N in 3..5,
+     * R a multiple of 32/sizeof(value), 32-byte aligned factors); other
+     * calls on such a tensor return SPTK_EUNSUPPORTED. */
+    SPTK_CREATE_DETERMINISTIC = 4
 };
 typedef enum { SPTK_IDX_I64 = 1, SPTK_IDX_U32 = 2 } sptk_idx_type;
 
@@ -85,7 +92,8 @@ const char *sptk_last_error(void);
  *   idx      device or host, nnz x nmodes row-major, 0-based; element type
  *            itype (int64 or uint32).  May be NULL iff nnz == 0.
  *   vals     device or host, nnz values of `dtype`.  NULL iff nnz == 0.
- *   flags    SPTK_CREATE_DEFAULT or SPTK_CREATE_PERM_GATHER (see above).
+ *   flags    SPTK_CREATE_DEFAULT, or SPTK_CREATE_PERM_GATHER or
+ *            SPTK_CREATE_DETERMINISTIC (see above; mutually exclusive).
  *            Duplicate coordinates are always allowed (MTTKRP is linear in X;
  *            DESIGN.md Z3).
  *   out      receives the handle

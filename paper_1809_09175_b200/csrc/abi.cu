@@ -144,8 +144,10 @@ sptk_status sptk_sptensor_create(int nmodes, const int64_t *dims, int64_t nnz, c
     if (nnz >= (int64_t(1) << 32)) return fail(SPTK_EUNSUPPORTED, "nnz must be < 2^32");
     if (dtype != SPTK_F32 && dtype != SPTK_F64) return fail(SPTK_EINVAL, "bad dtype");
     if (itype != SPTK_IDX_I64 && itype != SPTK_IDX_U32) return fail(SPTK_EINVAL, "bad idx type");
-    if (flags & ~(unsigned)SPTK_CREATE_PERM_GATHER)
+    if (flags & ~(unsigned)(SPTK_CREATE_PERM_GATHER | SPTK_CREATE_DETERMINISTIC))
         return fail(SPTK_EUNSUPPORTED, "unknown create flag");
+    if ((flags & SPTK_CREATE_PERM_GATHER) && (flags & SPTK_CREATE_DETERMINISTIC))
+        return fail(SPTK_EINVAL, "PERM_GATHER and DETERMINISTIC are mutually exclusive");
     if (nnz > 0 && (!idx || !vals)) return fail(SPTK_EINVAL, "idx/vals NULL with nnz > 0");
 
     cudaStream_t s = (cudaStream_t)stream;
@@ -157,6 +159,7 @@ sptk_status sptk_sptensor_create(int nmodes, const int64_t *dims, int64_t nnz, c
     t->dtype = dtype;
     t->rec_bytes = record_bytes(dtype, nmodes);
     t->perm_gather_only = (flags & SPTK_CREATE_PERM_GATHER) != 0;
+    t->deterministic = (flags & SPTK_CREATE_DETERMINISTIC) != 0;
     cudaGetDevice(&t->device);
 
     sptk_status st = SPTK_OK;

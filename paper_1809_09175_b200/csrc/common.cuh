@@ -107,6 +107,8 @@ struct sptk_tensor_s {
     bool has_srec[sptk::kMaxModes] = {false};
     sptk::DevBuf wrow[sptk::kMaxModes];         // worker start rows for the copy (cached)
     sptk::DevBuf sortws;                        // radix-sort workspace (cached)
+    bool deterministic = false;                 // SPTK_CREATE_DETERMINISTIC
+    sptk::DevBuf det_row, det_part;             // boundary-row partials (deterministic mode)
     int64_t wrow_key[sptk::kMaxModes][3] = {{-1, -1, -1}};  // (pos_begin, pos_end, run)
     bool perm_gather_only = false;              // SPTK_CREATE_PERM_GATHER
     std::vector<uint32_t> host_rowptr[sptk::kMaxModes];  // for partitioning (lazy)

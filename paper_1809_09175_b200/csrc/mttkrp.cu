@@ -66,6 +66,60 @@ sptk_status host_rowptr(sptk_tensor t, int mode, cudaStream_t s) {
     return SPTK_OK;
 }
 
+// Deterministic mode: sum the boundary-row partials (entries 2w, 2w+1, in
+// worker order = row order) per row and store them.  One warp per segment
+// head; lanes split the segment's entries (fixed assignment) and the sums are
+// combined with a fixed shuffle tree, so the result does not depend on timing.
+template <typename T>
+__global__ void det_fixup_kernel(const uint32_t *__restrict__ drow, const T *__restrict__ dpart,
+                                 int64_t nent, int R, T *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < nent; k += nw) {
+        const uint32_t row = drow[k];
+        if (row == kNoRow) continue;
+        uint32_t prev = kNoRow;
+        if (k > 0) prev = drow[k - 1];
+        if (prev == kNoRow && k > 1) prev = drow[k - 2];
+        if (prev == row) continue;  // not the first entry of its row
+        // segment end: first valid entry with another row
+        int64_t e = k + 1;
+        for (;; e += 32) {
+            const int64_t j = e + lane;
+            const bool stop = j >= nent || (drow[j] != kNoRow && drow[j] != row);
+            const uint32_t b = __ballot_sync(0xffffffffu, stop);
+            if (b) {
+                e += __ffs(b) - 1;
+                break;
+            }
+        }
+        for (int c0 = 0; c0 < R; c0 += 16) {
+            double acc[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+            for (int64_t q = k + lane; q < e; q += 32) {
+                if (drow[q] != row) continue;
+                const T *p = dpart + q * R + c0;
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < R) acc[j] += (double)p[j];
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+            }
+            if (lane < 16 && c0 + lane < R) {
+                double v = 0.0;
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (j == lane) v = acc[j];
+                out[(int64_t)row * R + c0 + lane] = (T)v;
+            }
+        }
+    }
+}
+
 // start row of every worker: the largest r with rowptr[r] <= s (binary search)
 __global__ void worker_rows_kernel(const uint32_t *__restrict__ rowptr, int64_t In, int64_t pb,
                                    int64_t run, int64_t nworkers, uint32_t *__restrict__ wrow) {
@@ -148,6 +202,16 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     }
     const int64_t chunk = var == 1 ? a.run * (32 / G0) : a.run;
     const int64_t workers = (pe - pb + chunk - 1) / chunk;
+    if (t->deterministic && !(fast && t->has_srec[mode]))
+        return fail(SPTK_EUNSUPPORTED,
+                    "deterministic MTTKRP needs the permuted-copy fast path (N in 3..5, R a "
+                    "multiple of 32/sizeof(value), 32-byte aligned factors/out/lambda)");
+    if (t->deterministic) {
+        SPTK_TRY(t->det_row.reserve(sizeof(uint32_t) * 2 * workers));
+        SPTK_TRY(t->det_part.reserve(es * 2 * workers * R));
+        a.drow = t->det_row.as<uint32_t>();
+        a.dpart = t->det_part.p;
+    }
     if (fast && t->has_srec[mode]) {  // stream the compact permuted copy instead
         SPTK_TRY(worker_rows(t, mode, pb, pe, chunk, workers, s));
         a.rec = t->srec[mode].as<uint8_t>();
@@ -176,6 +240,19 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
             if (t->dtype == SPTK_F64) SPTK_TRY(launch_generic<double>(G, a, workers, s));
             else SPTK_TRY(launch_generic<float>(G, a, workers, s));
         }
+    }
+    if (t->deterministic) {
+        const int64_t nent = 2 * workers;
+        int64_t blocks = (nent * 32 + 255) / 256;
+        if (blocks > (int64_t)dev_sms() * 16) blocks = (int64_t)dev_sms() * 16;
+        if (t->dtype == SPTK_F64)
+            det_fixup_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(
+                a.drow, static_cast<const double *>(a.dpart), nent, (int)R, static_cast<double *>(out));
+        else
+            det_fixup_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(
+                a.drow, static_cast<const float *>(a.dpart), nent, (int)R, static_cast<float *>(out));
+        count_launch();
+        SPTK_CUDA(cudaGetLastError());
     }
     SPTK_TRY(mttkrp_span_end(s, ev));
     return SPTK_OK;

@@ -48,6 +48,12 @@ struct MttkrpArgs {
     const void *A[kMaxModes];    // factor matrices (A[mode] unused)
     const void *lambda;          // NULL = ones
     void *out;
+    // deterministic mode (permuted copy only): boundary-row partials go to
+    // dpart[(2 w + slot) * ld + col] / drow[2 w + slot] instead of red.add
+    // (slot 0: the worker's first row if it ends inside the block, slot 1: its
+    // last row) and are summed in worker order by det_fixup_kernel
+    uint32_t *drow;
+    void *dpart;
 };
 
 // ----------------------------------------------------------------- loads
@@ -137,7 +143,10 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
     for (int v = 0; v < V; ++v) acc[v] = T(0);
     uint32_t cur = kNoRow, first = kNoRow;
 
-    auto flush = [&](uint32_t row, bool atomic) {
+    bool wrote0 = false;  // deterministic mode: slot 0 used
+    auto flush = [&](uint32_t row, bool atomic, int slot) {
+        if (atomic && a.dpart && q == 0) a.drow[2 * worker + slot] = row;
+        if (atomic && slot == 0) wrote0 = true;
         if (!lane_on) return;
         T o[V];
 #pragma unroll
@@ -148,9 +157,12 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
 #pragma unroll
             for (int v = 0; v < V; ++v) o[v] *= lam[v];
         }
-        T *dst = out + (int64_t)row * a.ld + c;
-        if (atomic) red_row(dst, o);
-        else st_row(dst, o);
+        if (atomic && a.dpart)
+            st_row(static_cast<T *>(a.dpart) + (2 * worker + slot) * a.ld + c, o);
+        else if (atomic)
+            red_row(out + (int64_t)row * a.ld + c, o);
+        else
+            st_row(out + (int64_t)row * a.ld + c, o);
     };
     auto load_rec = [&](uint32_t pos, uint32_t (&r)[8]) {
         if constexpr (RB == 32) ld_rec32(rec + (size_t)pos * 32, r);
@@ -234,7 +246,7 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
                 r = w[u][OFF + MODE];
             }
             if (r != cur) {
-                if (cur != kNoRow) flush(cur, cur == first);
+                if (cur != kNoRow) flush(cur, cur == first, 0);
 #pragma unroll
                 for (int v = 0; v < V; ++v) acc[v] = T(0);
                 if (first == kNoRow) first = r;
@@ -251,7 +263,8 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
             }
         }
     }
-    if (cur != kNoRow) flush(cur, true);
+    if (cur != kNoRow) flush(cur, true, 1);
+    if (a.dpart && !wrote0 && q == 0) a.drow[2 * worker] = kNoRow;
 }
 
 template <typename T, int N, int G, int U, int RB, bool SORTED, int MINB>
@@ -293,8 +306,12 @@ __device__ __forceinline__ void mttkrp_coop_body(const MttkrpArgs &a) {
     const uint8_t *__restrict__ rec = a.rec;
     T *__restrict__ out = static_cast<T *>(a.out);
 
-    auto flush = [&](uint32_t row, const T (&val)[V], bool atomic) {
-        if (g != 0 || !lane_on) return;
+    bool wrote0 = false;  // deterministic mode: slot 0 used
+    auto flush = [&](uint32_t row, const T (&val)[V], bool atomic, int slot) {
+        if (atomic && slot == 0) wrote0 = true;
+        if (g != 0) return;
+        if (atomic && a.dpart && q == 0) a.drow[2 * warp_id + slot] = row;
+        if (!lane_on) return;
         T o[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) o[v] = val[v];
@@ -304,9 +321,12 @@ __device__ __forceinline__ void mttkrp_coop_body(const MttkrpArgs &a) {
 #pragma unroll
             for (int v = 0; v < V; ++v) o[v] *= lam[v];
         }
-        T *dst = out + (int64_t)row * a.ld + c;
-        if (atomic) red_row(dst, o);
-        else st_row(dst, o);
+        if (atomic && a.dpart)
+            st_row(static_cast<T *>(a.dpart) + (2 * warp_id + slot) * a.ld + c, o);
+        else if (atomic)
+            red_row(out + (int64_t)row * a.ld + c, o);
+        else
+            st_row(out + (int64_t)row * a.ld + c, o);
     };
     auto load_rec = [&](uint32_t pos, uint32_t (&r)[8]) {
         if constexpr (RB == 32) ld_rec32(rec + (size_t)pos * 32, r);
@@ -389,7 +409,7 @@ __device__ __forceinline__ void mttkrp_coop_body(const MttkrpArgs &a) {
                 const uint32_t pos = base + u * NG + gg;
                 if (pos >= e) break;
                 if (pos >= nxt) {
-                    flush(row, tot, row == first);
+                    flush(row, tot, row == first, 0);
 #pragma unroll
                     for (int v = 0; v < V; ++v) tot[v] = T(0);
                     do {
@@ -414,7 +434,8 @@ __device__ __forceinline__ void mttkrp_coop_body(const MttkrpArgs &a) {
         for (int o = G; o < 32; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
         tot[v] = x;
     }
-    flush(row, tot, true);
+    flush(row, tot, true, 1);
+    if (a.dpart && !wrote0 && lane == 0) a.drow[2 * warp_id] = kNoRow;
 }
 
 template <typename T, int N, int G, int U, int RB, int MINB>

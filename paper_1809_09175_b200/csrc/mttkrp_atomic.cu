@@ -129,6 +129,8 @@ extern "C" sptk_status sptk_mttkrp_atomic(sptk_tensor t, int mode, int64_t R,
     if (!factors || !out) return fail(SPTK_EINVAL, "factors/out is NULL");
     for (int m = 0; m < t->N; ++m)
         if (m != mode && !factors[m]) return fail(SPTK_EINVAL, "factors[m] is NULL");
+    if (t->deterministic)
+        return fail(SPTK_EUNSUPPORTED, "the atomic-per-nonzero MTTKRP is not deterministic");
     cudaStream_t s = (cudaStream_t)stream;
     const size_t es = dtype_bytes(t->dtype);
     sptk_status st = SPTK_OK;

@@ -583,3 +583,39 @@ def test_mttkrp_property_random_shapes(sp):
             assert rel(V, Vo) <= TOL[dtype], (dims, P, R, n)
 
     run()
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_deterministic_mode_bitwise(sp, variant, dtype):
+    """SPTK_CREATE_DETERMINISTIC: boundary rows summed in worker order ->
+    repeated runs are bit-identical; values match the oracle; CP-ALS too."""
+    dims = (3000, 200, 64)
+    idx, vals = synth.tensor(61, dims, 40 * 4096 + 9, "powerlaw")   # hot rows span many workers
+    npd = np.float64 if dtype == torch.float64 else np.float32
+    vals = vals.astype(npd)
+    R = 16
+    A = factors_np(62, dims, R, npd)
+    t = sp.sptensor_create(dims, dev(idx.astype(np.int64)), dev(vals, dtype), deterministic=True)
+    sp.build_perm(t, -1)
+    try:
+        sp.set_tuning(variant, 16)
+        for n in range(3):
+            V1 = gpu_mttkrp(sp, t, n, A, R, dtype)
+            V2 = gpu_mttkrp(sp, t, n, A, R, dtype)
+            assert np.array_equal(V1, V2), n
+            Vo = oracle.mttkrp(dims, idx, vals.astype(np.float64), [a.astype(np.float64) for a in A], n,
+                               acc_long=True)
+            assert rel(V1, Vo) <= TOL[dtype], n
+    finally:
+        sp.set_tuning(-2, -2)
+    if dtype == torch.float64:
+        F1 = [torch.empty(I, R, dtype=dtype, device="cuda") for I in dims]
+        F2 = [torch.empty(I, R, dtype=dtype, device="cuda") for I in dims]
+        r1 = sp.cp_als(t, R, 5, F1, seed=3)
+        r2 = sp.cp_als(t, R, 5, F2, seed=3)
+        assert np.array_equal(r1["trace"], r2["trace"])
+        assert all(torch.equal(F1[m], F2[m]) for m in range(3))
+    with pytest.raises(sp.SptkError) as e:
+        gpu_mttkrp(sp, t, 0, factors_np(63, dims, 17, npd), 17, dtype)   # generic path
+    assert e.value.name == "EUNSUPPORTED"
