@@ -55,7 +55,15 @@ enum {
      * §8(f) NEXT-3).  Supported on the permuted-copy fast path (N in 3..5,
      * R a multiple of 32/sizeof(value), 32-byte aligned factors); other
      * calls on such a tensor return SPTK_EUNSUPPORTED. */
-    SPTK_CREATE_DETERMINISTIC = 4
+    SPTK_CREATE_DETERMINISTIC = 4,
+    /* Duplicate-coordinate policy (default: duplicates kept, MTTKRP
+     * is linear in X).  DUP_SUM merges equal coordinates into one nonzero at
+     * the position of the first occurrence with the values summed in storage
+     * order (the tensor's nnz shrinks accordingly); DUP_ERROR fails with
+     * SPTK_EDUP if any coordinate repeats.  Both use an on-GPU lexicographic
+     * stable sort (one radix sort per mode, last mode first). */
+    SPTK_CREATE_DUP_SUM = 8,
+    SPTK_CREATE_DUP_ERROR = 16
 };
 typedef enum { SPTK_IDX_I64 = 1, SPTK_IDX_U32 = 2 } sptk_idx_type;
 
@@ -63,7 +71,7 @@ typedef enum {
     SPTK_OK = 0,
     SPTK_EINVAL = 1,       /* bad argument (null pointer, dtype mismatch, shape) */
     SPTK_ERANGE = 2,       /* a coordinate >= dims[m] (or < 0) */
-    SPTK_EDUP = 3,         /* reserved: duplicate coordinate under a DUP_ERROR policy */
+    SPTK_EDUP = 3,         /* duplicate coordinate under SPTK_CREATE_DUP_ERROR */
     SPTK_ENOPERM = 4,      /* sptk_build_perm(mode) has not been run */
     SPTK_ENOMEM = 5,       /* device allocation failed */
     SPTK_ECUDA = 6,        /* CUDA runtime error (handle poisoned) */
@@ -93,7 +101,8 @@ const char *sptk_last_error(void);
  *            itype (int64 or uint32).  May be NULL iff nnz == 0.
  *   vals     device or host, nnz values of `dtype`.  NULL iff nnz == 0.
  *   flags    SPTK_CREATE_DEFAULT, or SPTK_CREATE_PERM_GATHER or
- *            SPTK_CREATE_DETERMINISTIC (see above; mutually exclusive).
+ *            SPTK_CREATE_DETERMINISTIC (mutually exclusive), optionally OR-ed
+ *            with one of SPTK_CREATE_DUP_SUM / SPTK_CREATE_DUP_ERROR.
  *            Duplicate coordinates are always allowed (MTTKRP is linear in X;
  *            DESIGN.md Z3).
  *   out      receives the handle

@@ -61,6 +61,7 @@ def lib():
         L.oracle_normalize.argtypes = [i64, i64, p, p]
         L.oracle_normalize.restype = None
         L.oracle_cp_als.argtypes = [i32, p, i64, p, p, i64, i32, dbl, p, p, p, p, p]
+        L.oracle_merge_duplicates.argtypes = [i64, i32, p, p, p, p, p]
         _lib = L
     return _lib
 
@@ -189,3 +190,16 @@ def cp_als(dims, idx, vals, init, max_iters: int, tol: float = 0.0):
                                _ptr(trace)), "oracle_cp_als")
     return {"A": arrs, "lam": lam, "fit": fit.value, "iters": iters.value,
             "trace": trace[: iters.value]}
+
+
+def merge_duplicates(idx, vals):
+    """Sum duplicate coordinates (first-occurrence position, storage-order sum)."""
+    idx = _idx(idx)
+    P, N = idx.shape
+    vals = np.ascontiguousarray(vals, dtype=np.float64)
+    io = np.empty_like(idx)
+    vo = np.empty_like(vals)
+    Pout = C.c_int64(0)
+    _check(lib().oracle_merge_duplicates(P, N, _ptr(idx), _ptr(vals), _ptr(io), _ptr(vo),
+                                         C.byref(Pout)), "oracle_merge_duplicates")
+    return io[: Pout.value], vo[: Pout.value]

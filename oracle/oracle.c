@@ -20,6 +20,8 @@
  *                                                    -> planted recovery, rank-1,
  *                                                       monotone residual, dense fit
  *   oracle_gram / oracle_chol_solve / oracle_normalize -> SPEC examples S:162
+ *   oracle_merge_duplicates  merge-sum     -> SPEC example S:56, dense
+ *                                                       equality (np.add.at), first-occurrence order
  */
 #include <math.h>
 #include <stdint.h>
@@ -360,4 +362,60 @@ done:
     if (iters_out) *iters_out = it;
     free(V); free(G); free(Gam);
     return st;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Duplicate merge (SPEC from_coo merge-sum): equal coordinates are
+ * combined into one nonzero whose value is the sum of the run's values in
+ * storage order, kept at the position of the first occurrence; the output
+ * keeps the storage order of first occurrences.  qsort of (coordinates,
+ * position) pairs, then one pass.  Returns the new nnz via *Pout. */
+static int g_merge_N;
+static const uint32_t *g_merge_idx;
+
+static int merge_cmp(const void *pa, const void *pb)
+{
+    const int64_t a = *(const int64_t *)pa, b = *(const int64_t *)pb;
+    for (int m = 0; m < g_merge_N; ++m) {
+        const uint32_t x = g_merge_idx[(size_t)a * g_merge_N + m];
+        const uint32_t y = g_merge_idx[(size_t)b * g_merge_N + m];
+        if (x != y) return x < y ? -1 : 1;
+    }
+    return a < b ? -1 : (a > b ? 1 : 0);
+}
+
+int oracle_merge_duplicates(int64_t P, int N, const uint32_t *idx, const double *vals,
+                            uint32_t *idx_out, double *vals_out, int64_t *Pout)
+{
+    if (P < 0 || N < 1) return OR_EINVAL;
+    int64_t *ord = (int64_t *)malloc(sizeof(int64_t) * (size_t)(P > 0 ? P : 1));
+    char *keep = (char *)calloc((size_t)(P > 0 ? P : 1), 1);
+    double *sum = (double *)malloc(sizeof(double) * (size_t)(P > 0 ? P : 1));
+    if (!ord || !keep || !sum) { free(ord); free(keep); free(sum); return OR_ENOMEM; }
+    for (int64_t i = 0; i < P; ++i) ord[i] = i;
+    g_merge_N = N;
+    g_merge_idx = idx;
+    qsort(ord, (size_t)P, sizeof(int64_t), merge_cmp);
+    for (int64_t i = 0; i < P;) {
+        int64_t j = i + 1;
+        double s = vals[ord[i]];
+        while (j < P && memcmp(idx + (size_t)ord[j] * N, idx + (size_t)ord[i] * N,
+                               sizeof(uint32_t) * (size_t)N) == 0) {
+            s += vals[ord[j]];
+            ++j;
+        }
+        keep[ord[i]] = 1;
+        sum[ord[i]] = s;
+        i = j;
+    }
+    int64_t q = 0;
+    for (int64_t i = 0; i < P; ++i) {
+        if (!keep[i]) continue;
+        memcpy(idx_out + (size_t)q * N, idx + (size_t)i * N, sizeof(uint32_t) * (size_t)N);
+        vals_out[q] = sum[i];
+        ++q;
+    }
+    *Pout = q;
+    free(ord); free(keep); free(sum);
+    return OR_OK;
 }

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libsptk.so")
 F32, F64 = 1, 2
 IDX_I64, IDX_U32 = 1, 2
 CREATE_DEFAULT, CREATE_PERM_GATHER, CREATE_DETERMINISTIC = 0, 2, 4
+CREATE_DUP_SUM, CREATE_DUP_ERROR = 8, 16
 STATUS = {0: "OK", 1: "EINVAL", 2: "ERANGE", 3: "EDUP", 4: "ENOPERM", 5: "ENOMEM",
           6: "ECUDA", 7: "ENCCL", 8: "ESINGULAR", 9: "EZERONORM", 10: "EUNSUPPORTED"}
 CODES = {v: k for k, v in STATUS.items()}
@@ -159,10 +160,12 @@ class SpTensor:
 
 # ------------------------------------------------------------------ API
 def sptensor_create(dims, idx, vals, stream=None, perm_gather: bool = False,
-                    deterministic: bool = False) -> SpTensor:
+                    deterministic: bool = False, duplicates: str = "allow") -> SpTensor:
     """perm_gather=True keeps the paper's literal traversal (gather records
     through perm_n) instead of materialising permuted copies at build_perm;
-    deterministic=True makes MTTKRP / CP-ALS bit-reproducible."""
+    deterministic=True makes MTTKRP / CP-ALS bit-reproducible; duplicates is
+    "allow" (default), "sum" (merge, S:49-57) or "error" (SPTK_EDUP)."""
+    dup = {"allow": 0, "sum": CREATE_DUP_SUM, "error": CREATE_DUP_ERROR}[duplicates]
     dims_a = np.ascontiguousarray(dims, dtype=np.int64)
     nnz = int(vals.shape[0])
     if nnz > 0 and tuple(idx.shape) != (nnz, len(dims_a)):
@@ -172,9 +175,12 @@ def sptensor_create(dims, idx, vals, stream=None, perm_gather: bool = False,
     _check(lib().sptk_sptensor_create(len(dims_a), dims_a.ctypes.data, nnz, _ptr(idx) if nnz else None,
                                       _idx_code(idx), _ptr(vals) if nnz else None, dt,
                                       (CREATE_PERM_GATHER if perm_gather else 0)
-                                      | (CREATE_DETERMINISTIC if deterministic else 0),
+                                      | (CREATE_DETERMINISTIC if deterministic else 0) | dup,
                                       _stream(stream), C.byref(out)), "sptensor_create")
-    return SpTensor(out.value, dims_a, nnz, dt)
+    tt = SpTensor(out.value, dims_a, nnz, dt)
+    if dup:
+        tt.nnz = sptensor_info(tt)["nnz"]
+    return tt
 
 
 def sptensor_info(t: SpTensor):

@@ -144,8 +144,11 @@ sptk_status sptk_sptensor_create(int nmodes, const int64_t *dims, int64_t nnz, c
     if (nnz >= (int64_t(1) << 32)) return fail(SPTK_EUNSUPPORTED, "nnz must be < 2^32");
     if (dtype != SPTK_F32 && dtype != SPTK_F64) return fail(SPTK_EINVAL, "bad dtype");
     if (itype != SPTK_IDX_I64 && itype != SPTK_IDX_U32) return fail(SPTK_EINVAL, "bad idx type");
-    if (flags & ~(unsigned)(SPTK_CREATE_PERM_GATHER | SPTK_CREATE_DETERMINISTIC))
+    if (flags & ~(unsigned)(SPTK_CREATE_PERM_GATHER | SPTK_CREATE_DETERMINISTIC |
+                            SPTK_CREATE_DUP_SUM | SPTK_CREATE_DUP_ERROR))
         return fail(SPTK_EUNSUPPORTED, "unknown create flag");
+    if ((flags & SPTK_CREATE_DUP_SUM) && (flags & SPTK_CREATE_DUP_ERROR))
+        return fail(SPTK_EINVAL, "DUP_SUM and DUP_ERROR are mutually exclusive");
     if ((flags & SPTK_CREATE_PERM_GATHER) && (flags & SPTK_CREATE_DETERMINISTIC))
         return fail(SPTK_EINVAL, "PERM_GATHER and DETERMINISTIC are mutually exclusive");
     if (nnz > 0 && (!idx || !vals)) return fail(SPTK_EINVAL, "idx/vals NULL with nnz > 0");
@@ -208,6 +211,10 @@ sptk_status sptk_sptensor_create(int nmodes, const int64_t *dims, int64_t nnz, c
             goto bad;
         }
         t->normX2 = h.norm;
+        if (flags & (SPTK_CREATE_DUP_SUM | SPTK_CREATE_DUP_ERROR)) {
+            st = merge_duplicates(t, (flags & SPTK_CREATE_DUP_ERROR) != 0, s);
+            if (st != SPTK_OK) goto bad;
+        }
     }
     *out = t;
     return SPTK_OK;

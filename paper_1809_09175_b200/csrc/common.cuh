@@ -149,6 +149,7 @@ sptk_status launch_pack(sptk_tensor t, const void *idx, sptk_idx_type itype, con
                         int *d_flag, double *d_normsq, cudaStream_t s);
 sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s);
 sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s);
+sptk_status merge_duplicates(sptk_tensor t, bool error_only, cudaStream_t s);
 sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const *factors,
                           const void *lambda, void *out, int64_t row_begin, int64_t row_end,
                           cudaStream_t s);

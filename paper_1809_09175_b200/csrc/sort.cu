@@ -381,6 +381,73 @@ static void drop_copies(sptk_tensor t) {
     }
 }
 
+// keys[i] = l_{in[i], mode}: the key of the i-th id of an input order
+__global__ void __launch_bounds__(256) extract_keys_through(const uint8_t *__restrict__ rec, int rb,
+                                                            int kw, const uint32_t *__restrict__ in,
+                                                            int64_t P, uint32_t *__restrict__ keys) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+         i += (int64_t)gridDim.x * blockDim.x)
+        keys[i] = __ldg(reinterpret_cast<const uint32_t *>(rec + (size_t)__ldg(in + i) * rb) + kw);
+}
+
+// Stable LSD radix sort of nonzero ids by l_{., mode}.  `in` is the input
+// order of ids (NULL = storage order 0..P-1); the sorted ids go to `out` (must
+// not alias `in`) and, if keys_out != NULL, the sorted keys to keys_out.
+// Uses the handle's cached workspace.
+static sptk_status stable_sort_ids(sptk_tensor t, int mode, const uint32_t *in, uint32_t *out,
+                                   uint32_t **keys_out, cudaStream_t s) {
+    const int64_t P = t->P, In = t->dims[mode];
+    int bits = 0;
+    while (bits < 32 && ((uint64_t)(In - 1) >> bits) != 0) ++bits;
+    const int npass = bits == 0 ? 1 : (bits + 7) / 8;
+    const int dbits = bits == 0 ? 1 : (bits + npass - 1) / npass;
+    const int64_t ntiles = (P + kSortTile - 1) / kSortTile;
+    // workspace (kept in the handle across calls; a cache like the permuted
+    // copies): keys x2, values, digit counts, scan block sums
+    const size_t nP = (size_t)P, ncnt = (size_t)ntiles * 256;
+    const size_t ws_words = 3 * nP + ncnt + (ncnt + kScanChunk - 1) / kScanChunk + 64;
+    if (t->sortws.reserve(sizeof(uint32_t) * ws_words) != SPTK_OK) {
+        drop_copies(t);  // permuted copies are caches: free them and retry
+        SPTK_TRY(t->sortws.reserve(sizeof(uint32_t) * ws_words));
+    }
+    uint32_t *ws = t->sortws.as<uint32_t>();
+    uint32_t *kA = ws, *kB = ws + nP, *vA = ws + 2 * nP, *counts = ws + 3 * nP;
+    uint32_t *tmp = counts + ncnt;
+    // ping-pong: vals end in `out` after the last pass
+    uint32_t *kbuf[2] = {kA, kB};
+    uint32_t *vbuf[2] = {vA, out};
+    const int kw = dtype_bytes(t->dtype) / 4 + mode;
+    // pass-0 keys: one pass over the records (kbuf of the other parity is free until then)
+    uint32_t *k0 = kbuf[(npass - 1) & 1] == kA ? kB : kA;
+    if (in)
+        extract_keys_through<<<grid_for(P), 256, 0, s>>>(t->rec.as<uint8_t>(), t->rec_bytes, kw, in,
+                                                         P, k0);
+    else
+        extract_keys<<<grid_for(P), 256, 0, s>>>(t->rec.as<uint8_t>(), t->rec_bytes, kw, P, k0);
+    count_launch();
+    SPTK_CUDA(cudaGetLastError());
+    const uint32_t *kin = k0, *vin = in;
+    for (int p = 0; p < npass; ++p) {
+        const int shift = p * dbits;
+        const int db = bits == 0 ? 1 : ((shift + dbits > bits) ? bits - shift : dbits);
+        uint32_t *kout = kbuf[(npass - 1 - p) & 1];
+        uint32_t *vout = vbuf[((npass - 1 - p) & 1) ^ 1];
+        radix_upsweep<<<(unsigned)ntiles, kSortThreads, 0, s>>>(kin, (uint32_t)P, shift, db,
+                                                                (uint32_t)ntiles, counts);
+        count_launch();
+        SPTK_CUDA(cudaGetLastError());
+        SPTK_TRY(exclusive_scan(counts, ntiles * ((int64_t)1 << db), tmp, s));
+        radix_downsweep<<<(unsigned)ntiles, kSortThreads, 0, s>>>(
+            kin, vin, (uint32_t)P, shift, db, (uint32_t)ntiles, counts, kout, vout);
+        count_launch();
+        SPTK_CUDA(cudaGetLastError());
+        kin = kout;
+        vin = vout;
+    }
+    if (keys_out) *keys_out = const_cast<uint32_t *>(kin);
+    return SPTK_OK;
+}
+
 sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s) {
     const int64_t P = t->P, In = t->dims[mode];
     SPTK_TRY(t->perm[mode].reserve(sizeof(uint32_t) * (P > 0 ? P : 1)));
@@ -394,9 +461,7 @@ sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s) {
         t->has_perm[mode] = true;
         return SPTK_OK;
     }
-    int bits = 0;
-    while (bits < 32 && ((uint64_t)(In - 1) >> bits) != 0) ++bits;
-    if (bits == 0) {  // I_n = 1: every key is 0, the stable order is the identity
+    if (In == 1) {  // every key is 0, the stable order is the identity
         iota_kernel<<<grid_for(P), 256, 0, s>>>(perm, P);
         fill_u32<<<1, 32, 0, s>>>(rowptr, 1, 0u);
         fill_u32<<<1, 32, 0, s>>>(rowptr + 1, 1, (uint32_t)P);
@@ -405,56 +470,153 @@ sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s) {
         t->has_perm[mode] = true;
         return SPTK_OK;
     }
-    const int npass = (bits + 7) / 8;
-    const int dbits = (bits + npass - 1) / npass;
-    const int64_t ntiles = (P + kSortTile - 1) / kSortTile;
-    // workspace (kept in the handle across build_perm calls; a cache like the
-    // permuted copies): keys x2, values, digit counts, scan block sums
-    const size_t nP = (size_t)P, ncnt = (size_t)ntiles * 256;
-    const size_t ws_words = 3 * nP + ncnt + (ncnt + kScanChunk - 1) / kScanChunk + 64;
-    if (t->sortws.reserve(sizeof(uint32_t) * ws_words) != SPTK_OK) {
-        drop_copies(t);  // permuted copies are caches: free them and retry
-        SPTK_TRY(t->sortws.reserve(sizeof(uint32_t) * ws_words));
-    }
-    uint32_t *ws = t->sortws.as<uint32_t>();
-    uint32_t *kA = ws, *kB = ws + nP, *vA = ws + 2 * nP, *counts = ws + 3 * nP;
-    uint32_t *tmp = counts + ncnt;
-    // ping-pong: vals end in `perm` after the last pass
-    uint32_t *kin = nullptr, *vin = nullptr;
-    uint32_t *kbuf[2] = {kA, kB};
-    uint32_t *vbuf[2] = {vA, perm};
-    const int kw = dtype_bytes(t->dtype) / 4 + mode;
-    // pass-0 keys: one streaming pass over the records (kbuf[1] is free until then)
-    uint32_t *k0 = kbuf[(npass - 1) & 1] == kA ? kB : kA;
-    extract_keys<<<grid_for(P), 256, 0, s>>>(t->rec.as<uint8_t>(), t->rec_bytes, kw, P, k0);
-    count_launch();
-    SPTK_CUDA(cudaGetLastError());
-    kin = k0;
-    vin = nullptr;
-    for (int p = 0; p < npass; ++p) {
-        const int shift = p * dbits;
-        const int db = (shift + dbits > bits) ? bits - shift : dbits;
-        // vals of the last pass land in `perm`; in/out buffers differ every pass
-        uint32_t *kout = kbuf[(npass - 1 - p) & 1];
-        uint32_t *vout = vbuf[((npass - 1 - p) & 1) ^ 1];
-        radix_upsweep<<<(unsigned)ntiles, kSortThreads, 0, s>>>(kin, (uint32_t)P, shift, db,
-                                                                (uint32_t)ntiles,
-                                                                counts);
-        count_launch();
-        SPTK_CUDA(cudaGetLastError());
-        SPTK_TRY(exclusive_scan(counts, ntiles * ((int64_t)1 << db), tmp, s));
-        radix_downsweep<<<(unsigned)ntiles, kSortThreads, 0, s>>>(
-            kin, vin, (uint32_t)P, shift, db, (uint32_t)ntiles, counts, kout, vout);
-        count_launch();
-        SPTK_CUDA(cudaGetLastError());
-        kin = kout;
-        vin = vout;
-    }
-    // kin = sorted keys, vin = perm
-    rowptr_from_sorted<<<grid_for(In + 1), 256, 0, s>>>(kin, P, In, rowptr);
+    uint32_t *keys = nullptr;
+    SPTK_TRY(stable_sort_ids(t, mode, nullptr, perm, &keys, s));
+    rowptr_from_sorted<<<grid_for(In + 1), 256, 0, s>>>(keys, P, In, rowptr);
     count_launch();
     SPTK_CUDA(cudaGetLastError());
     t->has_perm[mode] = true;
+    return SPTK_OK;
+}
+
+// ------------------------------------------------------------ duplicates
+// Coordinates of ids L[i] and L[i-1] equal? (L in lexicographic order)
+__device__ __forceinline__ bool same_coords(const uint8_t *rec, int rb, int kw0, int N, uint32_t a,
+                                            uint32_t b) {
+    const uint32_t *ra = reinterpret_cast<const uint32_t *>(rec + (size_t)a * rb) + kw0;
+    const uint32_t *rbp = reinterpret_cast<const uint32_t *>(rec + (size_t)b * rb) + kw0;
+    for (int m = 0; m < N; ++m)
+        if (ra[m] != rbp[m]) return false;
+    return true;
+}
+
+// keep[p] = 1 iff storage position p is the first occurrence of its coordinate
+// (the head of its run in lexicographic order L; ties are in storage order, so
+// the head is the earliest); sumv[p] = sum of the run's values in storage order
+template <typename T>
+__global__ void dup_heads_kernel(const uint8_t *__restrict__ rec, int rb, int N,
+                                 const uint32_t *__restrict__ L, int64_t P,
+                                 uint32_t *__restrict__ keep, T *__restrict__ sumv,
+                                 int *__restrict__ any_dup) {
+    const int kw0 = sizeof(T) / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = L[i];
+        const bool head = i == 0 || !same_coords(rec, rb, kw0, N, p, L[i - 1]);
+        keep[p] = head ? 1u : 0u;
+        if (!head) {
+            *any_dup = 1;
+            continue;
+        }
+        T s = *reinterpret_cast<const T *>(rec + (size_t)p * rb);
+        for (int64_t j = i + 1; j < P && same_coords(rec, rb, kw0, N, p, L[j]); ++j)
+            s += *reinterpret_cast<const T *>(rec + (size_t)L[j] * rb);
+        sumv[p] = s;
+    }
+}
+
+// compact the kept records (storage order) with their merged values
+template <typename T>
+__global__ void dup_compact_kernel(const uint8_t *__restrict__ rec, int rb, int64_t P,
+                                   const uint32_t *__restrict__ keep,
+                                   const uint32_t *__restrict__ newidx,
+                                   const T *__restrict__ sumv, uint8_t *__restrict__ out,
+                                   double *__restrict__ partial) {
+    __shared__ double sh[256];
+    double sq = 0.0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        if (!keep[p]) continue;
+        uint8_t *d = out + (size_t)newidx[p] * rb;
+        const uint4 *srcv = reinterpret_cast<const uint4 *>(rec + (size_t)p * rb);
+        uint4 *dv = reinterpret_cast<uint4 *>(d);
+        dv[0] = srcv[0];
+        if (rb == 32) dv[1] = srcv[1];
+        *reinterpret_cast<T *>(d) = sumv[p];
+        sq += (double)sumv[p] * (double)sumv[p];
+    }
+    sh[threadIdx.x] = sq;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+sptk_status launch_sum_f64(const double *in, int64_t n, double *out, cudaStream_t s);
+
+// SPTK_CREATE_DUP_SUM / DUP_ERROR: lexicographic stable order by chaining
+// stable sorts from the last mode to the first, heads of equal-coordinate
+// runs keep their storage position and the run's value sum.
+sptk_status merge_duplicates(sptk_tensor t, bool error_only, cudaStream_t s) {
+    const int64_t P = t->P;
+    if (P <= 1) return SPTK_OK;
+    DevBuf o1, o2, keep, sumv, flag;
+    SPTK_TRY(o1.reserve(sizeof(uint32_t) * P));
+    SPTK_TRY(o2.reserve(sizeof(uint32_t) * P));
+    uint32_t *cur = nullptr, *nxt = o1.as<uint32_t>(), *spare = o2.as<uint32_t>();
+    for (int m = t->N - 1; m >= 0; --m) {
+        SPTK_TRY(stable_sort_ids(t, m, cur, nxt, nullptr, s));
+        cur = nxt;
+        nxt = spare;
+        spare = cur;
+    }
+    const uint32_t *L = cur;
+    SPTK_TRY(keep.reserve(sizeof(uint32_t) * (P + 1)));
+    SPTK_TRY(sumv.reserve((size_t)dtype_bytes(t->dtype) * P));
+    SPTK_TRY(flag.reserve(64));
+    SPTK_CUDA(cudaMemsetAsync(flag.p, 0, 64, s));
+    int *any = flag.as<int>();
+    if (t->dtype == SPTK_F64)
+        dup_heads_kernel<double><<<grid_for(P), 256, 0, s>>>(t->rec.as<uint8_t>(), t->rec_bytes,
+                                                             t->N, L, P, keep.as<uint32_t>(),
+                                                             sumv.as<double>(), any);
+    else
+        dup_heads_kernel<float><<<grid_for(P), 256, 0, s>>>(t->rec.as<uint8_t>(), t->rec_bytes,
+                                                            t->N, L, P, keep.as<uint32_t>(),
+                                                            sumv.as<float>(), any);
+    count_launch();
+    SPTK_CUDA(cudaGetLastError());
+    int h_any = 0;
+    SPTK_CUDA(cudaMemcpyAsync(&h_any, any, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SPTK_CUDA(cudaStreamSynchronize(s));
+    if (!h_any) return SPTK_OK;
+    if (error_only) return fail(SPTK_EDUP, "duplicate coordinates (SPTK_CREATE_DUP_ERROR)");
+    // new index of each kept record: exclusive scan of keep (storage order)
+    DevBuf newidx, tmp, out, part;
+    SPTK_TRY(newidx.reserve(sizeof(uint32_t) * (P + 1)));
+    SPTK_CUDA(cudaMemcpyAsync(newidx.p, keep.p, sizeof(uint32_t) * P, cudaMemcpyDeviceToDevice, s));
+    SPTK_CUDA(cudaMemsetAsync(newidx.as<uint32_t>() + P, 0, sizeof(uint32_t), s));
+    SPTK_TRY(tmp.reserve(sizeof(uint32_t) * ((P + 1 + kScanChunk - 1) / kScanChunk + 1)));
+    SPTK_TRY(exclusive_scan(newidx.as<uint32_t>(), P + 1, tmp.as<uint32_t>(), s));
+    uint32_t newP = 0;
+    SPTK_CUDA(cudaMemcpyAsync(&newP, newidx.as<uint32_t>() + P, sizeof(uint32_t),
+                              cudaMemcpyDeviceToHost, s));
+    SPTK_CUDA(cudaStreamSynchronize(s));
+    SPTK_TRY(out.reserve((size_t)t->rec_bytes * (newP > 0 ? newP : 1)));
+    const int blocks = grid_for(P);
+    SPTK_TRY(part.reserve(sizeof(double) * (blocks + 1)));
+    if (t->dtype == SPTK_F64)
+        dup_compact_kernel<double><<<blocks, 256, 0, s>>>(
+            t->rec.as<uint8_t>(), t->rec_bytes, P, keep.as<uint32_t>(), newidx.as<uint32_t>(),
+            sumv.as<double>(), out.as<uint8_t>(), part.as<double>());
+    else
+        dup_compact_kernel<float><<<blocks, 256, 0, s>>>(
+            t->rec.as<uint8_t>(), t->rec_bytes, P, keep.as<uint32_t>(), newidx.as<uint32_t>(),
+            sumv.as<float>(), out.as<uint8_t>(), part.as<double>());
+    count_launch();
+    SPTK_CUDA(cudaGetLastError());
+    SPTK_TRY(launch_sum_f64(part.as<double>(), blocks, part.as<double>() + blocks, s));
+    double normX2 = 0.0;
+    SPTK_CUDA(cudaMemcpyAsync(&normX2, part.as<double>() + blocks, sizeof(double),
+                              cudaMemcpyDeviceToHost, s));
+    SPTK_CUDA(cudaStreamSynchronize(s));
+    std::swap(t->rec.p, out.p);
+    std::swap(t->rec.bytes, out.bytes);
+    t->P = newP;
+    t->normX2 = normX2;
+    t->sortws.release();  // sized for the old P
     return SPTK_OK;
 }
 

@@ -619,3 +619,32 @@ def test_deterministic_mode_bitwise(sp, variant, dtype):
     with pytest.raises(sp.SptkError) as e:
         gpu_mttkrp(sp, t, 0, factors_np(63, dims, 17, npd), 17, dtype)   # generic path
     assert e.value.name == "EUNSUPPORTED"
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_duplicate_policies(sp, dtype):
+    dims = (30, 20, 10)
+    idx, vals = synth.tensor(19, dims, 20000)            # 6000 cells: many duplicates
+    npd = np.float64 if dtype == torch.float64 else np.float32
+    vals = vals.astype(npd)
+    t = sp.sptensor_create(dims, dev(idx.astype(np.int64)), dev(vals, dtype), duplicates="sum")
+    io, vo = oracle.merge_duplicates(idx, vals.astype(np.float64))
+    assert t.nnz == len(io) == sptensor_nnz(sp, t)
+    sp.build_perm(t, -1)
+    A = factors_np(20, dims, 16, npd)
+    for n in range(3):
+        V = gpu_mttkrp(sp, t, n, A, 16, dtype)
+        assert rel(V, oracle.mttkrp(dims, io, vo, [a.astype(np.float64) for a in A], n)) <= TOL[dtype]
+        p, _ = gpu_perm(sp, t, n)
+        assert np.array_equal(p, oracle.perm(io, n, dims[n])[0])   # merged storage order
+    with pytest.raises(sp.SptkError) as e:
+        sp.sptensor_create(dims, dev(idx.astype(np.int64)), dev(vals, dtype), duplicates="error")
+    assert e.value.name == "EDUP"
+    u, uv = synth.unique_tensor(21, dims, 500)
+    tu = sp.sptensor_create(dims, dev(u.astype(np.int64)), dev(uv.astype(npd), dtype),
+                            duplicates="error")
+    assert tu.nnz == 500
+
+
+def sptensor_nnz(sp, t):
+    return sp.sptensor_info(t)["nnz"]

@@ -257,3 +257,19 @@ def test_cp_als_tol_stops_early_and_zero_norm():
     with pytest.raises(oracle.OracleError) as e:
         oracle.cp_als((3, 3), np.array([[0, 0]]), np.array([0.0]), [np.ones((3, 2))] * 2, 3)
     assert e.value.code == oracle.EZERONORM
+
+
+# ------------------------------------------------------------------ duplicates
+def test_merge_duplicates_golden_and_dense():
+    g = GOLD["dup_merge"]
+    io, vo = oracle.merge_duplicates(np.array(g["idx"]), np.array(g["vals"]))
+    assert io.tolist() == g["idx_out"] and vo.tolist() == g["vals_out"], g["cite"]
+    dims = (5, 4, 3)
+    idx, vals = synth.tensor(17, dims, 200)              # 60 cells: many duplicates
+    io, vo = oracle.merge_duplicates(idx, vals)
+    assert len(np.unique(io, axis=0)) == len(io) < len(idx)
+    np.testing.assert_allclose(dense.densify(dims, io, vo), dense.densify(dims, idx, vals),
+                               rtol=1e-14)
+    # kept order = storage order of first occurrences
+    _, first = np.unique(idx, axis=0, return_index=True)
+    assert np.array_equal(io, idx[np.sort(first)])
