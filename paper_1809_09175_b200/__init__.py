@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsptk.so")
+# SPTK_LIB overrides the in-tree library (A/B measurements of two builds)
+LIB_PATH = os.environ.get("SPTK_LIB") or os.path.join(_HERE, "libsptk.so")
 
 F32, F64 = 1, 2
 IDX_I64, IDX_U32 = 1, 2

@@ -72,15 +72,6 @@ sptk_status DevBuf::reserve(size_t n) {
     return SPTK_OK;
 }
 
-bool debug_enabled() {
-    static int on = -1;
-    if (on < 0) {
-        const char *e = getenv("SPTK_DEBUG");
-        on = (e && *e && *e != '0') ? 1 : 0;
-    }
-    return on == 1;
-}
-
 bool is_device_ptr(const void *p) {
     if (!p) return false;
     cudaPointerAttributes a;

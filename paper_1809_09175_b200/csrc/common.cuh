@@ -65,7 +65,6 @@ struct DevBuf {
 };
 
 bool is_device_ptr(const void *p);
-bool debug_enabled();
 
 // ------------------------------------------------------------------ tensor
 struct ALSWork {

@@ -57,6 +57,42 @@ struct MttkrpArgs {
 };
 
 // ----------------------------------------------------------------- loads
+// L2 eviction policies: the streamed records are read once (evict_first), the
+// gathered factor rows are reused (evict_last) -- keeps the record stream from
+// flushing factor lines out of L2 when the factors exceed it (C4/C5 shapes).
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void ld_rec32_p(const void *p, uint32_t (&r)[8], uint64_t pol) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                   "=r"(r[6]), "=r"(r[7])
+                 : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ld_rec16_p(const void *p, uint32_t (&r)[8], uint64_t pol) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "l"(p), "l"(pol));
+    r[4] = r[5] = r[6] = r[7] = 0;
+}
+__device__ __forceinline__ void ld_row_p(const double *p, double (&r)[4], uint64_t pol) {
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+                 : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ld_row_p(const float *p, float (&r)[8], uint64_t pol) {
+    asm volatile("ld.global.nc.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
+                   "=f"(r[6]), "=f"(r[7])
+                 : "l"(p), "l"(pol));
+}
 __device__ __forceinline__ void ld_rec32(const void *p, uint32_t (&r)[8]) {
     asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
@@ -164,9 +200,15 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
         else
             st_row(out + (int64_t)row * a.ld + c, o);
     };
+    const uint64_t pol_stream = policy_evict_first(), pol_factor = policy_evict_last();
     auto load_rec = [&](uint32_t pos, uint32_t (&r)[8]) {
-        if constexpr (RB == 32) ld_rec32(rec + (size_t)pos * 32, r);
-        else ld_rec16(rec + (size_t)pos * 16, r);
+        if constexpr (SORTED) {
+            if constexpr (RB == 32) ld_rec32_p(rec + (size_t)pos * 32, r, pol_stream);
+            else ld_rec16_p(rec + (size_t)pos * 16, r, pol_stream);
+        } else {
+            if constexpr (RB == 32) ld_rec32(rec + (size_t)pos * 32, r);
+            else ld_rec16(rec + (size_t)pos * 16, r);
+        }
     };
 
     uint32_t row = 0;   // SORTED: row of the current position
@@ -225,8 +267,8 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
                 if (m != MODE) {
                     const int word = SORTED ? OFF + (m < MODE ? m : m - 1) : OFF + m;
                     if (p[u] != kNoRow && lane_on)
-                        ld_row(static_cast<const T *>(a.A[m]) + (int64_t)w[u][word] * a.ld + c,
-                               f[u][m]);
+                        ld_row_p(static_cast<const T *>(a.A[m]) + (int64_t)w[u][word] * a.ld + c,
+                                 f[u][m], pol_factor);
                     else
 #pragma unroll
                         for (int v = 0; v < V; ++v) f[u][m][v] = T(0);
@@ -328,9 +370,10 @@ __device__ __forceinline__ void mttkrp_coop_body(const MttkrpArgs &a) {
         else
             st_row(out + (int64_t)row * a.ld + c, o);
     };
+    const uint64_t pol_stream = policy_evict_first(), pol_factor = policy_evict_last();
     auto load_rec = [&](uint32_t pos, uint32_t (&r)[8]) {
-        if constexpr (RB == 32) ld_rec32(rec + (size_t)pos * 32, r);
-        else ld_rec16(rec + (size_t)pos * 16, r);
+        if constexpr (RB == 32) ld_rec32_p(rec + (size_t)pos * 32, r, pol_stream);
+        else ld_rec16_p(rec + (size_t)pos * 16, r, pol_stream);
     };
 
     uint32_t row = __ldg(a.wrow + warp_id);
@@ -367,8 +410,8 @@ __device__ __forceinline__ void mttkrp_coop_body(const MttkrpArgs &a) {
                     if (m != MODE) {
                         const int word = OFF + (m < MODE ? m : m - 1);
                         if (base + u * NG + g < e && lane_on)
-                            ld_row(static_cast<const T *>(a.A[m]) + (int64_t)w[u][word] * a.ld + c,
-                                   f[u][m]);
+                            ld_row_p(static_cast<const T *>(a.A[m]) + (int64_t)w[u][word] * a.ld + c,
+                                     f[u][m], pol_factor);
                         else
 #pragma unroll
                             for (int v = 0; v < V; ++v) f[u][m][v] = T(0);
