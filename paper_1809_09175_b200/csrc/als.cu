@@ -19,6 +19,7 @@
 // Multi-GPU: each rank solves its own row range of every mode, the R column
 // sums of squares and <X,M> partials are all-reduced, the rows broadcast.
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -27,6 +28,7 @@
 namespace sptk {
 
 constexpr int kMaxAlsRank = 128;
+constexpr int kGramTileRows = 128;  // rows staged per shared-memory tile (R <= 32 kernels)
 
 // ---------------------------------------------------------------- kernels
 // Counter generator of DESIGN.md §3 (same text as synth/), for init = NULL.
@@ -47,28 +49,30 @@ __global__ void init_factor_kernel(uint64_t seed, uint64_t stream, int64_t n, T 
     }
 }
 
-// partial[b][e] = sum over the rows of block b of A(k,a) A(k,c), e = a*R + c
-template <typename T>
+// partial[b][e] = sum over the rows of block b of A(k,a) A(k,c), e = a*R + c;
+// KE = Gram entries per thread per pass (1 for R <= 16, 4 for R <= 32)
+template <typename T, int KE>
 __global__ void __launch_bounds__(256)
     gram_partial_kernel(const T *__restrict__ A, int64_t I, int R, int64_t rows_per_block,
                         double *__restrict__ partial) {
-    constexpr int TR = 32;  // rows staged per tile
+    constexpr int TR = kGramTileRows;  // rows staged per tile
     extern __shared__ double tile[];  // TR x R
     const int RR = R * R;
     const int64_t r0 = blockIdx.x * rows_per_block;
     const int64_t r1 = min(I, r0 + rows_per_block);
-    for (int e0 = 0; e0 < RR; e0 += 256 * 16) {
-        double acc[16];
+    for (int e0 = 0; e0 < RR; e0 += 256 * KE) {
+        double acc[KE];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+        for (int k = 0; k < KE; ++k) acc[k] = 0.0;
         for (int64_t rt = r0; rt < r1; rt += TR) {
             const int nr = (int)min((int64_t)TR, r1 - rt);
             __syncthreads();
+#pragma unroll 4
             for (int x = threadIdx.x; x < nr * R; x += blockDim.x)
                 tile[x] = (double)A[rt * R + x];
             __syncthreads();
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
+            for (int k = 0; k < KE; ++k) {
                 const int e = e0 + k * 256 + threadIdx.x;
                 if (e < RR) {
                     const int a = e / R, c = e % R;
@@ -79,7 +83,7 @@ __global__ void __launch_bounds__(256)
             }
         }
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < KE; ++k) {
             const int e = e0 + k * 256 + threadIdx.x;
             if (e < RR) partial[(int64_t)blockIdx.x * RR + e] = acc[k];
         }
@@ -213,12 +217,30 @@ __global__ void __launch_bounds__(256)
     const int j = threadIdx.x % R, l = threadIdx.x / R;
     const int64_t b0 = r0 + blockIdx.x * rows_per_block;
     const int64_t b1 = min(r1, b0 + rows_per_block);
+    const bool vec4 = (R % 4 == 0) && ((reinterpret_cast<uintptr_t>(V) & 15) == 0);
     double sq = 0.0, dot = 0.0;
     if (l < lanes) {
+#pragma unroll 2
         for (int64_t k = b0 + l; k < b1; k += lanes) {
             const T *v = V + k * R;
             double x = 0.0;
-            for (int i = 0; i < R; ++i) x += (double)v[i] * Gi[i * R + j];
+            if (vec4) {  // 4 values per load: one LDG per 4 columns of the row
+                for (int i = 0; i < R; i += 4) {
+                    T q[4];
+                    if constexpr (sizeof(T) == 8) {
+                        const double2 a0 = __ldg(reinterpret_cast<const double2 *>(v + i));
+                        const double2 a1 = __ldg(reinterpret_cast<const double2 *>(v + i + 2));
+                        q[0] = a0.x; q[1] = a0.y; q[2] = a1.x; q[3] = a1.y;
+                    } else {
+                        const float4 a0 = __ldg(reinterpret_cast<const float4 *>(v + i));
+                        q[0] = a0.x; q[1] = a0.y; q[2] = a0.z; q[3] = a0.w;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) x += (double)q[u] * Gi[(i + u) * R + j];
+                }
+            } else {
+                for (int i = 0; i < R; ++i) x += (double)v[i] * Gi[i * R + j];
+            }
             const T xt = (T)x;
             A[k * R + j] = xt;
             sq += (double)xt * (double)xt;
@@ -291,41 +313,35 @@ __global__ void __launch_bounds__(256)
 }
 
 // Tail of a mode update (single GPU), one grid: every block
-//   (a) reduces the apply_inv column partials to ||A_raw(:,j)||^2 (fixed-order
-//       warp trees, so every block gets identical bits) -> lambda,
+//   (a) takes lambda_j = sqrt(colsq_j) (colsq reduced once beforehand),
 //   (b) normalises its row chunk of A_n (zero column -> e_1),
 //   (c) writes the partial Gram matrix of its normalised rows (reduced in block
 //       order by reduce_partials_kernel); block 0 writes lambda.
-template <typename T>
+template <typename T, int KE>
 __global__ void __launch_bounds__(256)
     finish_kernel(T *__restrict__ A, int64_t I, int R, int64_t rows_per_block,
-                  const double *__restrict__ part_sq, int nb_in, double *__restrict__ gpart,
+                  const double *__restrict__ colsq, double *__restrict__ gpart,
                   double *__restrict__ lam) {
-    constexpr int TR = 32;
+    constexpr int TR = kGramTileRows;
     extern __shared__ double sm[];
     double *lam_s = sm;     // R
     double *tile = sm + R;  // TR x R
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     const int RR = R * R;
-    for (int j = warp; j < R; j += 8) {
-        double s = 0.0;
-        for (int b = lane; b < nb_in; b += 32) s += part_sq[(int64_t)b * R + j];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) lam_s[j] = sqrt(s);
-    }
+    for (int j = tid; j < R; j += blockDim.x) lam_s[j] = sqrt(colsq[j]);
     __syncthreads();
     if (blockIdx.x == 0)
         for (int j = tid; j < R; j += blockDim.x) lam[j] = lam_s[j];
     const int64_t r0 = blockIdx.x * rows_per_block;
     const int64_t r1 = min(I, r0 + rows_per_block);
-    for (int e0 = 0; e0 < RR; e0 += 256 * 16) {
-        double acc[16];
+    for (int e0 = 0; e0 < RR; e0 += 256 * KE) {
+        double acc[KE];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+        for (int k = 0; k < KE; ++k) acc[k] = 0.0;
         for (int64_t rt = r0; rt < r1; rt += TR) {
             const int nr = (int)min((int64_t)TR, r1 - rt);
             __syncthreads();
+#pragma unroll 4
             for (int x = tid; x < nr * R; x += blockDim.x) {
                 T *a = A + rt * R + x;
                 T v = *a;
@@ -338,7 +354,7 @@ __global__ void __launch_bounds__(256)
             }
             __syncthreads();
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
+            for (int k = 0; k < KE; ++k) {
                 const int e = e0 + k * 256 + tid;
                 if (e < RR) {
                     const int a = e / R, b = e % R;
@@ -349,7 +365,7 @@ __global__ void __launch_bounds__(256)
             }
         }
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < KE; ++k) {
             const int e = e0 + k * 256 + tid;
             if (e < RR) gpart[(int64_t)blockIdx.x * RR + e] = acc[k];
         }
@@ -532,7 +548,7 @@ static sptk_status gram(AlsCtx &c, int m, double *part = nullptr) {
     ALSWork &w = t->als;
     const int R = (int)c.R;
     const int64_t I = t->dims[m];
-    int nb = (int)std::min<int64_t>(c.nblocks, (I + 31) / 32);
+    int nb = (int)std::min<int64_t>(c.nblocks, (I + kGramTileRows - 1) / kGramTileRows);
     const int64_t rpb = (I + nb - 1) / nb;
     nb = (int)((I + rpb - 1) / rpb);
     if (!part) part = w.partial.as<double>();
@@ -541,9 +557,13 @@ static sptk_status gram(AlsCtx &c, int m, double *part = nullptr) {
         gram_tiled_kernel<T><<<dim3((unsigned)nb, (unsigned)(nt * nt)), 256, 0, c.s>>>(
             static_cast<const T *>(c.A[m]), I, R, rpb, part);
     } else {
-        const size_t sm = sizeof(double) * 32 * R;
-        gram_partial_kernel<T><<<nb, 256, sm, c.s>>>(static_cast<const T *>(c.A[m]), I, R, rpb,
-                                                     part);
+        const size_t sm = sizeof(double) * kGramTileRows * R;
+        if (R <= 16)
+            gram_partial_kernel<T, 1><<<nb, 256, sm, c.s>>>(static_cast<const T *>(c.A[m]), I, R,
+                                                            rpb, part);
+        else
+            gram_partial_kernel<T, 4><<<nb, 256, sm, c.s>>>(static_cast<const T *>(c.A[m]), I, R,
+                                                            rpb, part);
     }
     reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(
         part, nb, R * R, w.G.as<double>() + (int64_t)m * R * R);
@@ -561,7 +581,7 @@ static sptk_status apply_inverse(AlsCtx &c, const T *V, int64_t r0, int64_t r1, 
     const int R = (int)c.R;
     const double *Ginv = c.t->als.L.as<double>();
     const int64_t rows = r1 - r0;
-    if (R > 32) {
+    if (R > 32) {  // (measured: the 64x64 tiles lose 2.7x at R = 16)
         const int nrt = (int)((rows + kTB - 1) / kTB);
         const dim3 grid((unsigned)nrt, (unsigned)((R + kTB - 1) / kTB));
         apply_inv_tiled_kernel<T><<<grid, 256, 0, c.s>>>(V, r0, r1, R, Ginv, An, psq, pdot);
@@ -612,15 +632,22 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
         double *pdot = psq + c.part_stride;
         int nb = 0;
         SPTK_TRY(apply_inverse<T>(c, V, 0, I, An, psq, last ? pdot : nullptr, &nb));
-        if (R <= 32) {  // one fused tail: lambda, normalise, Gram partials
-            int nf = (int)std::min<int64_t>(c.nblocks, (I + 31) / 32);
+        if (R <= 32) {  // column norms, then one fused tail: lambda, normalise, Gram partials
+            double *colsq = w.colsq.as<double>();
+            reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(psq, nb, R, colsq);
+            int nf = (int)std::min<int64_t>(c.nblocks, (I + kGramTileRows - 1) / kGramTileRows);
             const int64_t fpb = (I + nf - 1) / nf;
             nf = (int)((I + fpb - 1) / fpb);
-            finish_kernel<T><<<nf, 256, sizeof(double) * (R + 32 * R), c.s>>>(
-                An, I, R, fpb, psq, nb, w.gpart.as<double>(), lam);
+            const size_t fsm = sizeof(double) * (R + kGramTileRows * R);
+            if (R <= 16)
+                finish_kernel<T, 1><<<nf, 256, fsm, c.s>>>(An, I, R, fpb, colsq,
+                                                           w.gpart.as<double>(), lam);
+            else
+                finish_kernel<T, 4><<<nf, 256, fsm, c.s>>>(An, I, R, fpb, colsq,
+                                                           w.gpart.as<double>(), lam);
             reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(
                 w.gpart.as<double>(), nf, R * R, w.G.as<double>() + (int64_t)n * R * R);
-            count_launch(2);
+            count_launch(3);
         } else {        // large R: reduce, normalise, tiled Gram
             double *colsq = w.colsq.as<double>();
             reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(psq, nb, R, colsq);
@@ -743,9 +770,8 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     SPTK_TRY(w.V.reserve(es * Imax * R));
     SPTK_TRY(w.G.reserve(sizeof(double) * N * R * R));
     SPTK_TRY(w.L.reserve(sizeof(double) * R * R));  // Gamma^{-1}
-    // R-vector partials: one per block (R <= 32) or per 64-row tile (R > 32)
-    const int64_t nparts_max =
-        R > 32 ? (Imax + kTB - 1) / kTB : std::max<int64_t>(c.nb_row, 1);
+    // R-vector partials: one per block (row-parallel kernel) or per 64-row tile
+    const int64_t nparts_max = std::max<int64_t>((Imax + kTB - 1) / kTB, c.nb_row);
     c.part_stride = (size_t)nparts_max * R;
     SPTK_TRY(w.partial.reserve(sizeof(double) * std::max<size_t>((size_t)c.nblocks * R * R,
                                                                 2 * c.part_stride)));
@@ -922,8 +948,10 @@ extern "C" sptk_status sptk_cp_als(sptk_tensor t, int64_t R, int max_iters, doub
         cudaFuncSetAttribute(apply_inv_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(apply_inv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(finish_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(finish_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(finish_kernel<double, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(finish_kernel<double, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(finish_kernel<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(finish_kernel<float, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
     sptk_status st =

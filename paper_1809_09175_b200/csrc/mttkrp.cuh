@@ -70,25 +70,31 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+#ifndef SPTK_REC_PREFETCH
+#define SPTK_REC_PREFETCH ""
+#endif
+#ifndef SPTK_ROW_L1
+#define SPTK_ROW_L1 ""
+#endif
 __device__ __forceinline__ void ld_rec32_p(const void *p, uint32_t (&r)[8], uint64_t pol) {
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint" SPTK_REC_PREFETCH ".v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
                    "=r"(r[6]), "=r"(r[7])
                  : "l"(p), "l"(pol));
 }
 __device__ __forceinline__ void ld_rec16_p(const void *p, uint32_t (&r)[8], uint64_t pol) {
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint" SPTK_REC_PREFETCH ".v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                  : "l"(p), "l"(pol));
     r[4] = r[5] = r[6] = r[7] = 0;
 }
 __device__ __forceinline__ void ld_row_p(const double *p, double (&r)[4], uint64_t pol) {
-    asm volatile("ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+    asm volatile("ld.global.nc" SPTK_ROW_L1 ".L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
                  : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
                  : "l"(p), "l"(pol));
 }
 __device__ __forceinline__ void ld_row_p(const float *p, float (&r)[8], uint64_t pol) {
-    asm volatile("ld.global.nc.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+    asm volatile("ld.global.nc" SPTK_ROW_L1 ".L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
                  : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
                    "=f"(r[6]), "=f"(r[7])
                  : "l"(p), "l"(pol));

@@ -1,0 +1,12 @@
+#!/bin/bash
+# Build libsptk.so with extra nvcc flags into $1 (A/B experiments), e.g.
+#   tools/ab_build.sh tools/ab/libA.so -DSPTK_ROW_L1='".L1::no_allocate"'
+out=$1; shift
+tmp=$(mktemp -d)
+for f in paper_1809_09175_b200/csrc/*.cu; do
+  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
+    -Xcompiler -fPIC -I include "$@" -c "$f" -o "$tmp/$(basename "$f" .cu).o" &
+done
+wait
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$out" "$tmp"/*.o -ldl
+rm -rf "$tmp"
