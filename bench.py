@@ -258,9 +258,12 @@ def main():
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
-    if world > 1:
+    # SPTK_FORCE_SHARDED=1 under torchrun with one rank exercises the N>1 path
+    # (process group, NCCL bootstrap, sharded ALS) on a single GPU
+    distributed = world > 1 or bool(os.environ.get("SPTK_FORCE_SHARDED")) and "RANK" in os.environ
+    if distributed:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    comm = sp.comm_from_process_group() if world > 1 else None
+    comm = sp.comm_from_process_group() if distributed else None
 
     c = synth.CONFIGS[args.config]
     R = args.rank
@@ -438,7 +441,7 @@ def main():
     t.close()
     if comm is not None:
         comm.close()
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
     return 0
 
