@@ -21,7 +21,7 @@
  *  - Factor matrices are row-major I_m x R ("row-wise memory
  *    layout"), element type = the tensor's dtype, caller-owned.
  *  - Limits: 1 <= nmodes <= 6 (cp_als: >= 2); 1 <= dims[m] < 2^32;
- *    0 <= nnz < 2^32; R >= 1.  Indices are 0-based (Z2).
+ *    0 <= nnz <= 2^32 - 4096 (32-bit positions); R >= 1 (cp_als: R <= 128).  Indices are 0-based (Z2).
  *  - A handle is immutable after sptk_build_perm and may be shared by
  *    concurrent sptk_mttkrp calls on different streams; it is not
  *    thread-safe during create / build_perm / cp_als.

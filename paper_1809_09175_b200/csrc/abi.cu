@@ -132,7 +132,8 @@ sptk_status sptk_sptensor_create(int nmodes, const int64_t *dims, int64_t nnz, c
         if (dims[m] < 1 || dims[m] >= (int64_t(1) << 32))
             return fail(SPTK_EUNSUPPORTED, "dims[m] must be in [1, 2^32)");
     if (nnz < 0) return fail(SPTK_EINVAL, "nnz < 0");
-    if (nnz >= (int64_t(1) << 32)) return fail(SPTK_EUNSUPPORTED, "nnz must be < 2^32");
+    // positions are 32-bit in the kernels with small look-ahead offsets
+    if (nnz > (int64_t(1) << 32) - 4096) return fail(SPTK_EUNSUPPORTED, "nnz must be <= 2^32 - 4096");
     if (dtype != SPTK_F32 && dtype != SPTK_F64) return fail(SPTK_EINVAL, "bad dtype");
     if (itype != SPTK_IDX_I64 && itype != SPTK_IDX_U32) return fail(SPTK_EINVAL, "bad idx type");
     if (flags & ~(unsigned)(SPTK_CREATE_PERM_GATHER | SPTK_CREATE_DETERMINISTIC |

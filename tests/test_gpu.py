@@ -648,3 +648,18 @@ def test_duplicate_policies(sp, dtype):
 
 def sptensor_nnz(sp, t):
     return sp.sptensor_info(t)["nnz"]
+
+
+def test_c_api_demo(sp, tmp_path):
+    """The C ABI from plain C (examples/c_api_demo.c): build with gcc, run."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "c_api_demo"
+    libdir = os.path.join(root, "paper_1809_09175_b200")
+    subprocess.check_call(["gcc", "-O2", "-I", os.path.join(root, "include"),
+                           "-I", "/usr/local/cuda/include", os.path.join(root, "examples", "c_api_demo.c"),
+                           "-L", libdir, "-l:libsptk.so", "-L", "/usr/local/cuda/lib64", "-lcudart",
+                           f"-Wl,-rpath,{libdir}:/usr/local/cuda/lib64", "-lm", "-o", str(exe)])
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "c_api_demo ok" in r.stdout
