@@ -262,4 +262,7 @@ CONFIGS = {
     # the paper's own synthetic CP-ALS / bandwidth-vs-R workload:
     # "30K x 40K x 50K with 10M nonzeros placed randomly", R = 128 and R in [8, 256]
     "paper_synth": Config(6, "paper_synth", (30000, 40000, 50000), 10_000_000, (128,), ("f64",)),
+    # VAST-like shape (not a BASELINE config): a length-2 mode, the
+    # short-mode / contention study of SURVEY §8(f) NEXT-4
+    "vast_shape": Config(7, "vast_shape", (165000, 11000, 2, 100, 89), 26_000_000, (16,), ("f64",)),
 }
