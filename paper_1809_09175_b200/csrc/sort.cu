@@ -8,7 +8,7 @@
 //   upsweep    per-tile digit histograms          counts[digit][tile]
 //   scan       exclusive scan of counts (digit-major) -> global offsets
 //   downsweep  stable scatter: inside a 4096-key tile, warp w owns keys
-//              [w*512, w*512+512) and ranks equal digits with __match_any_sync
+//              [w*512, w*512+512) and ranks equal digits with per-bit ballots
 //              in rounds of 32, so equal keys keep their storage order.
 // Then rowptr_n[r] = first sorted position with key >= r (boundary kernel).
 #include <algorithm>
@@ -30,6 +30,18 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
+// Lanes of the warp holding the same digit (bits < 9), from `bits` ballots
+// instead of __match_any_sync (MATCH is a slow MIO op); `valid` lanes only.
+__device__ __forceinline__ uint32_t digit_peers(uint32_t digit, int bits, bool valid) {
+    uint32_t peers = __ballot_sync(0xffffffffu, valid);
+    for (int b = 0; b < bits; ++b) {
+        const bool on = (digit >> b) & 1u;
+        const uint32_t m = __ballot_sync(0xffffffffu, on);
+        peers &= on ? m : ~m;
+    }
+    return peers;
+}
+
 // keys[i] = l_i,mode from the packed records (one streaming pass)
 __global__ void __launch_bounds__(256) extract_keys(const uint8_t *__restrict__ rec, int rb, int kw,
                                                     int64_t P, uint32_t *__restrict__ keys) {
@@ -41,13 +53,13 @@ __global__ void __launch_bounds__(256) extract_keys(const uint8_t *__restrict__ 
 __global__ void __launch_bounds__(kSortThreads)
     radix_upsweep(const uint32_t *__restrict__ keys, uint32_t P, int shift, int dbits,
                   uint32_t ntiles, uint32_t *__restrict__ counts) {
-    __shared__ uint32_t hist[256];
+    __shared__ uint32_t hist[kSortWarps][256];  // per-warp: fewer colliding smem atomics
     const int nd = 1 << dbits;
-    for (int d = threadIdx.x; d < nd; d += blockDim.x) hist[d] = 0;
+    const int warp = threadIdx.x >> 5;
+    for (int d = threadIdx.x; d < kSortWarps * 256; d += blockDim.x) (&hist[0][0])[d] = 0;
     __syncthreads();
     const uint32_t base = blockIdx.x * (uint32_t)kSortTile;
     const uint32_t mask = (uint32_t)nd - 1;
-    const uint32_t lt = lanemask_lt();
     uint32_t k[kSortItems];
 #pragma unroll
     for (int r = 0; r < kSortItems; ++r) {
@@ -55,20 +67,20 @@ __global__ void __launch_bounds__(kSortThreads)
         k[r] = i < P ? __ldg(keys + i) : 0u;
     }
 #pragma unroll
-    for (int r = 0; r < kSortItems; ++r) {
-        const bool valid = base + r * kSortThreads + threadIdx.x < P;
-        const uint32_t digit = valid ? (k[r] >> shift) & mask : 0xffffffffu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, digit);
-        if (valid && (peers & lt) == 0) atomicAdd(&hist[digit], __popc(peers));
-    }
+    for (int r = 0; r < kSortItems; ++r)
+        if (base + r * kSortThreads + threadIdx.x < P) atomicAdd(&hist[warp][(k[r] >> shift) & mask], 1u);
     __syncthreads();
-    for (int d = threadIdx.x; d < nd; d += blockDim.x)
-        counts[(size_t)d * ntiles + blockIdx.x] = hist[d];
+    for (int d = threadIdx.x; d < nd; d += blockDim.x) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int w = 0; w < kSortWarps; ++w) c += hist[w][d];
+        counts[(size_t)d * ntiles + blockIdx.x] = c;
+    }
 }
 
 // vals_in == NULL: the values are the positions i (first pass).
 // Stable tile-local ranking (warp w owns keys [w*512, w*512+512) of the 4096-
-// key tile; __match_any_sync ranks equal digits within each round of 32, in
+// key tile; per-bit ballots rank equal digits within each round of 32, in
 // storage order), then the tile is reordered by digit in shared memory and
 // written out so that consecutive threads write consecutive positions of each
 // digit's run (coalesced), global run start = scanned count of (digit, tile).
@@ -101,8 +113,8 @@ __global__ void __launch_bounds__(kSortThreads)
 #pragma unroll
     for (int r = 0; r < kSortItems; ++r) {
         const bool valid = base + r * 32 + lane < P;
-        const uint32_t digit = valid ? (key[r] >> shift) & mask : 0xffffffffu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, digit);
+        const uint32_t digit = valid ? (key[r] >> shift) & mask : 0u;
+        const uint32_t peers = digit_peers(digit, dbits, valid);
         if (valid && (peers & lt) == 0) whist[warp][digit] += __popc(peers);
         __syncwarp();
     }
@@ -143,8 +155,8 @@ __global__ void __launch_bounds__(kSortThreads)
     for (int r = 0; r < kSortItems; ++r) {
         const uint32_t i = base + r * 32 + lane;
         const bool valid = i < P;
-        const uint32_t digit = valid ? (key[r] >> shift) & mask : 0xffffffffu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, digit);
+        const uint32_t digit = valid ? (key[r] >> shift) & mask : 0u;
+        const uint32_t peers = digit_peers(digit, dbits, valid);
         uint32_t pos = 0;
         if (valid) pos = lstart[digit] + whist[warp][digit] + __popc(peers & lt);
         __syncwarp();
