@@ -60,14 +60,20 @@ struct MttkrpArgs {
 // L2 eviction policies: the streamed records are read once (evict_first), the
 // gathered factor rows are reused (evict_last) -- keeps the record stream from
 // flushing factor lines out of L2 when the factors exceed it (C4/C5 shapes).
+#ifndef SPTK_STREAM_POLICY
+#define SPTK_STREAM_POLICY "evict_first"
+#endif
+#ifndef SPTK_FACTOR_POLICY
+#define SPTK_FACTOR_POLICY "evict_last"
+#endif
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    asm volatile("createpolicy.fractional.L2::" SPTK_STREAM_POLICY ".b64 %0, 1.0;" : "=l"(p));
     return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    asm volatile("createpolicy.fractional.L2::" SPTK_FACTOR_POLICY ".b64 %0, 1.0;" : "=l"(p));
     return p;
 }
 #ifndef SPTK_REC_PREFETCH
