@@ -21,10 +21,13 @@
  *  - Factor matrices are row-major I_m x R ("row-wise memory
  *    layout"), element type = the tensor's dtype, caller-owned.
  *  - Limits: 1 <= nmodes <= 6 (cp_als: >= 2); 1 <= dims[m] < 2^32;
- *    0 <= nnz <= 2^32 - 4096 (32-bit positions); R >= 1 (cp_als: R <= 128).  Indices are 0-based (Z2).
- *  - A handle is immutable after sptk_build_perm and may be shared by
- *    concurrent sptk_mttkrp calls on different streams; it is not
- *    thread-safe during create / build_perm / cp_als.
+ *    0 <= nnz <= 2^32 - 4096 (32-bit positions); R >= 1 (cp_als: R <= 128).
+ *    Indices are 0-based (Z2).
+ *  - Concurrency: the tensor's values never change after create, but a
+ *    handle keeps per-handle caches (permuted copies, worker start rows,
+ *    scratch, ALS workspace) that MTTKRP / CP-ALS calls may (re)build, so
+ *    calls on ONE handle must be serialised (one host thread at a time; any
+ *    streams).  Different handles are independent.
  */
 #ifndef SPTK_H
 #define SPTK_H
