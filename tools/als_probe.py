@@ -1,5 +1,5 @@
 """CP-ALS on a config for a few iterations (for ncu launch lists).
-Usage: python tools/als_probe.py config R iters"""
+Usage: python tools/als_probe.py config R iters [f64|f32]"""
 import os
 import sys
 
@@ -12,11 +12,12 @@ from synth import device  # noqa: E402
 
 c = synth.CONFIGS[sys.argv[1]]
 R, iters = int(sys.argv[2]), int(sys.argv[3])
-idx, val = device.tensor(c.seed, c.dims, c.nnz, c.dist)
+dt = torch.float32 if len(sys.argv) > 4 and sys.argv[4] == "f32" else torch.float64
+idx, val = device.tensor(c.seed, c.dims, c.nnz, c.dist, dtype=dt)
 t = sp.sptensor_create(c.dims, idx, val)
 del idx, val
 sp.build_perm(t, -1)
-F = [torch.empty((I, R), dtype=torch.float64, device="cuda") for I in c.dims]
+F = [torch.empty((I, R), dtype=dt, device="cuda") for I in c.dims]
 res = sp.cp_als(t, R, iters, F, seed=c.seed_f)
 torch.cuda.synchronize()
 print(res)
