@@ -430,6 +430,9 @@ def main():
                                         "gathers hit L2 (P:716)",
                          "peak_source": peak_src,
                          "frac_of_8TBps": achieved / 8000.0,
+                         # the same launch measured by the DRAM bytes ncu saw it move
+                         "dram_traffic_frac": (traffic / (mttkrp_ms_launch * 1e-3) / 1e9 / peak
+                                               if traffic else None),
                          "timing": "per-launch CUDA events in a second K-iteration pass "
                                    "(eager launches), mean over all MTTKRP launches"},
             "clocks": clk.summary(),
