@@ -584,7 +584,13 @@ __global__ void __launch_bounds__(256) mttkrp_generic_kernel(const MttkrpArgs a)
 // (mttkrp_fast_kernel); variant 1: warp-cooperative steps
 // (mttkrp_coop_kernel, permuted copy only).
 constexpr int kNumVariants = 2;
-constexpr int kU = 2, kMinBlocks = 3;
+#ifndef SPTK_KU
+#define SPTK_KU 2
+#endif
+#ifndef SPTK_KMINB
+#define SPTK_KMINB 3
+#endif
+constexpr int kU = SPTK_KU, kMinBlocks = SPTK_KMINB;
 
 template <typename T, int N, int RB, bool SORTED, bool COOP>
 inline sptk_status fast_launch_g(int G, const MttkrpArgs &a, int64_t workers, cudaStream_t s) {
