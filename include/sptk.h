@@ -56,8 +56,8 @@ enum {
      * with its neighbours are not flushed with atomics but written to a
      * scratch slot and summed in worker order by a fix-up kernel (SURVEY
      * §8(f) NEXT-3).  Supported on the permuted-copy fast path (N in 3..5,
-     * R a multiple of 32/sizeof(value), 32-byte aligned factors); other
-     * calls on such a tensor return SPTK_EUNSUPPORTED. */
+     * any R, element-aligned factors; not with SPTK_CREATE_PERM_GATHER);
+     * other calls on such a tensor return SPTK_EUNSUPPORTED. */
     SPTK_CREATE_DETERMINISTIC = 4,
     /* Duplicate-coordinate policy (default: duplicates kept, MTTKRP
      * is linear in X).  DUP_SUM merges equal coordinates into one nonzero at

@@ -37,14 +37,28 @@ static int variant_setting() {
     return g_variant;
 }
 
-template <typename T>
-static sptk_status launch_fast(int N, int G, int variant, const MttkrpArgs &a, int64_t workers,
-                               cudaStream_t s) {
+template <typename T, int V>
+static sptk_status launch_fast_v(int N, int G, int variant, const MttkrpArgs &a, int64_t workers,
+                                 cudaStream_t s) {
     switch (N) {
-    case 3: return launch_fast_tn<T, 3>(G, variant, a, workers, s);
-    case 4: return launch_fast_tn<T, 4>(G, variant, a, workers, s);
-    case 5: return launch_fast_tn<T, 5>(G, variant, a, workers, s);
+    case 3: return launch_fast_tnv<T, 3, V>(G, variant, a, workers, s);
+    case 4: return launch_fast_tnv<T, 4, V>(G, variant, a, workers, s);
+    case 5: return launch_fast_tnv<T, 5, V>(G, variant, a, workers, s);
     default: return fail(SPTK_EINVAL, "fast MTTKRP: N must be 3..5");
+    }
+}
+
+template <typename T>
+static sptk_status launch_fast(int N, int V, int G, int variant, const MttkrpArgs &a,
+                               int64_t workers, cudaStream_t s) {
+    switch (V) {
+    case 1: return launch_fast_v<T, 1>(N, G, variant, a, workers, s);
+    case 2: return launch_fast_v<T, 2>(N, G, variant, a, workers, s);
+    case 4: return launch_fast_v<T, 4>(N, G, variant, a, workers, s);
+    case 8:
+        if constexpr (sizeof(T) == 4) return launch_fast_v<T, 8>(N, G, variant, a, workers, s);
+        [[fallthrough]];
+    default: return fail(SPTK_EINVAL, "fast MTTKRP: bad vector width");
     }
 }
 
@@ -54,7 +68,9 @@ static int pow2ceil(int x) {
     return g;
 }
 
-static bool aligned32(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; }
+static bool aligned_to(const void *p, size_t b) {
+    return (reinterpret_cast<uintptr_t>(p) & (b - 1)) == 0;
+}
 
 sptk_status host_rowptr(sptk_tensor t, int mode, cudaStream_t s) {
     std::vector<uint32_t> &h = t->host_rowptr[mode];
@@ -184,11 +200,22 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     a.lambda = lambda;
     a.out = out;
 
-    const int V = 32 / (int)es;
-    bool fast = t->N >= 3 && t->N <= 5 && R % V == 0 && aligned32(out) &&
-                (!lambda || aligned32(lambda));
-    for (int m = 0; m < t->N && fast; ++m)
-        if (m != mode && !aligned32(factors[m])) fast = false;
+    // Lane vector width V: the widest power of two <= 32 bytes that divides R
+    // and to which every factor / out / lambda pointer is aligned (rows then
+    // start on V-element boundaries).  32-byte vectors are the measured best;
+    // narrower ones keep any R on the fast path.  The perm-gather layout is
+    // compiled for 32-byte vectors only.
+    int V = 32 / (int)es;
+    auto ok_v = [&](int v) {
+        const size_t b = (size_t)v * es;
+        if (R % v != 0 || !aligned_to(out, b) || (lambda && !aligned_to(lambda, b))) return false;
+        for (int m = 0; m < t->N; ++m)
+            if (m != mode && !aligned_to(factors[m], b)) return false;
+        return true;
+    };
+    while (V > 1 && !ok_v(V)) V >>= 1;
+    bool fast = t->N >= 3 && t->N <= 5 && ok_v(V) &&
+                (t->has_srec[mode] || V * (int)es == 32);
     const int G0 = fast ? pow2ceil((int)((R < 32 * V ? R : 32 * V) / V)) : (R <= 16 ? 4 : 32);
     a.run = run_length(pe - pb, G0);
     // warp-cooperative steps pay off when rows are long (few boundary steps)
@@ -204,8 +231,8 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     const int64_t workers = (pe - pb + chunk - 1) / chunk;
     if (t->deterministic && !(fast && t->has_srec[mode]))
         return fail(SPTK_EUNSUPPORTED,
-                    "deterministic MTTKRP needs the permuted-copy fast path (N in 3..5, R a "
-                    "multiple of 32/sizeof(value), 32-byte aligned factors/out/lambda)");
+                    "deterministic MTTKRP needs the permuted-copy fast path (N in 3..5, "
+                    "element-aligned factors/out/lambda, default layout)");
     if (t->deterministic) {
         SPTK_TRY(t->det_row.reserve(sizeof(uint32_t) * 2 * workers));
         SPTK_TRY(t->det_part.reserve(es * 2 * workers * R));
@@ -228,8 +255,8 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
             a.col0 = (int)c0;
             a.ncols = (int)((R - c0) < tile ? (R - c0) : tile);
             const int G = pow2ceil(a.ncols / V);
-            if (t->dtype == SPTK_F64) SPTK_TRY(launch_fast<double>(t->N, G, var, a, workers, s));
-            else SPTK_TRY(launch_fast<float>(t->N, G, var, a, workers, s));
+            if (t->dtype == SPTK_F64) SPTK_TRY(launch_fast<double>(t->N, V, G, var, a, workers, s));
+            else SPTK_TRY(launch_fast<float>(t->N, V, G, var, a, workers, s));
         }
     } else {
         const int G = R <= 16 ? 4 : 32;

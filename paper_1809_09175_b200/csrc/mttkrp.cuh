@@ -152,6 +152,63 @@ __device__ __forceinline__ void red_row(float *p, const float (&r)[8]) {
                  : "memory");
 }
 
+
+// VW consecutive elements of T as one load/store (VW * sizeof(T) in {4..32}
+// bytes, aligned): the lane's slice of a factor row.  vld carries the L2
+// cache-hint policy; f64 reductions are scalar (red.global.add.v2.f64 is not
+// accepted for sm_100a), f32 uses .v4 when it can.
+template <typename T, int VW>
+__device__ __forceinline__ void vld(const T *p, T (&r)[VW], uint64_t pol) {
+    if constexpr (sizeof(T) * VW == 32) {
+        ld_row_p(p, r, pol);
+    } else if constexpr (sizeof(T) == 8 && VW == 2) {
+        asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                     : "=d"(r[0]), "=d"(r[1]) : "l"(p), "l"(pol));
+    } else if constexpr (sizeof(T) == 8 && VW == 1) {
+        asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r[0]) : "l"(p), "l"(pol));
+    } else if constexpr (sizeof(T) == 4 && VW == 4) {
+        asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]) : "l"(p), "l"(pol));
+    } else if constexpr (sizeof(T) == 4 && VW == 2) {
+        asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+                     : "=f"(r[0]), "=f"(r[1]) : "l"(p), "l"(pol));
+    } else {
+        asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r[0]) : "l"(p), "l"(pol));
+    }
+}
+template <typename T, int VW>
+__device__ __forceinline__ void vld_plain(const T *p, T (&r)[VW]) {
+#pragma unroll
+    for (int v = 0; v < VW; ++v) r[v] = __ldg(p + v);
+}
+template <typename T, int VW>
+__device__ __forceinline__ void vst(T *p, const T (&r)[VW]) {
+    if constexpr (sizeof(T) * VW == 32) {
+        st_row(p, r);
+    } else if constexpr (sizeof(T) * VW == 16) {
+        if constexpr (sizeof(T) == 8) *reinterpret_cast<double2 *>(p) = make_double2(r[0], r[1]);
+        else *reinterpret_cast<float4 *>(p) = make_float4(r[0], r[1], r[2], r[3]);
+    } else if constexpr (sizeof(T) * VW == 8 && sizeof(T) == 4) {
+        *reinterpret_cast<float2 *>(p) = make_float2(r[0], r[1]);
+    } else {
+#pragma unroll
+        for (int v = 0; v < VW; ++v) p[v] = r[v];
+    }
+}
+template <typename T, int VW>
+__device__ __forceinline__ void vred(T *p, const T (&r)[VW]) {
+    if constexpr (sizeof(T) == 4 && VW % 4 == 0) {
+#pragma unroll
+        for (int v = 0; v < VW; v += 4)
+            asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p + v), "f"(r[v]),
+                         "f"(r[v + 1]), "f"(r[v + 2]), "f"(r[v + 3])
+                         : "memory");
+    } else {
+#pragma unroll
+        for (int v = 0; v < VW; ++v) atomicAdd(p + v, r[v]);
+    }
+}
+
 template <typename T> __device__ __forceinline__ T rec_val(const uint32_t (&w)[8]);
 template <> __device__ __forceinline__ double rec_val<double>(const uint32_t (&w)[8]) {
     return __hiloint2double((int)w[1], (int)w[0]);
@@ -169,9 +226,8 @@ template <> __device__ __forceinline__ float rec_val<float>(const uint32_t (&w)[
 // the worker's start row `wrow` (rows only grow along the permutation).
 // Otherwise the paper's traversal: p = perm_n[i] (prefetched one step ahead),
 // gather the full record p and read l_pn from it.
-template <typename T, int N, int MODE, int G, int U, int RB, bool SORTED>
+template <typename T, int N, int MODE, int G, int U, int RB, bool SORTED, int V>
 __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
-    constexpr int V = 32 / sizeof(T);
     constexpr int OFF = sizeof(T) / 4;  // first index word in a record
     const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t worker = gtid / G;
@@ -201,16 +257,16 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
         for (int v = 0; v < V; ++v) o[v] = acc[v];
         if (a.lambda) {  // lambda applied once per flushed row (Z1)
             T lam[V];
-            ld_row(static_cast<const T *>(a.lambda) + c, lam);
+            vld_plain<T, V>(static_cast<const T *>(a.lambda) + c, lam);
 #pragma unroll
             for (int v = 0; v < V; ++v) o[v] *= lam[v];
         }
         if (atomic && a.dpart)
-            st_row(static_cast<T *>(a.dpart) + (2 * worker + slot) * a.ld + c, o);
+            vst<T, V>(static_cast<T *>(a.dpart) + (2 * worker + slot) * a.ld + c, o);
         else if (atomic)
-            red_row(out + (int64_t)row * a.ld + c, o);
+            vred<T, V>(out + (int64_t)row * a.ld + c, o);
         else
-            st_row(out + (int64_t)row * a.ld + c, o);
+            vst<T, V>(out + (int64_t)row * a.ld + c, o);
     };
     const uint64_t pol_stream = policy_evict_first(), pol_factor = policy_evict_last();
     auto load_rec = [&](uint32_t pos, uint32_t (&r)[8]) {
@@ -279,8 +335,8 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
                 if (m != MODE) {
                     const int word = SORTED ? OFF + (m < MODE ? m : m - 1) : OFF + m;
                     if (p[u] != kNoRow && lane_on)
-                        ld_row_p(static_cast<const T *>(a.A[m]) + (int64_t)w[u][word] * a.ld + c,
-                                 f[u][m], pol_factor);
+                        vld<T, V>(static_cast<const T *>(a.A[m]) + (int64_t)w[u][word] * a.ld + c,
+                                  f[u][m], pol_factor);
                     else
 #pragma unroll
                         for (int v = 0; v < V; ++v) f[u][m][v] = T(0);
@@ -321,13 +377,13 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
     if (a.dpart && !wrote0 && q == 0) a.drow[2 * worker] = kNoRow;
 }
 
-template <typename T, int N, int G, int U, int RB, bool SORTED, int MINB>
+template <typename T, int N, int G, int U, int RB, bool SORTED, int MINB, int V>
 __global__ void __launch_bounds__(256, MINB) mttkrp_fast_kernel(const MttkrpArgs a) {
-    if constexpr (N >= 1) if (a.mode == 0) { mttkrp_fast_body<T, N, 0, G, U, RB, SORTED>(a); return; }
-    if constexpr (N >= 2) if (a.mode == 1) { mttkrp_fast_body<T, N, 1, G, U, RB, SORTED>(a); return; }
-    if constexpr (N >= 3) if (a.mode == 2) { mttkrp_fast_body<T, N, 2, G, U, RB, SORTED>(a); return; }
-    if constexpr (N >= 4) if (a.mode == 3) { mttkrp_fast_body<T, N, 3, G, U, RB, SORTED>(a); return; }
-    if constexpr (N >= 5) if (a.mode == 4) { mttkrp_fast_body<T, N, 4, G, U, RB, SORTED>(a); return; }
+    if constexpr (N >= 1) if (a.mode == 0) { mttkrp_fast_body<T, N, 0, G, U, RB, SORTED, V>(a); return; }
+    if constexpr (N >= 2) if (a.mode == 1) { mttkrp_fast_body<T, N, 1, G, U, RB, SORTED, V>(a); return; }
+    if constexpr (N >= 3) if (a.mode == 2) { mttkrp_fast_body<T, N, 2, G, U, RB, SORTED, V>(a); return; }
+    if constexpr (N >= 4) if (a.mode == 3) { mttkrp_fast_body<T, N, 3, G, U, RB, SORTED, V>(a); return; }
+    if constexpr (N >= 5) if (a.mode == 4) { mttkrp_fast_body<T, N, 4, G, U, RB, SORTED, V>(a); return; }
 }
 
 // ------------------------------------------------- warp-cooperative body
@@ -343,9 +399,8 @@ __global__ void __launch_bounds__(256, MINB) mttkrp_fast_kernel(const MttkrpArgs
 // from the owning group) and every completed row is flushed -- atomically if
 // it is the chunk's first row, otherwise with a plain store; the last row of
 // the chunk is flushed atomically at the end (P:521-523 with worker = warp).
-template <typename T, int N, int MODE, int G, int U, int RB>
+template <typename T, int N, int MODE, int G, int U, int RB, int V>
 __device__ __forceinline__ void mttkrp_coop_body(const MttkrpArgs &a) {
-    constexpr int V = 32 / sizeof(T);
     constexpr int OFF = sizeof(T) / 4;
     constexpr int NG = 32 / G;
     const int64_t warp_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -371,16 +426,16 @@ __device__ __forceinline__ void mttkrp_coop_body(const MttkrpArgs &a) {
         for (int v = 0; v < V; ++v) o[v] = val[v];
         if (a.lambda) {
             T lam[V];
-            ld_row(static_cast<const T *>(a.lambda) + c, lam);
+            vld_plain<T, V>(static_cast<const T *>(a.lambda) + c, lam);
 #pragma unroll
             for (int v = 0; v < V; ++v) o[v] *= lam[v];
         }
         if (atomic && a.dpart)
-            st_row(static_cast<T *>(a.dpart) + (2 * warp_id + slot) * a.ld + c, o);
+            vst<T, V>(static_cast<T *>(a.dpart) + (2 * warp_id + slot) * a.ld + c, o);
         else if (atomic)
-            red_row(out + (int64_t)row * a.ld + c, o);
+            vred<T, V>(out + (int64_t)row * a.ld + c, o);
         else
-            st_row(out + (int64_t)row * a.ld + c, o);
+            vst<T, V>(out + (int64_t)row * a.ld + c, o);
     };
     const uint64_t pol_stream = policy_evict_first(), pol_factor = policy_evict_last();
     auto load_rec = [&](uint32_t pos, uint32_t (&r)[8]) {
@@ -422,8 +477,8 @@ __device__ __forceinline__ void mttkrp_coop_body(const MttkrpArgs &a) {
                     if (m != MODE) {
                         const int word = OFF + (m < MODE ? m : m - 1);
                         if (base + u * NG + g < e && lane_on)
-                            ld_row_p(static_cast<const T *>(a.A[m]) + (int64_t)w[u][word] * a.ld + c,
-                                     f[u][m], pol_factor);
+                            vld<T, V>(static_cast<const T *>(a.A[m]) + (int64_t)w[u][word] * a.ld + c,
+                                      f[u][m], pol_factor);
                         else
 #pragma unroll
                             for (int v = 0; v < V; ++v) f[u][m][v] = T(0);
@@ -493,13 +548,13 @@ __device__ __forceinline__ void mttkrp_coop_body(const MttkrpArgs &a) {
     if (a.dpart && !wrote0 && lane == 0) a.drow[2 * warp_id] = kNoRow;
 }
 
-template <typename T, int N, int G, int U, int RB, int MINB>
+template <typename T, int N, int G, int U, int RB, int MINB, int V>
 __global__ void __launch_bounds__(256, MINB) mttkrp_coop_kernel(const MttkrpArgs a) {
-    if constexpr (N >= 1) if (a.mode == 0) { mttkrp_coop_body<T, N, 0, G, U, RB>(a); return; }
-    if constexpr (N >= 2) if (a.mode == 1) { mttkrp_coop_body<T, N, 1, G, U, RB>(a); return; }
-    if constexpr (N >= 3) if (a.mode == 2) { mttkrp_coop_body<T, N, 2, G, U, RB>(a); return; }
-    if constexpr (N >= 4) if (a.mode == 3) { mttkrp_coop_body<T, N, 3, G, U, RB>(a); return; }
-    if constexpr (N >= 5) if (a.mode == 4) { mttkrp_coop_body<T, N, 4, G, U, RB>(a); return; }
+    if constexpr (N >= 1) if (a.mode == 0) { mttkrp_coop_body<T, N, 0, G, U, RB, V>(a); return; }
+    if constexpr (N >= 2) if (a.mode == 1) { mttkrp_coop_body<T, N, 1, G, U, RB, V>(a); return; }
+    if constexpr (N >= 3) if (a.mode == 2) { mttkrp_coop_body<T, N, 2, G, U, RB, V>(a); return; }
+    if constexpr (N >= 4) if (a.mode == 3) { mttkrp_coop_body<T, N, 3, G, U, RB, V>(a); return; }
+    if constexpr (N >= 5) if (a.mode == 4) { mttkrp_coop_body<T, N, 4, G, U, RB, V>(a); return; }
 }
 
 // ---------------------------------------------------- generic kernel
@@ -592,15 +647,15 @@ constexpr int kNumVariants = 2;
 #endif
 constexpr int kU = SPTK_KU, kMinBlocks = SPTK_KMINB;
 
-template <typename T, int N, int RB, bool SORTED, bool COOP>
+template <typename T, int N, int RB, bool SORTED, bool COOP, int V>
 inline sptk_status fast_launch_g(int G, const MttkrpArgs &a, int64_t workers, cudaStream_t s) {
     const int64_t threads = COOP ? workers * 32 : workers * G;
     const unsigned blocks = (unsigned)((threads + 255) / 256);
 #define SPTK_LAUNCH_G(GG)                                                                     \
     if constexpr (COOP)                                                                       \
-        mttkrp_coop_kernel<T, N, GG, kU, RB, kMinBlocks><<<blocks, 256, 0, s>>>(a);           \
+        mttkrp_coop_kernel<T, N, GG, kU, RB, kMinBlocks, V><<<blocks, 256, 0, s>>>(a);        \
     else                                                                                      \
-        mttkrp_fast_kernel<T, N, GG, kU, RB, SORTED, kMinBlocks><<<blocks, 256, 0, s>>>(a);
+        mttkrp_fast_kernel<T, N, GG, kU, RB, SORTED, kMinBlocks, V><<<blocks, 256, 0, s>>>(a);
     switch (G) {
     case 1: SPTK_LAUNCH_G(1) break;
     case 2: SPTK_LAUNCH_G(2) break;
@@ -616,21 +671,26 @@ inline sptk_status fast_launch_g(int G, const MttkrpArgs &a, int64_t workers, cu
     return SPTK_OK;
 }
 
-// Per-(T, N) launcher, explicitly instantiated in mttkrp_<t>_n<N>.cu.
-// `workers` counts groups (variant 0) or warps (variant 1).
-template <typename T, int N>
-sptk_status launch_fast_tn(int G, int variant, const MttkrpArgs &a, int64_t workers,
-                           cudaStream_t s);
+// Per-(T, N, V) launcher, explicitly instantiated in mttkrp_<t>_n<N>_v<V>.cu.
+// `workers` counts groups (variant 0) or warps (variant 1).  The perm-gather
+// layout is compiled for the widest vector only (other R use the generic kernel).
+template <typename T, int N, int V>
+sptk_status launch_fast_tnv(int G, int variant, const MttkrpArgs &a, int64_t workers,
+                            cudaStream_t s);
 
-#define SPTK_INSTANTIATE_FAST(T, N)                                                          \
+#define SPTK_INSTANTIATE_FAST(T, N, V)                                                       \
     template <>                                                                              \
-    sptk_status launch_fast_tn<T, N>(int G, int variant, const MttkrpArgs &a,                \
-                                     int64_t workers, cudaStream_t s) {                      \
+    sptk_status launch_fast_tnv<T, N, V>(int G, int variant, const MttkrpArgs &a,            \
+                                         int64_t workers, cudaStream_t s) {                  \
         constexpr int RB = (sizeof(T) + 4 * N <= 16) ? 16 : 32;        /* full record */      \
         constexpr int RC = (sizeof(T) + 4 * (N - 1) <= 16) ? 16 : 32;  /* compact copy */     \
-        if (a.perm) return fast_launch_g<T, N, RB, false, false>(G, a, workers, s);          \
-        if (variant == 1) return fast_launch_g<T, N, RC, true, true>(G, a, workers, s);      \
-        return fast_launch_g<T, N, RC, true, false>(G, a, workers, s);                       \
+        if (a.perm) {                                                                        \
+            if constexpr (V * sizeof(T) == 32)                                               \
+                return fast_launch_g<T, N, RB, false, false, V>(G, a, workers, s);           \
+            return fail(SPTK_EINVAL, "perm-gather fast path needs 32-byte vectors");         \
+        }                                                                                    \
+        if (variant == 1) return fast_launch_g<T, N, RC, true, true, V>(G, a, workers, s);   \
+        return fast_launch_g<T, N, RC, true, false, V>(G, a, workers, s);                    \
     }
 
 template <typename T>

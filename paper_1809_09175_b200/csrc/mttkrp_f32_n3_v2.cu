@@ -1,0 +1,6 @@
+// mttkrp_f32_n3_v2.cu -- fast MTTKRP kernels for float, N = 3, 2-element lane vectors (see mttkrp.cuh).
+#include "mttkrp.cuh"
+
+namespace sptk {
+SPTK_INSTANTIATE_FAST(float, 3, 2)
+}  // namespace sptk

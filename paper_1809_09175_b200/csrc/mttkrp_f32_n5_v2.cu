@@ -1,0 +1,6 @@
+// mttkrp_f32_n5_v2.cu -- fast MTTKRP kernels for float, N = 5, 2-element lane vectors (see mttkrp.cuh).
+#include "mttkrp.cuh"
+
+namespace sptk {
+SPTK_INSTANTIATE_FAST(float, 5, 2)
+}  // namespace sptk

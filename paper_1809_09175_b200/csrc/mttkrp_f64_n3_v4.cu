@@ -1,0 +1,6 @@
+// mttkrp_f64_n3_v4.cu -- fast MTTKRP kernels for double, N = 3, 4-element lane vectors (see mttkrp.cuh).
+#include "mttkrp.cuh"
+
+namespace sptk {
+SPTK_INSTANTIATE_FAST(double, 3, 4)
+}  // namespace sptk

@@ -1,0 +1,6 @@
+// mttkrp_f64_n4_v4.cu -- fast MTTKRP kernels for double, N = 4, 4-element lane vectors (see mttkrp.cuh).
+#include "mttkrp.cuh"
+
+namespace sptk {
+SPTK_INSTANTIATE_FAST(double, 4, 4)
+}  // namespace sptk

@@ -114,7 +114,10 @@ def test_perm_golden_and_empty(sp):
 @pytest.mark.parametrize("layout", ["sorted", "perm_gather"])
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
 @pytest.mark.parametrize("N,R", [(3, 8), (3, 16), (3, 64), (3, 128), (3, 256), (4, 16),
-                                 (5, 16), (3, 24), (4, 32)])
+                                 (5, 16), (3, 24), (4, 32),
+                                 # R not a multiple of 32 bytes: narrower lane vectors
+                                 (3, 1), (3, 10), (3, 17), (3, 20), (4, 6), (5, 13), (3, 100),
+                                 (3, 258)])
 def test_mttkrp_fast_path_parity(sp, layout, dtype, N, R):
     dims = [57, 1203, 311, 40, 9][:N]
     P = 5 * 4096 + 123
@@ -585,16 +588,15 @@ def test_mttkrp_property_random_shapes(sp):
     run()
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant,R", [(0, 16), (1, 16), (0, 10), (1, 6)])
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
-def test_deterministic_mode_bitwise(sp, variant, dtype):
+def test_deterministic_mode_bitwise(sp, variant, R, dtype):
     """SPTK_CREATE_DETERMINISTIC: boundary rows summed in worker order ->
     repeated runs are bit-identical; values match the oracle; CP-ALS too."""
     dims = (3000, 200, 64)
     idx, vals = synth.tensor(61, dims, 40 * 4096 + 9, "powerlaw")   # hot rows span many workers
     npd = np.float64 if dtype == torch.float64 else np.float32
     vals = vals.astype(npd)
-    R = 16
     A = factors_np(62, dims, R, npd)
     t = sp.sptensor_create(dims, dev(idx.astype(np.int64)), dev(vals, dtype), deterministic=True)
     sp.build_perm(t, -1)
@@ -616,8 +618,13 @@ def test_deterministic_mode_bitwise(sp, variant, dtype):
         r2 = sp.cp_als(t, R, 5, F2, seed=3)
         assert np.array_equal(r1["trace"], r2["trace"])
         assert all(torch.equal(F1[m], F2[m]) for m in range(3))
+    d2 = (300, 40)                                    # N = 2: generic kernel only
+    i2, v2 = synth.tensor(63, d2, 999, "uniform")
+    t2 = sp.sptensor_create(d2, dev(i2.astype(np.int64)), dev(v2.astype(npd), dtype),
+                            deterministic=True)
+    sp.build_perm(t2, -1)
     with pytest.raises(sp.SptkError) as e:
-        gpu_mttkrp(sp, t, 0, factors_np(63, dims, 17, npd), 17, dtype)   # generic path
+        gpu_mttkrp(sp, t2, 0, factors_np(64, d2, R, npd), R, dtype)
     assert e.value.name == "EUNSUPPORTED"
 
 
