@@ -634,8 +634,11 @@ __global__ void __launch_bounds__(256) mttkrp_generic_kernel(const MttkrpArgs a)
     if (cur != kNoRow) flush(cur, true);
 }
 
-// Launch shapes: U positions per step per group, >= 3 resident 256-thread
-// blocks per SM (register cap 85).  Variant 0: per-group runs
+// Launch shapes: U positions per step per group; >= 3 resident 256-thread
+// blocks per SM (register cap 80) for N = 3, >= 2 (cap 128) for N >= 4, whose
+// U(N-1) gathered 32-byte slices spill under the 80-register cap (measured on
+// the Delicious shape, N = 4: -9 % with 2 blocks; NELL-2, N = 3: +20 %
+// with 2 blocks, profiles/r01/ab_minblocks.log).  Variant 0: per-group runs
 // (mttkrp_fast_kernel); variant 1: warp-cooperative steps
 // (mttkrp_coop_kernel, permuted copy only).
 constexpr int kNumVariants = 2;
@@ -645,7 +648,11 @@ constexpr int kNumVariants = 2;
 #ifndef SPTK_KMINB
 #define SPTK_KMINB 3
 #endif
-constexpr int kU = SPTK_KU, kMinBlocks = SPTK_KMINB;
+#ifndef SPTK_KMINB_WIDE
+#define SPTK_KMINB_WIDE 2
+#endif
+constexpr int kU = SPTK_KU;
+template <int N> constexpr int kMinBlocks = N <= 3 ? SPTK_KMINB : SPTK_KMINB_WIDE;
 
 template <typename T, int N, int RB, bool SORTED, bool COOP, int V>
 inline sptk_status fast_launch_g(int G, const MttkrpArgs &a, int64_t workers, cudaStream_t s) {
@@ -653,9 +660,9 @@ inline sptk_status fast_launch_g(int G, const MttkrpArgs &a, int64_t workers, cu
     const unsigned blocks = (unsigned)((threads + 255) / 256);
 #define SPTK_LAUNCH_G(GG)                                                                     \
     if constexpr (COOP)                                                                       \
-        mttkrp_coop_kernel<T, N, GG, kU, RB, kMinBlocks, V><<<blocks, 256, 0, s>>>(a);        \
+        mttkrp_coop_kernel<T, N, GG, kU, RB, kMinBlocks<N>, V><<<blocks, 256, 0, s>>>(a);        \
     else                                                                                      \
-        mttkrp_fast_kernel<T, N, GG, kU, RB, SORTED, kMinBlocks, V><<<blocks, 256, 0, s>>>(a);
+        mttkrp_fast_kernel<T, N, GG, kU, RB, SORTED, kMinBlocks<N>, V><<<blocks, 256, 0, s>>>(a);
     switch (G) {
     case 1: SPTK_LAUNCH_G(1) break;
     case 2: SPTK_LAUNCH_G(2) break;
