@@ -651,7 +651,10 @@ constexpr int kNumVariants = 2;
 #ifndef SPTK_KMINB_WIDE
 #define SPTK_KMINB_WIDE 2
 #endif
-constexpr int kU = SPTK_KU;
+#ifndef SPTK_KU_WIDE
+#define SPTK_KU_WIDE SPTK_KU
+#endif
+template <int N> constexpr int kU = N <= 3 ? SPTK_KU : SPTK_KU_WIDE;
 template <int N> constexpr int kMinBlocks = N <= 3 ? SPTK_KMINB : SPTK_KMINB_WIDE;
 
 template <typename T, int N, int RB, bool SORTED, bool COOP, int V>
@@ -660,9 +663,9 @@ inline sptk_status fast_launch_g(int G, const MttkrpArgs &a, int64_t workers, cu
     const unsigned blocks = (unsigned)((threads + 255) / 256);
 #define SPTK_LAUNCH_G(GG)                                                                     \
     if constexpr (COOP)                                                                       \
-        mttkrp_coop_kernel<T, N, GG, kU, RB, kMinBlocks<N>, V><<<blocks, 256, 0, s>>>(a);        \
+        mttkrp_coop_kernel<T, N, GG, kU<N>, RB, kMinBlocks<N>, V><<<blocks, 256, 0, s>>>(a);        \
     else                                                                                      \
-        mttkrp_fast_kernel<T, N, GG, kU, RB, SORTED, kMinBlocks<N>, V><<<blocks, 256, 0, s>>>(a);
+        mttkrp_fast_kernel<T, N, GG, kU<N>, RB, SORTED, kMinBlocks<N>, V><<<blocks, 256, 0, s>>>(a);
     switch (G) {
     case 1: SPTK_LAUNCH_G(1) break;
     case 2: SPTK_LAUNCH_G(2) break;
