@@ -282,15 +282,24 @@ def main():
     torch.cuda.synchronize()
     del idx_d, val_d
     torch.cuda.empty_cache()  # return the COO staging to the driver (perm copies need it)
-    perm_ms, perm_first_ms = [], []
+    # the paper's preprocessing (Table `sorting_cost`): one
+    # build_perm of every mode right after ingest -- sorts from the keys the
+    # ingest pass emitted, allocations and the permuted copies included
+    a, b = ev(), ev()
+    h0 = time.perf_counter()
+    a.record()
+    sp.build_perm(t, -1)
+    b.record()
+    torch.cuda.synchronize()
+    perm_all_ms, perm_all_host_ms = a.elapsed_time(b), 1e3 * (time.perf_counter() - h0)
+    perm_ms = []   # steady-state re-sort per mode (keys extracted from the records)
     for n in range(c.N):
-        for rep in range(2):        # first call includes lazy module load + allocations
-            a, b = ev(), ev()
-            a.record()
-            sp.build_perm(t, n)
-            b.record()
-            torch.cuda.synchronize()
-            (perm_first_ms if rep == 0 else perm_ms).append(a.elapsed_time(b))
+        a, b = ev(), ev()
+        a.record()
+        sp.build_perm(t, n)
+        b.record()
+        torch.cuda.synchronize()
+        perm_ms.append(a.elapsed_time(b))
     F = [sdev.factor(c.seed_f, c.N, m, I, R, dtype=tdt) for m, I in enumerate(c.dims)]
     dev_bytes = sp.sptensor_device_bytes(t)
 
@@ -419,8 +428,9 @@ def main():
             "b_model_bytes_per_step": bm_total,
             "gflops": sum(metrics.flops(c.N, c.nnz, R) for _ in c.dims) / (ms_max * 1e-3) / 1e9,
             "setup": {"generate_ms": e0.elapsed_time(e1), "create_ms": e1.elapsed_time(e2),
-                      "build_perm_ms": perm_ms, "build_perm_first_call_ms": perm_first_ms,
-                      "sort_to_iteration_ratio": sum(perm_ms) / ms_max,
+                      "build_perm_all_ms": perm_all_ms, "build_perm_all_host_ms": perm_all_host_ms,
+                      "resort_ms_per_mode": perm_ms,
+                      "sort_to_iteration_ratio": perm_all_host_ms / ms_max,
                       "tensor_device_bytes": dev_bytes},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

@@ -180,6 +180,18 @@ sptk_status sptk_sptensor_create(int nmodes, const int64_t *dims, int64_t nnz, c
             }
             dvals = svals.p;
         }
+        if (!(flags & (SPTK_CREATE_DUP_SUM | SPTK_CREATE_DUP_ERROR))) {
+            // emit the sort keys at ingest when they fit next to a reserve
+            // (otherwise build_perm extracts them from the records per mode)
+            const size_t kb = sizeof(uint32_t) * (size_t)nnz * nmodes;
+            size_t free_b = 0, total_b = 0;
+            if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+                const size_t reserve = std::max<size_t>(total_b / 32, (size_t)4 << 30);
+                if (free_b >= kb + reserve && t->keys.reserve(kb) != SPTK_OK) set_error("");
+            } else {
+                cudaGetLastError();
+            }
+        }
         if ((st = flag.reserve(16)) != SPTK_OK) goto bad;
         int *d_flag = flag.as<int>();
         double *d_norm = reinterpret_cast<double *>(flag.as<char>() + 8);
@@ -237,7 +249,7 @@ sptk_status sptk_sptensor_device_bytes(sptk_tensor t, int64_t *bytes) {
     int64_t b = t->rec.bytes;
     for (int m = 0; m < t->N; ++m)
         b += t->perm[m].bytes + t->rowptr[m].bytes + t->srec[m].bytes + t->wrow[m].bytes;
-    b += t->sortws.bytes;
+    b += t->sortws.bytes + t->keys.bytes;
     const ALSWork &w = t->als;
     b += w.V.bytes + w.G.bytes + w.L.bytes + w.partial.bytes + w.colsq.bytes + w.lam.bytes +
          w.scal.bytes + w.stage.bytes + w.lamT.bytes;
@@ -255,6 +267,9 @@ sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream) {
         if (st == SPTK_ECUDA) t->poisoned = true;
         if (st != SPTK_OK) return st;
     }
+    bool all = true;  // the ingest keys are consumed once every mode is sorted
+    for (int m = 0; m < t->N; ++m) all = all && t->has_perm[m];
+    if (all) t->keys.release();
     for (int m = m0; m < m1; ++m) {  // then the permuted copies, while memory allows
         sptk_status st = ensure_sorted_copy(t, m, s);
         if (st == SPTK_ECUDA) t->poisoned = true;

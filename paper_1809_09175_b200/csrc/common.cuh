@@ -106,6 +106,8 @@ struct sptk_tensor_s {
     bool has_srec[sptk::kMaxModes] = {false};
     sptk::DevBuf wrow[sptk::kMaxModes];         // worker start rows for the copy (cached)
     sptk::DevBuf sortws;                        // radix-sort workspace (cached)
+    sptk::DevBuf keys;                          // uint32[N][P] sort keys emitted at ingest
+                                                // (consumed by build_perm, then released)
     bool deterministic = false;                 // SPTK_CREATE_DETERMINISTIC
     sptk::DevBuf det_row, det_part;             // boundary-row partials (deterministic mode)
     int64_t wrow_key[sptk::kMaxModes][3] = {{-1, -1, -1}};  // (pos_begin, pos_end, run)

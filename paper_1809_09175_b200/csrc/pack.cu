@@ -4,7 +4,10 @@
 // permuted access to nonzero p is a single aligned 16/32-byte load (§5 P:516:
 // "nonzeros are ... accessed in a more random fashion").  Also produces
 // ||X||^2 = sum x_i^2 (cached for the CP-ALS fit) with a deterministic
-// two-stage reduction.
+// two-stage reduction.  When memory allows, the same pass also emits every
+// mode's sort keys as uint32[N][P] (the conclusion's "sorting ... while the
+// tensor is being read"): build_perm's radix sorts then start from
+// them instead of re-reading the 16/32-byte records once per mode.
 #include "common.cuh"
 
 namespace sptk {
@@ -17,7 +20,8 @@ __global__ void __launch_bounds__(256) pack_kernel(const I *__restrict__ idx,
                                                    const int64_t *__restrict__ dims_unused,
                                                    uint64_t d0, uint64_t d1, uint64_t d2,
                                                    uint64_t d3, uint64_t d4, uint64_t d5,
-                                                   uint8_t *__restrict__ rec, int *flag,
+                                                   uint8_t *__restrict__ rec,
+                                                   uint32_t *__restrict__ keys, int *flag,
                                                    double *__restrict__ partial) {
     const uint64_t dims[6] = {d0, d1, d2, d3, d4, d5};
     double sq = 0.0;
@@ -42,6 +46,7 @@ __global__ void __launch_bounds__(256) pack_kernel(const I *__restrict__ idx,
                 const int64_t c = (int64_t)idx[i * N + m];
                 if (c < 0 || (uint64_t)c >= dims[m]) bad = 1;
                 if (off + m < RB / 4) w[off + m] = (uint32_t)c;
+                if (keys) keys[(size_t)m * P + i] = (uint32_t)c;
             }
         }
         uint4 *dst = reinterpret_cast<uint4 *>(rec + (size_t)i * RB);
@@ -70,11 +75,11 @@ static void pack_dispatch(sptk_tensor t, const void *idx, const void *vals, int 
     if (t->rec_bytes == 16)
         pack_kernel<T, I, 16><<<blocks, 256, 0, s>>>(
             (const I *)idx, (const T *)vals, t->P, t->N, nullptr, dm(0), dm(1), dm(2), dm(3),
-            dm(4), dm(5), t->rec.as<uint8_t>(), flag, partial);
+            dm(4), dm(5), t->rec.as<uint8_t>(), t->keys.as<uint32_t>(), flag, partial);
     else
         pack_kernel<T, I, 32><<<blocks, 256, 0, s>>>(
             (const I *)idx, (const T *)vals, t->P, t->N, nullptr, dm(0), dm(1), dm(2), dm(3),
-            dm(4), dm(5), t->rec.as<uint8_t>(), flag, partial);
+            dm(4), dm(5), t->rec.as<uint8_t>(), t->keys.as<uint32_t>(), flag, partial);
 }
 
 sptk_status launch_pack(sptk_tensor t, const void *idx, sptk_idx_type itype, const void *vals,

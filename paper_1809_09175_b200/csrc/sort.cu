@@ -103,21 +103,20 @@ __global__ void __launch_bounds__(kSortThreads)
     const uint32_t tile_n = min((uint32_t)kSortTile, P - tile0);
     const uint32_t base = tile0 + warp * (uint32_t)kWarpChunk;
     const uint32_t lt = lanemask_lt();
-    uint32_t key[kSortItems];
+    // all loads of the tile up front (the values too: loading them inside the
+    // ranking loop left pass 2 latency-bound on long-scoreboard stalls)
+    uint32_t key[kSortItems], val[kSortItems];
 #pragma unroll
     for (int r = 0; r < kSortItems; ++r) {
         const uint32_t i = base + r * 32 + lane;
         key[r] = i < P ? __ldg(keys_in + i) : 0xffffffffu;
+        val[r] = vals_in ? (i < P ? __ldg(vals_in + i) : 0u) : i;
     }
-    // A: per-warp digit histogram of its 512-key sub-chunk
+    // A: per-warp digit histogram of its 512-key sub-chunk (shared atomics:
+    //    the ballot ranking is needed only for the stable positions in C)
 #pragma unroll
-    for (int r = 0; r < kSortItems; ++r) {
-        const bool valid = base + r * 32 + lane < P;
-        const uint32_t digit = valid ? (key[r] >> shift) & mask : 0u;
-        const uint32_t peers = digit_peers(digit, dbits, valid);
-        if (valid && (peers & lt) == 0) whist[warp][digit] += __popc(peers);
-        __syncwarp();
-    }
+    for (int r = 0; r < kSortItems; ++r)
+        if (base + r * 32 + lane < P) atomicAdd(&whist[warp][(key[r] >> shift) & mask], 1u);
     __syncthreads();
     // B: tile-local digit starts (exclusive scan over digits of the tile counts)
     //    and per-warp starts within each digit
@@ -164,7 +163,7 @@ __global__ void __launch_bounds__(kSortThreads)
         __syncwarp();
         if (valid) {
             skey[pos] = key[r];
-            sval[pos] = vals_in ? __ldg(vals_in + i) : i;
+            sval[pos] = val[r];
         }
     }
     __syncthreads();
@@ -431,13 +430,17 @@ static sptk_status stable_sort_ids(sptk_tensor t, int mode, const uint32_t *in, 
     const int kw = dtype_bytes(t->dtype) / 4 + mode;
     // pass-0 keys: one pass over the records (kbuf of the other parity is free until then)
     uint32_t *k0 = kbuf[(npass - 1) & 1] == kA ? kB : kA;
-    if (in)
+    if (!in && t->keys.p) {
+        k0 = t->keys.as<uint32_t>() + (size_t)mode * P;  // emitted at ingest (pack.cu)
+    } else if (in)
         extract_keys_through<<<grid_for(P), 256, 0, s>>>(t->rec.as<uint8_t>(), t->rec_bytes, kw, in,
                                                          P, k0);
     else
         extract_keys<<<grid_for(P), 256, 0, s>>>(t->rec.as<uint8_t>(), t->rec_bytes, kw, P, k0);
-    count_launch();
-    SPTK_CUDA(cudaGetLastError());
+    if (in || !t->keys.p) {
+        count_launch();
+        SPTK_CUDA(cudaGetLastError());
+    }
     const uint32_t *kin = k0, *vin = in;
     for (int p = 0; p < npass; ++p) {
         const int shift = p * dbits;

@@ -87,12 +87,15 @@ def test_perm_bitexact(sp, case):
     dist, dims, P = case
     idx, vals = synth.tensor(41, dims, P, dist)
     t = make(sp, dims, idx, vals)
-    sp.build_perm(t, -1)
+    sp.build_perm(t, -1)            # sorts from the keys the ingest pass emitted
     for n in range(len(dims)):
         p, rp = gpu_perm(sp, t, n)
         po, rpo = oracle.perm(idx, n, dims[n])
         assert np.array_equal(p, po), f"mode {n}"
         assert np.array_equal(rp, rpo), f"mode {n}"
+    sp.build_perm(t, 0)             # keys released: re-sort extracts them from the records
+    p, rp = gpu_perm(sp, t, 0)
+    assert np.array_equal(p, oracle.perm(idx, 0, dims[0])[0])
 
 
 def test_perm_golden_and_empty(sp):
