@@ -267,14 +267,14 @@ sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream) {
         if (st == SPTK_ECUDA) t->poisoned = true;
         if (st != SPTK_OK) return st;
     }
-    bool all = true;  // the ingest keys are consumed once every mode is sorted
-    for (int m = 0; m < t->N; ++m) all = all && t->has_perm[m];
-    if (all) t->keys.release();
     for (int m = m0; m < m1; ++m) {  // then the permuted copies, while memory allows
         sptk_status st = ensure_sorted_copy(t, m, s);
         if (st == SPTK_ECUDA) t->poisoned = true;
         if (st != SPTK_OK) return st;
     }
+    bool all = true;  // the ingest keys are consumed once every mode is sorted
+    for (int m = 0; m < t->N; ++m) all = all && t->has_perm[m];
+    if (all) t->keys.release();
     // keep the sort workspace for the next build_perm only while memory is plentiful
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {

@@ -11,6 +11,8 @@
 //              [w*512, w*512+512) and ranks equal digits with per-bit ballots
 //              in rounds of 32, so equal keys keep their storage order.
 // Then rowptr_n[r] = first sorted position with key >= r (boundary kernel).
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -342,10 +344,30 @@ static int grid_for(int64_t n) {
     return b < 1 ? 1 : (int)b;
 }
 
+static sptk_status stable_sort_ids(sptk_tensor t, int mode, const uint32_t *in, uint32_t *out,
+                                   uint32_t **keys_out, cudaStream_t s);
+
+// Secondary key of the copy order: the shortest other mode whose factor does
+// not stay L1-resident (>= 2048 rows, 256 KB at R = 16 fp64), or -1.
+static int copy_secondary_mode(sptk_tensor t, int mode) {
+    const char *e = getenv("SPTK_COPY_ORDER");
+    if (e && *e == '0') return -1;
+    int a = -1;
+    for (int m = 0; m < t->N; ++m)
+        if (m != mode && t->dims[m] >= 2048 && (a < 0 || t->dims[m] < t->dims[a])) a = m;
+    return a;
+}
+
 // Materialise the compact permuted copy of `mode` unless the tensor keeps the
 // paper's perm-gather traversal or the copy would leave less than the reserve
 // free (then that mode keeps gathering through perm_n).  Copies are caches:
 // build_perm releases them if a sort needs their memory.
+//
+// Copy order: sorted by l_n like perm_n (same rows, same row segments, same
+// rowptr_n), but inside a row by the secondary mode a's index, then storage
+// order -- the stable sort by l_n of perm_a.  Nonzeros of one row that share
+// l_a are then adjacent and their A_a row is gathered once into L1 instead of
+// once per nonzero; the row's sum is the same up to summation order.
 sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
     if (t->has_srec[mode] || t->perm_gather_only || t->P == 0 || !t->has_perm[mode])
         return SPTK_OK;
@@ -357,7 +379,13 @@ sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
         return SPTK_OK;
     }
     const size_t reserve = std::max<size_t>(total_b / 32, (size_t)4 << 30);
-    if (free_b < need + reserve && t->sortws.p) {  // the sort workspace is a cache too
+    int a = copy_secondary_mode(t, mode);
+    // the secondary sort reuses the cached sort workspace; skip it (paper
+    // order) when that workspace is gone or memory is short
+    if (a >= 0 && (!t->has_perm[a] || !t->sortws.p)) a = -1;
+    const size_t order_bytes = a >= 0 ? sizeof(uint32_t) * (size_t)t->P : 0;
+    if (free_b < need + order_bytes + reserve) a = -1;
+    if (a < 0 && free_b < need + reserve && t->sortws.p) {  // the sort workspace is a cache too
         free_b += t->sortws.bytes;
         t->sortws.release();
     }
@@ -366,19 +394,27 @@ sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
         set_error("");
         return SPTK_OK;
     }
-    const uint32_t *perm = t->perm[mode].as<uint32_t>();
+    const uint32_t *order = t->perm[mode].as<uint32_t>();
+    DevBuf ord;
+    if (a >= 0 && ord.reserve(order_bytes) == SPTK_OK) {
+        SPTK_TRY(stable_sort_ids(t, mode, t->perm[a].as<uint32_t>(), ord.as<uint32_t>(), nullptr, s));
+        order = ord.as<uint32_t>();
+    } else {
+        set_error("");
+    }
     const int vw = dtype_bytes(t->dtype) / 4;
     const unsigned g = (unsigned)grid_for(t->P);
     uint8_t *dst = t->srec[mode].as<uint8_t>();
     const uint8_t *src = t->rec.as<uint8_t>();
     if (t->rec_bytes == 32 && rc == 32)
-        permute_records<32, 32><<<g, 256, 0, s>>>(src, perm, t->P, vw, t->N, mode, dst);
+        permute_records<32, 32><<<g, 256, 0, s>>>(src, order, t->P, vw, t->N, mode, dst);
     else if (t->rec_bytes == 32)
-        permute_records<32, 16><<<g, 256, 0, s>>>(src, perm, t->P, vw, t->N, mode, dst);
+        permute_records<32, 16><<<g, 256, 0, s>>>(src, order, t->P, vw, t->N, mode, dst);
     else
-        permute_records<16, 16><<<g, 256, 0, s>>>(src, perm, t->P, vw, t->N, mode, dst);
+        permute_records<16, 16><<<g, 256, 0, s>>>(src, order, t->P, vw, t->N, mode, dst);
     count_launch();
     SPTK_CUDA(cudaGetLastError());
+    if (ord.p) SPTK_CUDA(cudaStreamSynchronize(s));  // `ord` is freed on return
     t->has_srec[mode] = true;
     return SPTK_OK;
 }
@@ -399,6 +435,15 @@ __global__ void __launch_bounds__(256) extract_keys_through(const uint8_t *__res
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
          i += (int64_t)gridDim.x * blockDim.x)
         keys[i] = __ldg(reinterpret_cast<const uint32_t *>(rec + (size_t)__ldg(in + i) * rb) + kw);
+}
+
+// keys[i] = key_n[in[i]] from the ingest keys (4-byte gathers, not 16/32-byte records)
+__global__ void __launch_bounds__(256) gather_keys(const uint32_t *__restrict__ key_n,
+                                                   const uint32_t *__restrict__ in, int64_t P,
+                                                   uint32_t *__restrict__ keys) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+         i += (int64_t)gridDim.x * blockDim.x)
+        keys[i] = __ldg(key_n + __ldg(in + i));
 }
 
 // Stable LSD radix sort of nonzero ids by l_{., mode}.  `in` is the input
@@ -432,12 +477,14 @@ static sptk_status stable_sort_ids(sptk_tensor t, int mode, const uint32_t *in, 
     uint32_t *k0 = kbuf[(npass - 1) & 1] == kA ? kB : kA;
     if (!in && t->keys.p) {
         k0 = t->keys.as<uint32_t>() + (size_t)mode * P;  // emitted at ingest (pack.cu)
-    } else if (in)
+    } else if (in && t->keys.p)
+        gather_keys<<<grid_for(P), 256, 0, s>>>(t->keys.as<uint32_t>() + (size_t)mode * P, in, P, k0);
+    else if (in)
         extract_keys_through<<<grid_for(P), 256, 0, s>>>(t->rec.as<uint8_t>(), t->rec_bytes, kw, in,
                                                          P, k0);
     else
         extract_keys<<<grid_for(P), 256, 0, s>>>(t->rec.as<uint8_t>(), t->rec_bytes, kw, P, k0);
-    if (in || !t->keys.p) {
+    if (in || !t->keys.p) {  // a key kernel ran
         count_launch();
         SPTK_CUDA(cudaGetLastError());
     }
