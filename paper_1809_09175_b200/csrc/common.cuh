@@ -105,6 +105,10 @@ struct sptk_tensor_s {
     sptk::DevBuf srec[sptk::kMaxModes];         // compact records in perm_n order (optional)
     bool has_srec[sptk::kMaxModes] = {false};
     sptk::DevBuf wrow[sptk::kMaxModes];         // worker start rows for the copy (cached)
+    int copy_sec[sptk::kMaxModes] = {-1, -1, -1, -1, -1, -1};  // copy's secondary mode
+    sptk::DevBuf soff[sptk::kMaxModes];         // slice offsets (slice kernel, cached)
+    int64_t soff_key[sptk::kMaxModes][4] = {{-1, -1, -1, -1}};  // (row0, row1, nslice, S)
+    int64_t row_max[sptk::kMaxModes] = {-1, -1, -1, -1, -1, -1};  // max nnz of a row (lazy)
     sptk::DevBuf sortws;                        // radix-sort workspace (cached)
     sptk::DevBuf keys;                          // uint32[N][P] sort keys emitted at ingest
                                                 // (consumed by build_perm, then released)

@@ -2,6 +2,8 @@
 // tiles, row-range (multi-GPU) launches.  Kernels: mttkrp.cuh.
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "mttkrp.cuh"
 
 namespace sptk {
@@ -170,6 +172,112 @@ static sptk_status worker_rows(sptk_tensor t, int mode, int64_t pb, int64_t pe, 
     return SPTK_OK;
 }
 
+// Slice traversal (mttkrp_slice_kernel): soff[(r - row0)(K + 1) + k] = first
+// position of row r's segment of the copy whose secondary index is >= k*S
+// (binary search: the copy is sorted by the secondary index inside a row).
+__global__ void slice_offsets_kernel(const uint8_t *__restrict__ srec, int rc, int word,
+                                     const uint32_t *__restrict__ rowptr, int64_t row0,
+                                     int64_t rows, int K, int64_t S, uint32_t *__restrict__ soff) {
+    const int64_t n = rows * (K + 1);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = row0 + i / (K + 1);
+        const int k = (int)(i % (K + 1));
+        uint32_t lo = __ldg(rowptr + r), hi = __ldg(rowptr + r + 1);
+        if (k < K) {
+            const uint64_t target = (uint64_t)k * S;
+            while (lo < hi) {
+                const uint32_t mid = lo + ((hi - lo) >> 1);
+                const uint32_t key =
+                    __ldg(reinterpret_cast<const uint32_t *>(srec + (size_t)mid * rc) + word);
+                if (key < target) lo = mid + 1;
+                else hi = mid;
+            }
+        } else {
+            lo = hi;  // end of the row
+        }
+        soff[i] = lo;
+    }
+}
+
+// Rows of A_a per slice.  Measured (profiles/r01/sweep_slice.log): the
+// optimum is ~2048 rows for both fp64 (128 B rows) and fp32 (64 B) at R = 16 --
+// the slices keep the block's 8 warps sweeping the same window of A_a (their
+// reuse is temporal, the window need not be L1-resident), while longer slices
+// mean fewer partial flushes.  One slice (no slicing) loses the alignment.
+constexpr int64_t kSliceRows = 2048;
+
+static int slice_setting() {  // SPTK_SLICE=0 disables the slice traversal
+    static int v = -2;
+    if (v == -2) {
+        const char *e = getenv("SPTK_SLICE");
+        v = (e && *e == '0') ? 0 : 1;
+    }
+    return v;
+}
+
+static int64_t slice_rows() {  // SPTK_SLICE_ROWS overrides (tuning)
+    static int64_t r = -1;
+    if (r < 0) {
+        const char *e = getenv("SPTK_SLICE_ROWS");
+        r = (e && atoi(e) > 0) ? (int64_t)atoi(e) : kSliceRows;
+    }
+    return r;
+}
+
+// Number of slices for the slice traversal of `mode` over rows [r0, r1), or
+// 0 when it does not apply: the copy must be ordered by a secondary mode a
+// with more than one slice of rows, rows must be long enough to leave >= 32
+// nonzeros per (row, slice) and balanced (the block waits for its longest
+// row), and the grid must fill the GPU.  *S = rows of A_a per slice.
+static int slice_count(sptk_tensor t, int mode, int64_t r0, int64_t r1, int64_t nnz,
+                       cudaStream_t s, int64_t *S) {
+    const int a = t->copy_sec[mode];
+    if (a < 0 || t->deterministic || !slice_setting() || r1 <= r0) return 0;
+    const int64_t rows = r1 - r0;
+    const int64_t sa = slice_rows();
+    const int64_t K = (t->dims[a] + sa - 1) / sa;
+    if (K < 2 || K > 65535) return 0;
+    if (nnz < 32 * K * rows) return 0;
+    if (((rows + 7) / 8) * K < 2 * (int64_t)dev_sms()) return 0;
+    if (t->row_max[mode] < 0) {
+        if (host_rowptr(t, mode, s) != SPTK_OK) {
+            set_error("");
+            return 0;
+        }
+        const std::vector<uint32_t> &h = t->host_rowptr[mode];
+        int64_t mx = 0;
+        for (int64_t r = 0; r < t->dims[mode]; ++r) mx = std::max<int64_t>(mx, h[r + 1] - h[r]);
+        t->row_max[mode] = mx;
+    }
+    if (t->row_max[mode] * rows > 2 * nnz) return 0;  // longest row > 2x the mean
+    *S = sa;
+    return (int)K;
+}
+
+static sptk_status slice_offsets(sptk_tensor t, int mode, int64_t r0, int64_t r1, int K,
+                                 int64_t S, cudaStream_t s) {
+    int64_t *key = t->soff_key[mode];
+    if (key[0] == r0 && key[1] == r1 && key[2] == K && key[3] == S && t->soff[mode].p)
+        return SPTK_OK;
+    const int64_t n = (r1 - r0) * (K + 1);
+    SPTK_TRY(t->soff[mode].reserve(sizeof(uint32_t) * n));
+    const int a = t->copy_sec[mode];
+    const int word = (int)(dtype_bytes(t->dtype) / 4) + (a < mode ? a : a - 1);
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > (int64_t)dev_sms() * 16) blocks = (int64_t)dev_sms() * 16;
+    slice_offsets_kernel<<<(unsigned)blocks, 256, 0, s>>>(
+        t->srec[mode].as<uint8_t>(), compact_bytes(t->dtype, t->N), word,
+        t->rowptr[mode].as<uint32_t>(), r0, r1 - r0, K, S, t->soff[mode].as<uint32_t>());
+    count_launch();
+    SPTK_CUDA(cudaGetLastError());
+    key[0] = r0;
+    key[1] = r1;
+    key[2] = K;
+    key[3] = S;
+    return SPTK_OK;
+}
+
 sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const *factors,
                           const void *lambda, void *out, int64_t row_begin, int64_t row_end,
                           cudaStream_t s) {
@@ -245,6 +353,21 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
         a.perm = nullptr;
         a.rowptr = t->rowptr[mode].as<uint32_t>();
         a.wrow = t->wrow[mode].as<uint32_t>();
+    }
+
+    // slice traversal: one column tile (R <= 32 V), 32-byte vectors, the copy
+    int64_t S = 0;
+    int K = 0;
+    if (fast && t->has_srec[mode] && V * (int)es == 32 && R <= 32 * V)
+        K = slice_count(t, mode, row_begin, row_end, pe - pb, s, &S);
+    if (K > 0) {
+        SPTK_TRY(slice_offsets(t, mode, row_begin, row_end, K, S, s));
+        a.soff = t->soff[mode].as<uint32_t>();
+        a.row0 = row_begin;
+        a.row1 = row_end;
+        a.nslice = K;
+        a.sec = t->copy_sec[mode];
+        var = 2;
     }
 
     cudaEvent_t ev;

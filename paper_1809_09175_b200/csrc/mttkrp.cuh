@@ -54,6 +54,12 @@ struct MttkrpArgs {
     // last row) and are summed in worker order by det_fixup_kernel
     uint32_t *drow;
     void *dpart;
+    // slice traversal (mttkrp_slice_kernel): rows [row0, row1), row r's part
+    // of slice k is [soff[(r-row0)(nslice+1)+k], soff[...+k+1]); sec = the
+    // copy's secondary mode (its factor rows are L1-allocated, others not)
+    const uint32_t *soff;
+    int64_t row0, row1;
+    int nslice, sec;
 };
 
 // ----------------------------------------------------------------- loads
@@ -174,6 +180,26 @@ __device__ __forceinline__ void vld(const T *p, T (&r)[VW], uint64_t pol) {
                      : "=f"(r[0]), "=f"(r[1]) : "l"(p), "l"(pol));
     } else {
         asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r[0]) : "l"(p), "l"(pol));
+    }
+}
+// 32-byte gather that allocates in L1 only if `l1` (slice kernel: L1 is kept
+// for the secondary factor's slice); one predicated pair of loads
+template <typename T, int VW>
+__device__ __forceinline__ void vld_sel(const T *p, T (&r)[VW], uint64_t pol, bool l1) {
+    static_assert(sizeof(T) * VW == 32, "32-byte vectors only");
+    if constexpr (sizeof(T) == 8) {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t"
+                     "@q ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %6;\n\t"
+                     "@!q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %6;\n\t}"
+                     : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+                     : "l"(p), "r"((unsigned)l1), "l"(pol));
+    } else {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %9, 0;\n\t"
+                     "@q ld.global.nc.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %10;\n\t"
+                     "@!q ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %10;\n\t}"
+                     : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
+                       "=f"(r[6]), "=f"(r[7])
+                     : "l"(p), "r"((unsigned)l1), "l"(pol));
     }
 }
 template <typename T, int VW>
@@ -557,6 +583,109 @@ __global__ void __launch_bounds__(256, MINB) mttkrp_coop_kernel(const MttkrpArgs
     if constexpr (N >= 5) if (a.mode == 4) { mttkrp_coop_body<T, N, 4, G, U, RB, V>(a); return; }
 }
 
+// ---------------------------------------------------- slice kernel
+// Row-sliced traversal of the permuted copy (copy order: l_n, then the
+// secondary mode a's index).  A block of B = blockDim/32 warps takes B
+// consecutive rows and one slice k of a's index range; warp w walks row
+// (row0 + B*blockIdx.x + w)'s nonzeros whose l_a falls in slice k -- a
+// contiguous run of its row segment -- in permuted order, NG groups x U
+// positions per step like the cooperative kernel, with no row break inside
+// the run.  The B warps sweep the same A_a slice (sized to stay L1-resident),
+// so each A_a row is fetched from L2 about once per block instead of once per
+// nonzero; the other factors are gathered without L1 allocation.  Every row
+// receives one partial per slice, flushed with red.global.add (the row is
+// shared by the nslice blocks of its row group).
+template <typename T, int N, int MODE, int G, int U, int RB, int V>
+__device__ __forceinline__ void mttkrp_slice_body(const MttkrpArgs &a) {
+    constexpr int OFF = sizeof(T) / 4;
+    constexpr int NG = 32 / G;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane / G, q = lane % G;
+    const int64_t r = a.row0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (r >= a.row1) return;
+    const uint32_t *so = a.soff + (r - a.row0) * (a.nslice + 1) + blockIdx.y;
+    const uint32_t s = __ldg(so), e = __ldg(so + 1);
+    if (s >= e) return;
+    const bool lane_on = q * V < a.ncols;
+    const int c = a.col0 + q * V;
+    const uint8_t *__restrict__ rec = a.rec;
+    const uint64_t pol_stream = policy_evict_first(), pol_factor = policy_evict_last();
+    auto load_rec = [&](uint32_t pos, uint32_t (&w)[8]) {
+        if constexpr (RB == 32) ld_rec32_p(rec + (size_t)pos * 32, w, pol_stream);
+        else ld_rec16_p(rec + (size_t)pos * 16, w, pol_stream);
+    };
+    T acc[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = T(0);
+    uint32_t wn[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const uint32_t pos = s + u * NG + g;
+        if (pos < e) load_rec(pos, wn[u]);
+    }
+    for (uint32_t base = s; base < e; base += U * NG) {
+        uint32_t w[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) w[u][k] = wn[u][k];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t pos = base + U * NG + u * NG + g;
+            if (pos < e) load_rec(pos, wn[u]);
+        }
+        T f[U][N][V];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int m = 0; m < N; ++m)
+                if (m != MODE) {
+                    const int word = OFF + (m < MODE ? m : m - 1);
+                    const T *src = static_cast<const T *>(a.A[m]) + (int64_t)w[u][word] * a.ld + c;
+                    if (base + u * NG + g < e && lane_on) {
+                        vld_sel<T, V>(src, f[u][m], pol_factor, m == a.sec);
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < V; ++v) f[u][m][v] = T(0);
+                    }
+                }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const T x = (base + u * NG + g < e) ? rec_val<T>(w[u]) : T(0);
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                T p = x;
+#pragma unroll
+                for (int m = 0; m < N; ++m)
+                    if (m != MODE) p *= f[u][m][v];
+                acc[v] += p;
+            }
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+#pragma unroll
+        for (int o = G; o < 32; o <<= 1) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], o);
+    }
+    if (g != 0 || !lane_on) return;
+    if (a.lambda) {
+        T lam[V];
+        vld_plain<T, V>(static_cast<const T *>(a.lambda) + c, lam);
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[v] *= lam[v];
+    }
+    vred<T, V>(static_cast<T *>(a.out) + r * a.ld + c, acc);
+}
+
+template <typename T, int N, int G, int U, int RB, int MINB, int V>
+__global__ void __launch_bounds__(256, MINB) mttkrp_slice_kernel(const MttkrpArgs a) {
+    if constexpr (N >= 1) if (a.mode == 0) { mttkrp_slice_body<T, N, 0, G, U, RB, V>(a); return; }
+    if constexpr (N >= 2) if (a.mode == 1) { mttkrp_slice_body<T, N, 1, G, U, RB, V>(a); return; }
+    if constexpr (N >= 3) if (a.mode == 2) { mttkrp_slice_body<T, N, 2, G, U, RB, V>(a); return; }
+    if constexpr (N >= 4) if (a.mode == 3) { mttkrp_slice_body<T, N, 3, G, U, RB, V>(a); return; }
+    if constexpr (N >= 5) if (a.mode == 4) { mttkrp_slice_body<T, N, 4, G, U, RB, V>(a); return; }
+}
+
 // ---------------------------------------------------- generic kernel
 // Any N <= 6, any mode, any column tile: lane q of a G-lane worker owns
 // columns col0 + q + G*k (k < NV), scalar loads, runtime record offsets.
@@ -681,8 +810,29 @@ inline sptk_status fast_launch_g(int G, const MttkrpArgs &a, int64_t workers, cu
     return SPTK_OK;
 }
 
+// slice traversal: blocks of 8 rows x nslice slices (grid.y)
+template <typename T, int N, int RC, int V>
+inline sptk_status slice_launch_g(int G, const MttkrpArgs &a, cudaStream_t s) {
+    const dim3 grid((unsigned)((a.row1 - a.row0 + 7) / 8), (unsigned)a.nslice);
+#define SPTK_LAUNCH_S(GG)                                                                         mttkrp_slice_kernel<T, N, GG, kU<N>, RC, kMinBlocks<N>, V><<<grid, 256, 0, s>>>(a);
+    switch (G) {
+    case 1: SPTK_LAUNCH_S(1) break;
+    case 2: SPTK_LAUNCH_S(2) break;
+    case 4: SPTK_LAUNCH_S(4) break;
+    case 8: SPTK_LAUNCH_S(8) break;
+    case 16: SPTK_LAUNCH_S(16) break;
+    case 32: SPTK_LAUNCH_S(32) break;
+    default: return fail(SPTK_EINVAL, "slice MTTKRP: bad lane count");
+    }
+#undef SPTK_LAUNCH_S
+    count_launch();
+    SPTK_CUDA(cudaGetLastError());
+    return SPTK_OK;
+}
+
 // Per-(T, N, V) launcher, explicitly instantiated in mttkrp_<t>_n<N>_v<V>.cu.
-// `workers` counts groups (variant 0) or warps (variant 1).  The perm-gather
+// `workers` counts groups (variant 0) or warps (variant 1); variant 2 is the
+// slice traversal (32-byte vectors only).  The perm-gather
 // layout is compiled for the widest vector only (other R use the generic kernel).
 template <typename T, int N, int V>
 sptk_status launch_fast_tnv(int G, int variant, const MttkrpArgs &a, int64_t workers,
@@ -698,6 +848,10 @@ sptk_status launch_fast_tnv(int G, int variant, const MttkrpArgs &a, int64_t wor
             if constexpr (V * sizeof(T) == 32)                                               \
                 return fast_launch_g<T, N, RB, false, false, V>(G, a, workers, s);           \
             return fail(SPTK_EINVAL, "perm-gather fast path needs 32-byte vectors");         \
+        }                                                                                    \
+        if (variant == 2) {                                                                  \
+            if constexpr (V * sizeof(T) == 32) return slice_launch_g<T, N, RC, V>(G, a, s);  \
+            return fail(SPTK_EINVAL, "slice MTTKRP needs 32-byte vectors");                  \
         }                                                                                    \
         if (variant == 1) return fast_launch_g<T, N, RC, true, true, V>(G, a, workers, s);   \
         return fast_launch_g<T, N, RC, true, false, V>(G, a, workers, s);                    \

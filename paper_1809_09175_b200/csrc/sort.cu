@@ -396,9 +396,12 @@ sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
     }
     const uint32_t *order = t->perm[mode].as<uint32_t>();
     DevBuf ord;
+    t->copy_sec[mode] = -1;
+    t->soff_key[mode][0] = -1;
     if (a >= 0 && ord.reserve(order_bytes) == SPTK_OK) {
         SPTK_TRY(stable_sort_ids(t, mode, t->perm[a].as<uint32_t>(), ord.as<uint32_t>(), nullptr, s));
         order = ord.as<uint32_t>();
+        t->copy_sec[mode] = a;
     } else {
         set_error("");
     }
@@ -425,6 +428,9 @@ static void drop_copies(sptk_tensor t) {
         t->has_srec[m] = false;
         t->wrow[m].release();
         t->wrow_key[m][0] = -1;
+        t->copy_sec[m] = -1;
+        t->soff[m].release();
+        t->soff_key[m][0] = -1;
     }
 }
 
@@ -517,6 +523,7 @@ sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s) {
     uint32_t *perm = t->perm[mode].as<uint32_t>();
     uint32_t *rowptr = t->rowptr[mode].as<uint32_t>();
     t->host_rowptr[mode].clear();
+    t->row_max[mode] = -1;
     t->wrow_key[mode][0] = -1;
     if (P == 0) {
         SPTK_CUDA(cudaMemsetAsync(rowptr, 0, sizeof(uint32_t) * (In + 1), s));

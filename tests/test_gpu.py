@@ -161,6 +161,31 @@ def test_mttkrp_generic_path_parity(sp, layout, dtype, dims, R, offset):
         assert rel(V, Vo) <= TOL[dtype], n
 
 
+@pytest.mark.parametrize("dtype,R", [(torch.float64, 16), (torch.float32, 16),
+                                     (torch.float64, 8), (torch.float32, 32)])
+def test_mttkrp_slice_traversal(sp, dtype, R):
+    """Rows long enough for the slice traversal (mode 0: 1200 rows x ~6.7K
+    nonzeros, secondary mode 2 sliced): every slice of every row counted
+    once, lambda applied once, row sub-ranges (mttkrp_rows) included."""
+    dims = (1200, 9000, 5000)
+    idx, vals = synth.tensor(91, dims, 8_000_000, "uniform")
+    npd = np.float64 if dtype == torch.float64 else np.float32
+    vals = vals.astype(npd)
+    A = factors_np(92, dims, R, npd)
+    lam = np.linspace(0.5, 1.5, R).astype(npd)
+    t = make(sp, dims, idx, vals, dtype)
+    sp.build_perm(t, -1)
+    A64 = [a.astype(np.float64) for a in A]
+    Vo = oracle.mttkrp(dims, idx, vals.astype(np.float64), A64, 0, lam=lam.astype(np.float64))
+    V = gpu_mttkrp(sp, t, 0, A, R, dtype, lam=lam)
+    assert rel(V, Vo) <= TOL[dtype]
+    A_dev = [dev(a, dtype) for a in A]
+    out = torch.full((dims[0], R), float("nan"), dtype=dtype, device="cuda")
+    sp.mttkrp_rows(t, 0, A_dev, out, 37, 1151, lam=dev(lam, dtype))
+    got = out[37:1151].double().cpu().numpy()
+    assert rel(got, Vo[37:1151]) <= TOL[dtype]
+
+
 @pytest.mark.parametrize("layout", ["sorted", "perm_gather"])
 def test_mttkrp_contention_and_empty_rows(sp, layout):
     """All nonzeros in one row (maximum contention), a 2-long mode, many empty rows."""
