@@ -434,7 +434,7 @@ def main():
                       "tensor_device_bytes": dev_bytes},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "mttkrp_fast_kernel (permuted traversal)",
+                         "kernel": "MTTKRP launch (permuted copy; slice, warp-cooperative or per-group kernel chosen per mode)",
                          "bytes_model": "B_model per launch = P(N*4+s_v) + P(N-1)R*s_v + I_n*R*s_v "
                                         "(per-gather, SURVEY 8(d)); can exceed HBM peak when "
                                         "gathers hit L2 (P:716)",

@@ -267,13 +267,24 @@ sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream) {
         if (st == SPTK_ECUDA) t->poisoned = true;
         if (st != SPTK_OK) return st;
     }
+    bool all = true;  // the ingest keys are consumed once every mode is sorted
+    for (int m = 0; m < t->N; ++m) all = all && t->has_perm[m];
+    if (all && t->keys.p) {
+        // they also speed up the copies' secondary sorts; keep them through
+        // the copies only if every copy (+ its order buffer) fits beside them
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+            cudaGetLastError();
+            free_b = 0;
+        }
+        const size_t copies = (size_t)(m1 - m0) * (compact_bytes(t->dtype, t->N) + 4) * t->P;
+        if (free_b < copies + std::max<size_t>(total_b / 32, (size_t)4 << 30)) t->keys.release();
+    }
     for (int m = m0; m < m1; ++m) {  // then the permuted copies, while memory allows
         sptk_status st = ensure_sorted_copy(t, m, s);
         if (st == SPTK_ECUDA) t->poisoned = true;
         if (st != SPTK_OK) return st;
     }
-    bool all = true;  // the ingest keys are consumed once every mode is sorted
-    for (int m = 0; m < t->N; ++m) all = all && t->has_perm[m];
     if (all) t->keys.release();
     // keep the sort workspace for the next build_perm only while memory is plentiful
     size_t free_b = 0, total_b = 0;

@@ -1,5 +1,6 @@
 // mttkrp.cu -- host side of sptk_mttkrp: dispatch on (dtype, N, R), column
 // tiles, row-range (multi-GPU) launches.  Kernels: mttkrp.cuh.
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -206,6 +207,20 @@ __global__ void slice_offsets_kernel(const uint8_t *__restrict__ srec, int rc, i
 // reuse is temporal, the window need not be L1-resident), while longer slices
 // mean fewer partial flushes.  One slice (no slicing) loses the alignment.
 constexpr int64_t kSliceRows = 2048;
+// When A_a itself exceeds L2 (Amazon shape), a slice is instead an L2-sized
+// window of A_a: blocks are scheduled slice-major (grid.x = row blocks runs
+// fastest), so the whole GPU sweeps one window at a time and the A_a gathers
+// hit L2 instead of HBM.
+constexpr int64_t kSliceL2Bytes = 32 << 20;
+
+static bool debug_dispatch() {  // SPTK_DEBUG_DISPATCH=1: one stderr line per MTTKRP launch
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPTK_DEBUG_DISPATCH");
+        v = (e && *e && *e != '0') ? 1 : 0;
+    }
+    return v == 1;
+}
 
 static int slice_setting() {  // SPTK_SLICE=0 disables the slice traversal
     static int v = -2;
@@ -231,11 +246,12 @@ static int64_t slice_rows() {  // SPTK_SLICE_ROWS overrides (tuning)
 // nonzeros per (row, slice) and balanced (the block waits for its longest
 // row), and the grid must fill the GPU.  *S = rows of A_a per slice.
 static int slice_count(sptk_tensor t, int mode, int64_t r0, int64_t r1, int64_t nnz,
-                       cudaStream_t s, int64_t *S) {
+                       int64_t row_bytes, cudaStream_t s, int64_t *S) {
     const int a = t->copy_sec[mode];
     if (a < 0 || t->deterministic || !slice_setting() || r1 <= r0) return 0;
     const int64_t rows = r1 - r0;
-    const int64_t sa = slice_rows();
+    int64_t sa = slice_rows();
+    if (t->dims[a] * row_bytes > kSliceL2Bytes) sa = std::max<int64_t>(sa, kSliceL2Bytes / row_bytes);
     const int64_t K = (t->dims[a] + sa - 1) / sa;
     if (K < 2 || K > 65535) return 0;
     if (nnz < 32 * K * rows) return 0;
@@ -359,7 +375,7 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     int64_t S = 0;
     int K = 0;
     if (fast && t->has_srec[mode] && V * (int)es == 32 && R <= 32 * V)
-        K = slice_count(t, mode, row_begin, row_end, pe - pb, s, &S);
+        K = slice_count(t, mode, row_begin, row_end, pe - pb, R * (int64_t)es, s, &S);
     if (K > 0) {
         SPTK_TRY(slice_offsets(t, mode, row_begin, row_end, K, S, s));
         a.soff = t->soff[mode].as<uint32_t>();
@@ -369,6 +385,12 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
         a.sec = t->copy_sec[mode];
         var = 2;
     }
+
+    if (debug_dispatch())
+        fprintf(stderr, "[sptk] mttkrp mode %d rows [%lld,%lld) R %lld: %s V %d G0 %d variant %d "
+                "copy %d sec %d slices %d x %lld rows\n", mode, (long long)row_begin,
+                (long long)row_end, (long long)R, fast ? "fast" : "generic", V, G0, var,
+                (int)t->has_srec[mode], t->copy_sec[mode], K, (long long)S);
 
     cudaEvent_t ev;
     SPTK_TRY(mttkrp_span_begin(s, &ev));

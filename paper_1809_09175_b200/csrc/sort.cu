@@ -26,6 +26,12 @@ constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kWarpChunk = kSortTile / kSortWarps;          // 512 keys per warp
 constexpr int kScanChunk = 4096;
 
+// radix-sort workspace in 32-bit words: keys x2, values, digit counts, scan sums
+static size_t sort_ws_words(int64_t P) {
+    const size_t nP = (size_t)P, ncnt = (size_t)((P + kSortTile - 1) / kSortTile) * 256;
+    return 3 * nP + ncnt + (ncnt + kScanChunk - 1) / kScanChunk + 64;
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -345,7 +351,8 @@ static int grid_for(int64_t n) {
 }
 
 static sptk_status stable_sort_ids(sptk_tensor t, int mode, const uint32_t *in, uint32_t *out,
-                                   uint32_t **keys_out, cudaStream_t s);
+                                   uint32_t **keys_out, cudaStream_t s, void *ext_ws = nullptr,
+                                   size_t ext_bytes = 0);
 
 // Secondary key of the copy order: the shortest other mode whose factor does
 // not stay L1-resident (>= 2048 rows, 256 KB at R = 16 fp64), or -1.
@@ -380,15 +387,17 @@ sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
     }
     const size_t reserve = std::max<size_t>(total_b / 32, (size_t)4 << 30);
     int a = copy_secondary_mode(t, mode);
-    // the secondary sort reuses the cached sort workspace; skip it (paper
-    // order) when that workspace is gone or memory is short
-    if (a >= 0 && (!t->has_perm[a] || !t->sortws.p)) a = -1;
+    if (a >= 0 && !t->has_perm[a]) a = -1;
+    // the secondary sort runs inside the copy's own buffer (>= 16 B = 4 words
+    // per nonzero, the sort needs ~3.1) before the copy overwrites it; only
+    // the order itself (4 B per nonzero) is extra
     const size_t order_bytes = a >= 0 ? sizeof(uint32_t) * (size_t)t->P : 0;
-    if (free_b < need + order_bytes + reserve) a = -1;
-    if (a < 0 && free_b < need + reserve && t->sortws.p) {  // the sort workspace is a cache too
+    if (sizeof(uint32_t) * sort_ws_words(t->P) > need) a = -1;
+    if (free_b < need + order_bytes + reserve && t->sortws.p) {  // the sort workspace is a cache too
         free_b += t->sortws.bytes;
         t->sortws.release();
     }
+    if (free_b < need + order_bytes + reserve) a = -1;
     if (free_b < need + reserve) return SPTK_OK;
     if (t->srec[mode].reserve(need) != SPTK_OK) {
         set_error("");
@@ -399,7 +408,8 @@ sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
     t->copy_sec[mode] = -1;
     t->soff_key[mode][0] = -1;
     if (a >= 0 && ord.reserve(order_bytes) == SPTK_OK) {
-        SPTK_TRY(stable_sort_ids(t, mode, t->perm[a].as<uint32_t>(), ord.as<uint32_t>(), nullptr, s));
+        SPTK_TRY(stable_sort_ids(t, mode, t->perm[a].as<uint32_t>(), ord.as<uint32_t>(), nullptr, s,
+                                 t->srec[mode].p, need));
         order = ord.as<uint32_t>();
         t->copy_sec[mode] = a;
     } else {
@@ -456,8 +466,11 @@ __global__ void __launch_bounds__(256) gather_keys(const uint32_t *__restrict__ 
 // order of ids (NULL = storage order 0..P-1); the sorted ids go to `out` (must
 // not alias `in`) and, if keys_out != NULL, the sorted keys to keys_out.
 // Uses the handle's cached workspace.
+// ext_ws (optional, >= sort_ws_words(P) words): scratch to use instead of the
+// handle's cached workspace (the copy buffer about to be overwritten).
 static sptk_status stable_sort_ids(sptk_tensor t, int mode, const uint32_t *in, uint32_t *out,
-                                   uint32_t **keys_out, cudaStream_t s) {
+                                   uint32_t **keys_out, cudaStream_t s, void *ext_ws,
+                                   size_t ext_bytes) {
     const int64_t P = t->P, In = t->dims[mode];
     int bits = 0;
     while (bits < 32 && ((uint64_t)(In - 1) >> bits) != 0) ++bits;
@@ -467,12 +480,17 @@ static sptk_status stable_sort_ids(sptk_tensor t, int mode, const uint32_t *in, 
     // workspace (kept in the handle across calls; a cache like the permuted
     // copies): keys x2, values, digit counts, scan block sums
     const size_t nP = (size_t)P, ncnt = (size_t)ntiles * 256;
-    const size_t ws_words = 3 * nP + ncnt + (ncnt + kScanChunk - 1) / kScanChunk + 64;
-    if (t->sortws.reserve(sizeof(uint32_t) * ws_words) != SPTK_OK) {
-        drop_copies(t);  // permuted copies are caches: free them and retry
-        SPTK_TRY(t->sortws.reserve(sizeof(uint32_t) * ws_words));
+    const size_t ws_words = sort_ws_words(P);
+    uint32_t *ws;
+    if (ext_ws && ext_bytes >= sizeof(uint32_t) * ws_words) {
+        ws = static_cast<uint32_t *>(ext_ws);
+    } else {
+        if (t->sortws.reserve(sizeof(uint32_t) * ws_words) != SPTK_OK) {
+            drop_copies(t);  // permuted copies are caches: free them and retry
+            SPTK_TRY(t->sortws.reserve(sizeof(uint32_t) * ws_words));
+        }
+        ws = t->sortws.as<uint32_t>();
     }
-    uint32_t *ws = t->sortws.as<uint32_t>();
     uint32_t *kA = ws, *kB = ws + nP, *vA = ws + 2 * nP, *counts = ws + 3 * nP;
     uint32_t *tmp = counts + ncnt;
     // ping-pong: vals end in `out` after the last pass

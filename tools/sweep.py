@@ -29,8 +29,13 @@ def main():
     A = [device.factor(c.seed_f, c.N, m, I, R, dtype=dt) for m, I in enumerate(c.dims)]
     outs = [torch.empty((I, R), dtype=dt, device="cuda") for I in c.dims]
     s_v = 8 if dt == torch.float64 else 4
+    tensors = {}
     for layout in layouts:
-        t = sp.sptensor_create(c.dims, idx, val, perm_gather=layout == "perm_gather")
+        tensors[layout] = sp.sptensor_create(c.dims, idx, val, perm_gather=layout == "perm_gather")
+    del idx, val                 # the COO input is not needed after ingest (frees HBM for
+    torch.cuda.empty_cache()     # the permuted copies, as in bench.py)
+    for layout in layouts:
+        t = tensors.pop(layout)
         if layout != "atomic":
             sp.build_perm(t, -1)
         call = sp.mttkrp_atomic if layout == "atomic" else sp.mttkrp
