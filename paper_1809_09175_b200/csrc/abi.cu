@@ -3,6 +3,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #include <algorithm>
 #include <new>
@@ -257,15 +258,38 @@ sptk_status sptk_sptensor_device_bytes(sptk_tensor t, int64_t *bytes) {
     return SPTK_OK;
 }
 
+// SPTK_DEBUG_SETUP=1: synchronise and print the host time of every build_perm phase
+static double setup_clock(cudaStream_t s) {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("SPTK_DEBUG_SETUP");
+        on = (e && *e && *e != '0') ? 1 : 0;
+    }
+    if (!on) return -1.0;
+    cudaStreamSynchronize(s);
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+}
+
+static void setup_note(const char *what, int m, double &t0, cudaStream_t s) {
+    const double t1 = setup_clock(s);
+    if (t1 < 0) return;
+    fprintf(stderr, "[sptk] build_perm %s mode %d: %.2f ms\n", what, m, t1 - t0);
+    t0 = t1;
+}
+
 sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream) {
     CHECK_HANDLE(t);
     if (mode < -1 || mode >= t->N) return fail(SPTK_EINVAL, "mode out of range");
     cudaStream_t s = (cudaStream_t)stream;
     const int m0 = mode < 0 ? 0 : mode, m1 = mode < 0 ? t->N : mode + 1;
+    double tc = setup_clock(s);
     for (int m = m0; m < m1; ++m) {  // all sorts first: their temporaries are the peak
         sptk_status st = build_perm_mode(t, m, s);
         if (st == SPTK_ECUDA) t->poisoned = true;
         if (st != SPTK_OK) return st;
+        setup_note("sort", m, tc, s);
     }
     bool all = true;  // the ingest keys are consumed once every mode is sorted
     for (int m = 0; m < t->N; ++m) all = all && t->has_perm[m];
@@ -280,12 +304,15 @@ sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream) {
         const size_t copies = (size_t)(m1 - m0) * (compact_bytes(t->dtype, t->N) + 4) * t->P;
         if (free_b < copies + std::max<size_t>(total_b / 32, (size_t)4 << 30)) t->keys.release();
     }
+    setup_note("keys check", -1, tc, s);
     for (int m = m0; m < m1; ++m) {  // then the permuted copies, while memory allows
         sptk_status st = ensure_sorted_copy(t, m, s);
         if (st == SPTK_ECUDA) t->poisoned = true;
         if (st != SPTK_OK) return st;
+        setup_note("copy", m, tc, s);
     }
     if (all) t->keys.release();
+    setup_note("release keys", -1, tc, s);
     // keep the sort workspace for the next build_perm only while memory is plentiful
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {

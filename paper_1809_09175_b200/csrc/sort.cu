@@ -393,27 +393,34 @@ sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
     // the order itself (4 B per nonzero) is extra
     const size_t order_bytes = a >= 0 ? sizeof(uint32_t) * (size_t)t->P : 0;
     if (sizeof(uint32_t) * sort_ws_words(t->P) > need) a = -1;
-    if (free_b < need + order_bytes + reserve && t->sortws.p) {  // the sort workspace is a cache too
+    // the order lives in the idle sort workspace when that is cached
+    size_t extra = (t->sortws.p && t->sortws.bytes >= order_bytes) ? 0 : order_bytes;
+    if (free_b < need + extra + reserve && t->sortws.p) {  // the sort workspace is a cache too
         free_b += t->sortws.bytes;
         t->sortws.release();
+        extra = order_bytes;
     }
-    if (free_b < need + order_bytes + reserve) a = -1;
+    if (free_b < need + extra + reserve) a = -1;
     if (free_b < need + reserve) return SPTK_OK;
     if (t->srec[mode].reserve(need) != SPTK_OK) {
         set_error("");
         return SPTK_OK;
     }
     const uint32_t *order = t->perm[mode].as<uint32_t>();
-    DevBuf ord;
+    DevBuf ord;  // the order: in the idle sort workspace if it is cached, else its own buffer
+    uint32_t *ordp = nullptr;
+    if (a >= 0) {
+        if (t->sortws.p && t->sortws.bytes >= order_bytes) ordp = t->sortws.as<uint32_t>();
+        else if (ord.reserve(order_bytes) == SPTK_OK) ordp = ord.as<uint32_t>();
+        else set_error("");
+    }
     t->copy_sec[mode] = -1;
     t->soff_key[mode][0] = -1;
-    if (a >= 0 && ord.reserve(order_bytes) == SPTK_OK) {
-        SPTK_TRY(stable_sort_ids(t, mode, t->perm[a].as<uint32_t>(), ord.as<uint32_t>(), nullptr, s,
+    if (ordp) {
+        SPTK_TRY(stable_sort_ids(t, mode, t->perm[a].as<uint32_t>(), ordp, nullptr, s,
                                  t->srec[mode].p, need));
-        order = ord.as<uint32_t>();
+        order = ordp;
         t->copy_sec[mode] = a;
-    } else {
-        set_error("");
     }
     const int vw = dtype_bytes(t->dtype) / 4;
     const unsigned g = (unsigned)grid_for(t->P);
