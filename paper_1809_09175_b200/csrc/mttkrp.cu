@@ -338,6 +338,10 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
         return true;
     };
     while (V > 1 && !ok_v(V)) V >>= 1;
+    if (const char *fv = getenv("SPTK_FORCE_V")) {  // tuning: cap the lane vector width
+        const int cap = atoi(fv);
+        while (V > 1 && V > cap) V >>= 1;
+    }
     bool fast = t->N >= 3 && t->N <= 5 && ok_v(V) &&
                 (t->has_srec[mode] || V * (int)es == 32);
     const int G0 = fast ? pow2ceil((int)((R < 32 * V ? R : 32 * V) / V)) : (R <= 16 ? 4 : 32);
@@ -374,7 +378,7 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     // slice traversal: one column tile (R <= 32 V), 32-byte vectors, the copy
     int64_t S = 0;
     int K = 0;
-    if (fast && t->has_srec[mode] && V * (int)es == 32 && R <= 32 * V)
+    if (fast && t->has_srec[mode] && R <= 32 * V)
         K = slice_count(t, mode, row_begin, row_end, pe - pb, R * (int64_t)es, s, &S);
     if (K > 0) {
         SPTK_TRY(slice_offsets(t, mode, row_begin, row_end, K, S, s));

@@ -182,24 +182,48 @@ __device__ __forceinline__ void vld(const T *p, T (&r)[VW], uint64_t pol) {
         asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r[0]) : "l"(p), "l"(pol));
     }
 }
-// 32-byte gather that allocates in L1 only if `l1` (slice kernel: L1 is kept
-// for the secondary factor's slice); one predicated pair of loads
+// gather that allocates in L1 only if `l1` (slice kernel: L1 is kept for the
+// secondary factor's window); one predicated pair of loads, any vector width
 template <typename T, int VW>
 __device__ __forceinline__ void vld_sel(const T *p, T (&r)[VW], uint64_t pol, bool l1) {
-    static_assert(sizeof(T) * VW == 32, "32-byte vectors only");
-    if constexpr (sizeof(T) == 8) {
+    const unsigned f = l1;
+    if constexpr (sizeof(T) == 8 && VW == 4) {
         asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t"
                      "@q ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %6;\n\t"
                      "@!q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %6;\n\t}"
-                     : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
-                     : "l"(p), "r"((unsigned)l1), "l"(pol));
-    } else {
+                     : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p), "r"(f), "l"(pol));
+    } else if constexpr (sizeof(T) == 8 && VW == 2) {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t"
+                     "@q ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %4;\n\t"
+                     "@!q ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %4;\n\t}"
+                     : "=d"(r[0]), "=d"(r[1]) : "l"(p), "r"(f), "l"(pol));
+    } else if constexpr (sizeof(T) == 8) {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+                     "@q ld.global.nc.L2::cache_hint.f64 %0, [%1], %3;\n\t"
+                     "@!q ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %3;\n\t}"
+                     : "=d"(r[0]) : "l"(p), "r"(f), "l"(pol));
+    } else if constexpr (VW == 8) {
         asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %9, 0;\n\t"
                      "@q ld.global.nc.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %10;\n\t"
                      "@!q ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %10;\n\t}"
                      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
                        "=f"(r[6]), "=f"(r[7])
-                     : "l"(p), "r"((unsigned)l1), "l"(pol));
+                     : "l"(p), "r"(f), "l"(pol));
+    } else if constexpr (VW == 4) {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t"
+                     "@q ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %6;\n\t"
+                     "@!q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %6;\n\t}"
+                     : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]) : "l"(p), "r"(f), "l"(pol));
+    } else if constexpr (VW == 2) {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t"
+                     "@q ld.global.nc.L2::cache_hint.v2.f32 {%0,%1}, [%2], %4;\n\t"
+                     "@!q ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0,%1}, [%2], %4;\n\t}"
+                     : "=f"(r[0]), "=f"(r[1]) : "l"(p), "r"(f), "l"(pol));
+    } else {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+                     "@q ld.global.nc.L2::cache_hint.f32 %0, [%1], %3;\n\t"
+                     "@!q ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %3;\n\t}"
+                     : "=f"(r[0]) : "l"(p), "r"(f), "l"(pol));
     }
 }
 template <typename T, int VW>
@@ -832,7 +856,7 @@ inline sptk_status slice_launch_g(int G, const MttkrpArgs &a, cudaStream_t s) {
 
 // Per-(T, N, V) launcher, explicitly instantiated in mttkrp_<t>_n<N>_v<V>.cu.
 // `workers` counts groups (variant 0) or warps (variant 1); variant 2 is the
-// slice traversal (32-byte vectors only).  The perm-gather
+// slice traversal.  The perm-gather
 // layout is compiled for the widest vector only (other R use the generic kernel).
 template <typename T, int N, int V>
 sptk_status launch_fast_tnv(int G, int variant, const MttkrpArgs &a, int64_t workers,
@@ -849,10 +873,7 @@ sptk_status launch_fast_tnv(int G, int variant, const MttkrpArgs &a, int64_t wor
                 return fast_launch_g<T, N, RB, false, false, V>(G, a, workers, s);           \
             return fail(SPTK_EINVAL, "perm-gather fast path needs 32-byte vectors");         \
         }                                                                                    \
-        if (variant == 2) {                                                                  \
-            if constexpr (V * sizeof(T) == 32) return slice_launch_g<T, N, RC, V>(G, a, s);  \
-            return fail(SPTK_EINVAL, "slice MTTKRP needs 32-byte vectors");                  \
-        }                                                                                    \
+        if (variant == 2) return slice_launch_g<T, N, RC, V>(G, a, s);                       \
         if (variant == 1) return fast_launch_g<T, N, RC, true, true, V>(G, a, workers, s);   \
         return fast_launch_g<T, N, RC, true, false, V>(G, a, workers, s);                    \
     }

@@ -162,7 +162,8 @@ def test_mttkrp_generic_path_parity(sp, layout, dtype, dims, R, offset):
 
 
 @pytest.mark.parametrize("dtype,R", [(torch.float64, 16), (torch.float32, 16),
-                                     (torch.float64, 8), (torch.float32, 32)])
+                                     (torch.float64, 8), (torch.float32, 32),
+                                     (torch.float64, 10), (torch.float32, 13)])
 def test_mttkrp_slice_traversal(sp, dtype, R):
     """Rows long enough for the slice traversal (mode 0: 1200 rows x ~6.7K
     nonzeros, secondary mode 2 sliced): every slice of every row counted
