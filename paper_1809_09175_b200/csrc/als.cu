@@ -372,6 +372,176 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+
+// ------------------------------------------------- fused glue, R <= 32 (single GPU)
+// Deferred normalisation: A_n is kept as A_raw = V Gamma^{-1}; its column
+// scales s_n = 1/lambda_n are applied where the normalised factor is consumed
+// -- the next MTTKRPs take prod_{m != n} s_m as their column weights (applied
+// at the row flush, Eq. (2)'s lambda), the Gram matrix is D_s G_raw D_s -- and
+// once to every factor after the last iteration.  The tail of a mode update is
+// then one pass over V (A_raw, its Gram partials, the column partials) plus an
+// R x R finalisation, instead of apply + normalise + Gram (two passes over A).
+constexpr int kApplyTile = 64;
+
+// the deferred path for R <= 32 (SPTK_DEFERRED_NORM=0: explicit normalisation, for A/B)
+static bool deferred_norm(int64_t R) {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPTK_DEFERRED_NORM");
+        v = (e && *e == '0') ? 0 : 1;
+    }
+    return v == 1 && R <= 32;
+}
+
+// Rows [b0, b1) of the block: V tile -> shared memory (coalesced), A_raw tile =
+// V_tile Ginv (thread (j, l): column j, rows l, l + 256/R, ...), written to A
+// and to shared memory; Gram partials of the tile in 2 x 2 register blocks
+// (256 / ceil(R/2)^2 row groups); per-block partials: psq/pdot [blk][R],
+// gpart [blk][R*R].
+template <typename T>
+__global__ void __launch_bounds__(256)
+    apply_gram_kernel(const T *__restrict__ V, int64_t I, int R, int64_t rows_per_block,
+                      const double *__restrict__ Ginv, T *__restrict__ A,
+                      double *__restrict__ part_sq, double *__restrict__ part_dot,
+                      double *__restrict__ gpart) {
+    extern __shared__ double sm[];
+    double *Gi = sm;                         // R x R
+    double *Vt = Gi + R * R;                 // kApplyTile x R
+    double *At = Vt + kApplyTile * R;        // kApplyTile x R
+    double *red = At + kApplyTile * R;       // 4 x 256
+    const int tid = threadIdx.x;
+    for (int e = tid; e < R * R; e += blockDim.x) Gi[e] = Ginv[e];
+    const int lanes = 256 / R, j = tid % R, l = tid / R;
+    const int hb = (R + 1) / 2, nblk = hb * hb, groups = 256 / nblk;
+    const int bi = tid % nblk, grp = tid / nblk;
+    const int a0 = (bi / hb) * 2, c0 = (bi % hb) * 2;
+    const bool a1ok = a0 + 1 < R, c1ok = c0 + 1 < R;
+    double g00 = 0.0, g01 = 0.0, g10 = 0.0, g11 = 0.0, sq = 0.0, dot = 0.0;
+    const int64_t b0 = (int64_t)blockIdx.x * rows_per_block;
+    const int64_t b1 = min(I, b0 + rows_per_block);
+    for (int64_t rt = b0; rt < b1; rt += kApplyTile) {
+        const int nr = (int)min((int64_t)kApplyTile, b1 - rt);
+        __syncthreads();
+        for (int x = tid; x < nr * R; x += blockDim.x) Vt[x] = (double)V[rt * R + x];
+        __syncthreads();
+        if (l < lanes) {
+            for (int r = l; r < nr; r += lanes) {
+                const double *v = Vt + r * R;
+                double x = 0.0;
+                for (int i = 0; i < R; ++i) x += v[i] * Gi[i * R + j];
+                const T xt = (T)x;
+                A[(rt + r) * R + j] = xt;
+                const double xd = (double)xt;
+                At[r * R + j] = xd;
+                sq += xd * xd;
+                dot += xd * v[j];
+            }
+        }
+        __syncthreads();
+        if (grp < groups) {
+            for (int r = grp; r < nr; r += groups) {
+                const double *a = At + r * R;
+                const double x0 = a[a0], x1 = a1ok ? a[a0 + 1] : 0.0;
+                const double y0 = a[c0], y1 = c1ok ? a[c0 + 1] : 0.0;
+                g00 += x0 * y0;
+                g01 += x0 * y1;
+                g10 += x1 * y0;
+                g11 += x1 * y1;
+            }
+        }
+    }
+    __syncthreads();
+    red[tid] = sq;
+    red[256 + tid] = dot;
+    __syncthreads();
+    if (tid < R) {
+        double a = 0.0, d = 0.0;
+        for (int q = 0; q < lanes; ++q) {
+            a += red[q * R + tid];
+            d += red[256 + q * R + tid];
+        }
+        part_sq[(int64_t)blockIdx.x * R + tid] = a;
+        if (part_dot) part_dot[(int64_t)blockIdx.x * R + tid] = d;
+    }
+    __syncthreads();
+    // Gram partials: sum the row groups of each 2 x 2 block in group order
+    double *gs = red;  // [groups][nblk][4] fits in 4 x 256
+    if (grp < groups) {
+        double *o = gs + ((size_t)grp * nblk + bi) * 4;
+        o[0] = g00; o[1] = g01; o[2] = g10; o[3] = g11;
+    }
+    __syncthreads();
+    double *gp = gpart + (int64_t)blockIdx.x * R * R;
+    for (int e = tid; e < nblk * 4; e += blockDim.x) {
+        const int b = e >> 2, q = e & 3;
+        const int a = (b / hb) * 2 + (q >> 1), c = (b % hb) * 2 + (q & 1);
+        double acc = 0.0;
+        for (int g = 0; g < groups; ++g) acc += gs[((size_t)g * nblk + b) * 4 + q];
+        if (a < R && c < R) gp[a * R + c] = acc;
+    }
+}
+
+// One block.  lambda_n = sqrt(colsq); s_n = 1/lambda_n; the normalised Gram
+// G_n = D_s G_raw D_s.  A zero column j (lambda_j = 0) becomes e_1 as in the
+// oracle: A_raw(0, j) := 1 with s_j = 1, and its Gram entries are
+// e_1 . A_norm(:, b) = A_raw(0, b) s_b (1 against another zero column).  Then
+// the column scale of the next mode's MTTKRP: prod_{m != next} s_m.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    finalize_mode_kernel(const double *__restrict__ colsq, const double *__restrict__ graw,
+                         T *__restrict__ A, int N, int n, int R, int next,
+                         double *__restrict__ s_all, double *__restrict__ lam,
+                         double *__restrict__ G, T *__restrict__ scale_next) {
+    __shared__ double sn[128];
+    __shared__ double row0[128];
+    __shared__ int zero[128];
+    const int tid = threadIdx.x;
+    for (int j = tid; j < R; j += blockDim.x) {
+        const double l = sqrt(colsq[j]);
+        lam[j] = l;
+        zero[j] = !(l > 0.0);
+        sn[j] = l > 0.0 ? 1.0 / l : 1.0;
+        row0[j] = (double)A[j];
+    }
+    __syncthreads();
+    double *Gn = G + (int64_t)n * R * R;
+    for (int e = tid; e < R * R; e += blockDim.x) {
+        const int a = e / R, b = e % R;
+        double g;
+        if (!zero[a] && !zero[b]) g = graw[e] * sn[a] * sn[b];
+        else if (zero[a] && zero[b]) g = 1.0;
+        else if (zero[a]) g = row0[b] * sn[b];
+        else g = row0[a] * sn[a];
+        Gn[e] = g;
+    }
+    for (int j = tid; j < R; j += blockDim.x) {
+        if (zero[j]) A[j] = (T)1.0;
+        s_all[(int64_t)n * R + j] = sn[j];
+    }
+    __syncthreads();
+    for (int j = tid; j < R; j += blockDim.x) {
+        double p = 1.0;
+        for (int m = 0; m < N; ++m)
+            if (m != next) p *= (m == n) ? sn[j] : s_all[(int64_t)m * R + j];
+        scale_next[j] = (T)p;
+    }
+}
+
+// A(:, j) *= s_j (the deferred normalisation, once after the last iteration)
+template <typename T>
+__global__ void scale_columns_kernel(T *__restrict__ A, int64_t I, int R,
+                                     const double *__restrict__ s) {
+    const int64_t n = I * R;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        A[i] = (T)((double)A[i] * s[i % R]);
+}
+
+__global__ void fill_f64_kernel(double *__restrict__ out, int n, double v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = v;
+}
+
 // ---------------------------------------------------------- tiled glue (R > 32)
 // Register-blocked fp64 tiles for the two dense products of the glue when R
 // is large (the paper's R = 128 CP-ALS workload): A_raw = V Gamma^{-1} and the
@@ -614,6 +784,10 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
     int *status = reinterpret_cast<int *>(scal + 8);
     double *Ginv = w.L.as<double>();
     T *V = w.V.as<T>();
+    double *s_all = w.scl.as<double>();                      // N x R column scales
+    double *graw = s_all + (size_t)N * R;                    // R x R Gram of A_raw
+    T *scale = reinterpret_cast<T *>(graw + (size_t)R * R);  // R: next MTTKRP's weights
+    const bool deferred = deferred_norm(R);
     for (int n = 0; n < N; ++n) {
         const bool last = n == N - 1;
         const int64_t I = t->dims[n];
@@ -625,43 +799,68 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
         count_launch();
         SPTK_CUDA(cudaGetLastError());
         SPTK_CUDA(cudaEventRecord(w.ev_inv, w.side));
-        SPTK_TRY(mttkrp_launch(t, n, c.R, c.A.data(), nullptr, V, 0, I, c.s));
+        // V = MTTKRP with the normalised factors: raw factors, column scales at the flush
+        SPTK_TRY(mttkrp_launch(t, n, c.R, c.A.data(), deferred ? scale : nullptr, V, 0, I, c.s));
         SPTK_CUDA(cudaStreamWaitEvent(c.s, w.ev_inv, 0));
         T *An = static_cast<T *>(c.A[n]);
         double *psq = w.partial.as<double>();
         double *pdot = psq + c.part_stride;
-        int nb = 0;
-        SPTK_TRY(apply_inverse<T>(c, V, 0, I, An, psq, last ? pdot : nullptr, &nb));
-        if (R <= 32) {  // column norms, then one fused tail: lambda, normalise, Gram partials
-            double *colsq = w.colsq.as<double>();
+        double *colsq = w.colsq.as<double>();
+        if (deferred) {  // one pass: A_raw, its Gram partials, column partials; R x R finalise
+            int nb = (int)std::min<int64_t>(c.nblocks, (I + kApplyTile - 1) / kApplyTile);
+            if (nb < 1) nb = 1;
+            const int64_t rpb = (I + nb - 1) / nb;
+            nb = (int)((I + rpb - 1) / rpb);
+            const size_t smb = sizeof(double) * (R * R + 2 * kApplyTile * R + 4 * 256);
+            apply_gram_kernel<T><<<nb, 256, smb, c.s>>>(V, I, R, rpb, Ginv, An, psq,
+                                                        last ? pdot : nullptr,
+                                                        w.gpart.as<double>());
             reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(psq, nb, R, colsq);
-            int nf = (int)std::min<int64_t>(c.nblocks, (I + kGramTileRows - 1) / kGramTileRows);
-            const int64_t fpb = (I + nf - 1) / nf;
-            nf = (int)((I + fpb - 1) / fpb);
-            const size_t fsm = sizeof(double) * (R + kGramTileRows * R);
-            if (R <= 16)
-                finish_kernel<T, 1><<<nf, 256, fsm, c.s>>>(An, I, R, fpb, colsq,
-                                                           w.gpart.as<double>(), lam);
-            else
-                finish_kernel<T, 4><<<nf, 256, fsm, c.s>>>(An, I, R, fpb, colsq,
-                                                           w.gpart.as<double>(), lam);
-            reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(
-                w.gpart.as<double>(), nf, R * R, w.G.as<double>() + (int64_t)n * R * R);
-            count_launch(3);
-        } else {        // large R: reduce, normalise, tiled Gram
-            double *colsq = w.colsq.as<double>();
-            reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(psq, nb, R, colsq);
-            normalize_kernel<T><<<grid_for(std::max<int64_t>(I, 1) * R), 256, 0, c.s>>>(
-                An, 0, I, R, colsq, lam);
-            count_launch(2);
+            reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(w.gpart.as<double>(), nb,
+                                                                    R * R, graw);
+            finalize_mode_kernel<T><<<1, 256, 0, c.s>>>(colsq, graw, An, N, n, R, (n + 1) % N,
+                                                         s_all, lam, w.G.as<double>(), scale);
+            count_launch(4);
             SPTK_CUDA(cudaGetLastError());
-            SPTK_TRY(gram<T>(c, n, w.gpart.as<double>()));
-        }
-        if (last) {
-            double *dot = w.colsq.as<double>() + R;
-            reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(pdot, nb, R, dot);
-            fit_kernel<<<1, 256, 0, c.s>>>(dot, lam, w.G.as<double>(), N, R, t->normX2, scal);
-            count_launch(2);
+            if (last) {
+                double *dot = colsq + R;
+                reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(pdot, nb, R, dot);
+                fit_kernel<<<1, 256, 0, c.s>>>(dot, lam, w.G.as<double>(), N, R, t->normX2, scal);
+                count_launch(2);
+            }
+        } else {  // explicit normalisation: apply, reduce, normalise + Gram
+            int nb = 0;
+            SPTK_TRY(apply_inverse<T>(c, V, 0, I, An, psq, last ? pdot : nullptr, &nb));
+            reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(psq, nb, R, colsq);
+            count_launch();
+            if (R <= 32) {  // one fused tail: lambda, normalise, Gram partials
+                int nf = (int)std::min<int64_t>(c.nblocks, (I + kGramTileRows - 1) / kGramTileRows);
+                const int64_t fpb = (I + nf - 1) / nf;
+                nf = (int)((I + fpb - 1) / fpb);
+                const size_t fsm = sizeof(double) * (R + kGramTileRows * R);
+                if (R <= 16)
+                    finish_kernel<T, 1><<<nf, 256, fsm, c.s>>>(An, I, R, fpb, colsq,
+                                                               w.gpart.as<double>(), lam);
+                else
+                    finish_kernel<T, 4><<<nf, 256, fsm, c.s>>>(An, I, R, fpb, colsq,
+                                                               w.gpart.as<double>(), lam);
+                reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(
+                    w.gpart.as<double>(), nf, R * R, w.G.as<double>() + (int64_t)n * R * R);
+                count_launch(2);
+            } else {        // large R: normalise, tiled Gram
+                normalize_kernel<T><<<grid_for(std::max<int64_t>(I, 1) * R), 256, 0, c.s>>>(
+                    An, 0, I, R, colsq, lam);
+                count_launch();
+                SPTK_CUDA(cudaGetLastError());
+                SPTK_TRY(gram<T>(c, n, w.gpart.as<double>()));
+            }
+            SPTK_CUDA(cudaGetLastError());
+            if (last) {
+                double *dot = colsq + R;
+                reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(pdot, nb, R, dot);
+                fit_kernel<<<1, 256, 0, c.s>>>(dot, lam, w.G.as<double>(), N, R, t->normX2, scal);
+                count_launch(2);
+            }
         }
         SPTK_CUDA(cudaGetLastError());
     }
@@ -780,6 +979,7 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     SPTK_TRY(w.scal.reserve(sizeof(double) * 16));
     SPTK_TRY(w.lamT.reserve(es * R));
     SPTK_TRY(w.gpart.reserve(sizeof(double) * (size_t)c.nblocks * R * R));
+    SPTK_TRY(w.scl.reserve(sizeof(double) * ((size_t)N * R + (size_t)R * R + R)));
     if (!w.hres) SPTK_CUDA(cudaMallocHost(&w.hres, sizeof(double) * 16));
     if (!w.side) {
         SPTK_CUDA(cudaStreamCreateWithFlags(&w.side, cudaStreamNonBlocking));
@@ -832,6 +1032,19 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
         }
     }
     for (int m = 0; m < N; ++m) SPTK_TRY(gram<T>(c, m));
+    // deferred normalisation state (single GPU, R <= 32): all scales 1, and the
+    // first MTTKRP's column weights 1
+    const bool deferred = !sharded(comm) && deferred_norm(R);
+    if (deferred) {
+        double *s_all = w.scl.as<double>();
+        fill_f64_kernel<<<(unsigned)((N * R + 255) / 256), 256, 0, s>>>(s_all, N * (int)R, 1.0);
+        T *scale = reinterpret_cast<T *>(s_all + (size_t)N * R + (size_t)R * R);
+        std::vector<T> ones(R, T(1));
+        SPTK_CUDA(cudaMemcpyAsync(scale, ones.data(), sizeof(T) * R, cudaMemcpyHostToDevice, s));
+        SPTK_CUDA(cudaStreamSynchronize(s));
+        count_launch();
+        SPTK_CUDA(cudaGetLastError());
+    }
 
     double fit = 0.0, fit_prev = 0.0;
     int it = 0;
@@ -896,6 +1109,14 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     }
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
+    if (deferred && it > 0) {  // apply the deferred column normalisation once
+        for (int m = 0; m < N; ++m) {
+            scale_columns_kernel<T><<<grid_for(t->dims[m] * R), 256, 0, s>>>(
+                static_cast<T *>(c.A[m]), t->dims[m], (int)R, w.scl.as<double>() + (size_t)m * R);
+            count_launch();
+        }
+        SPTK_CUDA(cudaGetLastError());
+    }
     if (fit_out) *fit_out = fit;
     if (iters_out) *iters_out = it;
     if (st != SPTK_OK) return st;
@@ -948,6 +1169,8 @@ extern "C" sptk_status sptk_cp_als(sptk_tensor t, int64_t R, int max_iters, doub
         cudaFuncSetAttribute(apply_inv_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(apply_inv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(apply_gram_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(apply_gram_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(finish_kernel<double, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(finish_kernel<double, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(finish_kernel<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

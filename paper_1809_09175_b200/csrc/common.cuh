@@ -79,6 +79,8 @@ struct ALSWork {
     DevBuf stage;     // host<->device staging for factors
     DevBuf lamT;      // R (T) lambda in tensor dtype
     DevBuf gpart;     // per-block partial Gram matrices (f64)
+    DevBuf scl;       // deferred normalisation: s_m = 1/lambda_m (N x R f64), then the
+                      // next MTTKRP's column scale prod_{m != n} s_m (R, tensor dtype)
     cudaStream_t side = nullptr;              // Cholesky / inverse, overlapped with MTTKRP
     cudaEvent_t ev_gram = nullptr, ev_inv = nullptr;
     double *hres = nullptr;                   // pinned: fit, inner, ||M||^2, ..., status
