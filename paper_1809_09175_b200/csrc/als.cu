@@ -381,7 +381,15 @@ __global__ void __launch_bounds__(256)
 // once to every factor after the last iteration.  The tail of a mode update is
 // then one pass over V (A_raw, its Gram partials, the column partials) plus an
 // R x R finalisation, instead of apply + normalise + Gram (two passes over A).
-constexpr int kApplyTile = 64;
+constexpr int kApplyTileDefault = 64;
+static int apply_tile_rows() {  // SPTK_APPLY_TILE overrides (tuning)
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPTK_APPLY_TILE");
+        v = (e && atoi(e) >= 16) ? atoi(e) : kApplyTileDefault;
+    }
+    return v;
+}
 
 // the deferred path for R <= 32 (SPTK_DEFERRED_NORM=0: explicit normalisation, for A/B)
 static bool deferred_norm(int64_t R) {
@@ -398,55 +406,67 @@ static bool deferred_norm(int64_t R) {
 // and to shared memory; Gram partials of the tile in 2 x 2 register blocks
 // (256 / ceil(R/2)^2 row groups); per-block partials: psq/pdot [blk][R],
 // gpart [blk][R*R].
-template <typename T>
+template <typename T, int RM>  // RM >= R: Gamma^{-1} column length held in registers
 __global__ void __launch_bounds__(256)
-    apply_gram_kernel(const T *__restrict__ V, int64_t I, int R, int64_t rows_per_block,
+    apply_gram_kernel(const T *__restrict__ V, int64_t I, int R, int64_t rows_per_block, int kApplyTile,
                       const double *__restrict__ Ginv, T *__restrict__ A,
                       double *__restrict__ part_sq, double *__restrict__ part_dot,
                       double *__restrict__ gpart) {
-    extern __shared__ double sm[];
-    double *Gi = sm;                         // R x R
-    double *Vt = Gi + R * R;                 // kApplyTile x R
-    double *At = Vt + kApplyTile * R;        // kApplyTile x R
-    double *red = At + kApplyTile * R;       // 4 x 256
+    extern __shared__ __align__(16) double sm[];
+    const int RP = (R + 1) & ~1;              // padded row stride (16-byte aligned pairs)
+    double *Vt = sm;                          // kApplyTile x RP
+    double *At = Vt + kApplyTile * RP;        // kApplyTile x RP
+    double *red = At + kApplyTile * RP;       // 4 x 256
     const int tid = threadIdx.x;
-    for (int e = tid; e < R * R; e += blockDim.x) Gi[e] = Ginv[e];
     const int lanes = 256 / R, j = tid % R, l = tid / R;
+    double gi[RM];  // column j of Gamma^{-1}
+#pragma unroll
+    for (int i = 0; i < RM; ++i) gi[i] = (i < R && l < lanes) ? Ginv[i * R + j] : 0.0;
     const int hb = (R + 1) / 2, nblk = hb * hb, groups = 256 / nblk;
     const int bi = tid % nblk, grp = tid / nblk;
     const int a0 = (bi / hb) * 2, c0 = (bi % hb) * 2;
-    const bool a1ok = a0 + 1 < R, c1ok = c0 + 1 < R;
     double g00 = 0.0, g01 = 0.0, g10 = 0.0, g11 = 0.0, sq = 0.0, dot = 0.0;
     const int64_t b0 = (int64_t)blockIdx.x * rows_per_block;
     const int64_t b1 = min(I, b0 + rows_per_block);
     for (int64_t rt = b0; rt < b1; rt += kApplyTile) {
         const int nr = (int)min((int64_t)kApplyTile, b1 - rt);
         __syncthreads();
-        for (int x = tid; x < nr * R; x += blockDim.x) Vt[x] = (double)V[rt * R + x];
+        for (int x = tid; x < nr * R; x += blockDim.x) {
+            const int r = x / R, c = x - r * R;
+            Vt[r * RP + c] = (double)V[rt * R + x];
+        }
+        if (RP != R)
+            for (int r = tid; r < nr; r += blockDim.x) Vt[r * RP + R] = 0.0, At[r * RP + R] = 0.0;
         __syncthreads();
         if (l < lanes) {
             for (int r = l; r < nr; r += lanes) {
-                const double *v = Vt + r * R;
+                const double2 *v2 = reinterpret_cast<const double2 *>(Vt + r * RP);
                 double x = 0.0;
-                for (int i = 0; i < R; ++i) x += v[i] * Gi[i * R + j];
+#pragma unroll
+                for (int i = 0; i < RM; i += 2) {
+                    if (i < R) {
+                        const double2 q = v2[i >> 1];
+                        x += q.x * gi[i];
+                        x += q.y * gi[i + 1];
+                    }
+                }
                 const T xt = (T)x;
                 A[(rt + r) * R + j] = xt;
                 const double xd = (double)xt;
-                At[r * R + j] = xd;
+                At[r * RP + j] = xd;
                 sq += xd * xd;
-                dot += xd * v[j];
+                dot += xd * Vt[r * RP + j];
             }
         }
         __syncthreads();
         if (grp < groups) {
             for (int r = grp; r < nr; r += groups) {
-                const double *a = At + r * R;
-                const double x0 = a[a0], x1 = a1ok ? a[a0 + 1] : 0.0;
-                const double y0 = a[c0], y1 = c1ok ? a[c0 + 1] : 0.0;
-                g00 += x0 * y0;
-                g01 += x0 * y1;
-                g10 += x1 * y0;
-                g11 += x1 * y1;
+                const double2 x = *reinterpret_cast<const double2 *>(At + r * RP + a0);
+                const double2 y = *reinterpret_cast<const double2 *>(At + r * RP + c0);
+                g00 += x.x * y.x;
+                g01 += x.x * y.y;
+                g10 += x.y * y.x;
+                g11 += x.y * y.y;
             }
         }
     }
@@ -807,14 +827,20 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
         double *pdot = psq + c.part_stride;
         double *colsq = w.colsq.as<double>();
         if (deferred) {  // one pass: A_raw, its Gram partials, column partials; R x R finalise
-            int nb = (int)std::min<int64_t>(c.nblocks, (I + kApplyTile - 1) / kApplyTile);
+            const int tile = apply_tile_rows();
+            int nb = (int)std::min<int64_t>(c.nblocks, (I + tile - 1) / tile);
             if (nb < 1) nb = 1;
             const int64_t rpb = (I + nb - 1) / nb;
             nb = (int)((I + rpb - 1) / rpb);
-            const size_t smb = sizeof(double) * (R * R + 2 * kApplyTile * R + 4 * 256);
-            apply_gram_kernel<T><<<nb, 256, smb, c.s>>>(V, I, R, rpb, Ginv, An, psq,
-                                                        last ? pdot : nullptr,
-                                                        w.gpart.as<double>());
+            const size_t smb = sizeof(double) * (2 * tile * ((R + 1) & ~1) + 4 * 256);
+            if (R <= 16)
+                apply_gram_kernel<T, 16><<<nb, 256, smb, c.s>>>(V, I, R, rpb, tile, Ginv, An, psq,
+                                                                last ? pdot : nullptr,
+                                                                w.gpart.as<double>());
+            else
+                apply_gram_kernel<T, 32><<<nb, 256, smb, c.s>>>(V, I, R, rpb, tile, Ginv, An, psq,
+                                                                last ? pdot : nullptr,
+                                                                w.gpart.as<double>());
             reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(psq, nb, R, colsq);
             reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(w.gpart.as<double>(), nb,
                                                                     R * R, graw);
@@ -1169,8 +1195,10 @@ extern "C" sptk_status sptk_cp_als(sptk_tensor t, int64_t R, int max_iters, doub
         cudaFuncSetAttribute(apply_inv_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(apply_inv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(apply_gram_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(apply_gram_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(apply_gram_kernel<double, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(apply_gram_kernel<double, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(apply_gram_kernel<float, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(apply_gram_kernel<float, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(finish_kernel<double, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(finish_kernel<double, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(finish_kernel<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
