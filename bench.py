@@ -278,6 +278,8 @@ def main():
     idx_d, val_d = sdev.tensor(c.seed, c.dims, c.nnz, c.dist, dtype=tdt)
     e1.record()
     t = sp.sptensor_create(c.dims, idx_d, val_d, perm_gather=args.layout == "perm_gather")
+    if world > 1:  # each rank keeps permuted copies of its own row ranges only
+        sp.sptensor_set_shard(t, world, rank)
     e2.record()
     torch.cuda.synchronize()
     del idx_d, val_d

@@ -129,6 +129,16 @@ sptk_status sptk_sptensor_info(sptk_tensor t, int *nmodes, int64_t *dims, int64_
  * copies + workspace). */
 sptk_status sptk_sptensor_device_bytes(sptk_tensor t, int64_t *bytes);
 
+/* Declare that this handle serves rank `rank` of `nranks` row-range shards
+ * (rank g owns rows [b_g, b_{g+1}) of every mode, b =
+ * sptk_partition_rows over rowptr_n).  The permuted copies built afterwards
+ * (build_perm, or lazily by the first MTTKRP of a mode) then hold only this
+ * rank's positions: 1/nranks of the copy memory per rank.  MTTKRP calls whose
+ * rows fall outside the shard stay correct (they gather through perm_n, the
+ * paper's traversal).  Existing copies are dropped.  nranks = 1 restores the
+ * whole-tensor copies.  Errors: SPTK_EINVAL for rank outside [0, nranks). */
+sptk_status sptk_sptensor_set_shard(sptk_tensor t, int nranks, int rank);
+
 /* Build the mode-`mode` permutation (mode = -1: all modes).  P:513-515 (§5
  * "Permutation approach"): "a permutation array for each mode that sorts the
  * tensor nonzeros in increasing index along that mode"; the sort is STABLE

@@ -44,6 +44,7 @@ _SIGS = [
     ("sptk_sptensor_destroy", [_P], _I),
     ("sptk_sptensor_info", [_P, _P, _P, _P, _P], _I),
     ("sptk_sptensor_device_bytes", [_P, _P], _I),
+    ("sptk_sptensor_set_shard", [_P, _I, _I], _I),
     ("sptk_build_perm", [_P, _I, _P], _I),
     ("sptk_get_perm", [_P, _I, _P, _P], _I),
     ("sptk_get_rowptr", [_P, _I, _P, _P], _I),
@@ -199,6 +200,12 @@ def sptensor_device_bytes(t: SpTensor) -> int:
     b = C.c_int64(0)
     _check(lib().sptk_sptensor_device_bytes(t.handle, C.byref(b)), "sptensor_device_bytes")
     return b.value
+
+
+def sptensor_set_shard(t: SpTensor, nranks: int, rank: int):
+    """This handle serves rank `rank` of `nranks` row-range shards: the permuted
+    copies built afterwards hold only this rank's rows (1/nranks of the memory)."""
+    _check(lib().sptk_sptensor_set_shard(t.handle, nranks, rank), "sptensor_set_shard")
 
 
 def build_perm(t: SpTensor, mode: int = -1, stream=None):

@@ -279,6 +279,16 @@ static void setup_note(const char *what, int m, double &t0, cudaStream_t s) {
     t0 = t1;
 }
 
+sptk_status sptk_sptensor_set_shard(sptk_tensor t, int nranks, int rank) {
+    CHECK_HANDLE(t);
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SPTK_EINVAL, "bad shard");
+    if (t->shard_n == nranks && t->shard_r == rank) return SPTK_OK;
+    t->shard_n = nranks;
+    t->shard_r = rank;
+    drop_copies(t);  // rebuilt for the new row ranges by build_perm / the next MTTKRP
+    return SPTK_OK;
+}
+
 sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream) {
     CHECK_HANDLE(t);
     if (mode < -1 || mode >= t->N) return fail(SPTK_EINVAL, "mode out of range");

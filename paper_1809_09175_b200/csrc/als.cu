@@ -926,11 +926,16 @@ static sptk_status als_iteration(AlsCtx &c, double *fit_host, int *status_host) 
         const bool last = n == N - 1;
         const int64_t r0 = multi ? c.b[n][c.comm->rank] : 0;
         const int64_t r1 = multi ? c.b[n][c.comm->rank + 1] : t->dims[n];
-        SPTK_TRY(mttkrp_launch(t, n, c.R, c.A.data(), nullptr, V, r0, r1, c.s));
-        chol_inv_kernel<<<1, 256, sizeof(double) * (R * R + R), c.s>>>(w.G.as<double>(), N, n, R,
-                                                                     Ginv, status);
+        // Gamma^{-1} on the side stream while this rank's MTTKRP rows run
+        SPTK_CUDA(cudaEventRecord(w.ev_gram, c.s));
+        SPTK_CUDA(cudaStreamWaitEvent(w.side, w.ev_gram, 0));
+        chol_inv_kernel<<<1, 256, sizeof(double) * (R * R + R), w.side>>>(w.G.as<double>(), N, n,
+                                                                        R, Ginv, status);
         count_launch();
         SPTK_CUDA(cudaGetLastError());
+        SPTK_CUDA(cudaEventRecord(w.ev_inv, w.side));
+        SPTK_TRY(mttkrp_launch(t, n, c.R, c.A.data(), nullptr, V, r0, r1, c.s));
+        SPTK_CUDA(cudaStreamWaitEvent(c.s, w.ev_inv, 0));
         T *An = static_cast<T *>(c.A[n]);
         const int64_t rows = r1 - r0;
         if (rows > 0) {

@@ -108,6 +108,9 @@ struct sptk_tensor_s {
     bool has_srec[sptk::kMaxModes] = {false};
     sptk::DevBuf wrow[sptk::kMaxModes];         // worker start rows for the copy (cached)
     int copy_sec[sptk::kMaxModes] = {-1, -1, -1, -1, -1, -1};  // copy's secondary mode
+    int64_t copy_p0[sptk::kMaxModes] = {0}, copy_p1[sptk::kMaxModes] = {0};  // copy covers
+                                                // permuted positions [copy_p0, copy_p1)
+    int shard_n = 1, shard_r = 0;               // sptk_sptensor_set_shard
     sptk::DevBuf soff[sptk::kMaxModes];         // slice offsets (slice kernel, cached)
     int64_t soff_key[sptk::kMaxModes][4] = {{-1, -1, -1, -1}};  // (row0, row1, nslice, S)
     int64_t row_max[sptk::kMaxModes] = {-1, -1, -1, -1, -1, -1};  // max nnz of a row (lazy)
@@ -156,6 +159,7 @@ sptk_status launch_pack(sptk_tensor t, const void *idx, sptk_idx_type itype, con
                         int *d_flag, double *d_normsq, cudaStream_t s);
 sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s);
 sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s);
+void drop_copies(sptk_tensor t);
 sptk_status merge_duplicates(sptk_tensor t, bool error_only, cudaStream_t s);
 sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const *factors,
                           const void *lambda, void *out, int64_t row_begin, int64_t row_end,

@@ -282,8 +282,9 @@ static sptk_status slice_offsets(sptk_tensor t, int mode, int64_t r0, int64_t r1
     const int word = (int)(dtype_bytes(t->dtype) / 4) + (a < mode ? a : a - 1);
     int64_t blocks = (n + 255) / 256;
     if (blocks > (int64_t)dev_sms() * 16) blocks = (int64_t)dev_sms() * 16;
+    const int rc = compact_bytes(t->dtype, t->N);
     slice_offsets_kernel<<<(unsigned)blocks, 256, 0, s>>>(
-        t->srec[mode].as<uint8_t>(), compact_bytes(t->dtype, t->N), word,
+        t->srec[mode].as<uint8_t>() - (size_t)t->copy_p0[mode] * rc, rc, word,
         t->rowptr[mode].as<uint32_t>(), r0, r1 - r0, K, S, t->soff[mode].as<uint32_t>());
     count_launch();
     SPTK_CUDA(cudaGetLastError());
@@ -311,6 +312,9 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     if (pe <= pb) return SPTK_OK;
 
     SPTK_TRY(ensure_sorted_copy(t, mode, s));
+    // the copy serves this call if it covers the call's positions (a shard's
+    // copy covers only its own row range)
+    const bool copy = t->has_srec[mode] && pb >= t->copy_p0[mode] && pe <= t->copy_p1[mode];
     MttkrpArgs a{};
     a.rec = t->rec.as<uint8_t>();  // the paper's traversal: gather through perm_n
     a.perm = t->perm[mode].as<uint32_t>();
@@ -343,13 +347,13 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
         while (V > 1 && V > cap) V >>= 1;
     }
     bool fast = t->N >= 3 && t->N <= 5 && ok_v(V) &&
-                (t->has_srec[mode] || V * (int)es == 32);
+                (copy || V * (int)es == 32);
     const int G0 = fast ? pow2ceil((int)((R < 32 * V ? R : 32 * V) / V)) : (R <= 16 ? 4 : 32);
     a.run = run_length(pe - pb, G0);
     // warp-cooperative steps pay off when rows are long (few boundary steps)
     const int64_t rows = row_end - row_begin;
     int var = 0;
-    if (fast && t->has_srec[mode] && G0 < 32) {
+    if (fast && copy && G0 < 32) {
         var = variant_setting();
         // measured (profiles/r01/sweep_*.log): a win for >= 4 groups per warp on
         // rows averaging >= 64 nonzeros, a loss on short rows and for 2 groups
@@ -357,7 +361,7 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     }
     const int64_t chunk = var == 1 ? a.run * (32 / G0) : a.run;
     const int64_t workers = (pe - pb + chunk - 1) / chunk;
-    if (t->deterministic && !(fast && t->has_srec[mode]))
+    if (t->deterministic && !(fast && copy))
         return fail(SPTK_EUNSUPPORTED,
                     "deterministic MTTKRP needs the permuted-copy fast path (N in 3..5, "
                     "element-aligned factors/out/lambda, default layout)");
@@ -367,9 +371,11 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
         a.drow = t->det_row.as<uint32_t>();
         a.dpart = t->det_part.p;
     }
-    if (fast && t->has_srec[mode]) {  // stream the compact permuted copy instead
+    if (fast && copy) {  // stream the compact permuted copy instead
         SPTK_TRY(worker_rows(t, mode, pb, pe, chunk, workers, s));
-        a.rec = t->srec[mode].as<uint8_t>();
+        // indexed by absolute position: base shifted back by the copy's first position
+        a.rec = t->srec[mode].as<uint8_t>() -
+                (size_t)t->copy_p0[mode] * compact_bytes(t->dtype, t->N);
         a.perm = nullptr;
         a.rowptr = t->rowptr[mode].as<uint32_t>();
         a.wrow = t->wrow[mode].as<uint32_t>();
@@ -378,7 +384,7 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     // slice traversal: one column tile (R <= 32 V), 32-byte vectors, the copy
     int64_t S = 0;
     int K = 0;
-    if (fast && t->has_srec[mode] && R <= 32 * V)
+    if (fast && copy && R <= 32 * V)
         K = slice_count(t, mode, row_begin, row_end, pe - pb, R * (int64_t)es, s, &S);
     if (K > 0) {
         SPTK_TRY(slice_offsets(t, mode, row_begin, row_end, K, S, s));
@@ -394,7 +400,7 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
         fprintf(stderr, "[sptk] mttkrp mode %d rows [%lld,%lld) R %lld: %s V %d G0 %d variant %d "
                 "copy %d sec %d slices %d x %lld rows\n", mode, (long long)row_begin,
                 (long long)row_end, (long long)R, fast ? "fast" : "generic", V, G0, var,
-                (int)t->has_srec[mode], t->copy_sec[mode], K, (long long)S);
+                (int)copy, t->copy_sec[mode], K, (long long)S);
 
     cudaEvent_t ev;
     SPTK_TRY(mttkrp_span_begin(s, &ev));

@@ -14,6 +14,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "common.cuh"
 
@@ -359,6 +360,23 @@ static sptk_status stable_sort_ids(sptk_tensor t, int mode, const uint32_t *in, 
 static int copy_secondary_mode(sptk_tensor t, int mode) {
     const char *e = getenv("SPTK_COPY_ORDER");
     if (e && *e == '0') return -1;
+    // SPTK_COPY_SEC=a0,a1,...: per-mode override (tuning; -1 = none)
+    if (const char *o = getenv("SPTK_COPY_SEC")) {
+        int m = 0, v = 0, neg = 0, have = 0;
+        for (const char *c = o;; ++c) {
+            if (*c == '-') neg = 1;
+            else if (*c >= '0' && *c <= '9') v = v * 10 + (*c - '0'), have = 1;
+            else {
+                if (m == mode && have) {
+                    const int a = neg ? -v : v;
+                    return (a >= 0 && a < t->N && a != mode) ? a : -1;
+                }
+                ++m;
+                v = neg = have = 0;
+                if (!*c) break;
+            }
+        }
+    }
     int a = -1;
     for (int m = 0; m < t->N; ++m)
         if (m != mode && t->dims[m] >= 2048 && (a < 0 || t->dims[m] < t->dims[a])) a = m;
@@ -378,8 +396,19 @@ static int copy_secondary_mode(sptk_tensor t, int mode) {
 sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
     if (t->has_srec[mode] || t->perm_gather_only || t->P == 0 || !t->has_perm[mode])
         return SPTK_OK;
+    // positions covered: all, or this shard's row range (sptk_sptensor_set_shard)
+    int64_t p0 = 0, p1 = t->P;
+    if (t->shard_n > 1) {
+        SPTK_TRY(host_rowptr(t, mode, s));
+        std::vector<int64_t> b((size_t)t->shard_n + 1);
+        SPTK_TRY(sptk_partition_rows(t->host_rowptr[mode].data(), t->dims[mode], t->shard_n,
+                                     b.data()));
+        p0 = t->host_rowptr[mode][b[t->shard_r]];
+        p1 = t->host_rowptr[mode][b[t->shard_r + 1]];
+    }
+    const bool whole = p0 == 0 && p1 == t->P;
     const int rc = compact_bytes(t->dtype, t->N);
-    const size_t need = (size_t)rc * t->P;
+    const size_t need = (size_t)rc * (size_t)std::max<int64_t>(p1 - p0, 1);
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
         cudaGetLastError();
@@ -388,29 +417,38 @@ sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
     const size_t reserve = std::max<size_t>(total_b / 32, (size_t)4 << 30);
     int a = copy_secondary_mode(t, mode);
     if (a >= 0 && !t->has_perm[a]) a = -1;
-    // the secondary sort runs inside the copy's own buffer (>= 16 B = 4 words
-    // per nonzero, the sort needs ~3.1) before the copy overwrites it; only
-    // the order itself (4 B per nonzero) is extra
+    // The secondary sort (over all P ids) runs inside the copy's own buffer
+    // (>= 16 B = 4 words per nonzero, the sort needs ~3.1) before the copy
+    // overwrites it; a shard's smaller copy uses the cached sort workspace
+    // instead.  Only the order itself (4 B per nonzero) is extra.
     const size_t order_bytes = a >= 0 ? sizeof(uint32_t) * (size_t)t->P : 0;
-    if (sizeof(uint32_t) * sort_ws_words(t->P) > need) a = -1;
-    // the order lives in the idle sort workspace when that is cached
-    size_t extra = (t->sortws.p && t->sortws.bytes >= order_bytes) ? 0 : order_bytes;
-    if (free_b < need + extra + reserve && t->sortws.p) {  // the sort workspace is a cache too
-        free_b += t->sortws.bytes;
+    const bool ws_in_copy = whole && sizeof(uint32_t) * sort_ws_words(t->P) <= need;
+    if (a >= 0 && !ws_in_copy && !t->sortws.p) a = -1;
+    // the order lives in the idle sort workspace when the sort does not need it
+    size_t extra = (ws_in_copy && t->sortws.p && t->sortws.bytes >= order_bytes) ? 0 : order_bytes;
+    if (free_b < need + extra + reserve && t->sortws.p && (ws_in_copy || a < 0)) {
+        free_b += t->sortws.bytes;  // the sort workspace is a cache too
         t->sortws.release();
         extra = order_bytes;
+        if (!ws_in_copy) a = -1;
     }
-    if (free_b < need + extra + reserve) a = -1;
+    if (free_b < need + extra + reserve) {
+        a = -1;
+        if (free_b < need + reserve && t->sortws.p) {
+            free_b += t->sortws.bytes;
+            t->sortws.release();
+        }
+    }
     if (free_b < need + reserve) return SPTK_OK;
     if (t->srec[mode].reserve(need) != SPTK_OK) {
         set_error("");
         return SPTK_OK;
     }
     const uint32_t *order = t->perm[mode].as<uint32_t>();
-    DevBuf ord;  // the order: in the idle sort workspace if it is cached, else its own buffer
+    DevBuf ord;
     uint32_t *ordp = nullptr;
     if (a >= 0) {
-        if (t->sortws.p && t->sortws.bytes >= order_bytes) ordp = t->sortws.as<uint32_t>();
+        if (ws_in_copy && t->sortws.p && t->sortws.bytes >= order_bytes) ordp = t->sortws.as<uint32_t>();
         else if (ord.reserve(order_bytes) == SPTK_OK) ordp = ord.as<uint32_t>();
         else set_error("");
     }
@@ -418,28 +456,33 @@ sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
     t->soff_key[mode][0] = -1;
     if (ordp) {
         SPTK_TRY(stable_sort_ids(t, mode, t->perm[a].as<uint32_t>(), ordp, nullptr, s,
-                                 t->srec[mode].p, need));
+                                 ws_in_copy ? t->srec[mode].p : nullptr, ws_in_copy ? need : 0));
         order = ordp;
         t->copy_sec[mode] = a;
     }
     const int vw = dtype_bytes(t->dtype) / 4;
-    const unsigned g = (unsigned)grid_for(t->P);
+    const int64_t np = p1 - p0;
+    const unsigned g = (unsigned)grid_for(std::max<int64_t>(np, 1));
     uint8_t *dst = t->srec[mode].as<uint8_t>();
     const uint8_t *src = t->rec.as<uint8_t>();
-    if (t->rec_bytes == 32 && rc == 32)
-        permute_records<32, 32><<<g, 256, 0, s>>>(src, order, t->P, vw, t->N, mode, dst);
-    else if (t->rec_bytes == 32)
-        permute_records<32, 16><<<g, 256, 0, s>>>(src, order, t->P, vw, t->N, mode, dst);
-    else
-        permute_records<16, 16><<<g, 256, 0, s>>>(src, order, t->P, vw, t->N, mode, dst);
-    count_launch();
-    SPTK_CUDA(cudaGetLastError());
+    if (np > 0) {
+        if (t->rec_bytes == 32 && rc == 32)
+            permute_records<32, 32><<<g, 256, 0, s>>>(src, order + p0, np, vw, t->N, mode, dst);
+        else if (t->rec_bytes == 32)
+            permute_records<32, 16><<<g, 256, 0, s>>>(src, order + p0, np, vw, t->N, mode, dst);
+        else
+            permute_records<16, 16><<<g, 256, 0, s>>>(src, order + p0, np, vw, t->N, mode, dst);
+        count_launch();
+        SPTK_CUDA(cudaGetLastError());
+    }
     if (ord.p) SPTK_CUDA(cudaStreamSynchronize(s));  // `ord` is freed on return
+    t->copy_p0[mode] = p0;
+    t->copy_p1[mode] = p1;
     t->has_srec[mode] = true;
     return SPTK_OK;
 }
 
-static void drop_copies(sptk_tensor t) {
+void drop_copies(sptk_tensor t) {
     for (int m = 0; m < t->N; ++m) {
         t->srec[m].release();
         t->has_srec[m] = false;

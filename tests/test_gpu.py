@@ -499,6 +499,40 @@ def test_simulated_row_shards(sp, G):
         assert rel(out.cpu().numpy(), oracle.mttkrp(dims, idx, vals, A, n)) <= 1e-12, n
 
 
+@pytest.mark.parametrize("G", [2, 3])
+def test_shard_local_copies(sp, G):
+    """sptk_sptensor_set_shard: each rank's handle holds copies of its own row
+    range only (smaller device footprint); its own rows match the oracle
+    through the copy, and rows outside the shard still match (perm-gather)."""
+    dims = (1200, 9000, 5000)
+    idx, vals = synth.tensor(95, dims, 4_000_000, "uniform")
+    A = factors_np(96, dims, 16)
+    A_d = [dev(a) for a in A]
+    full = make(sp, dims, idx, vals)
+    sp.build_perm(full, -1)
+    full_bytes = sp.sptensor_device_bytes(full)
+    full.close()
+    Vo = [oracle.mttkrp(dims, idx, vals, A, n) for n in range(3)]
+    for g in range(G):
+        t = make(sp, dims, idx, vals)
+        sp.sptensor_set_shard(t, G, g)
+        sp.build_perm(t, -1)
+        assert sp.sptensor_device_bytes(t) < full_bytes
+        for n in range(3):
+            rp = gpu_perm(sp, t, n)[1]
+            b = sp.partition_rows(rp, G)
+            out = torch.full((dims[n], 16), float("nan"), dtype=torch.float64, device="cuda")
+            sp.mttkrp_rows(t, n, A_d, out, int(b[g]), int(b[g + 1]))
+            got = out[int(b[g]):int(b[g + 1])].cpu().numpy()
+            assert rel(got, Vo[n][int(b[g]):int(b[g + 1])]) <= 1e-12, (g, n)
+            other = (g + 1) % G   # rows of another shard: correct through perm_n
+            out2 = torch.full((dims[n], 16), float("nan"), dtype=torch.float64, device="cuda")
+            sp.mttkrp_rows(t, n, A_d, out2, int(b[other]), int(b[other + 1]))
+            got2 = out2[int(b[other]):int(b[other + 1])].cpu().numpy()
+            assert rel(got2, Vo[n][int(b[other]):int(b[other + 1])]) <= 1e-12, (g, n, "other")
+        t.close()
+
+
 def test_sharded_code_path_one_rank(sp, monkeypatch):
     """The N>1 code path (partition, per-rank launches, NCCL all-reduce and
     grouped broadcasts) driven through a real 1-rank NCCL communicator with
