@@ -231,6 +231,19 @@ static int slice_setting() {  // SPTK_SLICE=0 disables the slice traversal
     return v;
 }
 
+// L2 policy of the other factors' gathers in the slice kernel: in the L2-window
+// regime (A_a > L2 budget) they are evicted first so the window stays
+// resident (Amazon -4 %); otherwise evict_last like every factor row (LBNL:
+// evict_first loses 4 %).  SPTK_SLICE_OTHER_FIRST=0/1 overrides (tuning).
+static int slice_other_first(bool l2_window) {
+    static int v = -2;
+    if (v == -2) {
+        const char *e = getenv("SPTK_SLICE_OTHER_FIRST");
+        v = e ? (*e == '1' ? 1 : 0) : -1;
+    }
+    return v >= 0 ? v : (l2_window ? 1 : 0);
+}
+
 static int64_t slice_rows() {  // SPTK_SLICE_ROWS overrides (tuning)
     static int64_t r = -1;
     if (r < 0) {
@@ -393,6 +406,7 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
         a.row1 = row_end;
         a.nslice = K;
         a.sec = t->copy_sec[mode];
+        a.other_first = slice_other_first(t->dims[a.sec] * R * (int64_t)es > kSliceL2Bytes);
         var = 2;
     }
 

@@ -60,6 +60,7 @@ struct MttkrpArgs {
     const uint32_t *soff;
     int64_t row0, row1;
     int nslice, sec;
+    int other_first;             // slice kernel: non-secondary gathers L2 evict_first
 };
 
 // ----------------------------------------------------------------- loads
@@ -634,6 +635,9 @@ __device__ __forceinline__ void mttkrp_slice_body(const MttkrpArgs &a) {
     const int c = a.col0 + q * V;
     const uint8_t *__restrict__ rec = a.rec;
     const uint64_t pol_stream = policy_evict_first(), pol_factor = policy_evict_last();
+    // the window of the secondary factor stays in L2 (evict_last); with
+    // other_first the other factors' random rows are evicted first
+    const uint64_t pol_other = a.other_first ? pol_stream : pol_factor;
     auto load_rec = [&](uint32_t pos, uint32_t (&w)[8]) {
         if constexpr (RB == 32) ld_rec32_p(rec + (size_t)pos * 32, w, pol_stream);
         else ld_rec16_p(rec + (size_t)pos * 16, w, pol_stream);
@@ -667,7 +671,8 @@ __device__ __forceinline__ void mttkrp_slice_body(const MttkrpArgs &a) {
                     const int word = OFF + (m < MODE ? m : m - 1);
                     const T *src = static_cast<const T *>(a.A[m]) + (int64_t)w[u][word] * a.ld + c;
                     if (base + u * NG + g < e && lane_on) {
-                        vld_sel<T, V>(src, f[u][m], pol_factor, m == a.sec);
+                        vld_sel<T, V>(src, f[u][m], m == a.sec ? pol_factor : pol_other,
+                                      m == a.sec);
                     } else {
 #pragma unroll
                         for (int v = 0; v < V; ++v) f[u][m][v] = T(0);
