@@ -16,6 +16,7 @@ dt = torch.float32 if len(sys.argv) > 4 and sys.argv[4] == "f32" else torch.floa
 idx, val = device.tensor(c.seed, c.dims, c.nnz, c.dist, dtype=dt)
 t = sp.sptensor_create(c.dims, idx, val)
 del idx, val
+torch.cuda.empty_cache()  # return the COO input to the driver (room for the copies)
 sp.build_perm(t, -1)
 F = [torch.empty((I, R), dtype=dt, device="cuda") for I in c.dims]
 res = sp.cp_als(t, R, iters, F, seed=c.seed_f)
