@@ -281,11 +281,11 @@ __global__ void normalize_kernel(T *__restrict__ A, int64_t r0, int64_t r1, int 
 }
 
 // fit from dot_j = sum_k A_raw(k,j) V(k,j) (= lambda_j sum_k A(k,j) V(k,j)),
-// lambda and the Gram matrices -> out[0] = fit, out[1] = <X,M>, out[2] = ||M||^2
-__global__ void __launch_bounds__(256)
-    fit_kernel(const double *__restrict__ dot, const double *__restrict__ lam,
-               const double *__restrict__ G, int N, int R, double normX2,
-               double *__restrict__ out) {
+// lambda and the Gram matrices -> out[0] = fit, out[1] = <X,M>, out[2] = ||M||^2.
+// Called by all 256 threads of one block.
+__device__ void fit_block(const double *__restrict__ dot, const double *__restrict__ lam,
+                          const double *__restrict__ G, int N, int R, double normX2,
+                          double *__restrict__ out) {
     __shared__ double sh[256];
     double acc = 0.0;
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
@@ -310,6 +310,13 @@ __global__ void __launch_bounds__(256)
         out[1] = inner;
         out[2] = normM2;
     }
+}
+
+__global__ void __launch_bounds__(256)
+    fit_kernel(const double *__restrict__ dot, const double *__restrict__ lam,
+               const double *__restrict__ G, int N, int R, double normX2,
+               double *__restrict__ out) {
+    fit_block(dot, lam, G, N, R, normX2, out);
 }
 
 // Tail of a mode update (single GPU), one grid: every block
@@ -382,6 +389,7 @@ __global__ void __launch_bounds__(256)
 // then one pass over V (A_raw, its Gram partials, the column partials) plus an
 // R x R finalisation, instead of apply + normalise + Gram (two passes over A).
 constexpr int kApplyTileDefault = 64;
+constexpr int kTailBlocks = 32;  // apply_gram grids up to this size finalise in their last block
 static int apply_tile_rows() {  // SPTK_APPLY_TILE overrides (tuning)
     static int v = -1;
     if (v < 0) {
@@ -406,12 +414,80 @@ static bool deferred_norm(int64_t R) {
 // and to shared memory; Gram partials of the tile in 2 x 2 register blocks
 // (256 / ceil(R/2)^2 row groups); per-block partials: psq/pdot [blk][R],
 // gpart [blk][R*R].
+// One block.  lambda_n = sqrt(colsq); s_n = 1/lambda_n; the normalised Gram
+// G_n = D_s G_raw D_s.  A zero column j (lambda_j = 0) becomes e_1 as in the
+// oracle (S:160): A_raw(0, j) := 1 with s_j = 1, and its Gram entries are
+// e_1 . A_norm(:, b) = A_raw(0, b) s_b (1 against another zero column).  Then
+// the column scale of the next mode's MTTKRP: prod_{m != next} s_m.
+template <typename T>
+__device__ void finalize_mode_block(const double *__restrict__ colsq,
+                                    const double *__restrict__ graw, T *__restrict__ A, int N,
+                                    int n, int R, int next, double *__restrict__ s_all,
+                                    double *__restrict__ lam, double *__restrict__ G,
+                                    T *__restrict__ scale_next) {
+    __shared__ double sn[128];
+    __shared__ double row0[128];
+    __shared__ int zero[128];
+    const int tid = threadIdx.x;
+    for (int j = tid; j < R; j += blockDim.x) {
+        const double l = sqrt(colsq[j]);
+        lam[j] = l;
+        zero[j] = !(l > 0.0);
+        sn[j] = l > 0.0 ? 1.0 / l : 1.0;
+        row0[j] = (double)A[j];
+    }
+    __syncthreads();
+    double *Gn = G + (int64_t)n * R * R;
+    for (int e = tid; e < R * R; e += blockDim.x) {
+        const int a = e / R, b = e % R;
+        double g;
+        if (!zero[a] && !zero[b]) g = graw[e] * sn[a] * sn[b];
+        else if (zero[a] && zero[b]) g = 1.0;
+        else if (zero[a]) g = row0[b] * sn[b];
+        else g = row0[a] * sn[a];
+        Gn[e] = g;
+    }
+    for (int j = tid; j < R; j += blockDim.x) {
+        if (zero[j]) A[j] = (T)1.0;
+        s_all[(int64_t)n * R + j] = sn[j];
+    }
+    __syncthreads();
+    for (int j = tid; j < R; j += blockDim.x) {
+        double p = 1.0;
+        for (int m = 0; m < N; ++m)
+            if (m != next) p *= (m == n) ? sn[j] : s_all[(int64_t)m * R + j];
+        scale_next[j] = (T)p;
+    }
+    __syncthreads();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+    finalize_mode_kernel(const double *__restrict__ colsq, const double *__restrict__ graw,
+                         T *__restrict__ A, int N, int n, int R, int next,
+                         double *__restrict__ s_all, double *__restrict__ lam,
+                         double *__restrict__ G, T *__restrict__ scale_next) {
+    finalize_mode_block<T>(colsq, graw, A, N, n, R, next, s_all, lam, G, scale_next);
+}
+
+// Where the last block of apply_gram leaves the mode's results (counter NULL:
+// the partials are reduced by separate kernels instead).
+struct ModeTail {
+    int *counter;          // zero-initialised; reset by the last block
+    double *colsq;         // [0,R) sum A_raw^2, [R,2R) sum A_raw V (last mode)
+    double *graw;          // R x R
+    double *s_all, *lam, *G, *fit;
+    void *scale_next;      // R values of the tensor dtype
+    double normX2;
+    int N, n, next;
+};
+
 template <typename T, int RM>  // RM >= R: Gamma^{-1} column length held in registers
 __global__ void __launch_bounds__(256)
     apply_gram_kernel(const T *__restrict__ V, int64_t I, int R, int64_t rows_per_block, int kApplyTile,
                       const double *__restrict__ Ginv, T *__restrict__ A,
                       double *__restrict__ part_sq, double *__restrict__ part_dot,
-                      double *__restrict__ gpart) {
+                      double *__restrict__ gpart, const ModeTail tail) {
     extern __shared__ __align__(16) double sm[];
     const int RP = (R + 1) & ~1;              // padded row stride (16-byte aligned pairs)
     double *Vt = sm;                          // kApplyTile x RP
@@ -499,52 +575,45 @@ __global__ void __launch_bounds__(256)
         for (int g = 0; g < groups; ++g) acc += gs[((size_t)g * nblk + b) * 4 + q];
         if (a < R && c < R) gp[a * R + c] = acc;
     }
-}
-
-// One block.  lambda_n = sqrt(colsq); s_n = 1/lambda_n; the normalised Gram
-// G_n = D_s G_raw D_s.  A zero column j (lambda_j = 0) becomes e_1 as in the
-// oracle (S:160): A_raw(0, j) := 1 with s_j = 1, and its Gram entries are
-// e_1 . A_norm(:, b) = A_raw(0, b) s_b (1 against another zero column).  Then
-// the column scale of the next mode's MTTKRP: prod_{m != next} s_m.
-template <typename T>
-__global__ void __launch_bounds__(256)
-    finalize_mode_kernel(const double *__restrict__ colsq, const double *__restrict__ graw,
-                         T *__restrict__ A, int N, int n, int R, int next,
-                         double *__restrict__ s_all, double *__restrict__ lam,
-                         double *__restrict__ G, T *__restrict__ scale_next) {
-    __shared__ double sn[128];
-    __shared__ double row0[128];
-    __shared__ int zero[128];
-    const int tid = threadIdx.x;
-    for (int j = tid; j < R; j += blockDim.x) {
-        const double l = sqrt(colsq[j]);
-        lam[j] = l;
-        zero[j] = !(l > 0.0);
-        sn[j] = l > 0.0 ? 1.0 / l : 1.0;
-        row0[j] = (double)A[j];
-    }
+    if (!tail.counter) return;
+    // the last block to finish reduces every block's partials (block order,
+    // four interleaved sums combined in a fixed order: deterministic) and
+    // finalises the mode: lambda, scales, normalised Gram, next MTTKRP's
+    // weights, and the fit after the last mode
+    __shared__ int last_block;
+    __threadfence();
     __syncthreads();
-    double *Gn = G + (int64_t)n * R * R;
-    for (int e = tid; e < R * R; e += blockDim.x) {
-        const int a = e / R, b = e % R;
-        double g;
-        if (!zero[a] && !zero[b]) g = graw[e] * sn[a] * sn[b];
-        else if (zero[a] && zero[b]) g = 1.0;
-        else if (zero[a]) g = row0[b] * sn[b];
-        else g = row0[a] * sn[a];
-        Gn[e] = g;
-    }
-    for (int j = tid; j < R; j += blockDim.x) {
-        if (zero[j]) A[j] = (T)1.0;
-        s_all[(int64_t)n * R + j] = sn[j];
-    }
+    if (tid == 0) last_block = atomicAdd(tail.counter, 1) == (int)gridDim.x - 1;
     __syncthreads();
-    for (int j = tid; j < R; j += blockDim.x) {
-        double p = 1.0;
-        for (int m = 0; m < N; ++m)
-            if (m != next) p *= (m == n) ? sn[j] : s_all[(int64_t)m * R + j];
-        scale_next[j] = (T)p;
+    if (!last_block) return;
+    __threadfence();
+    const int nb = gridDim.x, RR = R * R;
+    auto sum_parts = [&](const double *part, int stride, int e) {
+        double acc[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] = 0.0;
+        int b = 0;
+        for (; b + 7 < nb; b += 8) {  // 8 independent loads in flight per thread
+            double v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = __ldcg(part + (int64_t)(b + k) * stride + e);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[k] += v[k];
+        }
+        for (; b < nb; ++b) acc[0] += __ldcg(part + (int64_t)b * stride + e);
+        return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    };
+    for (int e = tid; e < R; e += blockDim.x) {
+        tail.colsq[e] = sum_parts(part_sq, R, e);
+        if (part_dot) tail.colsq[R + e] = sum_parts(part_dot, R, e);
     }
+    for (int e = tid; e < RR; e += blockDim.x) tail.graw[e] = sum_parts(gpart, RR, e);
+    __threadfence_block();
+    __syncthreads();
+    finalize_mode_block<T>(tail.colsq, tail.graw, A, tail.N, tail.n, R, tail.next, tail.s_all,
+                           tail.lam, tail.G, static_cast<T *>(tail.scale_next));
+    if (part_dot) fit_block(tail.colsq + R, tail.lam, tail.G, tail.N, R, tail.normX2, tail.fit);
+    if (tid == 0) *tail.counter = 0;  // ready for the next launch (graph replays)
 }
 
 // A(:, j) *= s_j (the deferred normalisation, once after the last iteration)
@@ -833,26 +902,48 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
             const int64_t rpb = (I + nb - 1) / nb;
             nb = (int)((I + rpb - 1) / rpb);
             const size_t smb = sizeof(double) * (2 * tile * ((R + 1) & ~1) + 4 * 256);
+            // few blocks (small modes): the last block reduces and finalises
+            // in place; many blocks: a single block's reduction is latency-
+            // bound (measured slower than the parallel reduction kernels)
+            ModeTail tail{};
+            tail.counter = nb <= kTailBlocks ? reinterpret_cast<int *>(scale + R) : nullptr;
+            tail.colsq = colsq;
+            tail.graw = graw;
+            tail.s_all = s_all;
+            tail.lam = lam;
+            tail.G = w.G.as<double>();
+            tail.fit = scal;
+            tail.scale_next = scale;
+            tail.normX2 = t->normX2;
+            tail.N = N;
+            tail.n = n;
+            tail.next = (n + 1) % N;
             if (R <= 16)
                 apply_gram_kernel<T, 16><<<nb, 256, smb, c.s>>>(V, I, R, rpb, tile, Ginv, An, psq,
                                                                 last ? pdot : nullptr,
-                                                                w.gpart.as<double>());
+                                                                w.gpart.as<double>(), tail);
             else
                 apply_gram_kernel<T, 32><<<nb, 256, smb, c.s>>>(V, I, R, rpb, tile, Ginv, An, psq,
                                                                 last ? pdot : nullptr,
-                                                                w.gpart.as<double>());
-            reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(psq, nb, R, colsq);
-            reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(w.gpart.as<double>(), nb,
-                                                                    R * R, graw);
-            finalize_mode_kernel<T><<<1, 256, 0, c.s>>>(colsq, graw, An, N, n, R, (n + 1) % N,
-                                                         s_all, lam, w.G.as<double>(), scale);
-            count_launch(4);
+                                                                w.gpart.as<double>(), tail);
+            count_launch();
             SPTK_CUDA(cudaGetLastError());
-            if (last) {
-                double *dot = colsq + R;
-                reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(pdot, nb, R, dot);
-                fit_kernel<<<1, 256, 0, c.s>>>(dot, lam, w.G.as<double>(), N, R, t->normX2, scal);
-                count_launch(2);
+            if (!tail.counter) {  // many blocks: parallel reductions, then one finalise block
+                reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(psq, nb, R, colsq);
+                reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(w.gpart.as<double>(),
+                                                                        nb, R * R, graw);
+                finalize_mode_kernel<T><<<1, 256, 0, c.s>>>(colsq, graw, An, N, n, R,
+                                                             (n + 1) % N, s_all, lam,
+                                                             w.G.as<double>(), scale);
+                count_launch(3);
+                if (last) {
+                    double *dot = colsq + R;
+                    reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(pdot, nb, R, dot);
+                    fit_kernel<<<1, 256, 0, c.s>>>(dot, lam, w.G.as<double>(), N, R, t->normX2,
+                                                   scal);
+                    count_launch(2);
+                }
+                SPTK_CUDA(cudaGetLastError());
             }
         } else {  // explicit normalisation: apply, reduce, normalise + Gram
             int nb = 0;
@@ -1010,7 +1101,7 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     SPTK_TRY(w.scal.reserve(sizeof(double) * 16));
     SPTK_TRY(w.lamT.reserve(es * R));
     SPTK_TRY(w.gpart.reserve(sizeof(double) * (size_t)c.nblocks * R * R));
-    SPTK_TRY(w.scl.reserve(sizeof(double) * ((size_t)N * R + (size_t)R * R + R)));
+    SPTK_TRY(w.scl.reserve(sizeof(double) * ((size_t)N * R + (size_t)R * R + R + 1)));
     if (!w.hres) SPTK_CUDA(cudaMallocHost(&w.hres, sizeof(double) * 16));
     if (!w.side) {
         SPTK_CUDA(cudaStreamCreateWithFlags(&w.side, cudaStreamNonBlocking));
@@ -1072,6 +1163,7 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
         T *scale = reinterpret_cast<T *>(s_all + (size_t)N * R + (size_t)R * R);
         std::vector<T> ones(R, T(1));
         SPTK_CUDA(cudaMemcpyAsync(scale, ones.data(), sizeof(T) * R, cudaMemcpyHostToDevice, s));
+        SPTK_CUDA(cudaMemsetAsync(scale + R, 0, sizeof(int), s));  // apply_gram's block counter
         SPTK_CUDA(cudaStreamSynchronize(s));
         count_launch();
         SPTK_CUDA(cudaGetLastError());
