@@ -355,10 +355,12 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
         return true;
     };
     while (V > 1 && !ok_v(V)) V >>= 1;
-    if (const char *fv = getenv("SPTK_FORCE_V")) {  // tuning: cap the lane vector width
-        const int cap = atoi(fv);
-        while (V > 1 && V > cap) V >>= 1;
-    }
+    static const int v_cap = [] {  // SPTK_FORCE_V: cap the lane vector width (tuning)
+        const char *fv = getenv("SPTK_FORCE_V");
+        return fv ? atoi(fv) : 0;
+    }();
+    if (v_cap > 0)
+        while (V > 1 && V > v_cap) V >>= 1;
     bool fast = t->N >= 3 && t->N <= 5 && ok_v(V) &&
                 (copy || V * (int)es == 32);
     const int G0 = fast ? pow2ceil((int)((R < 32 * V ? R : 32 * V) / V)) : (R <= 16 ? 4 : 32);
