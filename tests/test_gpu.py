@@ -187,6 +187,52 @@ def test_mttkrp_slice_traversal(sp, dtype, R):
     assert rel(got, Vo[37:1151]) <= TOL[dtype]
 
 
+def test_max_size_mode_beyond_int32(sp):
+    """A mode longer than 2^31 (32-bit keys: four radix passes; row offsets,
+    rowptr searches and factor/out addresses past 2^32 elements need 64-bit
+    arithmetic).  The oracle sees the same tensor with the long mode's used
+    indices relabelled densely (MTTKRP is invariant under that relabelling)."""
+    free, _ = torch.cuda.mem_get_info()
+    if free < 100 * (1 << 30):
+        pytest.skip("needs ~80 GB of free device memory")
+    I0, R, P = (1 << 31) + 12345, 4, 60_000
+    dims = (I0, 7, 5)
+    rng = np.random.default_rng(7)
+    used = np.unique(np.concatenate([rng.integers(0, I0, P // 3), [0, I0 - 1]]))
+    idx = np.stack([rng.choice(used, P), rng.integers(0, 7, P), rng.integers(0, 5, P)], axis=1)
+    vals = rng.random(P).astype(np.float32) + 0.5
+    t = sp.sptensor_create(dims, dev(idx.astype(np.int64)), dev(vals))
+    sp.build_perm(t, -1)
+    p0, rp0 = gpu_perm(sp, t, 0)
+    assert np.array_equal(p0, np.argsort(idx[:, 0], kind="stable").astype(np.uint32))
+    assert int(rp0[-1]) == P and int(rp0[I0 - 1]) == P - int((idx[:, 0] == I0 - 1).sum())
+    A0 = torch.rand(I0, R, dtype=torch.float32, device="cuda")
+    A_d = [A0, dev(rng.random((7, R)).astype(np.float32)), dev(rng.random((5, R)).astype(np.float32))]
+    # dense relabelling for the oracle
+    rel_idx = idx.copy()
+    rel_idx[:, 0] = np.searchsorted(used, idx[:, 0])
+    A_h = [A0[torch.from_numpy(used).cuda()].double().cpu().numpy(),
+           A_d[1].double().cpu().numpy(), A_d[2].double().cpu().numpy()]
+    rdims = (len(used), 7, 5)
+    for n in (1, 2):
+        out = torch.empty((dims[n], R), dtype=torch.float32, device="cuda")
+        sp.mttkrp(t, n, A_d, out)
+        Vo = oracle.mttkrp(rdims, rel_idx, vals.astype(np.float64), A_h, n)
+        assert rel(out.double().cpu().numpy(), Vo) <= TOL[torch.float32], n
+    out0 = torch.empty((I0, R), dtype=torch.float32, device="cuda")
+    sp.mttkrp(t, 0, A_d, out0)
+    sample = np.array([0, 1, len(used) // 2, len(used) - 1])
+    Vo = oracle.mttkrp_rows(rdims, rel_idx, vals.astype(np.float64), A_h, 0, sample)
+    got = out0[torch.from_numpy(used[sample]).cuda()].double().cpu().numpy()
+    assert rel(got, Vo) <= TOL[torch.float32]
+    used_set = set(used[:64].tolist())
+    empty = next(r for r in range(1, 64) if r not in used_set)
+    assert float(out0[empty].abs().sum()) == 0.0                    # empty rows are exactly 0
+    del out0, A0, A_d
+    t.close()
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("layout", ["sorted", "perm_gather"])
 def test_mttkrp_contention_and_empty_rows(sp, layout):
     """All nonzeros in one row (maximum contention), a 2-long mode, many empty rows."""
