@@ -283,9 +283,12 @@ __global__ void normalize_kernel(T *__restrict__ A, int64_t r0, int64_t r1, int 
 // fit from dot_j = sum_k A_raw(k,j) V(k,j) (= lambda_j sum_k A(k,j) V(k,j)),
 // lambda and the Gram matrices -> out[0] = fit, out[1] = <X,M>, out[2] = ||M||^2.
 // Called by all 256 threads of one block.
+// trace (nullable): the fit is also appended at trace[(*trace_n)++] (device-side
+// fit history, so iterations can be replayed back to back without a host sync)
 __device__ void fit_block(const double *__restrict__ dot, const double *__restrict__ lam,
                           const double *__restrict__ G, int N, int R, double normX2,
-                          double *__restrict__ out) {
+                          double *__restrict__ out, double *__restrict__ trace = nullptr,
+                          int *__restrict__ trace_n = nullptr) {
     __shared__ double sh[256];
     double acc = 0.0;
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
@@ -309,14 +312,16 @@ __device__ void fit_block(const double *__restrict__ dot, const double *__restri
         out[0] = 1.0 - sqrt(res2) / sqrt(normX2);
         out[1] = inner;
         out[2] = normM2;
+        if (trace) trace[(*trace_n)++] = out[0];
     }
 }
 
 __global__ void __launch_bounds__(256)
     fit_kernel(const double *__restrict__ dot, const double *__restrict__ lam,
                const double *__restrict__ G, int N, int R, double normX2,
-               double *__restrict__ out) {
-    fit_block(dot, lam, G, N, R, normX2, out);
+               double *__restrict__ out, double *__restrict__ trace = nullptr,
+               int *__restrict__ trace_n = nullptr) {
+    fit_block(dot, lam, G, N, R, normX2, out, trace, trace_n);
 }
 
 // Tail of a mode update (single GPU), one grid: every block
@@ -477,6 +482,8 @@ struct ModeTail {
     double *colsq;         // [0,R) sum A_raw^2, [R,2R) sum A_raw V (last mode)
     double *graw;          // R x R
     double *s_all, *lam, *G, *fit;
+    double *trace;         // device fit history (see fit_block)
+    int *trace_n;
     void *scale_next;      // R values of the tensor dtype
     double normX2;
     int N, n, next;
@@ -612,7 +619,9 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     finalize_mode_block<T>(tail.colsq, tail.graw, A, tail.N, tail.n, R, tail.next, tail.s_all,
                            tail.lam, tail.G, static_cast<T *>(tail.scale_next));
-    if (part_dot) fit_block(tail.colsq + R, tail.lam, tail.G, tail.N, R, tail.normX2, tail.fit);
+    if (part_dot)
+        fit_block(tail.colsq + R, tail.lam, tail.G, tail.N, R, tail.normX2, tail.fit, tail.trace,
+                  tail.trace_n);
     if (tid == 0) *tail.counter = 0;  // ready for the next launch (graph replays)
 }
 
@@ -876,6 +885,8 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
     double *s_all = w.scl.as<double>();                      // N x R column scales
     double *graw = s_all + (size_t)N * R;                    // R x R Gram of A_raw
     T *scale = reinterpret_cast<T *>(graw + (size_t)R * R);  // R: next MTTKRP's weights
+    double *trace = w.trace.as<double>();                     // device fit history
+    int *trace_n = reinterpret_cast<int *>(scal + 12);
     const bool deferred = deferred_norm(R);
     for (int n = 0; n < N; ++n) {
         const bool last = n == N - 1;
@@ -913,6 +924,8 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
             tail.lam = lam;
             tail.G = w.G.as<double>();
             tail.fit = scal;
+            tail.trace = trace;
+            tail.trace_n = trace_n;
             tail.scale_next = scale;
             tail.normX2 = t->normX2;
             tail.N = N;
@@ -940,7 +953,7 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
                     double *dot = colsq + R;
                     reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(pdot, nb, R, dot);
                     fit_kernel<<<1, 256, 0, c.s>>>(dot, lam, w.G.as<double>(), N, R, t->normX2,
-                                                   scal);
+                                                   scal, trace, trace_n);
                     count_launch(2);
                 }
                 SPTK_CUDA(cudaGetLastError());
@@ -975,7 +988,8 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
             if (last) {
                 double *dot = colsq + R;
                 reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(pdot, nb, R, dot);
-                fit_kernel<<<1, 256, 0, c.s>>>(dot, lam, w.G.as<double>(), N, R, t->normX2, scal);
+                fit_kernel<<<1, 256, 0, c.s>>>(dot, lam, w.G.as<double>(), N, R, t->normX2, scal,
+                                               trace, trace_n);
                 count_launch(2);
             }
         }
@@ -1099,6 +1113,7 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     SPTK_TRY(w.colsq.reserve(sizeof(double) * 2 * R));
     SPTK_TRY(w.lam.reserve(sizeof(double) * R));
     SPTK_TRY(w.scal.reserve(sizeof(double) * 16));
+    SPTK_TRY(w.trace.reserve(sizeof(double) * (size_t)std::max(max_iters, 1)));
     SPTK_TRY(w.lamT.reserve(es * R));
     SPTK_TRY(w.gpart.reserve(sizeof(double) * (size_t)c.nblocks * R * R));
     SPTK_TRY(w.scl.reserve(sizeof(double) * ((size_t)N * R + (size_t)R * R + R + 1)));
@@ -1211,6 +1226,34 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
             }
             if (cudaGraphLaunch(exec, s) != cudaSuccess) {
                 st = cuda_fail(cudaGetLastError(), "cudaGraphLaunch(ALS iteration)");
+                break;
+            }
+            if (tol <= 0.0 && it >= 2) {
+                // no convergence test: replay the remaining iterations back to
+                // back (no host round trip per iteration); the fits are taken
+                // from the device-side history afterwards, the Cholesky status
+                // (sticky) once at the end
+                for (int k = it + 1; k < max_iters; ++k) {
+                    profile().launches += launches_per_iter;
+                    if (cudaGraphLaunch(exec, s) != cudaSuccess) {
+                        st = cuda_fail(cudaGetLastError(), "cudaGraphLaunch(ALS iteration)");
+                        break;
+                    }
+                }
+                if (st != SPTK_OK) break;
+                st = complete_iteration(c, &fit, &bad);
+                if (st != SPTK_OK) break;
+                std::vector<double> hist((size_t)max_iters);
+                SPTK_CUDA(cudaMemcpy(hist.data(), w.trace.p, sizeof(double) * max_iters,
+                                     cudaMemcpyDeviceToHost));
+                if (bad) {
+                    st = fail(SPTK_ESINGULAR, "Gamma is singular after the ridge retry");
+                    break;
+                }
+                if (fit_trace)
+                    for (int k = it; k < max_iters; ++k) fit_trace[k] = hist[k];
+                fit = hist[max_iters - 1];
+                it = max_iters;
                 break;
             }
             st = complete_iteration(c, &fit, &bad);

@@ -79,6 +79,7 @@ struct ALSWork {
     DevBuf stage;     // host<->device staging for factors
     DevBuf lamT;      // R (T) lambda in tensor dtype
     DevBuf gpart;     // per-block partial Gram matrices (f64)
+    DevBuf trace;     // device fit history, one double per iteration
     DevBuf scl;       // deferred normalisation: s_m = 1/lambda_m (N x R f64), then the
                       // next MTTKRP's column scale prod_{m != n} s_m (R, tensor dtype)
     cudaStream_t side = nullptr;              // Cholesky / inverse, overlapped with MTTKRP
