@@ -810,12 +810,21 @@ struct AlsCtx {
 // G_m = A_m^T A_m (fixed-order reduction of per-block partials in `part`,
 // default w.partial; the fused path passes w.gpart so w.partial keeps the
 // fit's column partials)
+// rows [r0, r1) only when r1 >= 0 (a rank's own rows; an empty range gives 0)
 template <typename T>
-static sptk_status gram(AlsCtx &c, int m, double *part = nullptr) {
+static sptk_status gram(AlsCtx &c, int m, double *part = nullptr, int64_t r0 = 0,
+                        int64_t r1 = -1) {
     sptk_tensor t = c.t;
     ALSWork &w = t->als;
     const int R = (int)c.R;
-    const int64_t I = t->dims[m];
+    if (r1 < 0) r1 = t->dims[m];
+    const int64_t I = r1 - r0;
+    if (I <= 0) {
+        SPTK_CUDA(cudaMemsetAsync(w.G.as<double>() + (int64_t)m * R * R, 0,
+                                  sizeof(double) * R * R, c.s));
+        return SPTK_OK;
+    }
+    const T *Am = static_cast<const T *>(c.A[m]) + r0 * R;
     int nb = (int)std::min<int64_t>(c.nblocks, (I + kGramTileRows - 1) / kGramTileRows);
     const int64_t rpb = (I + nb - 1) / nb;
     nb = (int)((I + rpb - 1) / rpb);
@@ -823,15 +832,13 @@ static sptk_status gram(AlsCtx &c, int m, double *part = nullptr) {
     if (R > 32) {
         const int nt = (R + kTB - 1) / kTB;
         gram_tiled_kernel<T><<<dim3((unsigned)nb, (unsigned)(nt * nt)), 256, 0, c.s>>>(
-            static_cast<const T *>(c.A[m]), I, R, rpb, part);
+            Am, I, R, rpb, part);
     } else {
         const size_t sm = sizeof(double) * kGramTileRows * R;
         if (R <= 16)
-            gram_partial_kernel<T, 1><<<nb, 256, sm, c.s>>>(static_cast<const T *>(c.A[m]), I, R,
-                                                            rpb, part);
+            gram_partial_kernel<T, 1><<<nb, 256, sm, c.s>>>(Am, I, R, rpb, part);
         else
-            gram_partial_kernel<T, 4><<<nb, 256, sm, c.s>>>(static_cast<const T *>(c.A[m]), I, R,
-                                                            rpb, part);
+            gram_partial_kernel<T, 4><<<nb, 256, sm, c.s>>>(Am, I, R, rpb, part);
     }
     reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(
         part, nb, R * R, w.G.as<double>() + (int64_t)m * R * R);
@@ -1031,8 +1038,10 @@ static sptk_status als_iteration(AlsCtx &c, double *fit_host, int *status_host) 
         const bool last = n == N - 1;
         const int64_t r0 = multi ? c.b[n][c.comm->rank] : 0;
         const int64_t r1 = multi ? c.b[n][c.comm->rank + 1] : t->dims[n];
-        // Gamma^{-1} on the side stream while this rank's MTTKRP rows run
-        SPTK_CUDA(cudaEventRecord(w.ev_gram, c.s));
+        // Gamma^{-1} on the side stream while this rank's MTTKRP rows run; it
+        // needs only the Gram matrices, final once G_{n-1} was all-reduced
+        // (the event was recorded there, before the row broadcast)
+        if (n == 0) SPTK_CUDA(cudaEventRecord(w.ev_gram, c.s));
         SPTK_CUDA(cudaStreamWaitEvent(w.side, w.ev_gram, 0));
         chol_inv_kernel<<<1, 256, sizeof(double) * (R * R + R), w.side>>>(w.G.as<double>(), N, n,
                                                                         R, Ginv, status);
@@ -1064,8 +1073,14 @@ static sptk_status als_iteration(AlsCtx &c, double *fit_host, int *status_host) 
             An, r0, r1, R, colsq, lam);
         count_launch();
         SPTK_CUDA(cudaGetLastError());
+        // G_n = sum over ranks of the Gram matrix of each rank's own normalised
+        // rows (R x R all-reduce), so the next mode's Cholesky can run on the
+        // side stream while the rows are being broadcast
+        SPTK_TRY(gram<T>(c, n, nullptr, r0, r1));
+        if (multi) SPTK_TRY(comm_allreduce_f64(c.comm, w.G.as<double>() + (int64_t)n * R * R,
+                                               (int64_t)R * R, c.s));
+        SPTK_CUDA(cudaEventRecord(w.ev_gram, c.s));
         if (multi) SPTK_TRY(comm_bcast_rows(c.comm, An, c.R, t->dtype, c.b[n].data(), c.s));
-        SPTK_TRY(gram<T>(c, n));
     }
     fit_kernel<<<1, 256, 0, c.s>>>(colsq + R, lam, w.G.as<double>(), N, R, t->normX2, scal);
     count_launch();
