@@ -112,6 +112,7 @@ struct sptk_tensor_s {
     int64_t copy_p0[sptk::kMaxModes] = {0}, copy_p1[sptk::kMaxModes] = {0};  // copy covers
                                                 // permuted positions [copy_p0, copy_p1)
     int shard_n = 1, shard_r = 0;               // sptk_sptensor_set_shard
+    bool copy_rowrec[sptk::kMaxModes] = {false};  // copy records carry the row index
     sptk::DevBuf soff[sptk::kMaxModes];         // slice offsets (slice kernel, cached)
     int64_t soff_key[sptk::kMaxModes][4] = {{-1, -1, -1, -1}};  // (row0, row1, nslice, S)
     int64_t row_max[sptk::kMaxModes] = {-1, -1, -1, -1, -1, -1};  // max nnz of a row (lazy)

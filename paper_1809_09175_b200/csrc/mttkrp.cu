@@ -213,6 +213,15 @@ constexpr int64_t kSliceRows = 2048;
 // hit L2 instead of HBM.
 constexpr int64_t kSliceL2Bytes = 32 << 20;
 
+static bool rowrec_setting() {  // SPTK_ROWREC=0: per-group kernel tracks rows via rowptr (A/B)
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPTK_ROWREC");
+        v = (e && *e == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 static bool debug_dispatch() {  // SPTK_DEBUG_DISPATCH=1: one stderr line per MTTKRP launch
     static int v = -1;
     if (v < 0) {
@@ -386,6 +395,7 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
         a.drow = t->det_row.as<uint32_t>();
         a.dpart = t->det_part.p;
     }
+    a.rowrec = copy && t->copy_rowrec[mode] && var == 0 && rowrec_setting();
     if (fast && copy) {  // stream the compact permuted copy instead
         SPTK_TRY(worker_rows(t, mode, pb, pe, chunk, workers, s));
         // indexed by absolute position: base shifted back by the copy's first position

@@ -61,6 +61,7 @@ struct MttkrpArgs {
     int64_t row0, row1;
     int nslice, sec;
     int other_first;             // slice kernel: non-secondary gathers L2 evict_first
+    int rowrec;                  // per-group kernel: row index stored in the copy's spare word
 };
 
 // ----------------------------------------------------------------- loads
@@ -277,7 +278,10 @@ template <> __device__ __forceinline__ float rec_val<float>(const uint32_t (&w)[
 // the worker's start row `wrow` (rows only grow along the permutation).
 // Otherwise the paper's traversal: p = perm_n[i] (prefetched one step ahead),
 // gather the full record p and read l_pn from it.
-template <typename T, int N, int MODE, int G, int U, int RB, bool SORTED, int V>
+// ROWREC (permuted copy with a spare record word): the row is read from the
+// record instead of advancing through rowptr_n -- no dependent rowptr load per
+// row change (short rows) or per empty row (power-law modes)
+template <typename T, int N, int MODE, int G, int U, int RB, bool SORTED, int V, bool ROWREC>
 __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
     constexpr int OFF = sizeof(T) / 4;  // first index word in a record
     const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -332,7 +336,7 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
 
     uint32_t row = 0;   // SORTED: row of the current position
     uint32_t nxt = 0;   // SORTED: first position of row + 1
-    if constexpr (SORTED) {
+    if constexpr (SORTED && !ROWREC) {
         row = __ldg(a.wrow + worker);
         nxt = __ldg(a.rowptr + row + 1);
     }
@@ -396,7 +400,9 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
         for (int u = 0; u < U; ++u) {
             if (p[u] == kNoRow) continue;
             uint32_t r;
-            if constexpr (SORTED) {
+            if constexpr (SORTED && ROWREC) {
+                r = w[u][OFF + N - 1];
+            } else if constexpr (SORTED) {
                 const uint32_t pos = i + u;
                 while (pos >= nxt) {
                     ++row;
@@ -428,13 +434,13 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
     if (a.dpart && !wrote0 && q == 0) a.drow[2 * worker] = kNoRow;
 }
 
-template <typename T, int N, int G, int U, int RB, bool SORTED, int MINB, int V>
+template <typename T, int N, int G, int U, int RB, bool SORTED, int MINB, int V, bool ROWREC>
 __global__ void __launch_bounds__(256, MINB) mttkrp_fast_kernel(const MttkrpArgs a) {
-    if constexpr (N >= 1) if (a.mode == 0) { mttkrp_fast_body<T, N, 0, G, U, RB, SORTED, V>(a); return; }
-    if constexpr (N >= 2) if (a.mode == 1) { mttkrp_fast_body<T, N, 1, G, U, RB, SORTED, V>(a); return; }
-    if constexpr (N >= 3) if (a.mode == 2) { mttkrp_fast_body<T, N, 2, G, U, RB, SORTED, V>(a); return; }
-    if constexpr (N >= 4) if (a.mode == 3) { mttkrp_fast_body<T, N, 3, G, U, RB, SORTED, V>(a); return; }
-    if constexpr (N >= 5) if (a.mode == 4) { mttkrp_fast_body<T, N, 4, G, U, RB, SORTED, V>(a); return; }
+    if constexpr (N >= 1) if (a.mode == 0) { mttkrp_fast_body<T, N, 0, G, U, RB, SORTED, V, ROWREC>(a); return; }
+    if constexpr (N >= 2) if (a.mode == 1) { mttkrp_fast_body<T, N, 1, G, U, RB, SORTED, V, ROWREC>(a); return; }
+    if constexpr (N >= 3) if (a.mode == 2) { mttkrp_fast_body<T, N, 2, G, U, RB, SORTED, V, ROWREC>(a); return; }
+    if constexpr (N >= 4) if (a.mode == 3) { mttkrp_fast_body<T, N, 3, G, U, RB, SORTED, V, ROWREC>(a); return; }
+    if constexpr (N >= 5) if (a.mode == 4) { mttkrp_fast_body<T, N, 4, G, U, RB, SORTED, V, ROWREC>(a); return; }
 }
 
 // ------------------------------------------------- warp-cooperative body
@@ -815,7 +821,7 @@ constexpr int kNumVariants = 2;
 template <int N> constexpr int kU = N <= 3 ? SPTK_KU : SPTK_KU_WIDE;
 template <int N> constexpr int kMinBlocks = N <= 3 ? SPTK_KMINB : SPTK_KMINB_WIDE;
 
-template <typename T, int N, int RB, bool SORTED, bool COOP, int V>
+template <typename T, int N, int RB, bool SORTED, bool COOP, int V, bool ROWREC = false>
 inline sptk_status fast_launch_g(int G, const MttkrpArgs &a, int64_t workers, cudaStream_t s) {
     const int64_t threads = COOP ? workers * 32 : workers * G;
     const unsigned blocks = (unsigned)((threads + 255) / 256);
@@ -823,7 +829,7 @@ inline sptk_status fast_launch_g(int G, const MttkrpArgs &a, int64_t workers, cu
     if constexpr (COOP)                                                                       \
         mttkrp_coop_kernel<T, N, GG, kU<N>, RB, kMinBlocks<N>, V><<<blocks, 256, 0, s>>>(a);        \
     else                                                                                      \
-        mttkrp_fast_kernel<T, N, GG, kU<N>, RB, SORTED, kMinBlocks<N>, V><<<blocks, 256, 0, s>>>(a);
+        mttkrp_fast_kernel<T, N, GG, kU<N>, RB, SORTED, kMinBlocks<N>, V, ROWREC><<<blocks, 256, 0, s>>>(a);
     switch (G) {
     case 1: SPTK_LAUNCH_G(1) break;
     case 2: SPTK_LAUNCH_G(2) break;
@@ -880,6 +886,8 @@ sptk_status launch_fast_tnv(int G, int variant, const MttkrpArgs &a, int64_t wor
         }                                                                                    \
         if (variant == 2) return slice_launch_g<T, N, RC, V>(G, a, s);                       \
         if (variant == 1) return fast_launch_g<T, N, RC, true, true, V>(G, a, workers, s);   \
+        if constexpr (RC / 4 >= (int)sizeof(T) / 4 + N)       /* spare word: row in record */ \
+            if (a.rowrec) return fast_launch_g<T, N, RC, true, false, V, true>(G, a, workers, s); \
         return fast_launch_g<T, N, RC, true, false, V>(G, a, workers, s);                    \
     }
 

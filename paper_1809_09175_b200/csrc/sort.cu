@@ -338,6 +338,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int m = 0; m < kMaxModes; ++m)
             if (m < N && m != mode && vw + m < 8 && d < 8) o[d++] = w[vw + m];
+        if (d < RC / 4) o[d] = w[vw + mode];  // spare word: the row (mode-n index) itself
         uint4 *dst = reinterpret_cast<uint4 *>(srec + (size_t)i * RC);
         dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
         if constexpr (RC == 32) dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
@@ -478,6 +479,7 @@ sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
     if (ord.p) SPTK_CUDA(cudaStreamSynchronize(s));  // `ord` is freed on return
     t->copy_p0[mode] = p0;
     t->copy_p1[mode] = p1;
+    t->copy_rowrec[mode] = rc / 4 >= vw + t->N;
     t->has_srec[mode] = true;
     return SPTK_OK;
 }
