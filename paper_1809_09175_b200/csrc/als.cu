@@ -405,6 +405,15 @@ static int apply_tile_rows() {  // SPTK_APPLY_TILE overrides (tuning)
 }
 
 // the deferred path for R <= 32 (SPTK_DEFERRED_NORM=0: explicit normalisation, for A/B)
+static int apply_nb_mult() {  // SPTK_APPLY_NB_MULT: apply_gram block cap = mult x 8 x SMs
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPTK_APPLY_NB_MULT");
+        v = (e && atoi(e) > 0) ? atoi(e) : 1;
+    }
+    return v;
+}
+
 static bool deferred_norm(int64_t R) {
     static int v = -1;
     if (v < 0) {
@@ -805,6 +814,7 @@ struct AlsCtx {
     int nblocks;                           // blocks of the R x R partial-sum kernels
     int nb_row;                            // blocks of the R-vector partial-sum kernels
     size_t part_stride;                    // doubles between the psq and pdot partials
+    int nb_apply = 0;                      // block cap of apply_gram
 };
 
 // G_m = A_m^T A_m (fixed-order reduction of per-block partials in `part`,
@@ -915,7 +925,7 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
         double *colsq = w.colsq.as<double>();
         if (deferred) {  // one pass: A_raw, its Gram partials, column partials; R x R finalise
             const int tile = apply_tile_rows();
-            int nb = (int)std::min<int64_t>(c.nblocks, (I + tile - 1) / tile);
+            int nb = (int)std::min<int64_t>(c.nb_apply, (I + tile - 1) / tile);
             if (nb < 1) nb = 1;
             const int64_t rpb = (I + nb - 1) / nb;
             nb = (int)((I + rpb - 1) / rpb);
@@ -1130,7 +1140,8 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     SPTK_TRY(w.scal.reserve(sizeof(double) * 16));
     SPTK_TRY(w.trace.reserve(sizeof(double) * (size_t)std::max(max_iters, 1)));
     SPTK_TRY(w.lamT.reserve(es * R));
-    SPTK_TRY(w.gpart.reserve(sizeof(double) * (size_t)c.nblocks * R * R));
+    c.nb_apply = c.nblocks * apply_nb_mult();
+    SPTK_TRY(w.gpart.reserve(sizeof(double) * (size_t)c.nb_apply * R * R));
     SPTK_TRY(w.scl.reserve(sizeof(double) * ((size_t)N * R + (size_t)R * R + R + 1)));
     if (!w.hres) SPTK_CUDA(cudaMallocHost(&w.hres, sizeof(double) * 16));
     if (!w.side) {
