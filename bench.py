@@ -65,6 +65,15 @@ def peaks():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
+def limiter_for(workload_key: str):
+    """What ncu showed bounds the MTTKRP launch (committed capture), if any."""
+    try:
+        j = json.load(open(os.path.join(ROOT, "profiles", "ncu_limiter.json")))
+        return j.get(workload_key)
+    except Exception:
+        return None
+
+
 def traffic_for(workload_key: str):
     """ncu DRAM bytes per MTTKRP launch from the committed capture, if any."""
     try:
@@ -454,7 +463,8 @@ def main():
                          "dram_traffic_frac": (traffic / (mttkrp_ms_launch * 1e-3) / 1e9 / peak
                                                if traffic else None),
                          "timing": "per-launch CUDA events in a second K-iteration pass "
-                                   "(eager launches), mean over all MTTKRP launches"},
+                                   "(eager launches), mean over all MTTKRP launches",
+                         "ncu": limiter_for(f"{args.config}_R{R}_{args.dtype}")},
             "clocks": clk.summary(),
             "gpu_launches": launches,
             "e2e": e2e,
