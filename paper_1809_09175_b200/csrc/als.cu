@@ -414,6 +414,15 @@ static int apply_nb_mult() {  // SPTK_APPLY_NB_MULT: apply_gram block cap = mult
     return v;
 }
 
+static int64_t tail_rows() {  // SPTK_TAIL_ROWS (tuning); 0 = grid by tile only
+    static int64_t v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPTK_TAIL_ROWS");
+        v = e ? (int64_t)atoll(e) : 0;
+    }
+    return v;
+}
+
 static bool deferred_norm(int64_t R) {
     static int v = -1;
     if (v < 0) {
@@ -926,6 +935,9 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
         if (deferred) {  // one pass: A_raw, its Gram partials, column partials; R x R finalise
             const int tile = apply_tile_rows();
             int nb = (int)std::min<int64_t>(c.nb_apply, (I + tile - 1) / tile);
+            // modes up to tail_rows() rows: few fat blocks, so the mode tail
+            // (reductions, finalise, fit) runs in the last block, no extra launches
+            if (I <= tail_rows()) nb = std::min(nb, kTailBlocks);
             if (nb < 1) nb = 1;
             const int64_t rpb = (I + nb - 1) / nb;
             nb = (int)((I + rpb - 1) / rpb);
