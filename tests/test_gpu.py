@@ -737,6 +737,29 @@ def test_deterministic_mode_bitwise(sp, variant, R, dtype):
     assert e.value.name == "EUNSUPPORTED"
 
 
+@pytest.mark.parametrize("variant", [0, 1])
+def test_deterministic_rowrec_n4(sp, variant):
+    """Deterministic mode on an N = 4 fp64 tensor, whose 32-byte copy records
+    carry the row index (per-group kernel reads it from the record):
+    repeated runs bit-identical, values match the oracle."""
+    dims = (700, 90, 40, 2000)
+    idx, vals = synth.tensor(65, dims, 30 * 4096 + 11, "powerlaw")
+    R = 16
+    A = factors_np(66, dims, R)
+    t = sp.sptensor_create(dims, dev(idx.astype(np.int64)), dev(vals), deterministic=True)
+    sp.build_perm(t, -1)
+    try:
+        sp.set_tuning(variant, 16)
+        for n in range(4):
+            V1 = gpu_mttkrp(sp, t, n, A, R, torch.float64)
+            V2 = gpu_mttkrp(sp, t, n, A, R, torch.float64)
+            assert np.array_equal(V1, V2), n
+            Vo = oracle.mttkrp(dims, idx, vals, A, n, acc_long=True)
+            assert rel(V1, Vo) <= 1e-12, n
+    finally:
+        sp.set_tuning(-2, -2)
+
+
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
 def test_duplicate_policies(sp, dtype):
     dims = (30, 20, 10)
