@@ -6,6 +6,9 @@
 #include <time.h>
 
 #include <algorithm>
+#include <vector>
+#include <mutex>
+#include <thread>
 #include <new>
 
 #include "common.cuh"
@@ -105,6 +108,160 @@ sptk_status launch_sum_f64(const double *in, int64_t n, double *out, cudaStream_
     return SPTK_OK;
 }
 
+
+// ------------------------------------------------------------ host ingest
+// Inputs in host memory are streamed in chunks: chunk k is copied into a
+// pinned staging buffer (pageable sources; several CPU threads) and DMA'd on a
+// copy stream while chunk k-1 is packed on the caller's stream -- the transfer
+// overlaps the pack (and its sort-key emission), device staging is two
+// chunks instead of the whole COO input, and pageable arrays reach PCIe rates.
+constexpr int64_t kIngestChunk = 1 << 20;  // nonzeros per chunk (SPTK_INGEST_CHUNK overrides)
+static int64_t ingest_chunk() {
+    static int64_t v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPTK_INGEST_CHUNK");
+        v = (e && atoll(e) >= 4096) ? (int64_t)atoll(e) : kIngestChunk;
+    }
+    return v;
+}
+
+static bool host_pinned(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// two pinned staging buffers, kept for the process (pinning is slow)
+struct PinnedStage {
+    std::mutex mu;
+    void *buf[2] = {nullptr, nullptr};
+    size_t bytes = 0;
+};
+static PinnedStage &pinned_stage() {
+    static PinnedStage p;
+    return p;
+}
+
+static void parallel_copy(void *dst, const void *src, size_t n) {
+    const size_t kMin = (size_t)8 << 20;
+    unsigned nt = std::thread::hardware_concurrency();
+    nt = std::max(1u, std::min(nt, 8u));
+    if (n < kMin || nt == 1) {
+        memcpy(dst, src, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    const size_t per = (n + nt - 1) / nt;
+    for (unsigned k = 0; k < nt; ++k) {
+        const size_t a = k * per, b = std::min(n, a + per);
+        if (a >= b) break;
+        th.emplace_back([=] { memcpy(static_cast<char *>(dst) + a, static_cast<const char *>(src) + a, b - a); });
+    }
+    for (auto &x : th) x.join();
+}
+
+static sptk_status ingest_chunked(sptk_tensor t, const void *idx, sptk_idx_type itype,
+                                  const void *vals, int *d_flag, double *d_norm, cudaStream_t s) {
+    const int64_t P = t->P;
+    const size_t irow = (itype == SPTK_IDX_I64 ? 8 : 4) * (size_t)t->N, vsz = dtype_bytes(t->dtype);
+    const int64_t C = std::min<int64_t>(P, ingest_chunk());
+    const int64_t nchunks = (P + C - 1) / C;
+    const bool dev_i = is_device_ptr(idx), dev_v = is_device_ptr(vals);
+    const bool pin_i = !dev_i && host_pinned(idx), pin_v = !dev_v && host_pinned(vals);
+    const bool stage_i = !dev_i && !pin_i, stage_v = !dev_v && !pin_v;
+    const size_t chunk_bytes = (size_t)C * (irow + vsz);
+    DevBuf dstage, parts;
+    SPTK_TRY(dstage.reserve(2 * chunk_bytes));
+    const int pb = pack_blocks(C);
+    SPTK_TRY(parts.reserve(sizeof(double) * (size_t)nchunks * pb));
+    SPTK_CUDA(cudaMemsetAsync(parts.p, 0, sizeof(double) * (size_t)nchunks * pb, s));
+    PinnedStage &ps = pinned_stage();
+    std::unique_lock<std::mutex> lock(ps.mu, std::defer_lock);
+    if (stage_i || stage_v) {
+        lock.lock();
+        if (ps.bytes < chunk_bytes) {
+            for (void *&b : ps.buf)
+                if (b) cudaFreeHost(b), b = nullptr;
+            ps.bytes = 0;
+            for (void *&b : ps.buf) SPTK_CUDA(cudaHostAlloc(&b, chunk_bytes, cudaHostAllocPortable));
+            ps.bytes = chunk_bytes;
+        }
+    }
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_pack[2] = {nullptr, nullptr};
+    sptk_status st = SPTK_OK;
+    auto cleanup = [&] {
+        cudaStreamSynchronize(s);
+        if (cs) cudaStreamSynchronize(cs), cudaStreamDestroy(cs);
+        for (int b = 0; b < 2; ++b) {
+            if (ev_copy[b]) cudaEventDestroy(ev_copy[b]);
+            if (ev_pack[b]) cudaEventDestroy(ev_pack[b]);
+        }
+    };
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
+        cleanup();
+        return cuda_fail(cudaGetLastError(), "ingest stream");
+    }
+    for (int b = 0; b < 2; ++b)
+        if (cudaEventCreateWithFlags(&ev_copy[b], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ev_pack[b], cudaEventDisableTiming) != cudaSuccess) {
+            cleanup();
+            return cuda_fail(cudaGetLastError(), "ingest events");
+        }
+    for (int64_t k = 0; k < nchunks && st == SPTK_OK; ++k) {
+        const int b = (int)(k & 1);
+        const int64_t off = k * C, n = std::min(C, P - off);
+        char *di = dstage.as<char>() + b * chunk_bytes, *dv = di + (size_t)C * irow;
+        const char *si = static_cast<const char *>(idx) + (size_t)off * irow;
+        const char *sv = static_cast<const char *>(vals) + (size_t)off * vsz;
+        if (k >= 2 && cudaStreamWaitEvent(cs, ev_pack[b], 0) != cudaSuccess) {  // device buffer free
+            st = cuda_fail(cudaGetLastError(), "ingest wait");
+            break;
+        }
+        if ((stage_i || stage_v) && k >= 2 && cudaEventSynchronize(ev_copy[b]) != cudaSuccess) {
+            st = cuda_fail(cudaGetLastError(), "ingest wait");  // pinned buffer b free
+            break;
+        }
+        char *hp = static_cast<char *>(ps.buf[b]);
+        const void *src_i = dev_i ? (const void *)si : si, *src_v = dev_v ? (const void *)sv : sv;
+        if (stage_i) {
+            parallel_copy(hp, si, (size_t)n * irow);
+            src_i = hp;
+        }
+        if (stage_v) {
+            parallel_copy(hp + (size_t)C * irow, sv, (size_t)n * vsz);
+            src_v = hp + (size_t)C * irow;
+        }
+        const void *pi = di, *pv = dv;
+        if (!dev_i) {
+            if (cudaMemcpyAsync(di, src_i, (size_t)n * irow, cudaMemcpyHostToDevice, cs) != cudaSuccess)
+                st = cuda_fail(cudaGetLastError(), "H2D idx");
+        } else {
+            pi = si;
+        }
+        if (st == SPTK_OK && !dev_v) {
+            if (cudaMemcpyAsync(dv, src_v, (size_t)n * vsz, cudaMemcpyHostToDevice, cs) != cudaSuccess)
+                st = cuda_fail(cudaGetLastError(), "H2D vals");
+        } else if (dev_v) {
+            pv = sv;
+        }
+        if (st != SPTK_OK) break;
+        if (cudaEventRecord(ev_copy[b], cs) != cudaSuccess ||
+            cudaStreamWaitEvent(s, ev_copy[b], 0) != cudaSuccess) {
+            st = cuda_fail(cudaGetLastError(), "ingest events");
+            break;
+        }
+        st = launch_pack_chunk(t, pi, itype, pv, n, off, d_flag, parts.as<double>() + k * pb, s);
+        if (st == SPTK_OK && cudaEventRecord(ev_pack[b], s) != cudaSuccess)
+            st = cuda_fail(cudaGetLastError(), "ingest events");
+    }
+    if (st == SPTK_OK) st = launch_sum_f64(parts.as<double>(), nchunks * pb, d_norm, s);
+    cleanup();  // the staging buffers are released on return
+    return st;
+}
 }  // namespace sptk
 
 using namespace sptk;
@@ -160,27 +317,9 @@ sptk_status sptk_sptensor_create(int nmodes, const int64_t *dims, int64_t nnz, c
 
     sptk_status st = SPTK_OK;
     if (nnz > 0) {
-        DevBuf sidx, svals, flag;
-        const size_t ib = (itype == SPTK_IDX_I64 ? 8 : 4) * (size_t)nnz * nmodes;
-        const size_t vb = (size_t)dtype_bytes(dtype) * nnz;
-        const void *didx = idx, *dvals = vals;
+        DevBuf flag;
+        const bool host_input = !is_device_ptr(idx) || !is_device_ptr(vals);
         if ((st = t->rec.reserve((size_t)t->rec_bytes * nnz)) != SPTK_OK) goto bad;
-        if (!is_device_ptr(idx)) {
-            if ((st = sidx.reserve(ib)) != SPTK_OK) goto bad;
-            if (cudaMemcpyAsync(sidx.p, idx, ib, cudaMemcpyHostToDevice, s) != cudaSuccess) {
-                st = cuda_fail(cudaGetLastError(), "H2D idx");
-                goto bad;
-            }
-            didx = sidx.p;
-        }
-        if (!is_device_ptr(vals)) {
-            if ((st = svals.reserve(vb)) != SPTK_OK) goto bad;
-            if (cudaMemcpyAsync(svals.p, vals, vb, cudaMemcpyHostToDevice, s) != cudaSuccess) {
-                st = cuda_fail(cudaGetLastError(), "H2D vals");
-                goto bad;
-            }
-            dvals = svals.p;
-        }
         if (!(flags & (SPTK_CREATE_DUP_SUM | SPTK_CREATE_DUP_ERROR))) {
             // emit the sort keys at ingest when they fit next to a reserve
             // (otherwise build_perm extracts them from the records per mode)
@@ -200,7 +339,9 @@ sptk_status sptk_sptensor_create(int nmodes, const int64_t *dims, int64_t nnz, c
             st = cuda_fail(cudaGetLastError(), "memset flag");
             goto bad;
         }
-        if ((st = launch_pack(t, didx, itype, dvals, d_flag, d_norm, s)) != SPTK_OK) goto bad;
+        st = host_input ? ingest_chunked(t, idx, itype, vals, d_flag, d_norm, s)
+                        : launch_pack(t, idx, itype, vals, d_flag, d_norm, s);
+        if (st != SPTK_OK) goto bad;
         struct {
             int flag;
             int pad;

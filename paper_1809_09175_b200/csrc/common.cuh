@@ -157,6 +157,11 @@ inline int compact_bytes(sptk_dtype dt, int N) {
 }
 
 // --- kernels implemented in the .cu files (host launchers) ---
+int pack_blocks(int64_t P);
+sptk_status launch_pack_chunk(sptk_tensor t, const void *idx, sptk_idx_type itype,
+                              const void *vals, int64_t P, int64_t off, int *d_flag,
+                              double *partial, cudaStream_t s);
+sptk_status launch_sum_f64(const double *in, int64_t n, double *out, cudaStream_t s);
 sptk_status launch_pack(sptk_tensor t, const void *idx, sptk_idx_type itype, const void *vals,
                         int *d_flag, double *d_normsq, cudaStream_t s);
 sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s);
