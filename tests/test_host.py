@@ -97,3 +97,23 @@ def test_synth_deterministic_and_ranges():
     assert abs(top - np.log(2) / np.log(1401)) < 0.01    # Zipf(1) head mass
     f = synth.factor(3, 3, 1, 5, 4)
     assert f.shape == (5, 4) and (f >= 0).all() and (f < 1).all()
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference (the oracle arm, CPU only) prints one JSON
+    line with the driver's keys; run on the tiny config."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                        "--config", "tiny", "--steps", "2", "--warmup", "1"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "impl", "cpu_baseline", "e2e", "config", "dtype"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["steps"] == 2
