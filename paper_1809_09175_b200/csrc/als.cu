@@ -423,13 +423,9 @@ static int64_t tail_rows() {  // SPTK_TAIL_ROWS (tuning); 0 = grid by tile only
     return v;
 }
 
-static bool deferred_norm(int64_t R) {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("SPTK_DEFERRED_NORM");
-        v = (e && *e == '0') ? 0 : 1;
-    }
-    return v == 1 && R <= 32;
+static bool deferred_norm(int64_t R) {  // read per call: tests switch it per case
+    const char *e = getenv("SPTK_DEFERRED_NORM");
+    return !(e && *e == '0') && R <= 32;
 }
 
 // Rows [b0, b1) of the block: V tile -> shared memory (coalesced), A_raw tile =

@@ -363,6 +363,36 @@ def test_cp_als_tiny_trajectory(sp):
     assert rel(lamh, lam.cpu().numpy()) <= 1e-12
 
 
+@pytest.mark.parametrize("deferred", ["1", "0"])
+def test_cp_als_zero_column_ridge(sp, deferred, monkeypatch):
+    """Initial factors with a zero column make every Gamma singular (ridge
+    retry) and that column of A_raw exactly zero (lambda_j = 0, column := e_1);
+    the trajectory, factors and lambda still follow the oracle -- through the
+    deferred-normalisation tail and the explicit one."""
+    monkeypatch.setenv("SPTK_DEFERRED_NORM", deferred)
+    c = synth.CONFIGS["tiny"]
+    idx, vals = synth.unique_tensor(c.seed, c.dims, c.nnz)
+    R = 6
+    init = factors_np(c.seed_f, c.dims, R)
+    for a in init:
+        a[:, 2] = 0.0
+    t = make(sp, c.dims, idx, vals)
+    A = [dev(a) for a in init]
+    lam = torch.empty(R, dtype=torch.float64, device="cuda")
+    res = sp.cp_als(t, R, 6, A, init=[dev(a) for a in init], lambda_out=lam)
+    ref = oracle.cp_als(c.dims, idx, vals, init, 6)
+    assert np.max(np.abs(res["trace"] - ref["trace"])) <= 1e-9
+    assert rel(lam.cpu().numpy(), ref["lam"]) <= 1e-8
+    for m in range(3):
+        assert rel(A[m].cpu().numpy(), ref["A"][m]) <= 1e-8
+    # one iteration: mode 0's column 2 is exactly e_1 (lambda = 0 on the way)
+    A1 = [dev(a) for a in init]
+    sp.cp_als(t, R, 1, A1, init=[dev(a) for a in init])
+    ref1 = oracle.cp_als(c.dims, idx, vals, init, 1)
+    col = A1[0][:, 2].cpu().numpy()
+    assert col[0] == 1.0 and not col[1:].any() and np.array_equal(col, ref1["A"][0][:, 2])
+
+
 def test_cp_als_planted_recovery_and_f32(sp):
     dims = (400, 300, 500)
     idx, vals, mu, B = synth.planted_tensor(21, dims, 5, (60, 25, 20))
