@@ -610,13 +610,15 @@ def test_simulated_row_shards(sp, G):
         assert rel(out.cpu().numpy(), oracle.mttkrp(dims, idx, vals, A, n)) <= 1e-12, n
 
 
-@pytest.mark.parametrize("G", [2, 3])
-def test_shard_local_copies(sp, G):
+@pytest.mark.parametrize("G,dims,P", [(2, (1200, 9000, 5000), 4_000_000),
+                                      (3, (1200, 9000, 5000), 4_000_000),
+                                      (2, (4800, 9000, 5000), 8_000_000)])   # slice path per shard
+def test_shard_local_copies(sp, G, dims, P):
     """sptk_sptensor_set_shard: each rank's handle holds copies of its own row
     range only (smaller device footprint); its own rows match the oracle
-    through the copy, and rows outside the shard still match (perm-gather)."""
-    dims = (1200, 9000, 5000)
-    idx, vals = synth.tensor(95, dims, 4_000_000, "uniform")
+    through the copy (per-group / cooperative / slice kernels, shifted copy
+    base), and rows outside the shard still match (perm-gather)."""
+    idx, vals = synth.tensor(95, dims, P, "uniform")
     A = factors_np(96, dims, 16)
     A_d = [dev(a) for a in A]
     full = make(sp, dims, idx, vals)
