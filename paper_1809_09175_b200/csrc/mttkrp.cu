@@ -212,6 +212,14 @@ constexpr int64_t kSliceRows = 2048;
 // fastest), so the whole GPU sweeps one window at a time and the A_a gathers
 // hit L2 instead of HBM.
 constexpr int64_t kSliceL2Bytes = 32 << 20;
+static int64_t slice_l2_bytes() {  // SPTK_SLICE_L2_MB overrides the L2 window (tuning)
+    static int64_t v = -1;
+    if (v < 0) {
+        const char *e = getenv("SPTK_SLICE_L2_MB");
+        v = (e && atoi(e) > 0) ? (int64_t)atoi(e) << 20 : kSliceL2Bytes;
+    }
+    return v;
+}
 
 static bool rowrec_setting() {  // SPTK_ROWREC=0: per-group kernel tracks rows via rowptr (A/B)
     static int v = -1;
@@ -273,7 +281,15 @@ static int slice_count(sptk_tensor t, int mode, int64_t r0, int64_t r1, int64_t 
     if (a < 0 || t->deterministic || !slice_setting() || r1 <= r0) return 0;
     const int64_t rows = r1 - r0;
     int64_t sa = slice_rows();
-    if (t->dims[a] * row_bytes > kSliceL2Bytes) sa = std::max<int64_t>(sa, kSliceL2Bytes / row_bytes);
+    if (t->dims[a] * row_bytes > slice_l2_bytes()) {
+        sa = std::max<int64_t>(sa, slice_l2_bytes() / row_bytes);
+        // L2-window regime: short rows would leave few nonzeros per (row,
+        // window); widen the windows (up to 2x) to keep ~96 per run (measured
+        // on Amazon's 354-nonzero rows: 32 -> 57 MB windows, -7 %)
+        const int64_t k32 = (t->dims[a] + sa - 1) / sa;
+        const int64_t kfit = std::max<int64_t>(2, nnz / (rows * 96));
+        if (kfit < k32) sa = std::min<int64_t>(2 * sa, (t->dims[a] + kfit - 1) / kfit);
+    }
     const int64_t K = (t->dims[a] + sa - 1) / sa;
     if (K < 2 || K > 65535) return 0;
     if (nnz < 32 * K * rows) return 0;
@@ -418,7 +434,7 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
         a.row1 = row_end;
         a.nslice = K;
         a.sec = t->copy_sec[mode];
-        a.other_first = slice_other_first(t->dims[a.sec] * R * (int64_t)es > kSliceL2Bytes);
+        a.other_first = slice_other_first(t->dims[a.sec] * R * (int64_t)es > slice_l2_bytes());
         var = 2;
     }
 
