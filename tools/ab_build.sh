@@ -1,6 +1,7 @@
 #!/bin/bash
 # Build libsptk.so with extra nvcc flags into $1 (A/B experiments), e.g.
-#   tools/ab_build.sh tools/ab/libA.so -DSPTK_ROW_L1='".L1::no_allocate"'
+#   tools/ab_build.sh tools/abx/libA.so -DSPTK_ROW_L1='".L1::no_allocate"'
+# (tools/abx/ travels to the GPU box with gpurun; tools/ab/ is gpurun-ignored; both git-ignored *.so)
 out=$1; shift
 tmp=$(mktemp -d)
 for f in paper_1809_09175_b200/csrc/*.cu; do
