@@ -162,7 +162,12 @@ sptk_status sptk_get_rowptr(sptk_tensor t, int mode, uint32_t *out, void *stream
  * are visited in perm_n order (through perm_n, or streaming the permuted copy
  * of the records), a row is accumulated in registers and written
  * when the mode-n index changes -- plain store for rows interior to a
- * worker's block, atomic add for a block's first/last row.
+ * worker's block, atomic add for a block's first/last row.  On
+ * long balanced rows the B200 slice traversal splits each row's run by the
+ * copy's secondary index and adds one partial per (row, slice) atomically
+ * (DESIGN.md §4); the result is the same sum.  The first call for a mode may
+ * synchronise `stream` once (host copy of rowptr_n for launch decisions);
+ * later calls do not, so they can be captured in a CUDA graph.
  *   mode     n in [0, nmodes)
  *   R        rank (columns), >= 1
  *   factors  HOST array of nmodes DEVICE pointers, factors[m] is I_m x R
