@@ -33,3 +33,40 @@ for pg in (False, True):
         sp.cp_als(t, R, 5, F, seed=1)
     torch.cuda.synchronize()
 print("sanitize case done")
+
+# later paths: slice traversal (L1 windows), row index in 32-byte copy records
+# (N = 4 fp64), chunked host ingest (2 chunks), shard-local copies, deterministic
+dims = (2400, 4096, 3000)
+idx, vals = synth.tensor(93, dims, 200_000, "uniform")
+t = sp.sptensor_create(dims, idx.astype(np.int64), vals)          # host ingest path
+sp.build_perm(t, -1)
+A = [torch.rand(I, 16, dtype=torch.float64, device="cuda") for I in dims]
+for n in range(3):
+    out = torch.empty(dims[n], 16, dtype=torch.float64, device="cuda")
+    sp.mttkrp(t, n, A, out)
+    sp.mttkrp_rows(t, n, A, out, 100, dims[n] - 100)
+t.close()
+big = synth.tensor(94, (300, 200, 100), 1_100_000, "uniform")       # > 1 ingest chunk
+t = sp.sptensor_create((300, 200, 100), big[0].astype(np.int64), big[1])
+sp.sptensor_set_shard(t, 2, 1)
+sp.build_perm(t, -1)
+A = [torch.rand(I, 8, dtype=torch.float64, device="cuda") for I in (300, 200, 100)]
+for n in range(3):
+    out = torch.empty((300, 200, 100)[n], 8, dtype=torch.float64, device="cuda")
+    sp.mttkrp(t, n, A, out)
+t.close()
+d4 = (200, 90, 40, 300)
+i4, v4 = synth.tensor(95, d4, 50_000, "powerlaw")
+for det in (False, True):
+    t = sp.sptensor_create(d4, torch.from_numpy(i4.astype(np.int64)).cuda(),
+                           torch.from_numpy(v4).cuda(), deterministic=det)
+    sp.build_perm(t, -1)
+    A = [torch.rand(I, 16, dtype=torch.float64, device="cuda") for I in d4]
+    for n in range(4):
+        out = torch.empty(d4[n], 16, dtype=torch.float64, device="cuda")
+        sp.mttkrp(t, n, A, out)
+    F = [torch.empty(I, 16, dtype=torch.float64, device="cuda") for I in d4]
+    sp.cp_als(t, 16, 5, F, seed=1)
+    t.close()
+torch.cuda.synchronize()
+print("sanitize case done")
