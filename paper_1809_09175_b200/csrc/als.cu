@@ -649,6 +649,11 @@ __global__ void scale_columns_kernel(T *__restrict__ A, int64_t I, int R,
         A[i] = (T)((double)A[i] * s[i % R]);
 }
 
+template <typename T>
+__global__ void fill_kernel(T *__restrict__ out, int n, T v) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = v;
+}
+
 __global__ void fill_f64_kernel(double *__restrict__ out, int n, double v) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = v;
@@ -1210,11 +1215,9 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
         double *s_all = w.scl.as<double>();
         fill_f64_kernel<<<(unsigned)((N * R + 255) / 256), 256, 0, s>>>(s_all, N * (int)R, 1.0);
         T *scale = reinterpret_cast<T *>(s_all + (size_t)N * R + (size_t)R * R);
-        std::vector<T> ones(R, T(1));
-        SPTK_CUDA(cudaMemcpyAsync(scale, ones.data(), sizeof(T) * R, cudaMemcpyHostToDevice, s));
+        fill_kernel<T><<<1, 128, 0, s>>>(scale, (int)R, T(1));  // no host staging, no sync
         SPTK_CUDA(cudaMemsetAsync(scale + R, 0, sizeof(int), s));  // apply_gram's block counter
-        SPTK_CUDA(cudaStreamSynchronize(s));
-        count_launch();
+        count_launch(2);
         SPTK_CUDA(cudaGetLastError());
     }
 
