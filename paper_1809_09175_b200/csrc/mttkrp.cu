@@ -201,12 +201,14 @@ __global__ void slice_offsets_kernel(const uint8_t *__restrict__ srec, int rc, i
     }
 }
 
-// Rows of A_a per slice.  Measured (profiles/r01/sweep_slice.log): the
-// optimum is ~2048 rows for both fp64 (128 B rows) and fp32 (64 B) at R = 16 --
+// Rows of A_a per slice.  Measured (profiles/r01/sweep_slice.log): 1024-4096
+// rows are within ~2 % at R = 16; 4096 is best for fp64 (128 B rows), 2048
+// for fp32 (64 B) --
 // the slices keep the block's 8 warps sweeping the same window of A_a (their
 // reuse is temporal, the window need not be L1-resident), while longer slices
 // mean fewer partial flushes.  One slice (no slicing) loses the alignment.
-constexpr int64_t kSliceRows = 2048;
+constexpr int64_t kSliceRows = 2048;      // fp32
+constexpr int64_t kSliceRowsF64 = 4096;   // fp64: -0.9 % CP-ALS on NELL-2 vs 2048 (3 reps, same box)
 // When A_a itself exceeds L2 (Amazon shape), a slice is instead an L2-sized
 // window of A_a: blocks are scheduled slice-major (grid.x = row blocks runs
 // fastest), so the whole GPU sweeps one window at a time and the A_a gathers
@@ -261,13 +263,13 @@ static int slice_other_first(bool l2_window) {
     return v >= 0 ? v : (l2_window ? 1 : 0);
 }
 
-static int64_t slice_rows() {  // SPTK_SLICE_ROWS overrides (tuning)
+static int64_t slice_rows(size_t es) {  // SPTK_SLICE_ROWS overrides (tuning)
     static int64_t r = -1;
     if (r < 0) {
         const char *e = getenv("SPTK_SLICE_ROWS");
-        r = (e && atoi(e) > 0) ? (int64_t)atoi(e) : kSliceRows;
+        r = (e && atoi(e) > 0) ? (int64_t)atoi(e) : 0;
     }
-    return r;
+    return r > 0 ? r : (es == 8 ? kSliceRowsF64 : kSliceRows);
 }
 
 // Number of slices for the slice traversal of `mode` over rows [r0, r1), or
@@ -280,7 +282,7 @@ static int slice_count(sptk_tensor t, int mode, int64_t r0, int64_t r1, int64_t 
     const int a = t->copy_sec[mode];
     if (a < 0 || t->deterministic || !slice_setting() || r1 <= r0) return 0;
     const int64_t rows = r1 - r0;
-    int64_t sa = slice_rows();
+    int64_t sa = slice_rows(dtype_bytes(t->dtype));
     if (t->dims[a] * row_bytes > slice_l2_bytes()) {
         sa = std::max<int64_t>(sa, slice_l2_bytes() / row_bytes);
         // L2-window regime: short rows would leave few nonzeros per (row,
