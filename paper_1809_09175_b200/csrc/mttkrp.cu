@@ -202,13 +202,13 @@ __global__ void slice_offsets_kernel(const uint8_t *__restrict__ srec, int rc, i
 }
 
 // Rows of A_a per slice.  Measured (profiles/r01/sweep_slice.log): 1024-4096
-// rows are within ~2 % at R = 16; 4096 is best for fp64 (128 B rows), 2048
-// for fp32 (64 B) --
+// rows are within ~2-3 %; fp64 is best at ~512 KB of A_a per slice (R = 16:
+// 4096 rows, R = 64: 1024), fp32 at 2048 rows --
 // the slices keep the block's 8 warps sweeping the same window of A_a (their
 // reuse is temporal, the window need not be L1-resident), while longer slices
 // mean fewer partial flushes.  One slice (no slicing) loses the alignment.
-constexpr int64_t kSliceRows = 2048;      // fp32
-constexpr int64_t kSliceRowsF64 = 4096;   // fp64: -0.9 % CP-ALS on NELL-2 vs 2048 (3 reps, same box)
+constexpr int64_t kSliceRows = 2048;          // fp32
+constexpr int64_t kSliceBytesF64 = 512 << 10;  // fp64: 512 KB of A_a rows (R=16: 4096, R=64: 1024)
 // When A_a itself exceeds L2 (Amazon shape), a slice is instead an L2-sized
 // window of A_a: blocks are scheduled slice-major (grid.x = row blocks runs
 // fastest), so the whole GPU sweeps one window at a time and the A_a gathers
@@ -263,13 +263,15 @@ static int slice_other_first(bool l2_window) {
     return v >= 0 ? v : (l2_window ? 1 : 0);
 }
 
-static int64_t slice_rows(size_t es) {  // SPTK_SLICE_ROWS overrides (tuning)
+static int64_t slice_rows(size_t es, int64_t row_bytes) {  // SPTK_SLICE_ROWS overrides (tuning)
     static int64_t r = -1;
     if (r < 0) {
         const char *e = getenv("SPTK_SLICE_ROWS");
         r = (e && atoi(e) > 0) ? (int64_t)atoi(e) : 0;
     }
-    return r > 0 ? r : (es == 8 ? kSliceRowsF64 : kSliceRows);
+    if (r > 0) return r;
+    if (es == 8) return std::min<int64_t>(8192, std::max<int64_t>(512, kSliceBytesF64 / row_bytes));
+    return kSliceRows;
 }
 
 // Number of slices for the slice traversal of `mode` over rows [r0, r1), or
@@ -282,7 +284,7 @@ static int slice_count(sptk_tensor t, int mode, int64_t r0, int64_t r1, int64_t 
     const int a = t->copy_sec[mode];
     if (a < 0 || t->deterministic || !slice_setting() || r1 <= r0) return 0;
     const int64_t rows = r1 - r0;
-    int64_t sa = slice_rows(dtype_bytes(t->dtype));
+    int64_t sa = slice_rows(dtype_bytes(t->dtype), row_bytes);
     if (t->dims[a] * row_bytes > slice_l2_bytes()) {
         sa = std::max<int64_t>(sa, slice_l2_bytes() / row_bytes);
         // L2-window regime: short rows would leave few nonzeros per (row,
