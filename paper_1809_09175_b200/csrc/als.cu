@@ -200,6 +200,83 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+
+// Gamma^{-1} by in-place Gauss-Jordan in shared memory, all threads per step
+// (R steps x 3 barriers) -- the Cholesky above has a long dependent chain on
+// one warp and sits on the critical path when the MTTKRP is short.  Without
+// pivoting, the pivots of an SPD matrix are the squared Cholesky diagonal, so
+// a non-positive pivot is exactly the Cholesky failure: same ridge retry.
+__global__ void __launch_bounds__(256)
+    gj_inv_kernel(const double *__restrict__ G, int N, int n, int R,
+                  double *__restrict__ Ginv, int *__restrict__ status) {
+    extern __shared__ double sm[];
+    double *M = sm;           // R x R
+    double *f = sm + R * R;   // R: column j before the update
+    __shared__ double piv;
+    __shared__ int bad;
+    const int tid = threadIdx.x, RR = R * R;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        double ridge = 0.0;
+        if (attempt) {
+            double tr = 0.0;  // every thread: trace of Gamma (R products, tiny)
+            for (int j = 0; j < R; ++j) {
+                double h = 1.0;
+                for (int m = 0; m < N; ++m)
+                    if (m != n) h *= G[(int64_t)m * RR + j * R + j];
+                tr += h;
+            }
+            ridge = 1e-12 * (tr / (double)R);
+        }
+        for (int e = tid; e < RR; e += blockDim.x) {
+            double h = 1.0;
+            for (int m = 0; m < N; ++m)
+                if (m != n) h *= G[(int64_t)m * RR + e];
+            M[e] = h + ((e / R == e % R) ? ridge : 0.0);
+        }
+        if (tid == 0) bad = 0;
+        __syncthreads();
+        for (int j = 0; j < R; ++j) {
+            if (tid == 0) {
+                double p = M[j * R + j];
+                if (!(p > 0.0)) {
+                    bad = 1;
+                    p = 1.0;
+                }
+                piv = 1.0 / p;
+            }
+            for (int i = tid; i < R; i += blockDim.x) f[i] = M[i * R + j];
+            __syncthreads();
+            const double rp = piv;
+            for (int k = tid; k < R; k += blockDim.x)
+                M[j * R + k] = (k == j ? 1.0 : M[j * R + k]) * rp;
+            __syncthreads();
+            for (int e = tid; e < RR; e += blockDim.x) {
+                const int i = e / R, k = e % R;
+                if (i != j) M[e] = (k == j ? 0.0 : M[e]) - f[i] * M[j * R + k];
+            }
+            __syncthreads();
+        }
+        const int failed = bad;
+        __syncthreads();
+        if (!failed) break;
+        if (attempt == 1 && tid == 0) atomicOr(status, 1);
+    }
+    for (int e = tid; e < RR; e += blockDim.x) Ginv[e] = M[e];
+}
+
+// Gamma^{-1} for mode n (SPTK_GAMMA_INV=chol forces the Cholesky kernel)
+static void launch_ginv(const double *G, int N, int n, int R, double *Ginv, int *status,
+                        cudaStream_t s) {
+    static const bool chol = [] {
+        const char *e = getenv("SPTK_GAMMA_INV");
+        return e && e[0] == 'c';
+    }();
+    if (chol)
+        chol_inv_kernel<<<1, 256, sizeof(double) * (R * R + R), s>>>(G, N, n, R, Ginv, status);
+    else
+        gj_inv_kernel<<<1, 256, sizeof(double) * (R * R + R), s>>>(G, N, n, R, Ginv, status);
+}
+
 // A_raw(k,:) = V(k,:) Gamma^{-1} for rows [r0, r1); per-block partial column
 // sums of squares of A_raw (-> lambda) and, for the fit, of A_raw(k,j) V(k,j).
 // Thread t: column j = t % R, row lane t / R (R <= 256).
@@ -921,8 +998,7 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
         // side stream: Gamma^{-1} for mode n once G_{n-1} is final
         SPTK_CUDA(cudaEventRecord(w.ev_gram, c.s));
         SPTK_CUDA(cudaStreamWaitEvent(w.side, w.ev_gram, 0));
-        chol_inv_kernel<<<1, 256, sizeof(double) * (R * R + R), w.side>>>(w.G.as<double>(), N, n,
-                                                                        R, Ginv, status);
+        launch_ginv(w.G.as<double>(), N, n, R, Ginv, status, w.side);
         count_launch();
         SPTK_CUDA(cudaGetLastError());
         SPTK_CUDA(cudaEventRecord(w.ev_inv, w.side));
@@ -1066,8 +1142,7 @@ static sptk_status als_iteration(AlsCtx &c, double *fit_host, int *status_host) 
         // (the event was recorded there, before the row broadcast)
         if (n == 0) SPTK_CUDA(cudaEventRecord(w.ev_gram, c.s));
         SPTK_CUDA(cudaStreamWaitEvent(w.side, w.ev_gram, 0));
-        chol_inv_kernel<<<1, 256, sizeof(double) * (R * R + R), w.side>>>(w.G.as<double>(), N, n,
-                                                                        R, Ginv, status);
+        launch_ginv(w.G.as<double>(), N, n, R, Ginv, status, w.side);
         count_launch();
         SPTK_CUDA(cudaGetLastError());
         SPTK_CUDA(cudaEventRecord(w.ev_inv, w.side));
@@ -1372,6 +1447,7 @@ extern "C" sptk_status sptk_cp_als(sptk_tensor t, int64_t R, int max_iters, doub
         cudaFuncSetAttribute(apply_inv_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(apply_inv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(gj_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(apply_gram_kernel<double, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(apply_gram_kernel<double, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(apply_gram_kernel<float, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
