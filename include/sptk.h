@@ -79,7 +79,7 @@ typedef enum {
     SPTK_ENOMEM = 5,       /* device allocation failed */
     SPTK_ECUDA = 6,        /* CUDA runtime error (handle poisoned) */
     SPTK_ENCCL = 7,        /* NCCL missing or failed */
-    SPTK_ESINGULAR = 8,    /* Cholesky of Gamma failed after the ridge retry */
+    SPTK_ESINGULAR = 8,    /* Gamma not positive definite after the ridge retry */
     SPTK_EZERONORM = 9,    /* ||X|| = 0 in cp_als */
     SPTK_EUNSUPPORTED = 10 /* outside the limits above */
 } sptk_status;
@@ -207,8 +207,9 @@ sptk_status sptk_mttkrp_rows(sptk_tensor t, int mode, int64_t R, const void *con
 /* CP-ALS (the paper omits the algorithm and defers to Kolda &
  * Bader): textbook alternating least squares, readings in DESIGN.md §2.
  * For it < max_iters, for n = 0..N-1: V = MTTKRP(n); Gamma = Hadamard of
- * A_m^T A_m (m != n); A_n = V Gamma^{-1} (Cholesky; one ridge retry with
- * 1e-12 tr(Gamma)/R); lambda = column 2-norms; normalise.  fit = 1 - ||X - M||
+ * A_m^T A_m (m != n); A_n = V Gamma^{-1} (Gamma SPD: inverse by unpivoted
+ * Gauss-Jordan, whose pivots are the squared Cholesky diagonal, so a
+ * non-positive pivot = Cholesky failure; one ridge retry with 1e-12 tr(Gamma)/R); lambda = column 2-norms; normalise.  fit = 1 - ||X - M||
  * / ||X|| after each iteration; stop when tol > 0 and |fit - fit_prev| < tol.
  *   init        HOST array of nmodes pointers (device or host) with the
  *               initial factors, or NULL: A_m(r, c) = U[0,1) drawn from the

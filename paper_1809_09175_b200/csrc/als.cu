@@ -4,7 +4,8 @@
 // readings Z11, Z12):
 //   per mode n:  V = MTTKRP(X, A, n)          (mttkrp.cuh, lambda = NULL)
 //                Gamma = Hadamard_{m!=n} G_m  (G_m = A_m^T A_m, cached)
-//                Gamma = L L^T, Gamma^{-1} = L^{-T} L^{-1}  (one block; ridge retry)
+//                Gamma^{-1} by unpivoted Gauss-Jordan (one block; ridge retry;
+//                the Cholesky L^{-T} L^{-1} kernel with SPTK_GAMMA_INV=chol)
 //                A_n = V Gamma^{-1}           (row-parallel product, fused with the
 //                                              column sums of squares for lambda)
 //                lambda_j = ||A_n(:,j)||_2, normalise (zero column -> e_1)
