@@ -472,6 +472,11 @@ __global__ void __launch_bounds__(256)
 // then one pass over V (A_raw, its Gram partials, the column partials) plus an
 // R x R finalisation, instead of apply + normalise + Gram (two passes over A).
 constexpr int kApplyTileDefault = 64;
+// V elements per thread per tile of apply_gram<T, RM> (its register prefetch)
+#ifndef SPTK_APPLY_PF_DIV  // A/B builds only
+#define SPTK_APPLY_PF_DIV 4
+#endif
+__host__ __device__ constexpr int apply_pf(int RM) { return RM / SPTK_APPLY_PF_DIV; }
 constexpr int kTailBlocks = 32;  // apply_gram grids up to this size finalise in their last block
 static int apply_tile_rows() {  // SPTK_APPLY_TILE overrides (tuning)
     static int v = -1;
@@ -603,13 +608,32 @@ __global__ void __launch_bounds__(256)
     double g00 = 0.0, g01 = 0.0, g10 = 0.0, g11 = 0.0, sq = 0.0, dot = 0.0;
     const int64_t b0 = (int64_t)blockIdx.x * rows_per_block;
     const int64_t b1 = min(I, b0 + rows_per_block);
+    // the next tile of V is loaded into registers while this one is computed
+    // (kApplyTile * R <= kApplyPf * 256, clamped by the host): without it each
+    // block waits for its 8 KB tile, and a tall mode's pass is latency-bound
+    constexpr int kApplyPf = apply_pf(RM);
+    T pf[kApplyPf];
+    auto fetch = [&](int64_t rt) {
+        const int n = (int)(min((int64_t)kApplyTile, b1 - rt) * R);
+#pragma unroll
+        for (int k = 0; k < kApplyPf; ++k) {
+            const int x = tid + k * 256;
+            pf[k] = x < n ? V[rt * R + x] : T(0);
+        }
+    };
+    if (b0 < b1) fetch(b0);
     for (int64_t rt = b0; rt < b1; rt += kApplyTile) {
         const int nr = (int)min((int64_t)kApplyTile, b1 - rt);
         __syncthreads();
-        for (int x = tid; x < nr * R; x += blockDim.x) {
-            const int r = x / R, c = x - r * R;
-            Vt[r * RP + c] = (double)V[rt * R + x];
+#pragma unroll
+        for (int k = 0; k < kApplyPf; ++k) {
+            const int x = tid + k * 256;
+            if (x < nr * R) {
+                const int r = x / R, c = x - r * R;
+                Vt[r * RP + c] = (double)pf[k];
+            }
         }
+        if (rt + kApplyTile < b1) fetch(rt + kApplyTile);
         if (RP != R)
             for (int r = tid; r < nr; r += blockDim.x) Vt[r * RP + R] = 0.0, At[r * RP + R] = 0.0;
         __syncthreads();
@@ -718,6 +742,24 @@ __global__ void __launch_bounds__(256)
 }
 
 // A(:, j) *= s_j (the deferred normalisation, once after the last iteration)
+
+// apply_gram grid cap: one full wave of resident blocks (SPTK_APPLY_WAVE=0: the
+// 8-per-SM cap alone, for A/B) -- a tall mode's pass otherwise runs ~2.7 waves
+template <typename T>
+static int apply_block_cap(int cap, int R, size_t smb) {
+    static const bool wave = [] {
+        const char *e = getenv("SPTK_APPLY_WAVE");
+        return !(e && e[0] == '0');
+    }();
+    if (!wave) return cap;
+    int occ = 0;
+    if (R <= 16)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, apply_gram_kernel<T, 16>, 256, smb);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, apply_gram_kernel<T, 32>, 256, smb);
+    return occ > 0 ? std::min(cap, occ * dev_sms()) : cap;
+}
+
 template <typename T>
 __global__ void scale_columns_kernel(T *__restrict__ A, int64_t I, int R,
                                      const double *__restrict__ s) {
@@ -1011,15 +1053,15 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
         double *pdot = psq + c.part_stride;
         double *colsq = w.colsq.as<double>();
         if (deferred) {  // one pass: A_raw, its Gram partials, column partials; R x R finalise
-            const int tile = apply_tile_rows();
-            int nb = (int)std::min<int64_t>(c.nb_apply, (I + tile - 1) / tile);
+            const int tile = std::min(apply_tile_rows(), apply_pf(R <= 16 ? 16 : 32) * 256 / R);
+            const size_t smb = sizeof(double) * (2 * tile * ((R + 1) & ~1) + 4 * 256);
+            int nb = (int)std::min<int64_t>(apply_block_cap<T>(c.nb_apply, R, smb), (I + tile - 1) / tile);
             // modes up to tail_rows() rows: few fat blocks, so the mode tail
             // (reductions, finalise, fit) runs in the last block, no extra launches
             if (I <= tail_rows()) nb = std::min(nb, kTailBlocks);
             if (nb < 1) nb = 1;
             const int64_t rpb = (I + nb - 1) / nb;
             nb = (int)((I + rpb - 1) / rpb);
-            const size_t smb = sizeof(double) * (2 * tile * ((R + 1) & ~1) + 4 * 256);
             // few blocks (small modes): the last block reduces and finalises
             // in place; many blocks: a single block's reduction is latency-
             // bound (measured slower than the parallel reduction kernels)
