@@ -586,14 +586,17 @@ struct ModeTail {
     int N, n, next;
 };
 
+#ifndef SPTK_APPLY_MINB  // A/B builds only
+#define SPTK_APPLY_MINB 1
+#endif
 template <typename T, int RM>  // RM >= R: Gamma^{-1} column length held in registers
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, SPTK_APPLY_MINB)
     apply_gram_kernel(const T *__restrict__ V, int64_t I, int R, int64_t rows_per_block, int kApplyTile,
                       const double *__restrict__ Ginv, T *__restrict__ A,
                       double *__restrict__ part_sq, double *__restrict__ part_dot,
                       double *__restrict__ gpart, const ModeTail tail) {
     extern __shared__ __align__(16) double sm[];
-    const int RP = (R + 1) & ~1;              // padded row stride (16-byte aligned pairs)
+    const int RP = (R + 3) & ~3;              // padded row stride (whole 4-column blocks)
     double *Vt = sm;                          // kApplyTile x RP
     double *At = Vt + kApplyTile * RP;        // kApplyTile x RP
     double *red = At + kApplyTile * RP;       // 4 x 256
@@ -602,10 +605,23 @@ __global__ void __launch_bounds__(256)
     double gi[RM];  // column j of Gamma^{-1}
 #pragma unroll
     for (int i = 0; i < RM; ++i) gi[i] = (i < R && l < lanes) ? Ginv[i * R + j] : 0.0;
-    const int hb = (R + 1) / 2, nblk = hb * hb, groups = 256 / nblk;
+    // Gram partials in 4 x 4 register blocks of the upper triangle (4 shared
+    // loads per 16 FMAs; mirrored on output); the group count is what the
+    // V/A tiles can hold when they are reused to stage the partials
+    const int hb = RP / 4, nblk = hb * (hb + 1) / 2;
+    const int groups = max(1, min(256 / nblk, (2 * kApplyTile * RP) / (nblk * 16)));
     const int bi = tid % nblk, grp = tid / nblk;
-    const int a0 = (bi / hb) * 2, c0 = (bi % hb) * 2;
-    double g00 = 0.0, g01 = 0.0, g10 = 0.0, g11 = 0.0, sq = 0.0, dot = 0.0;
+    auto block_of = [hb](int b, int &a0, int &c0) {
+        int ba = 0;
+        while (b >= hb - ba) b -= hb - ba, ++ba;
+        a0 = 4 * ba, c0 = 4 * (ba + b);
+    };
+    int a0, c0;
+    block_of(bi, a0, c0);
+    double g[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) g[q] = 0.0;
+    double sq = 0.0, dot = 0.0;
     const int64_t b0 = (int64_t)blockIdx.x * rows_per_block;
     const int64_t b1 = min(I, b0 + rows_per_block);
     // the next tile of V is loaded into registers while this one is computed
@@ -635,7 +651,10 @@ __global__ void __launch_bounds__(256)
         }
         if (rt + kApplyTile < b1) fetch(rt + kApplyTile);
         if (RP != R)
-            for (int r = tid; r < nr; r += blockDim.x) Vt[r * RP + R] = 0.0, At[r * RP + R] = 0.0;
+            for (int x = tid; x < nr * (RP - R); x += blockDim.x) {
+                const int r = x / (RP - R), c = R + x - r * (RP - R);
+                Vt[r * RP + c] = 0.0, At[r * RP + c] = 0.0;
+            }
         __syncthreads();
         if (l < lanes) {
             for (int r = l; r < nr; r += lanes) {
@@ -660,12 +679,16 @@ __global__ void __launch_bounds__(256)
         __syncthreads();
         if (grp < groups) {
             for (int r = grp; r < nr; r += groups) {
-                const double2 x = *reinterpret_cast<const double2 *>(At + r * RP + a0);
-                const double2 y = *reinterpret_cast<const double2 *>(At + r * RP + c0);
-                g00 += x.x * y.x;
-                g01 += x.x * y.y;
-                g10 += x.y * y.x;
-                g11 += x.y * y.y;
+                const double2 x01 = *reinterpret_cast<const double2 *>(At + r * RP + a0);
+                const double2 x23 = *reinterpret_cast<const double2 *>(At + r * RP + a0 + 2);
+                const double2 y01 = *reinterpret_cast<const double2 *>(At + r * RP + c0);
+                const double2 y23 = *reinterpret_cast<const double2 *>(At + r * RP + c0 + 2);
+                const double x[4] = {x01.x, x01.y, x23.x, x23.y};
+                const double y[4] = {y01.x, y01.y, y23.x, y23.y};
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) g[p * 4 + q] += x[p] * y[q];
             }
         }
     }
@@ -683,20 +706,23 @@ __global__ void __launch_bounds__(256)
         if (part_dot) part_dot[(int64_t)blockIdx.x * R + tid] = d;
     }
     __syncthreads();
-    // Gram partials: sum the row groups of each 2 x 2 block in group order
-    double *gs = red;  // [groups][nblk][4] fits in 4 x 256
+    // Gram partials: sum the row groups of each 4 x 4 block in group order
+    double *gs = sm;  // [groups][nblk][16] in the V/A tiles (no longer read)
     if (grp < groups) {
-        double *o = gs + ((size_t)grp * nblk + bi) * 4;
-        o[0] = g00; o[1] = g01; o[2] = g10; o[3] = g11;
+        double *o = gs + ((size_t)grp * nblk + bi) * 16;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) o[q] = g[q];
     }
     __syncthreads();
     double *gp = gpart + (int64_t)blockIdx.x * R * R;
-    for (int e = tid; e < nblk * 4; e += blockDim.x) {
-        const int b = e >> 2, q = e & 3;
-        const int a = (b / hb) * 2 + (q >> 1), c = (b % hb) * 2 + (q & 1);
+    for (int e = tid; e < nblk * 16; e += blockDim.x) {
+        const int b = e >> 4, q = e & 15;
+        int ba0, bc0;
+        block_of(b, ba0, bc0);
+        const int a = ba0 + (q >> 2), c = bc0 + (q & 3);
         double acc = 0.0;
-        for (int g = 0; g < groups; ++g) acc += gs[((size_t)g * nblk + b) * 4 + q];
-        if (a < R && c < R) gp[a * R + c] = acc;
+        for (int gg = 0; gg < groups; ++gg) acc += gs[((size_t)gg * nblk + b) * 16 + q];
+        if (a < R && c < R) gp[a * R + c] = gp[c * R + a] = acc;
     }
     if (!tail.counter) return;
     // the last block to finish reduces every block's partials (block order,
@@ -741,8 +767,6 @@ __global__ void __launch_bounds__(256)
     if (tid == 0) *tail.counter = 0;  // ready for the next launch (graph replays)
 }
 
-// A(:, j) *= s_j (the deferred normalisation, once after the last iteration)
-
 // apply_gram grid cap: one full wave of resident blocks (SPTK_APPLY_WAVE=0: the
 // 8-per-SM cap alone, for A/B) -- a tall mode's pass otherwise runs ~2.7 waves
 template <typename T>
@@ -760,6 +784,7 @@ static int apply_block_cap(int cap, int R, size_t smb) {
     return occ > 0 ? std::min(cap, occ * dev_sms()) : cap;
 }
 
+// A(:, j) *= s_j (the deferred normalisation, once after the last iteration)
 template <typename T>
 __global__ void scale_columns_kernel(T *__restrict__ A, int64_t I, int R,
                                      const double *__restrict__ s) {
@@ -1054,7 +1079,7 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
         double *colsq = w.colsq.as<double>();
         if (deferred) {  // one pass: A_raw, its Gram partials, column partials; R x R finalise
             const int tile = std::min(apply_tile_rows(), apply_pf(R <= 16 ? 16 : 32) * 256 / R);
-            const size_t smb = sizeof(double) * (2 * tile * ((R + 1) & ~1) + 4 * 256);
+            const size_t smb = sizeof(double) * (2 * tile * ((R + 3) & ~3) + 4 * 256);
             int nb = (int)std::min<int64_t>(apply_block_cap<T>(c.nb_apply, R, smb), (I + tile - 1) / tile);
             // modes up to tail_rows() rows: few fat blocks, so the mode tail
             // (reductions, finalise, fit) runs in the last block, no extra launches
