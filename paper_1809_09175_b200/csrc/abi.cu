@@ -436,6 +436,12 @@ sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     const int m0 = mode < 0 ? 0 : mode, m1 = mode < 0 ? t->N : mode + 1;
     double tc = setup_clock(s);
+    // what this call may allocate: the sort workspace, copies, (released) keys
+    const void *ws0 = t->sortws.p;
+    const size_t ws_bytes0 = t->sortws.bytes;
+    const bool keys0 = t->keys.p != nullptr;
+    int copies0 = 0;
+    for (int m = 0; m < t->N; ++m) copies0 += t->has_srec[m] ? 1 : 0;
     for (int m = m0; m < m1; ++m) {  // all sorts first: their temporaries are the peak
         sptk_status st = build_perm_mode(t, m, s);
         if (st == SPTK_ECUDA) t->poisoned = true;
@@ -464,8 +470,16 @@ sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream) {
     }
     if (all) t->keys.release();
     setup_note("release keys", -1, tc, s);
-    // keep the sort workspace for the next build_perm only while memory is plentiful
+    // keep the sort workspace for the next build_perm only while memory is
+    // plentiful.  A steady-state re-sort allocates nothing, so the last
+    // decision stands and cudaMemGetInfo (which can stall the host for tens of
+    // ms while the sort is in flight: profiles/r01/perm_timing_async.log) is skipped.
+    int copies1 = 0;
+    for (int m = 0; m < t->N; ++m) copies1 += t->has_srec[m] ? 1 : 0;
+    const bool allocated = t->sortws.p != ws0 || t->sortws.bytes != ws_bytes0 ||
+                           copies1 != copies0 || keys0 != (t->keys.p != nullptr);
     size_t free_b = 0, total_b = 0;
+    if (!t->sortws.p || !allocated) return SPTK_OK;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
         if (free_b < total_b / 4) t->sortws.release();
     } else {

@@ -1,4 +1,4 @@
-"""Host-timed build_perm per mode (repeated) on a device-generated config.
+"""Host-timed build_perm per mode (repeated; argv[2] repetitions, default 3) on a device-generated config.
 The tensor is created twice: the first pass includes one-time costs (lazy
 module loading, first allocations); the second shows build_perm right after
 ingest (sort keys emitted by the pack kernel) and then repeated calls (keys
@@ -25,7 +25,7 @@ for tensor_pass in range(2):
           f"(device bytes {sp.sptensor_device_bytes(t) / 1e9:.2f} GB)", flush=True)
     del idx, val
     torch.cuda.empty_cache()
-    for rep in range(3):
+    for rep in range(int(sys.argv[2]) if len(sys.argv) > 2 else 3):
         for n in range(c.N):
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
