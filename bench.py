@@ -65,22 +65,39 @@ def peaks():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
+def _profile_json(name: str):
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", name)))
+    except Exception:
+        return {}
+
+
 def limiter_for(workload_key: str):
     """What ncu showed bounds the MTTKRP launch (committed capture), if any."""
-    try:
-        j = json.load(open(os.path.join(ROOT, "profiles", "ncu_limiter.json")))
-        return j.get(workload_key)
-    except Exception:
-        return None
+    return _profile_json("ncu_limiter.json").get(workload_key)
 
 
 def traffic_for(workload_key: str):
-    """ncu DRAM bytes per MTTKRP launch from the committed capture, if any."""
-    try:
-        j = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        return j.get(workload_key)
-    except Exception:
-        return None
+    """ncu DRAM bytes per MTTKRP launch from the committed capture, if any
+    (keyed <config>_R<R>_<dtype>[_perm_gather]: the layout changes the bytes)."""
+    return _profile_json("ncu_traffic.json").get(workload_key)
+
+
+def gather_ceilings(row_bytes: int):
+    """Measured random-row gather ceilings (tools/ceilings.cu ->
+    profiles/ceilings.json) for rows of `row_bytes`: L1-resident table (the
+    L1 data-pipe rate: no gather can beat it), L2-resident (L2 -> SM) and
+    HBM-resident tables."""
+    j = _profile_json("ceilings.json")
+    rb = min((64, 128, 256, 512), key=lambda b: abs(b - row_bytes))
+
+    def v(k):
+        e = j.get(k)
+        return e["value"] if isinstance(e, dict) else None
+    return {"row_bytes": rb, "l1_resident": v(f"gather_l1_l1_{rb}"),
+            "l2_resident": v(f"gather_l2_nol1_{rb}"), "l2_resident_l1alloc": v(f"gather_l2_l1_{rb}"),
+            "hbm_resident": v(f"gather_hbm_nol1_{rb}"), "hbm_read": v("hbm_read"),
+            "source": "profiles/ceilings.json (tools/ceilings.cu)" if j else None}
 
 
 # ------------------------------------------------------------------ clocks
@@ -323,15 +340,22 @@ def main():
     dev_bytes = sp.sptensor_device_bytes(t)
 
     # per-rank share of the work (row-range sharding) for the byte model
-    bounds, pos = [], []
+    bounds, pos, rowptrs = [], [], []
     for n, I in enumerate(c.dims):
         rp = torch.empty(I + 1, dtype=torch.int32, device="cuda")
         sp.get_rowptr(t, n, rp)
         rph = rp.cpu().numpy().view(np.uint32)
+        rowptrs.append(rph)
         bd = sp.partition_rows(rph, world)
         bounds.append(bd)
         pos.append((int(rph[bd[rank]]), int(rph[bd[rank + 1]])))
     bm_total = sum(metrics.b_model(c.N, c.nnz, R, I, s_v) for I in c.dims)
+    # B_comp: compulsory HBM bytes -- the nonzeros' indices and
+    # values, the perm, each distinct factor row touched once, the output
+    nonempty = [int(np.count_nonzero(np.diff(rp_n.astype(np.int64)))) for rp_n in rowptrs]
+    bc_modes = [metrics.b_comp(c.N, c.nnz, R, c.dims[n],
+                               sum(nonempty[m] for m in range(c.N) if m != n), s_v)
+                for n in range(c.N)]
     bm_rank = sum(metrics.b_model(c.N, pos[n][1] - pos[n][0], R,
                                   int(bounds[n][rank + 1] - bounds[n][rank]), s_v)
                   for n in range(c.N))
@@ -383,12 +407,30 @@ def main():
     value = bm_total / (ms_max * 1e-3) / 1e9
     ms_eager = pa.elapsed_time(pb) / args.steps
 
-    # dominant kernel (MTTKRP) roofline on this rank
+    # dominant kernel (MTTKRP) roofline on this rank.  achieved = ALGORITHMIC
+    # bytes per launch (B_comp: compulsory HBM bytes) / mean launch
+    # time; the per-gather north-star model B_model is reported beside it as
+    # frac_model (it counts L2/L1-served factor rows as memory traffic)
     mttkrp_ms_launch = prof["mttkrp_ms"] / max(1, prof["mttkrp_launches"])
-    achieved = (bm_rank / c.N) / (mttkrp_ms_launch * 1e-3) / 1e9
+    t_launch = mttkrp_ms_launch * 1e-3
+    bc_launch = sum(bc_modes) / c.N / world   # rank share (row-range shards)
+    bm_launch = bm_rank / c.N
+    achieved = bc_launch / t_launch / 1e9
     peak, peak_src = peaks()
-    key = f"{args.config}_R{R}_{args.dtype}"
+    key = f"{args.config}_R{R}_{args.dtype}" + ("_perm_gather" if args.layout == "perm_gather" else "")
     traffic = traffic_for(key)
+    ncu = limiter_for(key)
+    gathered = c.nnz * (c.N - 1) * R * s_v / world   # per launch, counted per gather
+    ceil = gather_ceilings(R * s_v)
+    gather_rate = gathered / t_launch / 1e9
+    binding = None
+    if ncu and ncu.get("l1tex_data_pipe_lsu_wavefronts_pct") is not None:
+        binding = {"unit": "L1 data pipe (LSU wavefronts: every gathered factor row, hit or miss)",
+                   "frac": ncu["l1tex_data_pipe_lsu_wavefronts_pct"] / 100.0,
+                   "lts_frac": (ncu.get("lts_throughput_pct") or 0) / 100.0 or None,
+                   "source": ncu.get("source")}
+    elif ncu:
+        binding = {"unit": ncu.get("limiter"), "frac": None, "source": ncu.get("source")}
 
     # ---- end to end through the public API with host buffers
     e2e = None
@@ -458,18 +500,28 @@ def main():
                       "tensor_device_bytes": dev_bytes},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "MTTKRP launch (permuted copy; slice, warp-cooperative or per-group kernel chosen per mode)",
-                         "bytes_model": "B_model per launch = P(N*4+s_v) + P(N-1)R*s_v + I_n*R*s_v "
-                                        "(per-gather, SURVEY 8(d)); can exceed HBM peak when "
-                                        "gathers hit L2 (P:716)",
+                         "kernel": ncu.get("kernel") if ncu else
+                                   "MTTKRP launch (permuted copy; slice, warp-cooperative or per-group kernel chosen per mode)",
+                         "bytes_algorithmic": "B_comp per launch = P(N*4+s_v) + 4P + sum_{m!=n} U_m*R*s_v "
+                                              "+ I_n*R*s_v (SURVEY 8(d), U_m = nonempty rows), mean over modes",
+                         "bytes_algorithmic_per_launch": bc_launch,
                          "peak_source": peak_src,
-                         "frac_of_8TBps": achieved / 8000.0,
                          # the same launch measured by the DRAM bytes ncu saw it move
-                         "dram_traffic_frac": (traffic / (mttkrp_ms_launch * 1e-3) / 1e9 / peak
-                                               if traffic else None),
+                         "frac_dram": (traffic / t_launch / 1e9 / peak) if traffic else None,
+                         # the north star's per-gather byte model: > 1 when the
+                         # gathered rows are served from L2/L1
+                         "frac_model": bm_launch / t_launch / 1e9 / peak,
+                         "bytes_model_per_launch": bm_launch,
+                         # what actually bounds the launch (ncu) and the gather rate
+                         # against the measured random-row gather ceilings
+                         "binding": binding,
+                         "gather": {"achieved": gather_rate, "unit": "GB/s",
+                                    "bytes_per_launch": gathered,
+                                    "ceilings": ceil,
+                                    "frac_of_l1_resident": (gather_rate / ceil["l1_resident"]
+                                                            if ceil.get("l1_resident") else None)},
                          "timing": "per-launch CUDA events in a second K-iteration pass "
-                                   "(eager launches), mean over all MTTKRP launches",
-                         "ncu": limiter_for(f"{args.config}_R{R}_{args.dtype}")},
+                                   "(eager launches), mean over all MTTKRP launches"},
             "clocks": clk.summary(),
             "gpu_launches": launches,
             "e2e": e2e,

@@ -275,6 +275,31 @@ sptk_status sptk_profile_read(double *mttkrp_ms, int64_t *mttkrp_launches,
  * from SPTK_VARIANT / SPTK_RUN. */
 sptk_status sptk_set_tuning(int variant, int64_t run);
 
+/* Process-wide options (traversal selection and tuning).
+ * Each starts from its default, or from the environment variable SPTK_<NAME>
+ * (upper case, integer) if set.  Names and defaults:
+ *   run 0 (positions per worker, 0 = adaptive), variant -1 (auto; 0 per-group,
+ *   1 warp-cooperative), slice 1 (0 disables the slice traversal, 2 forces
+ *   it wherever the permuted copy has a secondary mode),
+ *   slice_l2_mb 32 (L2 window of the slice traversal when the secondary
+ *   factor exceeds it), slice_rows 0 (auto), slice_other_first -1 (auto),
+ *   rowrec 1, force_v 0 (cap of the lane vector width in elements),
+ *   generic 0 (1 forces the generic scalar kernel), debug_dispatch 0,
+ *   copy_order 1 (0: permuted copies in perm_n order), deferred_norm 1,
+ *   no_graph 0, gamma_inv_chol 0, use_copy 1 (0: gather the records through
+ *   perm_n, the paper's traversal, even where a permuted copy exists).
+ * Every choice gives the same result up to summation order; options change
+ * which kernel computes it.  Not synchronised with calls in flight on other
+ * threads.  SPTK_EINVAL for an unknown name. */
+sptk_status sptk_set_option(const char *name, int64_t value);
+sptk_status sptk_get_option(const char *name, int64_t *value);
+/* back to the defaults / environment values */
+sptk_status sptk_reset_options(void);
+/* The traversal the last MTTKRP call on this thread ran, e.g. "slice V4",
+ * "coop V4", "fast_rowrec V4", "perm_gather V4", "generic V1",
+ * "slice_l2window V4", "fast+det V4", "atomic" ("" before the first call). */
+const char *sptk_last_dispatch(void);
+
 #ifdef __cplusplus
 }
 #endif

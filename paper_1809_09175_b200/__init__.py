@@ -60,6 +60,10 @@ _SIGS = [
     ("sptk_profile_reset", [], _I),
     ("sptk_profile_read", [_P, _P, _P], _I),
     ("sptk_set_tuning", [_I, _I64], _I),
+    ("sptk_set_option", [C.c_char_p, _I64], _I),
+    ("sptk_get_option", [C.c_char_p, _P], _I),
+    ("sptk_reset_options", [], _I),
+    ("sptk_last_dispatch", [], C.c_char_p),
 ]
 EXPORTS = [s[0] for s in _SIGS]
 
@@ -138,11 +142,12 @@ def _stream(stream):
 class SpTensor:
     """Owning wrapper of an sptk_tensor handle."""
 
-    def __init__(self, handle: int, dims, nnz: int, dtype: int):
+    def __init__(self, handle: int, dims, nnz: int, dtype: int, device: int = 0):
         self.handle = C.c_void_p(handle)
         self.dims = tuple(int(d) for d in dims)
         self.nnz = int(nnz)
         self.dtype = dtype
+        self.device = device   # CUDA device the handle's memory lives on
 
     @property
     def N(self) -> int:
@@ -158,6 +163,73 @@ class SpTensor:
             self.close()
         except Exception:
             pass
+
+
+def _current_device() -> int:
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_device()
+    except Exception:  # pragma: no cover
+        pass
+    return 0
+
+
+def _is_cuda(x) -> bool:
+    return bool(getattr(x, "is_cuda", False))
+
+
+def _check_buf(t: "SpTensor", x, shape, what: str, device_only: bool):
+    """Validate one factor / output / lambda buffer before its raw address
+    crosses the C ABI (which cannot see shapes or dtypes): exact shape, the
+    tensor's dtype, C-contiguous, and -- for device buffers -- the tensor's
+    device.  device_only: host buffers are refused (mttkrp takes device
+    pointers only)."""
+    if x is None:
+        raise ValueError(f"{what} is None")
+    got = tuple(int(d) for d in getattr(x, "shape", ()))
+    if got != tuple(shape):
+        raise ValueError(f"{what}: shape {got}, expected {tuple(shape)}")
+    try:
+        code = _dtype_code(x)
+    except TypeError as e:
+        raise ValueError(f"{what}: {e}") from None
+    if code != t.dtype:
+        raise ValueError(f"{what}: dtype {getattr(x, 'dtype', '?')} does not match the tensor's "
+                         f"{'float64' if t.dtype == F64 else 'float32'}")
+    contig = x.flags["C_CONTIGUOUS"] if isinstance(x, np.ndarray) else x.is_contiguous()
+    if not contig:
+        raise ValueError(f"{what}: must be C-contiguous")
+    if _is_cuda(x):
+        if x.device.index != t.device:
+            raise ValueError(f"{what}: on cuda:{x.device.index}, the tensor lives on cuda:{t.device}")
+    elif device_only:
+        raise ValueError(f"{what}: must be a CUDA tensor (device pointer)")
+
+
+def _check_factors(t: "SpTensor", factors, R: int, what: str, skip_mode=None,
+                   device_only: bool = True):
+    if len(factors) != t.N:
+        raise ValueError(f"{what}: {len(factors)} matrices for a {t.N}-way tensor")
+    for m, a in enumerate(factors):
+        if m == skip_mode and a is None:
+            continue
+        _check_buf(t, a, (t.dims[m], R), f"{what}[{m}]", device_only)
+
+
+def _check_mttkrp_args(t: "SpTensor", mode: int, factors, out, lam):
+    if not 0 <= mode < t.N:
+        raise ValueError(f"mode {mode} outside [0, {t.N})")
+    if len(factors) != t.N:
+        raise ValueError(f"factors: {len(factors)} matrices for a {t.N}-way tensor")
+    R = int(out.shape[1]) if getattr(out, "shape", None) is not None and len(out.shape) == 2 else -1
+    if R < 1:
+        raise ValueError("out must be a 2-D (I_mode, R) buffer")
+    _check_buf(t, out, (t.dims[mode], R), "out", True)
+    _check_factors(t, factors, R, "factors", skip_mode=mode)
+    if lam is not None:
+        _check_buf(t, lam, (R,), "lam", True)
+    return R
 
 
 # ------------------------------------------------------------------ API
@@ -179,7 +251,7 @@ def sptensor_create(dims, idx, vals, stream=None, perm_gather: bool = False,
                                       (CREATE_PERM_GATHER if perm_gather else 0)
                                       | (CREATE_DETERMINISTIC if deterministic else 0) | dup,
                                       _stream(stream), C.byref(out)), "sptensor_create")
-    tt = SpTensor(out.value, dims_a, nnz, dt)
+    tt = SpTensor(out.value, dims_a, nnz, dt, _current_device())
     if dup:
         tt.nnz = sptensor_info(tt)["nnz"]
     return tt
@@ -228,7 +300,7 @@ def _ptr_table(arrs):
 
 def mttkrp(t: SpTensor, mode: int, factors, out, lam=None, comm=None, stream=None):
     """out <- MTTKRP(X, factors, mode) (Eq. (2)); factors[mode] may be None."""
-    R = int(out.shape[1])
+    R = _check_mttkrp_args(t, mode, factors, out, lam)
     table = _ptr_table(factors)
     _check(lib().sptk_mttkrp(t.handle, mode, R, table, _ptr(lam), _ptr(out),
                              comm.handle if comm is not None else None, _stream(stream)),
@@ -238,7 +310,7 @@ def mttkrp(t: SpTensor, mode: int, factors, out, lam=None, comm=None, stream=Non
 
 def mttkrp_atomic(t: SpTensor, mode: int, factors, out, lam=None, stream=None):
     """The paper's atomic-per-nonzero MTTKRP (VerA/VerB): storage order, no perm."""
-    R = int(out.shape[1])
+    R = _check_mttkrp_args(t, mode, factors, out, lam)
     _check(lib().sptk_mttkrp_atomic(t.handle, mode, R, _ptr_table(factors), _ptr(lam), _ptr(out),
                                     _stream(stream)), "mttkrp_atomic")
     return out
@@ -247,7 +319,7 @@ def mttkrp_atomic(t: SpTensor, mode: int, factors, out, lam=None, stream=None):
 def mttkrp_rows(t: SpTensor, mode: int, factors, out, row_begin: int, row_end: int, lam=None,
                 stream=None):
     """out[row_begin:row_end] <- those rows of MTTKRP(X, factors, mode)."""
-    R = int(out.shape[1])
+    R = _check_mttkrp_args(t, mode, factors, out, lam)
     _check(lib().sptk_mttkrp_rows(t.handle, mode, R, _ptr_table(factors), _ptr(lam), _ptr(out),
                                   row_begin, row_end, _stream(stream)), "mttkrp_rows")
     return out
@@ -256,7 +328,15 @@ def mttkrp_rows(t: SpTensor, mode: int, factors, out, row_begin: int, row_end: i
 def cp_als(t: SpTensor, R: int, max_iters: int, factors_out, tol: float = 0.0, seed: int = 0,
            init=None, lambda_out=None, comm=None, stream=None, trace: bool = True):
     """Runs CP-ALS; factors_out (and init) are lists of per-mode buffers.
-    Returns dict(fit, iters, trace)."""
+    Returns dict(fit, iters, trace).  Buffers may be device (the tensor's
+    device) or host; each must be (I_m, R) of the tensor's dtype."""
+    if int(R) < 1:
+        raise ValueError("R must be >= 1")
+    _check_factors(t, factors_out, R, "factors_out", device_only=False)
+    if init is not None:
+        _check_factors(t, init, R, "init", device_only=False)
+    if lambda_out is not None:
+        _check_buf(t, lambda_out, (R,), "lambda_out", False)
     fit = C.c_double(0.0)
     iters = C.c_int(0)
     tr = np.zeros(max(max_iters, 1), dtype=np.float64)
@@ -320,6 +400,46 @@ def partition_rows(rowptr, nranks: int) -> np.ndarray:
 def set_tuning(variant: int = -1, run: int = 0):
     """variant: 0 per-group, 1 warp-cooperative, -1 keep, -2 automatic; run: 0 keep, -2 adaptive."""
     _check(lib().sptk_set_tuning(variant, run), "set_tuning")
+
+
+def set_option(name: str, value: int):
+    """Process-wide launch option (names and meaning in include/sptk.h)."""
+    _check(lib().sptk_set_option(name.encode(), int(value)), "set_option")
+
+
+def get_option(name: str) -> int:
+    v = C.c_int64(0)
+    _check(lib().sptk_get_option(name.encode(), C.byref(v)), "get_option")
+    return v.value
+
+
+def reset_options():
+    _check(lib().sptk_reset_options(), "reset_options")
+
+
+def last_dispatch() -> str:
+    """Traversal of the last MTTKRP call on this thread (e.g. "slice V4")."""
+    return lib().sptk_last_dispatch().decode()
+
+
+class options:
+    """Context manager: ``with sp.options(slice=0, variant=1): ...`` sets the
+    options and restores their previous values on exit."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.prev = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.prev[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.prev.items():
+            set_option(k, v)
+        return False
 
 
 def profile_enable(on: bool = True):

@@ -6,6 +6,7 @@
 #include <time.h>
 
 #include <algorithm>
+#include <atomic>
 #include <vector>
 #include <mutex>
 #include <thread>
@@ -49,16 +50,22 @@ sptk_status mttkrp_span_end(cudaStream_t s, cudaEvent_t b) {
     return SPTK_OK;
 }
 
+// SM count per device (a process may drive several GPUs): filled once per
+// device under a mutex
 int dev_sms() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-            sms <= 0)
-            sms = kNumSMs;
+    constexpr int kMaxDev = 64;
+    static std::atomic<int> sms[kMaxDev];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDev) return kNumSMs;
+    int v = sms[dev].load(std::memory_order_relaxed);
+    if (v > 0) return v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+        cudaGetLastError();
+        v = kNumSMs;
     }
-    return sms;
+    sms[dev].store(v, std::memory_order_relaxed);
+    return v;
 }
 
 sptk_status DevBuf::reserve(size_t n) {

@@ -23,6 +23,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -268,11 +269,7 @@ __global__ void __launch_bounds__(256)
 // Gamma^{-1} for mode n (SPTK_GAMMA_INV=chol forces the Cholesky kernel)
 static void launch_ginv(const double *G, int N, int n, int R, double *Ginv, int *status,
                         cudaStream_t s) {
-    static const bool chol = [] {
-        const char *e = getenv("SPTK_GAMMA_INV");
-        return e && e[0] == 'c';
-    }();
-    if (chol)
+    if (opt(OPT_GAMMA_INV_CHOL))
         chol_inv_kernel<<<1, 256, sizeof(double) * (R * R + R), s>>>(G, N, n, R, Ginv, status);
     else
         gj_inv_kernel<<<1, 256, sizeof(double) * (R * R + R), s>>>(G, N, n, R, Ginv, status);
@@ -507,8 +504,7 @@ static int64_t tail_rows() {  // SPTK_TAIL_ROWS (tuning); 0 = grid by tile only
 }
 
 static bool deferred_norm(int64_t R) {  // read per call: tests switch it per case
-    const char *e = getenv("SPTK_DEFERRED_NORM");
-    return !(e && *e == '0') && R <= 32;
+    return opt(OPT_DEFERRED_NORM) != 0 && R <= 32;
 }
 
 // Rows [b0, b1) of the block: V tile -> shared memory (coalesced), A_raw tile =
@@ -1371,8 +1367,7 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     // launches read), capture one iteration -- both streams, ~4N+2 kernels and
     // the fit copy -- into a CUDA graph and replay it.  Not while profiling
     // (kernel-span events cannot be timed inside graphs) or for < 4 iterations.
-    const char *ng = getenv("SPTK_NO_GRAPH");
-    bool use_graph = !multi && !profile().on && max_iters >= 4 && !(ng && *ng && *ng != '0');
+    bool use_graph = !multi && !profile().on && max_iters >= 4 && !opt(OPT_NO_GRAPH);
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int64_t launches_per_iter = 0;
@@ -1510,8 +1505,16 @@ extern "C" sptk_status sptk_cp_als(sptk_tensor t, int64_t R, int max_iters, doub
     if (!(t->normX2 > 0.0)) return fail(SPTK_EZERONORM, "||X|| = 0");
     cudaStream_t s = (cudaStream_t)stream;
     // Gamma^{-1} staging can exceed the 48 KB default shared memory for R > 64
-    static bool attr = false;
-    if (!attr) {
+    // the attribute is per device (context): set it once for each device used,
+    // under a mutex (several host threads may drive several GPUs)
+    static std::mutex attr_mu;
+    static bool attr_done[64] = {false};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64)
+        return fail(SPTK_ECUDA, "cudaGetDevice failed");
+    {
+    std::lock_guard<std::mutex> attr_lk(attr_mu);
+    if (!attr_done[dev]) {
         cudaFuncSetAttribute(apply_inv_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(apply_inv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1524,7 +1527,8 @@ extern "C" sptk_status sptk_cp_als(sptk_tensor t, int64_t R, int max_iters, doub
         cudaFuncSetAttribute(finish_kernel<double, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(finish_kernel<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(finish_kernel<float, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
+        attr_done[dev] = true;
+    }
     }
     sptk_status st =
         t->dtype == SPTK_F64

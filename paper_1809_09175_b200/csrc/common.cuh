@@ -45,6 +45,17 @@ sptk_status mttkrp_span_end(cudaStream_t s, cudaEvent_t b);
 
 int dev_sms();
 
+// ------------------------------------------------------------------ options
+// Process-wide launch options (options.cu): default, else SPTK_<NAME> from the
+// environment, else sptk_set_option.  Order = kOpts in options.cu.
+enum Opt {
+    OPT_RUN, OPT_VARIANT, OPT_SLICE, OPT_SLICE_L2_MB, OPT_SLICE_ROWS, OPT_SLICE_OTHER_FIRST,
+    OPT_ROWREC, OPT_FORCE_V, OPT_GENERIC, OPT_DEBUG_DISPATCH, OPT_COPY_ORDER, OPT_DEFERRED_NORM,
+    OPT_NO_GRAPH, OPT_GAMMA_INV_CHOL, OPT_USE_COPY, OPT_COUNT
+};
+int64_t opt(Opt o);
+void set_dispatch(const std::string &s);  // what the last MTTKRP call ran (sptk_last_dispatch)
+
 // ------------------------------------------------------------------ memory
 // RAII device buffer (cudaMallocAsync-free, plain cudaMalloc for large,
 // long-lived buffers; workspaces are kept in the handle).
@@ -107,6 +118,7 @@ struct sptk_tensor_s {
     bool has_perm[sptk::kMaxModes] = {false};
     sptk::DevBuf srec[sptk::kMaxModes];         // compact records in perm_n order (optional)
     bool has_srec[sptk::kMaxModes] = {false};
+    bool copy_declined[sptk::kMaxModes] = {false};  // no memory for the copy: do not retry
     sptk::DevBuf wrow[sptk::kMaxModes];         // worker start rows for the copy (cached)
     int copy_sec[sptk::kMaxModes] = {-1, -1, -1, -1, -1, -1};  // copy's secondary mode
     int64_t copy_p0[sptk::kMaxModes] = {0}, copy_p1[sptk::kMaxModes] = {0};  // copy covers

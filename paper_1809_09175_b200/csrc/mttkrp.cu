@@ -9,19 +9,13 @@
 
 namespace sptk {
 
-static int64_t g_run = -1;  // -1: unset, 0: adaptive, > 0: fixed
-static int g_variant = -2;
-
-// Nonzeros per worker (the paper's NZPTM block).  Adaptive by default:
-// long runs amortise the two boundary atomics, but the grid must still cover
-// every SM several times, so small tensors get short runs (>= 16).
+// Nonzeros per worker (the paper's NZPTM block).  Adaptive by default
+// (option "run" = 0): long runs amortise the two boundary atomics, but the
+// grid must still cover every SM several times, so small tensors get short
+// runs (>= 16).
 static int64_t run_length(int64_t npos, int G) {
-    if (g_run < 0) {
-        const char *e = getenv("SPTK_RUN");
-        g_run = e ? atoll(e) : 0;
-        if (g_run < 0) g_run = 0;
-    }
-    if (g_run > 0) return g_run;
+    const int64_t fixed = opt(OPT_RUN);
+    if (fixed > 0) return fixed < 4 ? 4 : (fixed + 3) / 4 * 4;
     const int64_t workers_per_sm = 768 / G;  // ~3 resident 256-thread blocks
     const int64_t target = (int64_t)dev_sms() * workers_per_sm * 4;
     int64_t run = npos / (target > 0 ? target : 1);
@@ -30,14 +24,10 @@ static int64_t run_length(int64_t npos, int G) {
     return (run + 3) / 4 * 4;
 }
 
-// -2: not read yet; -1: automatic (warp-cooperative for long rows); 0/1: forced
+// -1: automatic (warp-cooperative for long rows); 0/1: forced
 static int variant_setting() {
-    if (g_variant == -2) {
-        const char *e = getenv("SPTK_VARIANT");
-        g_variant = e ? atoi(e) : -1;
-        if (g_variant < -1 || g_variant >= kNumVariants) g_variant = -1;
-    }
-    return g_variant;
+    const int64_t v = opt(OPT_VARIANT);
+    return (v < -1 || v >= kNumVariants) ? -1 : (int)v;
 }
 
 template <typename T, int V>
@@ -214,61 +204,22 @@ constexpr int64_t kSliceBytesF64 = 512 << 10;  // fp64: 512 KB of A_a rows (R=16
 // fastest), so the whole GPU sweeps one window at a time and the A_a gathers
 // hit L2 instead of HBM.
 constexpr int64_t kSliceL2Bytes = 32 << 20;
-static int64_t slice_l2_bytes() {  // SPTK_SLICE_L2_MB overrides the L2 window (tuning)
-    static int64_t v = -1;
-    if (v < 0) {
-        const char *e = getenv("SPTK_SLICE_L2_MB");
-        v = (e && atoi(e) > 0) ? (int64_t)atoi(e) << 20 : kSliceL2Bytes;
-    }
-    return v;
-}
-
-static bool rowrec_setting() {  // SPTK_ROWREC=0: per-group kernel tracks rows via rowptr (A/B)
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("SPTK_ROWREC");
-        v = (e && *e == '0') ? 0 : 1;
-    }
-    return v == 1;
-}
-
-static bool debug_dispatch() {  // SPTK_DEBUG_DISPATCH=1: one stderr line per MTTKRP launch
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("SPTK_DEBUG_DISPATCH");
-        v = (e && *e && *e != '0') ? 1 : 0;
-    }
-    return v == 1;
-}
-
-static int slice_setting() {  // SPTK_SLICE=0 disables the slice traversal
-    static int v = -2;
-    if (v == -2) {
-        const char *e = getenv("SPTK_SLICE");
-        v = (e && *e == '0') ? 0 : 1;
-    }
-    return v;
+static int64_t slice_l2_bytes() {  // option slice_l2_mb (tests force the window regime)
+    const int64_t mb = opt(OPT_SLICE_L2_MB);
+    return mb > 0 ? mb << 20 : kSliceL2Bytes;
 }
 
 // L2 policy of the other factors' gathers in the slice kernel: in the L2-window
 // regime (A_a > L2 budget) they are evicted first so the window stays
 // resident (Amazon -4 %); otherwise evict_last like every factor row (LBNL:
-// evict_first loses 4 %).  SPTK_SLICE_OTHER_FIRST=0/1 overrides (tuning).
+// evict_first loses 4 %).  Option slice_other_first = 0/1 overrides.
 static int slice_other_first(bool l2_window) {
-    static int v = -2;
-    if (v == -2) {
-        const char *e = getenv("SPTK_SLICE_OTHER_FIRST");
-        v = e ? (*e == '1' ? 1 : 0) : -1;
-    }
-    return v >= 0 ? v : (l2_window ? 1 : 0);
+    const int64_t v = opt(OPT_SLICE_OTHER_FIRST);
+    return v >= 0 ? (v ? 1 : 0) : (l2_window ? 1 : 0);
 }
 
-static int64_t slice_rows(size_t es, int64_t row_bytes) {  // SPTK_SLICE_ROWS overrides (tuning)
-    static int64_t r = -1;
-    if (r < 0) {
-        const char *e = getenv("SPTK_SLICE_ROWS");
-        r = (e && atoi(e) > 0) ? (int64_t)atoi(e) : 0;
-    }
+static int64_t slice_rows(size_t es, int64_t row_bytes) {  // option slice_rows overrides
+    const int64_t r = opt(OPT_SLICE_ROWS);
     if (r > 0) return r;
     if (es == 8) return std::min<int64_t>(8192, std::max<int64_t>(512, kSliceBytesF64 / row_bytes));
     return kSliceRows;
@@ -282,7 +233,7 @@ static int64_t slice_rows(size_t es, int64_t row_bytes) {  // SPTK_SLICE_ROWS ov
 static int slice_count(sptk_tensor t, int mode, int64_t r0, int64_t r1, int64_t nnz,
                        int64_t row_bytes, cudaStream_t s, int64_t *S) {
     const int a = t->copy_sec[mode];
-    if (a < 0 || t->deterministic || !slice_setting() || r1 <= r0) return 0;
+    if (a < 0 || t->deterministic || !opt(OPT_SLICE) || r1 <= r0) return 0;
     const int64_t rows = r1 - r0;
     int64_t sa = slice_rows(dtype_bytes(t->dtype), row_bytes);
     if (t->dims[a] * row_bytes > slice_l2_bytes()) {
@@ -296,6 +247,10 @@ static int slice_count(sptk_tensor t, int mode, int64_t r0, int64_t r1, int64_t 
     }
     const int64_t K = (t->dims[a] + sa - 1) / sa;
     if (K < 2 || K > 65535) return 0;
+    if (opt(OPT_SLICE) == 2) {  // forced (tests): structural conditions only
+        *S = sa;
+        return (int)K;
+    }
     if (nnz < 32 * K * rows) return 0;
     if (((rows + 7) / 8) * K < 2 * (int64_t)dev_sms()) return 0;
     if (t->row_max[mode] < 0) {
@@ -356,7 +311,8 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     SPTK_TRY(ensure_sorted_copy(t, mode, s));
     // the copy serves this call if it covers the call's positions (a shard's
     // copy covers only its own row range)
-    const bool copy = t->has_srec[mode] && pb >= t->copy_p0[mode] && pe <= t->copy_p1[mode];
+    const bool copy = t->has_srec[mode] && pb >= t->copy_p0[mode] && pe <= t->copy_p1[mode] &&
+                      opt(OPT_USE_COPY) != 0;
     MttkrpArgs a{};
     a.rec = t->rec.as<uint8_t>();  // the paper's traversal: gather through perm_n
     a.perm = t->perm[mode].as<uint32_t>();
@@ -384,14 +340,11 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
         return true;
     };
     while (V > 1 && !ok_v(V)) V >>= 1;
-    static const int v_cap = [] {  // SPTK_FORCE_V: cap the lane vector width (tuning)
-        const char *fv = getenv("SPTK_FORCE_V");
-        return fv ? atoi(fv) : 0;
-    }();
+    const int64_t v_cap = opt(OPT_FORCE_V);  // cap the lane vector width (tests, tuning)
     if (v_cap > 0)
         while (V > 1 && V > v_cap) V >>= 1;
     bool fast = t->N >= 3 && t->N <= 5 && ok_v(V) &&
-                (copy || V * (int)es == 32);
+                (copy || V * (int)es == 32) && !opt(OPT_GENERIC);
     const int G0 = fast ? pow2ceil((int)((R < 32 * V ? R : 32 * V) / V)) : (R <= 16 ? 4 : 32);
     a.run = run_length(pe - pb, G0);
     // warp-cooperative steps pay off when rows are long (few boundary steps)
@@ -415,7 +368,7 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
         a.drow = t->det_row.as<uint32_t>();
         a.dpart = t->det_part.p;
     }
-    a.rowrec = copy && t->copy_rowrec[mode] && var == 0 && rowrec_setting();
+    a.rowrec = copy && t->copy_rowrec[mode] && var == 0 && opt(OPT_ROWREC) != 0;
     if (fast && copy) {  // stream the compact permuted copy instead
         SPTK_TRY(worker_rows(t, mode, pb, pe, chunk, workers, s));
         // indexed by absolute position: base shifted back by the copy's first position
@@ -442,7 +395,16 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
         var = 2;
     }
 
-    if (debug_dispatch())
+    {
+        static const char *kind[] = {"fast", "coop", "slice"};
+        std::string d = !fast ? "generic" : !copy ? "perm_gather" : kind[var];
+        if (fast && copy && var == 0 && a.rowrec) d += "_rowrec";
+        if (var == 2 && t->dims[a.sec] * R * (int64_t)es > slice_l2_bytes()) d += "_l2window";
+        if (t->deterministic) d += "+det";
+        d += " V" + std::to_string(fast ? V : 1);
+        set_dispatch(d);
+    }
+    if (opt(OPT_DEBUG_DISPATCH))
         fprintf(stderr, "[sptk] mttkrp mode %d rows [%lld,%lld) R %lld: %s V %d G0 %d variant %d "
                 "copy %d sec %d slices %d x %lld rows\n", mode, (long long)row_begin,
                 (long long)row_end, (long long)R, fast ? "fast" : "generic", V, G0, var,
@@ -493,10 +455,10 @@ using namespace sptk;
 extern "C" sptk_status sptk_set_tuning(int variant, int64_t run) {
     if (variant >= kNumVariants || variant < -2 || run < -2)
         return fail(SPTK_EINVAL, "set_tuning: variant in [-2, 1], run >= -2");
-    if (variant >= 0) g_variant = variant;
-    if (variant == -2) g_variant = -1;  // back to automatic
-    if (run > 0) g_run = run < 4 ? 4 : (run + 3) / 4 * 4;
-    if (run == -2) g_run = 0;  // back to adaptive
+    if (variant >= 0) SPTK_TRY(sptk_set_option("variant", variant));
+    if (variant == -2) SPTK_TRY(sptk_set_option("variant", -1));  // back to automatic
+    if (run > 0) SPTK_TRY(sptk_set_option("run", run < 4 ? 4 : (run + 3) / 4 * 4));
+    if (run == -2) SPTK_TRY(sptk_set_option("run", 0));  // back to adaptive
     return SPTK_OK;
 }
 

@@ -153,6 +153,7 @@ extern "C" sptk_status sptk_mttkrp_atomic(sptk_tensor t, int mode, int64_t R,
         bool vec = R % V == 0 && al(out) && (!lambda || al(lambda));
         for (int m = 0; m < t->N && vec; ++m)
             if (m != mode && !al(factors[m])) vec = false;
+        set_dispatch(vec ? "atomic V" + std::to_string(V) : std::string("atomic V1"));
         cudaEvent_t ev;
         st = mttkrp_span_begin(s, &ev);
         if (st == SPTK_OK)

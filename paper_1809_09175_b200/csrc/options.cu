@@ -1,0 +1,112 @@
+// options.cu -- process-wide launch options (traversal selection and tuning).
+//
+// Every option starts from its default, or from the environment variable
+// SPTK_<NAME> (upper case) when that is set, and can be changed at run time
+// with sptk_set_option -- the tests force each MTTKRP traversal in-process
+// this way, and sptk_last_dispatch() reports which traversal a call ran.
+#include <stdlib.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+
+namespace sptk {
+
+namespace {
+struct OptDef {
+    const char *name;
+    int64_t def;
+};
+// keep in the order of enum Opt (common.cuh)
+constexpr OptDef kOpts[OPT_COUNT] = {
+    {"run", 0},                 // positions per worker: 0 adaptive, > 0 fixed
+    {"variant", -1},            // fast kernel worker shape: -1 auto, 0 per-group, 1 warp-coop
+    {"slice", 1},               // 0 disables the slice traversal, 2 forces it wherever the
+                                //   copy has a secondary mode (no profitability test)
+    {"slice_l2_mb", 32},        // L2 window of the slice traversal (MB of A_a rows)
+    {"slice_rows", 0},          // rows of A_a per slice: 0 auto
+    {"slice_other_first", -1},  // slice kernel: other factors evict-first (-1 auto)
+    {"rowrec", 1},              // per-group kernel reads the row from the record's spare word
+    {"force_v", 0},             // cap of the lane vector width (elements), 0 = none
+    {"generic", 0},             // 1 forces the generic (scalar, runtime-N) kernel
+    {"debug_dispatch", 0},      // one stderr line per MTTKRP launch
+    {"copy_order", 1},          // 0: permuted copies in perm_n order (no secondary key)
+    {"deferred_norm", 1},       // CP-ALS deferred column normalisation (R <= 32)
+    {"no_graph", 0},            // CP-ALS: 1 disables the CUDA-graph replay
+    {"gamma_inv_chol", 0},      // CP-ALS: 1 = Cholesky inverse instead of Gauss-Jordan
+    {"use_copy", 1},            // 0: MTTKRP gathers through perm_n even where a copy exists
+};
+
+std::mutex g_mu;
+std::atomic<bool> g_init{false};
+std::atomic<int64_t> g_val[OPT_COUNT];
+
+int64_t env_value(const char *name, int64_t def) {
+    std::string env = "SPTK_";
+    for (const char *c = name; *c; ++c) env += (char)(*c >= 'a' && *c <= 'z' ? *c - 32 : *c);
+    const char *e = getenv(env.c_str());
+    if (!e || !*e) return def;
+    char *end = nullptr;
+    const long long v = strtoll(e, &end, 10);
+    return end == e ? def : (int64_t)v;
+}
+
+void init_locked() {
+    for (int i = 0; i < OPT_COUNT; ++i) g_val[i] = env_value(kOpts[i].name, kOpts[i].def);
+    // legacy spelling: SPTK_GAMMA_INV=chol
+    if (const char *g = getenv("SPTK_GAMMA_INV"))
+        if (g[0] == 'c') g_val[OPT_GAMMA_INV_CHOL] = 1;
+    g_init = true;
+}
+
+int find(const char *name) {
+    if (!name) return -1;
+    for (int i = 0; i < OPT_COUNT; ++i)
+        if (strcmp(kOpts[i].name, name) == 0) return i;
+    return -1;
+}
+
+thread_local std::string g_dispatch;
+}  // namespace
+
+int64_t opt(Opt o) {
+    if (!g_init) {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (!g_init) init_locked();
+    }
+    return g_val[o].load(std::memory_order_relaxed);
+}
+
+void set_dispatch(const std::string &s) { g_dispatch = s; }
+
+}  // namespace sptk
+
+using namespace sptk;
+
+extern "C" sptk_status sptk_set_option(const char *name, int64_t value) {
+    const int i = find(name);
+    if (i < 0) return fail(SPTK_EINVAL, std::string("unknown option '") + (name ? name : "") + "'");
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_init) init_locked();
+    g_val[i] = value;
+    return SPTK_OK;
+}
+
+extern "C" sptk_status sptk_get_option(const char *name, int64_t *value) {
+    const int i = find(name);
+    if (i < 0 || !value)
+        return fail(SPTK_EINVAL, std::string("unknown option '") + (name ? name : "") + "'");
+    *value = opt((Opt)i);
+    return SPTK_OK;
+}
+
+extern "C" sptk_status sptk_reset_options(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    init_locked();
+    return SPTK_OK;
+}
+
+extern "C" const char *sptk_last_dispatch(void) { return g_dispatch.c_str(); }

@@ -359,8 +359,7 @@ static sptk_status stable_sort_ids(sptk_tensor t, int mode, const uint32_t *in, 
 // Secondary key of the copy order: the shortest other mode whose factor does
 // not stay L1-resident (>= 2048 rows, 256 KB at R = 16 fp64), or -1.
 static int copy_secondary_mode(sptk_tensor t, int mode) {
-    const char *e = getenv("SPTK_COPY_ORDER");
-    if (e && *e == '0') return -1;
+    if (!opt(OPT_COPY_ORDER)) return -1;
     // SPTK_COPY_SEC=a0,a1,...: per-mode override (tuning; -1 = none)
     if (const char *o = getenv("SPTK_COPY_SEC")) {
         int m = 0, v = 0, neg = 0, have = 0;
@@ -395,7 +394,8 @@ static int copy_secondary_mode(sptk_tensor t, int mode) {
 // l_a are then adjacent and their A_a row is gathered once into L1 instead of
 // once per nonzero; the row's sum is the same up to summation order.
 sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
-    if (t->has_srec[mode] || t->perm_gather_only || t->P == 0 || !t->has_perm[mode])
+    if (t->has_srec[mode] || t->perm_gather_only || t->P == 0 || !t->has_perm[mode] ||
+        t->copy_declined[mode])
         return SPTK_OK;
     // positions covered: all, or this shard's row range (sptk_sptensor_set_shard)
     int64_t p0 = 0, p1 = t->P;
@@ -440,9 +440,16 @@ sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
             t->sortws.release();
         }
     }
-    if (free_b < need + reserve) return SPTK_OK;
+    // declined: remembered, so later MTTKRPs of this mode do not query the
+    // free memory again (a host stall while kernels are in flight) -- cleared
+    // when memory is released (drop_copies) or the mode is re-sorted
+    if (free_b < need + reserve) {
+        t->copy_declined[mode] = true;
+        return SPTK_OK;
+    }
     if (t->srec[mode].reserve(need) != SPTK_OK) {
         set_error("");
+        t->copy_declined[mode] = true;
         return SPTK_OK;
     }
     const uint32_t *order = t->perm[mode].as<uint32_t>();
@@ -493,6 +500,7 @@ void drop_copies(sptk_tensor t) {
         t->copy_sec[m] = -1;
         t->soff[m].release();
         t->soff_key[m][0] = -1;
+        t->copy_declined[m] = false;
     }
 }
 
@@ -595,6 +603,7 @@ sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s) {
     t->host_rowptr[mode].clear();
     t->row_max[mode] = -1;
     t->wrow_key[mode][0] = -1;
+    t->copy_declined[mode] = false;
     if (P == 0) {
         SPTK_CUDA(cudaMemsetAsync(rowptr, 0, sizeof(uint32_t) * (In + 1), s));
         t->has_perm[mode] = true;

@@ -4,7 +4,7 @@ This module holds NO arithmetic of the method (no MTTKRP, no sort, no ALS).
 It only draws numbers: a counter-based generator (SURVEY.md §8(d) "The
 generator spec") implemented twice from the same text -- here in numpy for
 the host, and in ``synth/gen.cu`` for the device -- so that both sides see
-bit-identical inputs.  ``tests/test_synth.py`` checks the two agree.
+bit-identical inputs.  ``tests/test_gpu.py::test_device_generator_matches_host`` checks the two agree.
 
 Generator text (DESIGN.md §3 "Input recipe"):
 
@@ -132,6 +132,31 @@ def factor(seed_f: int, N: int, m: int, I: int, R: int, dtype=np.float64) -> np.
     """Factor matrix A_m (I x R, row-major), entries u in [0,1) (stream N+1+m)."""
     i = np.arange(0, I * R, dtype=np.uint64)
     return unit(draw(seed_f, N + 1 + m, i)).reshape(I, R).astype(dtype)
+
+
+# Integer-valued variants (the integer-exact parity pins, tests/test_gpu_exact.py):
+# a draw u in [0,1) becomes the small integer 1 + floor(k*u) in {1..k}.  Both
+# sides apply this same map to bit-identical draws (k*u and floor are exact
+# IEEE operations), so host and device hold the same integers; every sum of
+# products of them below 2^53 (fp64) / 2^24 (fp32) is exact in any order.
+INT_VALUE_LEVELS = 4    # values in {1, 2, 3, 4}
+INT_FACTOR_LEVELS = 3   # factor entries in {1, 2, 3}
+
+
+def int_from_unit(u, k: int):
+    """1 + floor(k*u) for u in [0,1) (numpy or torch arrays alike)."""
+    return (u * k) // 1 + 1
+
+
+def int_values(seed: int, N: int, i0: int, count: int) -> np.ndarray:
+    """Integer values 1 + floor(4u), u the same draw as ``values`` (x = 1 - u)."""
+    i = np.arange(i0, i0 + count, dtype=np.uint64)
+    return int_from_unit(unit(draw(seed, N, i)), INT_VALUE_LEVELS)
+
+
+def int_factor(seed_f: int, N: int, m: int, I: int, R: int) -> np.ndarray:
+    """Integer factor 1 + floor(3u), u the same draw as ``factor``."""
+    return int_from_unit(factor(seed_f, N, m, I, R), INT_FACTOR_LEVELS)
 
 
 def tensor(seed: int, dims, P: int, dist: str = "uniform", i0: int = 0,

@@ -93,3 +93,19 @@ def values_at(seed: int, N: int, ids):
     if st:
         raise RuntimeError(f"synth_values_at failed: cuda error {st}")
     return out
+
+
+def int_values_from(vals):
+    """Integer values 1 + floor(4u) from device values x = 1 - u (fp64; 1 - x is
+    exactly u for u a multiple of 2^-53 in [0,1)) -- same integers as
+    ``synth.int_values``."""
+    from . import INT_VALUE_LEVELS, int_from_unit
+    return int_from_unit(1.0 - vals.double(), INT_VALUE_LEVELS)
+
+
+def int_factor(seed_f: int, N: int, m: int, I: int, R: int, dtype=None, device="cuda"):
+    """Integer factor 1 + floor(3u) (same integers as ``synth.int_factor``)."""
+    import torch
+    from . import INT_FACTOR_LEVELS, int_from_unit
+    u = factor(seed_f, N, m, I, R, dtype=torch.float64, device=device)
+    return int_from_unit(u, INT_FACTOR_LEVELS).to(dtype or torch.float64)

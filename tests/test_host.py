@@ -117,3 +117,51 @@ def test_bench_reference_arm_contract():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["steps"] == 2
+
+
+def test_options_roundtrip_and_unknown_name(sp):
+    """Launch options (include/sptk.h): set/get/restore in-process, unknown
+    names are SPTK_EINVAL, the context manager restores the previous value."""
+    assert sp.get_option("slice") == 1
+    with sp.options(slice=0, slice_l2_mb=3):
+        assert sp.get_option("slice") == 0 and sp.get_option("slice_l2_mb") == 3
+    assert sp.get_option("slice") == 1 and sp.get_option("slice_l2_mb") == 32
+    with pytest.raises(sp.SptkError) as e:
+        sp.set_option("no_such_option", 1)
+    assert e.value.name == "EINVAL"
+    sp.set_tuning(1, 64)
+    assert sp.get_option("variant") == 1 and sp.get_option("run") == 64
+    sp.reset_options()
+    assert sp.get_option("variant") == -1 and sp.get_option("run") == 0
+    assert sp.last_dispatch() == ""
+
+
+def test_binding_validates_buffers_before_the_abi(sp):
+    """shapes, dtypes, contiguity and placement are checked in the
+    binding before raw addresses cross the C ABI (a float32 factor for an f64
+    tensor, a short factor, a host buffer where a device pointer is required,
+    or a wrong-dtype host buffer for cp_als's device-to-host copies)."""
+    t = sp.SpTensor(0, (4, 5, 6), 10, sp.F64)
+    ok = [np.zeros((I, 3)) for I in (4, 5, 6)]
+    out = np.zeros((5, 3))
+    # mttkrp takes device pointers only: host numpy is refused up front
+    with pytest.raises(ValueError, match="CUDA tensor"):
+        sp.mttkrp(t, 1, ok, out)
+    with pytest.raises(ValueError, match="shape"):
+        sp.mttkrp(t, 1, ok, np.zeros((4, 3)))
+    with pytest.raises(ValueError, match="mode"):
+        sp.mttkrp(t, 3, ok, out)
+    with pytest.raises(ValueError, match="matrices"):
+        sp.mttkrp_rows(t, 0, ok[:2], np.zeros((4, 3)), 0, 4)
+    # cp_als accepts host buffers, but each must be (I_m, R) of the dtype
+    with pytest.raises(ValueError, match="dtype"):
+        sp.cp_als(t, 3, 1, [a.astype(np.float32) for a in ok])
+    with pytest.raises(ValueError, match="shape"):
+        sp.cp_als(t, 3, 1, [ok[0], ok[1], np.zeros((5, 3))])
+    with pytest.raises(ValueError, match="contiguous"):
+        sp.cp_als(t, 3, 1, [ok[0], ok[1], np.zeros((3, 6)).T])
+    with pytest.raises(ValueError, match="lambda_out"):
+        sp.cp_als(t, 3, 1, ok, lambda_out=np.zeros(4))
+    with pytest.raises(ValueError, match="init"):
+        sp.cp_als(t, 3, 1, ok, init=[ok[0], ok[1], np.zeros((6, 2))])
+    t.handle = None  # never a real handle: nothing to destroy

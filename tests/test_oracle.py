@@ -182,6 +182,45 @@ def test_chol_solve_cases():
         oracle.chol_solve(np.zeros((3, 3)), np.ones((1, 3)))
 
 
+def test_chol_solve_ridge_branch():
+    """The ridge retry (SURVEY §8(c) CP-ALS step 3.3, DESIGN.md §2 Z11/Z12):
+    when Cholesky of Gamma fails, X = B (Gamma + 1e-12 tr(Gamma)/R I)^{-1}.
+    Pinned against numpy's LU solve of that explicitly ridged matrix."""
+    R = 5
+    A = synth.factor(7, 3, 0, 40, R)
+    A[:, 3] = 0.0                                  # a zero column: pivot 3 is exactly 0
+    G = A.T @ A
+    B = synth.factor(8, 3, 1, 6, R) + 0.25
+    with np.errstate(all="ignore"):
+        assert not np.all(np.linalg.eigvalsh(G) > 0)
+    delta = 1e-12 * np.trace(G) / R
+    X = oracle.chol_solve(G, B)
+    Xr = np.linalg.solve(G + delta * np.eye(R), B.T).T
+    # block-diagonal ridged matrix: both solves are well conditioned per block,
+    # so they agree to rounding -- including X[:, 3] = B[:, 3] / delta (~1e12)
+    np.testing.assert_allclose(X, Xr, rtol=1e-10)
+    np.testing.assert_allclose(X[:, 3], B[:, 3] / delta, rtol=1e-14)
+    # a wrong ridge (tr(Gamma) instead of tr(Gamma)/R, or no /R at all) is off by R
+    assert not np.allclose(X[:, 3], B[:, 3] / (1e-12 * np.trace(G)), rtol=1e-3)
+    # rank-deficient but not block-diagonal (two equal columns): the ridged
+    # system is ill conditioned (cond ~ 1e12), so pin the residual of the
+    # oracle's solve against the ridged matrix instead of forward digits: the
+    # right ridge leaves ~u cond(Gr) ~ 1e-4 of ||B||, a ridge off by 10x leaves
+    # ~9 delta ||X|| ~ ||B||, twice the ridge ~0.1 ||B||
+    A2 = synth.factor(9, 3, 2, 40, R)
+    A2[:, 1] = A2[:, 4]
+    G2 = A2.T @ A2
+    d2 = 1e-12 * np.trace(G2) / R
+    X2 = oracle.chol_solve(G2, B)
+
+    def resid(Gx):
+        return np.linalg.norm(X2 @ Gx - B) / np.linalg.norm(B)
+    assert resid(G2 + d2 * np.eye(R)) <= 1e-3
+    assert resid(G2 + 10 * d2 * np.eye(R)) >= 0.1
+    assert resid(G2 + 2 * d2 * np.eye(R)) >= 0.05
+    assert resid(G2) >= 0.05                      # the unridged matrix
+
+
 # ------------------------------------------------------------------- CP-ALS
 def _dense_as_sparse(T):
     idx = np.argwhere(T != 0).astype(np.uint32)
