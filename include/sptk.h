@@ -281,7 +281,7 @@ sptk_status sptk_set_tuning(int variant, int64_t run);
  *   run 0 (positions per worker, 0 = adaptive), variant -1 (auto; 0 per-group,
  *   1 warp-cooperative), slice 1 (0 disables the slice traversal, 2 forces
  *   it wherever the permuted copy has a secondary mode),
- *   slice_l2_mb 32 (L2 window of the slice traversal when the secondary
+ *   slice_l2_kb 32768 (L2 window of the slice traversal when the secondary
  *   factor exceeds it), slice_rows 0 (auto), slice_other_first -1 (auto),
  *   rowrec 1, force_v 0 (cap of the lane vector width in elements),
  *   generic 0 (1 forces the generic scalar kernel), debug_dispatch 0,

@@ -49,7 +49,7 @@ int dev_sms();
 // Process-wide launch options (options.cu): default, else SPTK_<NAME> from the
 // environment, else sptk_set_option.  Order = kOpts in options.cu.
 enum Opt {
-    OPT_RUN, OPT_VARIANT, OPT_SLICE, OPT_SLICE_L2_MB, OPT_SLICE_ROWS, OPT_SLICE_OTHER_FIRST,
+    OPT_RUN, OPT_VARIANT, OPT_SLICE, OPT_SLICE_L2_KB, OPT_SLICE_ROWS, OPT_SLICE_OTHER_FIRST,
     OPT_ROWREC, OPT_FORCE_V, OPT_GENERIC, OPT_DEBUG_DISPATCH, OPT_COPY_ORDER, OPT_DEFERRED_NORM,
     OPT_NO_GRAPH, OPT_GAMMA_INV_CHOL, OPT_USE_COPY, OPT_COUNT
 };

@@ -204,9 +204,9 @@ constexpr int64_t kSliceBytesF64 = 512 << 10;  // fp64: 512 KB of A_a rows (R=16
 // fastest), so the whole GPU sweeps one window at a time and the A_a gathers
 // hit L2 instead of HBM.
 constexpr int64_t kSliceL2Bytes = 32 << 20;
-static int64_t slice_l2_bytes() {  // option slice_l2_mb (tests force the window regime)
-    const int64_t mb = opt(OPT_SLICE_L2_MB);
-    return mb > 0 ? mb << 20 : kSliceL2Bytes;
+static int64_t slice_l2_bytes() {  // option slice_l2_kb (tests force the window regime)
+    const int64_t kb = opt(OPT_SLICE_L2_KB);
+    return kb > 0 ? kb << 10 : kSliceL2Bytes;
 }
 
 // L2 policy of the other factors' gathers in the slice kernel: in the L2-window

@@ -26,7 +26,7 @@ constexpr OptDef kOpts[OPT_COUNT] = {
     {"variant", -1},            // fast kernel worker shape: -1 auto, 0 per-group, 1 warp-coop
     {"slice", 1},               // 0 disables the slice traversal, 2 forces it wherever the
                                 //   copy has a secondary mode (no profitability test)
-    {"slice_l2_mb", 32},        // L2 window of the slice traversal (MB of A_a rows)
+    {"slice_l2_kb", 32768},     // L2 window of the slice traversal (KB of A_a rows)
     {"slice_rows", 0},          // rows of A_a per slice: 0 auto
     {"slice_other_first", -1},  // slice kernel: other factors evict-first (-1 auto)
     {"rowrec", 1},              // per-group kernel reads the row from the record's spare word

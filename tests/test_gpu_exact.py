@@ -42,7 +42,7 @@ EXACT_LIMIT = {"f64": 2.0 ** 53, "f32": 2.0 ** 24}
 TRAVERSALS = {
     "default": ({}, "", None),
     "slice": ({"slice": 2}, "slice", None),
-    "slice_l2window": ({"slice": 2, "slice_l2_mb": 1}, "slice_l2window", None),
+    "slice_l2window": ({"slice": 2, "slice_l2_kb": 64}, "slice_l2window", None),
     "coop": ({"slice": 0, "variant": 1}, "coop", None),
     "fast": ({"slice": 0, "variant": 0, "rowrec": 0}, "fast V", None),
     "fast_rowrec": ({"slice": 0, "variant": 0, "rowrec": 1}, "fast_rowrec",

@@ -123,9 +123,9 @@ def test_options_roundtrip_and_unknown_name(sp):
     """Launch options (include/sptk.h): set/get/restore in-process, unknown
     names are SPTK_EINVAL, the context manager restores the previous value."""
     assert sp.get_option("slice") == 1
-    with sp.options(slice=0, slice_l2_mb=3):
-        assert sp.get_option("slice") == 0 and sp.get_option("slice_l2_mb") == 3
-    assert sp.get_option("slice") == 1 and sp.get_option("slice_l2_mb") == 32
+    with sp.options(slice=0, slice_l2_kb=3):
+        assert sp.get_option("slice") == 0 and sp.get_option("slice_l2_kb") == 3
+    assert sp.get_option("slice") == 1 and sp.get_option("slice_l2_kb") == 32768
     with pytest.raises(sp.SptkError) as e:
         sp.set_option("no_such_option", 1)
     assert e.value.name == "EINVAL"
