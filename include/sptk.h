@@ -244,6 +244,15 @@ sptk_status sptk_comm_unique_id(void *id128);
 sptk_status sptk_comm_create(const void *id128, int nranks, int rank, sptk_comm *out);
 sptk_status sptk_comm_destroy(sptk_comm c);
 
+/* How a sharded sptk_cp_als (R <= 32) replicates each updated factor's rows
+ * (DESIGN.md §7): 2 = NVLS multimem stores and 1 = NVLink peer stores, both
+ * issued by the kernel that computes the rows into the communicator's
+ * symmetric buffer (ncclMemAlloc + ncclCommWindowRegister); 0 = grouped NCCL
+ * broadcasts after it; -1 = not decided yet (no sharded cp_als has run on
+ * this communicator).  The mode is the best one every rank supports, capped
+ * by the `exchange` option (sptk_set_option). */
+sptk_status sptk_comm_exchange(sptk_comm c, int *mode);
+
 /* Host-only (no GPU needed): split rows [0, In) into nranks contiguous ranges
  * of near-equal nonzero counts.  rowptr (host, In+1 entries, non-decreasing,
  * rowptr[0] = 0, rowptr[In] = nnz).  bounds (host, nranks+1): rank g owns rows

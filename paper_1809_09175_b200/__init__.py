@@ -55,6 +55,7 @@ _SIGS = [
     ("sptk_comm_unique_id", [_P], _I),
     ("sptk_comm_create", [_P, _I, _I, _P], _I),
     ("sptk_comm_destroy", [_P], _I),
+    ("sptk_comm_exchange", [_P, _P], _I),
     ("sptk_partition_rows", [_P, _I64, _I, _P], _I),
     ("sptk_profile_enable", [_I], _I),
     ("sptk_profile_reset", [], _I),
@@ -372,6 +373,14 @@ def comm_create(uid: bytes, nranks: int, rank: int) -> Comm:
     buf = (C.c_char * 128).from_buffer_copy(uid)
     _check(lib().sptk_comm_create(buf, nranks, rank, C.byref(out)), "comm_create")
     return Comm(out.value, nranks, rank)
+
+
+def comm_exchange(comm: Comm) -> int:
+    """Row-exchange mode of the sharded CP-ALS on this communicator: 2 NVLS
+    multimem stores, 1 peer stores, 0 NCCL broadcasts, -1 not decided yet."""
+    v = C.c_int(0)
+    _check(lib().sptk_comm_exchange(comm.handle, C.byref(v)), "comm_exchange")
+    return v.value
 
 
 def comm_from_process_group(group=None) -> Comm:

@@ -23,6 +23,32 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
 LIB = os.path.join(PKG, "libsptk.so")
+
+
+def _nccl_device_include():
+    """Include dir of the NCCL runtime torch ships (2.28+: nccl_device.h, the
+    symmetric-memory window and device-communicator API used by comm.cu), or
+    None -- comm.cu then builds without the fused exchange (NCCL broadcast)."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for d in (spec.submodule_search_locations or []):
+            inc = os.path.join(d, "include")
+            if os.path.exists(os.path.join(inc, "nccl_device.h")):
+                return inc
+    except Exception:
+        pass
+    return None
+
+
+def _extra_flags(src):
+    if os.path.basename(src) == "comm.cu":
+        inc = _nccl_device_include()
+        if inc:
+            return ["-I", inc, "-DSPTK_NCCL_DEVICE_API=1"]
+    return []
+
+
 SYNTH_SRC = os.path.join(ROOT, "synth", "gen.cu")
 SYNTH_LIB = os.path.join(ROOT, "synth", "libsynth.so")
 
@@ -52,7 +78,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
             todo.append((src, obj))
     ptxas = ["-Xptxas", "-v"] if verbose else []
     with cf.ThreadPoolExecutor(max_workers=jobs or os.cpu_count() or 4) as ex:
-        futs = {ex.submit(_run, [NVCC, *ARCH, *FLAGS, *ptxas, "-c", src, "-o", obj + ".tmp"]): (src, obj)
+        futs = {ex.submit(_run, [NVCC, *ARCH, *FLAGS, *_extra_flags(src), *ptxas, "-c", src, "-o",
+                                 obj + ".tmp"]): (src, obj)
                 for src, obj in todo}
         for f in cf.as_completed(futs):
             src, obj = futs[f]

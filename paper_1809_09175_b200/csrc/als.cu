@@ -582,15 +582,32 @@ struct ModeTail {
     int N, n, next;
 };
 
+// Where apply_gram also stores the rows it computes (sharded CP-ALS with the
+// fused exchange): every rank's replica of A_n by NVLink peer
+// stores (np > 0), or one NVLS multicast store that reaches every rank (mc).
+struct ExchOut {
+    int np = 0;
+    char *peer[kMaxPeers] = {};  // A_n on rank p (byte address in this process)
+    char *mc = nullptr;          // multicast address of A_n
+};
+
+__device__ __forceinline__ void mm_store(double *p, double v) {
+    asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void mm_store(float *p, float v) {
+    asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
 #ifndef SPTK_APPLY_MINB  // A/B builds only
 #define SPTK_APPLY_MINB 1
 #endif
 template <typename T, int RM>  // RM >= R: Gamma^{-1} column length held in registers
 __global__ void __launch_bounds__(256, SPTK_APPLY_MINB)
-    apply_gram_kernel(const T *__restrict__ V, int64_t I, int R, int64_t rows_per_block, int kApplyTile,
+    apply_gram_kernel(const T *__restrict__ V, int64_t r_begin, int64_t I, int R,
+                      int64_t rows_per_block, int kApplyTile,
                       const double *__restrict__ Ginv, T *__restrict__ A,
                       double *__restrict__ part_sq, double *__restrict__ part_dot,
-                      double *__restrict__ gpart, const ModeTail tail) {
+                      double *__restrict__ gpart, const ModeTail tail, const ExchOut ex) {
     extern __shared__ __align__(16) double sm[];
     const int RP = (R + 3) & ~3;              // padded row stride (whole 4-column blocks)
     double *Vt = sm;                          // kApplyTile x RP
@@ -618,7 +635,7 @@ __global__ void __launch_bounds__(256, SPTK_APPLY_MINB)
 #pragma unroll
     for (int q = 0; q < 16; ++q) g[q] = 0.0;
     double sq = 0.0, dot = 0.0;
-    const int64_t b0 = (int64_t)blockIdx.x * rows_per_block;
+    const int64_t b0 = r_begin + (int64_t)blockIdx.x * rows_per_block;  // rows [r_begin, I)
     const int64_t b1 = min(I, b0 + rows_per_block);
     // the next tile of V is loaded into registers while this one is computed
     // (kApplyTile * R <= kApplyPf * 256, clamped by the host): without it each
@@ -665,7 +682,14 @@ __global__ void __launch_bounds__(256, SPTK_APPLY_MINB)
                     }
                 }
                 const T xt = (T)x;
-                A[(rt + r) * R + j] = xt;
+                const int64_t ix = (rt + r) * R + j;
+                if (ex.mc) {
+                    mm_store(reinterpret_cast<T *>(ex.mc) + ix, xt);
+                } else if (ex.np) {
+                    for (int p = 0; p < ex.np; ++p) reinterpret_cast<T *>(ex.peer[p])[ix] = xt;
+                } else {
+                    A[ix] = xt;
+                }
                 const double xd = (double)xt;
                 At[r * RP + j] = xd;
                 sq += xd * xd;
@@ -688,6 +712,9 @@ __global__ void __launch_bounds__(256, SPTK_APPLY_MINB)
             }
         }
     }
+    // the stores to the other ranks' replicas are visible before this rank's
+    // next collective (the all-reduce of the partials) is issued
+    if (ex.np || ex.mc) __threadfence_system();
     __syncthreads();
     red[tid] = sq;
     red[256 + tid] = dot;
@@ -966,6 +993,9 @@ struct AlsCtx {
     int nb_row;                            // blocks of the R-vector partial-sum kernels
     size_t part_stride;                    // doubles between the psq and pdot partials
     int nb_apply = 0;                      // block cap of apply_gram
+    // sharded deferred path: factor replicas in the comm's symmetric buffer
+    bool sym_iter = false;
+    std::vector<size_t> off;               // byte offset of A_m in c.comm->sym
 };
 
 // G_m = A_m^T A_m (fixed-order reduction of per-block partials in `part`,
@@ -1102,13 +1132,13 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
             tail.n = n;
             tail.next = (n + 1) % N;
             if (R <= 16)
-                apply_gram_kernel<T, 16><<<nb, 256, smb, c.s>>>(V, I, R, rpb, tile, Ginv, An, psq,
+                apply_gram_kernel<T, 16><<<nb, 256, smb, c.s>>>(V, 0, I, R, rpb, tile, Ginv, An, psq,
                                                                 last ? pdot : nullptr,
-                                                                w.gpart.as<double>(), tail);
+                                                                w.gpart.as<double>(), tail, ExchOut{});
             else
-                apply_gram_kernel<T, 32><<<nb, 256, smb, c.s>>>(V, I, R, rpb, tile, Ginv, An, psq,
+                apply_gram_kernel<T, 32><<<nb, 256, smb, c.s>>>(V, 0, I, R, rpb, tile, Ginv, An, psq,
                                                                 last ? pdot : nullptr,
-                                                                w.gpart.as<double>(), tail);
+                                                                w.gpart.as<double>(), tail, ExchOut{});
             count_launch();
             SPTK_CUDA(cudaGetLastError());
             if (!tail.counter) {  // many blocks: parallel reductions, then one finalise block
@@ -1170,6 +1200,102 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
     return SPTK_OK;
 }
 
+// Sharded iteration (R <= 32, deferred normalisation): rank g
+// owns rows [b_g, b_{g+1}) of every mode.  Per mode: Gamma^{-1} on the side
+// stream; the rank's MTTKRP rows (other factors' column scales at the flush);
+// apply_gram on its rows, which writes A_raw = V Gamma^{-1} straight into
+// every rank's replica of A_n (NVLS multimem or NVLink peer stores: the
+// exchange is fused into the kernel that computes the rows) and leaves the
+// column / Gram / fit partials; one all-reduce of [colsq, dot, G_raw]
+// (2R + R^2 doubles) -- which also orders every rank's stores before anyone
+// reads A_n; then the same finalisation as one GPU on every rank.  Without
+// peer access the rows go out by grouped NCCL broadcasts instead.
+template <typename T>
+static sptk_status enqueue_iteration_sharded(AlsCtx &c) {
+    sptk_tensor t = c.t;
+    ALSWork &w = t->als;
+    const int N = t->N, R = (int)c.R;
+    SymMem &sm = c.comm->sym;
+    double *lam = w.lam.as<double>();
+    double *scal = w.scal.as<double>();
+    int *status = reinterpret_cast<int *>(scal + 8);
+    double *Ginv = w.L.as<double>();
+    T *V = w.V.as<T>();
+    double *s_all = w.scl.as<double>();
+    double *graw_unused = s_all + (size_t)N * R;
+    (void)graw_unused;
+    T *scale = reinterpret_cast<T *>(s_all + (size_t)N * R + (size_t)R * R);
+    double *trace = w.trace.as<double>();
+    int *trace_n = reinterpret_cast<int *>(scal + 12);
+    double *ared = w.colsq.as<double>();   // [colsq R][dot R][G_raw R^2], all-reduced
+    double *psq = w.partial.as<double>();
+    double *pdot = psq + c.part_stride;
+    const int rank = c.comm->rank;
+    for (int n = 0; n < N; ++n) {
+        const bool last = n == N - 1;
+        const int64_t r0 = c.b[n][rank], r1 = c.b[n][rank + 1], rows = r1 - r0;
+        SPTK_CUDA(cudaEventRecord(w.ev_gram, c.s));
+        SPTK_CUDA(cudaStreamWaitEvent(w.side, w.ev_gram, 0));
+        launch_ginv(w.G.as<double>(), N, n, R, Ginv, status, w.side);
+        count_launch();
+        SPTK_CUDA(cudaGetLastError());
+        SPTK_CUDA(cudaEventRecord(w.ev_inv, w.side));
+        SPTK_TRY(mttkrp_launch(t, n, c.R, c.A.data(), scale, V, r0, r1, c.s));
+        SPTK_CUDA(cudaStreamWaitEvent(c.s, w.ev_inv, 0));
+        T *An = static_cast<T *>(c.A[n]);
+        if (rows > 0) {
+            const int tile = std::min(apply_tile_rows(), apply_pf(R <= 16 ? 16 : 32) * 256 / R);
+            const size_t smb = sizeof(double) * (2 * tile * ((R + 3) & ~3) + 4 * 256);
+            int nb = (int)std::min<int64_t>(apply_block_cap<T>(c.nb_apply, R, smb),
+                                            (rows + tile - 1) / tile);
+            if (nb < 1) nb = 1;
+            const int64_t rpb = (rows + nb - 1) / nb;
+            nb = (int)((rows + rpb - 1) / rpb);
+            ExchOut ex{};
+            if (sm.exchange == 2) {
+                ex.mc = sm.mc + c.off[n];
+            } else if (sm.exchange == 1) {
+                ex.np = sm.npeer;
+                for (int p = 0; p < sm.npeer; ++p) ex.peer[p] = sm.peer[p] + c.off[n];
+            }
+            ModeTail tail{};  // counter NULL: partials reduced below, across ranks
+            if (R <= 16)
+                apply_gram_kernel<T, 16><<<nb, 256, smb, c.s>>>(V, r0, r1, R, rpb, tile, Ginv, An,
+                                                                psq, last ? pdot : nullptr,
+                                                                w.gpart.as<double>(), tail, ex);
+            else
+                apply_gram_kernel<T, 32><<<nb, 256, smb, c.s>>>(V, r0, r1, R, rpb, tile, Ginv, An,
+                                                                psq, last ? pdot : nullptr,
+                                                                w.gpart.as<double>(), tail, ex);
+            reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(psq, nb, R, ared);
+            reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(w.gpart.as<double>(), nb,
+                                                                    R * R, ared + 2 * R);
+            count_launch(3);
+            if (last) {
+                reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(pdot, nb, R, ared + R);
+                count_launch();
+            }
+            SPTK_CUDA(cudaGetLastError());
+        } else {
+            SPTK_CUDA(cudaMemsetAsync(ared, 0, sizeof(double) * (2 * R + R * R), c.s));
+        }
+        SPTK_TRY(comm_allreduce_f64(c.comm, ared, 2 * R + (int64_t)R * R, c.s));
+        if (sm.exchange == 0)
+            SPTK_TRY(comm_bcast_rows(c.comm, An, c.R, t->dtype, c.b[n].data(), c.s));
+        finalize_mode_kernel<T><<<1, 256, 0, c.s>>>(ared, ared + 2 * R, An, N, n, R, (n + 1) % N,
+                                                     s_all, lam, w.G.as<double>(), scale);
+        count_launch();
+        if (last) {
+            fit_kernel<<<1, 256, 0, c.s>>>(ared + R, lam, w.G.as<double>(), N, R, t->normX2, scal,
+                                           trace, trace_n);
+            count_launch();
+        }
+        SPTK_CUDA(cudaGetLastError());
+    }
+    SPTK_CUDA(cudaMemcpyAsync(w.hres, scal, sizeof(double) * 9, cudaMemcpyDeviceToHost, c.s));
+    return SPTK_OK;
+}
+
 // wait for the iteration and read (fit, status) from the pinned buffer
 static sptk_status complete_iteration(AlsCtx &c, double *fit_host, int *status_host) {
     SPTK_CUDA(cudaStreamSynchronize(c.s));
@@ -1182,9 +1308,14 @@ static sptk_status complete_iteration(AlsCtx &c, double *fit_host, int *status_h
 }
 
 template <typename T>
+static sptk_status enqueue_iteration(AlsCtx &c) {
+    return c.sym_iter ? enqueue_iteration_sharded<T>(c) : enqueue_iteration_fused<T>(c);
+}
+
+template <typename T>
 static sptk_status als_iteration(AlsCtx &c, double *fit_host, int *status_host) {
-    if (!sharded(c.comm)) {
-        SPTK_TRY(enqueue_iteration_fused<T>(c));
+    if (!sharded(c.comm) || c.sym_iter) {
+        SPTK_TRY(enqueue_iteration<T>(c));
         return complete_iteration(c, fit_host, status_host);
     }
     sptk_tensor t = c.t;
@@ -1287,7 +1418,7 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     c.part_stride = (size_t)nparts_max * R;
     SPTK_TRY(w.partial.reserve(sizeof(double) * std::max<size_t>((size_t)c.nblocks * R * R,
                                                                 2 * c.part_stride)));
-    SPTK_TRY(w.colsq.reserve(sizeof(double) * 2 * R));
+    SPTK_TRY(w.colsq.reserve(sizeof(double) * (2 * R + R * R)));
     SPTK_TRY(w.lam.reserve(sizeof(double) * R));
     SPTK_TRY(w.scal.reserve(sizeof(double) * 16));
     SPTK_TRY(w.trace.reserve(sizeof(double) * (size_t)std::max(max_iters, 1)));
@@ -1304,16 +1435,29 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     SPTK_CUDA(cudaMemsetAsync(w.scal.p, 0, sizeof(double) * 16, s));
     w.R = R;
 
-    // factor storage: caller's device buffers, or staging for host buffers
+    // factor storage: caller's device buffers, or staging for host buffers;
+    // the sharded deferred path keeps the replicas in the communicator's
+    // symmetric buffer (other ranks store rows into it) and copies out at the end
+    const bool multi = sharded(comm);
+    c.sym_iter = multi && deferred_norm(R);
     std::vector<bool> host_out(N);
     bool any_host = false;
     for (int m = 0; m < N; ++m) {
-        host_out[m] = !is_device_ptr(factors_out[m]);
-        any_host = any_host || host_out[m];
+        host_out[m] = c.sym_iter || !is_device_ptr(factors_out[m]);
+        any_host = any_host || !is_device_ptr(factors_out[m]);
     }
-    if (any_host) SPTK_TRY(w.stage.reserve(es * Isum * R));
     c.A.resize(N);
-    {
+    if (c.sym_iter) {
+        c.off.assign(N, 0);
+        size_t bytes = 0;
+        for (int m = 0; m < N; ++m) {
+            c.off[m] = bytes;
+            bytes += (es * t->dims[m] * R + 255) / 256 * 256;
+        }
+        SPTK_TRY(comm_sym_reserve(comm, bytes, s));
+        for (int m = 0; m < N; ++m) c.A[m] = static_cast<char *>(comm->sym.local) + c.off[m];
+    } else {
+        if (any_host) SPTK_TRY(w.stage.reserve(es * Isum * R));
         char *st = w.stage.as<char>();
         for (int m = 0; m < N; ++m) {
             if (host_out[m]) {
@@ -1337,7 +1481,6 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     }
     for (int m = 0; m < N; ++m)
         if (!t->has_perm[m]) SPTK_TRY(build_perm_mode(t, m, s));
-    const bool multi = sharded(comm);
     if (multi) {
         c.b.assign(N, std::vector<int64_t>(comm->nranks + 1));
         for (int m = 0; m < N; ++m) {
@@ -1349,7 +1492,7 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     for (int m = 0; m < N; ++m) SPTK_TRY(gram<T>(c, m));
     // deferred normalisation state (single GPU, R <= 32): all scales 1, and the
     // first MTTKRP's column weights 1
-    const bool deferred = !sharded(comm) && deferred_norm(R);
+    const bool deferred = (!multi || c.sym_iter) && deferred_norm(R);
     if (deferred) {
         double *s_all = w.scl.as<double>();
         fill_f64_kernel<<<(unsigned)((N * R + 255) / 256), 256, 0, s>>>(s_all, N * (int)R, 1.0);
@@ -1367,7 +1510,7 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     // launches read), capture one iteration -- both streams, ~4N+2 kernels and
     // the fit copy -- into a CUDA graph and replay it.  Not while profiling
     // (kernel-span events cannot be timed inside graphs) or for < 4 iterations.
-    bool use_graph = !multi && !profile().on && max_iters >= 4 && !opt(OPT_NO_GRAPH);
+    bool use_graph = (!multi || c.sym_iter) && !profile().on && max_iters >= 4 && !opt(OPT_NO_GRAPH);
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int64_t launches_per_iter = 0;
@@ -1377,7 +1520,7 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
             if (!exec) {
                 const int64_t l0 = profile().launches;
                 bool ok = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
-                sptk_status est = ok ? enqueue_iteration_fused<T>(c) : SPTK_ECUDA;
+                sptk_status est = ok ? enqueue_iteration<T>(c) : SPTK_ECUDA;
                 cudaGraph_t g = nullptr;
                 const bool ended = cudaStreamEndCapture(s, &g) == cudaSuccess;
                 ok = ok && est == SPTK_OK && ended && g &&
@@ -1391,7 +1534,7 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
                     exec = nullptr;
                     use_graph = false;
                     profile().launches = l0;
-                    st = enqueue_iteration_fused<T>(c);
+                    st = enqueue_iteration<T>(c);
                     if (st == SPTK_OK) st = complete_iteration(c, &fit, &bad);
                     if (st != SPTK_OK) break;
                     goto have_fit;
@@ -1471,7 +1614,7 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     for (int m = 0; m < N; ++m)
         if (host_out[m])
             SPTK_CUDA(cudaMemcpyAsync(factors_out[m], c.A[m], es * t->dims[m] * R,
-                                      cudaMemcpyDeviceToHost, s));
+                                      cudaMemcpyDefault, s));
     if (lambda_out) {
         cast_kernel<T><<<(unsigned)((R + 127) / 128), 128, 0, s>>>(w.lam.as<double>(), (int)R,
                                                                   w.lamT.as<T>());

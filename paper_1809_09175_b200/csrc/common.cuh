@@ -51,7 +51,7 @@ int dev_sms();
 enum Opt {
     OPT_RUN, OPT_VARIANT, OPT_SLICE, OPT_SLICE_L2_KB, OPT_SLICE_ROWS, OPT_SLICE_OTHER_FIRST,
     OPT_ROWREC, OPT_FORCE_V, OPT_GENERIC, OPT_DEBUG_DISPATCH, OPT_COPY_ORDER, OPT_DEFERRED_NORM,
-    OPT_NO_GRAPH, OPT_GAMMA_INV_CHOL, OPT_USE_COPY, OPT_COUNT
+    OPT_NO_GRAPH, OPT_GAMMA_INV_CHOL, OPT_USE_COPY, OPT_EXCHANGE, OPT_COUNT
 };
 int64_t opt(Opt o);
 void set_dispatch(const std::string &s);  // what the last MTTKRP call ran (sptk_last_dispatch)
@@ -142,11 +142,32 @@ struct sptk_tensor_s {
     sptk::ALSWork als;
 };
 
+namespace sptk {
+constexpr int kMaxPeers = 8;  // ranks of one NVLink domain the fused exchange stores to
+// Symmetric device memory (comm.cu): the same-size buffer on every rank,
+// registered as an NCCL window; peer[p] is rank p's copy mapped into this
+// process (NVLink load/store), mc its NVLS multicast address (one store
+// reaches every rank).  Without NCCL >= 2.28 it is plain device memory.
+struct SymMem {
+    void *local = nullptr;
+    size_t bytes = 0;
+    void *win = nullptr;           // ncclWindow_t, NULL for plain device memory
+    int npeer = 0;                 // ranks reachable by stores (== nranks) or 0
+    char *peer[kMaxPeers] = {};
+    char *mc = nullptr;
+    bool nccl_mem = false;         // ncclMemAlloc'd
+    int exchange = 0;              // agreed by all ranks: 0 NCCL broadcast, 1 peer stores, 2 multimem
+};
+}  // namespace sptk
+
 struct sptk_comm_s {
     void *nccl = nullptr;  // ncclComm_t
     int nranks = 1;
     int rank = 0;
     bool force_sharded = false;  // SPTK_FORCE_SHARDED=1: take the N>1 code path at N=1
+    sptk::SymMem sym;            // factor replicas of the sharded CP-ALS (grown on demand)
+    void *devcomm = nullptr;     // ncclDevComm (multimem handle), if created
+    bool devcomm_tried = false;
 };
 
 namespace sptk {
@@ -187,5 +208,7 @@ sptk_status host_rowptr(sptk_tensor t, int mode, cudaStream_t s);
 sptk_status comm_bcast_rows(sptk_comm c, void *buf, int64_t R, sptk_dtype dt,
                             const int64_t *bounds, cudaStream_t s);
 sptk_status comm_allreduce_f64(sptk_comm c, double *buf, int64_t count, cudaStream_t s);
+// grow c->sym to >= bytes (collective: every rank calls it with the same size)
+sptk_status comm_sym_reserve(sptk_comm c, size_t bytes, cudaStream_t s);
 
 }  // namespace sptk

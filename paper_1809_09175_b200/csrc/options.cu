@@ -38,6 +38,8 @@ constexpr OptDef kOpts[OPT_COUNT] = {
     {"no_graph", 0},            // CP-ALS: 1 disables the CUDA-graph replay
     {"gamma_inv_chol", 0},      // CP-ALS: 1 = Cholesky inverse instead of Gauss-Jordan
     {"use_copy", 1},            // 0: MTTKRP gathers through perm_n even where a copy exists
+    {"exchange", -1},           // sharded CP-ALS row exchange: -1 best available, 0 NCCL
+                                //   broadcast, 1 peer stores, 2 NVLS multimem stores
 };
 
 std::mutex g_mu;

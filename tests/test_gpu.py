@@ -675,15 +675,25 @@ def test_shard_local_copies(sp, G, dims, P):
         t.close()
 
 
-def test_sharded_code_path_one_rank(sp, monkeypatch):
-    """The N>1 code path (partition, per-rank launches, NCCL all-reduce and
-    grouped broadcasts) driven through a real 1-rank NCCL communicator with
-    SPTK_FORCE_SHARDED=1; results must match the oracle."""
+@pytest.mark.parametrize("exchange", [0, 1, -1])
+def test_sharded_code_path_one_rank(sp, monkeypatch, exchange):
+    """The N>1 code path (partition, per-rank launches, NCCL all-reduce, the
+    row exchange) driven through a real 1-rank NCCL communicator with
+    SPTK_FORCE_SHARDED=1; results must match the oracle.  exchange = 0: rows
+    replicated by grouped NCCL broadcasts; 1: the fused exchange, rows stored
+    by the apply kernel through the symmetric window's peer mapping (here the
+    rank's own copy seen through it); -1: the best the communicator supports
+    (NVLS multimem where available)."""
     monkeypatch.setenv("SPTK_FORCE_SHARDED", "1")
     try:
         comm = sp.comm_create(sp.comm_unique_id(), 1, 0)
     except sp.SptkError as e:
         pytest.skip(f"NCCL unavailable: {e}")
+    with sp.options(exchange=exchange):
+        _sharded_one_rank(sp, comm, exchange)
+
+
+def _sharded_one_rank(sp, comm, exchange):
     c = synth.CONFIGS["tiny"]
     idx, vals = synth.unique_tensor(c.seed, c.dims, c.nnz)
     R = 8
@@ -697,11 +707,24 @@ def test_sharded_code_path_one_rank(sp, monkeypatch):
         torch.cuda.synchronize()
         assert rel(out.cpu().numpy(), oracle.mttkrp(c.dims, idx, vals, A, n)) <= 1e-12
     F = [torch.empty(I, R, dtype=torch.float64, device="cuda") for I in c.dims]
-    res = sp.cp_als(t, R, 10, F, seed=c.seed_f, comm=comm)
+    lam = torch.empty(R, dtype=torch.float64, device="cuda")
+    res = sp.cp_als(t, R, 10, F, seed=c.seed_f, comm=comm, lambda_out=lam)
     ref = oracle.cp_als(c.dims, idx, vals, A, 10)
     assert np.max(np.abs(res["trace"] - ref["trace"])) <= 1e-9
     for m in range(3):
         assert rel(F[m].cpu().numpy(), ref["A"][m]) <= 1e-8
+    assert rel(lam.cpu().numpy(), ref["lam"]) <= 1e-8
+    mode = sp.comm_exchange(comm)
+    print(f"exchange option {exchange}: agreed mode {mode}")
+    if exchange >= 0:
+        assert mode <= exchange
+    # host factor buffers and a second call (the symmetric buffer is reused)
+    Fh = [np.zeros((I, R)) for I in c.dims]
+    res2 = sp.cp_als(t, R, 4, Fh, seed=c.seed_f, comm=comm)
+    ref2 = oracle.cp_als(c.dims, idx, vals, A, 4)
+    assert abs(res2["fit"] - ref2["fit"]) <= 1e-9
+    for m in range(3):
+        assert rel(Fh[m], ref2["A"][m]) <= 1e-8
     comm.close()
 
 
@@ -743,6 +766,39 @@ def test_cp_als_large_rank_tiled_glue(sp, R):
     assert np.max(np.abs(res["trace"] - ref["trace"])) <= 1e-8
     for m in range(3):
         assert rel(F[m].cpu().numpy(), ref["A"][m]) <= 1e-6
+
+
+@pytest.mark.parametrize("exchange", [0, 1])
+def test_sharded_zero_column_e1(sp, monkeypatch, exchange):
+    """A zero initial column through the sharded deferred path: every Gamma
+    is singular (ridge retry), lambda_j = 0 and column j becomes e_1 on every
+    replica -- the finalisation runs on each rank after the row exchange."""
+    monkeypatch.setenv("SPTK_FORCE_SHARDED", "1")
+    try:
+        comm = sp.comm_create(sp.comm_unique_id(), 1, 0)
+    except sp.SptkError as e:
+        pytest.skip(f"NCCL unavailable: {e}")
+    c = synth.CONFIGS["tiny"]
+    idx, vals = synth.unique_tensor(c.seed, c.dims, c.nnz)
+    R = 6
+    init = factors_np(c.seed_f, c.dims, R)
+    for a in init:
+        a[:, 2] = 0.0
+    t = make(sp, c.dims, idx, vals)
+    with sp.options(exchange=exchange):
+        A = [dev(a) for a in init]
+        lam = torch.empty(R, dtype=torch.float64, device="cuda")
+        res = sp.cp_als(t, R, 6, A, init=[dev(a) for a in init], lambda_out=lam, comm=comm)
+        ref = oracle.cp_als(c.dims, idx, vals, init, 6)
+        assert np.max(np.abs(res["trace"] - ref["trace"])) <= 1e-9
+        assert rel(lam.cpu().numpy(), ref["lam"]) <= 1e-8
+        for m in range(3):
+            assert rel(A[m].cpu().numpy(), ref["A"][m]) <= 1e-8
+        A1 = [dev(a) for a in init]
+        sp.cp_als(t, R, 1, A1, init=[dev(a) for a in init], comm=comm)
+        col = A1[0][:, 2].cpu().numpy()
+        assert col[0] == 1.0 and not col[1:].any()
+    comm.close()
 
 
 def test_cp_als_large_rank_sharded_path(sp, monkeypatch):

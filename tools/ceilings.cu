@@ -15,7 +15,12 @@
 //
 // Every number is useful bytes (or flops / ops) / best-of-5 CUDA-event time.
 // Output: one JSON object on stdout (bench.py reads profiles/ceilings.json).
-// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -o tools/ceilings tools/ceilings.cu
+//   tma_gather4_<loc>  the same random 128-byte rows fetched by TMA
+//                   (cp.async.bulk.tensor.2d ... tile::gather4: 4 rows per
+//                   instruction, one issuing lane per warp, S-stage smem ring
+//                   with mbarriers) -- the LSU-free gather path
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -o tools/ceilings tools/ceilings.cu -lcuda
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -84,6 +89,56 @@ __global__ void __launch_bounds__(256) gather_rows(const uint32_t *__restrict__ 
         for (int u = 0; u < U; ++u) ld32(A + (int64_t)row[u] * ROWD + q * 4, f[u], L1);
 #pragma unroll
         for (int u = 0; u < U; ++u) acc += (f[u][0] + f[u][1]) + (f[u][2] + f[u][3]);
+    }
+    if (acc == 1.2345) out[0] = acc;
+}
+
+// TMA gather4: lane 0 of each warp keeps S gather4 copies (4 rows each) in
+// flight into a per-warp smem ring; the warp reads one word of every landed
+// row set (checksum) before re-arming the slot
+template <int S>
+__global__ void __launch_bounds__(256) tma_gather4(const __grid_constant__ CUtensorMap tm,
+                                                   const uint32_t *__restrict__ idx, int64_t n,
+                                                   double *out) {
+    constexpr int kRowB = 128, kSet = 4 * kRowB;
+    extern __shared__ __align__(1024) uint8_t sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    uint8_t *ring = sm + (size_t)warp * S * kSet;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + (size_t)nw * S * kSet) + warp * S;
+    if (lane == 0)
+        for (int k = 0; k < S; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar + k)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    const int64_t gw = (blockIdx.x * (int64_t)nw + warp), tw = (int64_t)gridDim.x * nw;
+    const int64_t sets = n / 4;
+    double acc = 0;
+    int64_t it = 0;
+    for (int64_t q = gw; q < sets; q += tw, ++it) {
+        const int slot = (int)(it % S);
+        const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar + slot);
+        if (it >= S) {  // wait for the set issued S iterations ago, consume it
+            const uint32_t par = (uint32_t)((it / S - 1) & 1);
+            asm volatile("{\n\t.reg .pred p;\nW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W;\n\t}" ::"r"(b), "r"(par) : "memory");
+            acc += reinterpret_cast<const double *>(ring + slot * kSet)[lane * 2];
+            __syncwarp();
+        }
+        if (lane == 0) {
+            const uint4 r = *reinterpret_cast<const uint4 *>(idx + 4 * q);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kSet) : "memory");
+            asm volatile("cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+                         " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                         ::"r"((uint32_t)__cvta_generic_to_shared(ring + slot * kSet)), "l"(&tm), "r"(0),
+                           "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w), "r"(b) : "memory");
+        }
+        __syncwarp();
+    }
+    for (int64_t k = (it > S ? it - S : 0); k < it; ++k) {  // drain
+        const int slot = (int)(k % S);
+        const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar + slot);
+        const uint32_t par = (uint32_t)((k / S) & 1);
+        asm volatile("{\n\t.reg .pred p;\nW2: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W2;\n\t}" ::"r"(b), "r"(par) : "memory");
+        acc += reinterpret_cast<const double *>(ring + slot * kSet)[lane * 2];
     }
     if (acc == 1.2345) out[0] = acc;
 }
@@ -192,6 +247,41 @@ int main(int argc, char **argv) {
                 snprintf(what, sizeof what, "random %d B rows from a %.1f MB table, %s, ids streamed",
                          rb, tb.bytes / 1048576.0, l1 ? "L1-allocating" : "L1::no_allocate");
                 emit(key, (double)n * rb / ms / 1e6, "GB/s", what);
+            }
+        }
+    }
+    // ---- TMA gather4 of 128-byte rows (precomputed ids, as above)
+    {
+        const struct { const char *loc; int64_t bytes; } tt[] = {{"l2", (int64_t)6400 << 10},
+                                                               {"hbm", (int64_t)2200 << 20}};
+        for (auto &tb : tt) {
+            const int64_t rows = tb.bytes / 128;
+            for (int64_t k = 0; k < n; ++k) h[k] = (uint32_t)(raw[k] % (uint64_t)rows);
+            CK(cudaMemcpy(idx, h.data(), n * 4, cudaMemcpyHostToDevice));
+            CUtensorMap tm;
+            cuuint64_t gdim[2] = {16, (cuuint64_t)rows};
+            cuuint64_t gstr[1] = {128};
+            cuuint32_t box[2] = {16, 1}, es[2] = {1, 1};
+            CUresult r = cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, H, gdim, gstr,
+                                                box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                                CU_TENSOR_MAP_SWIZZLE_NONE,
+                                                CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) {
+                fprintf(stderr, "cuTensorMapEncodeTiled failed %d\n", (int)r);
+                continue;
+            }
+            constexpr int S = 8;
+            const size_t smb = 8 * (S * 512 + S * 8);
+            CK(cudaFuncSetAttribute(tma_gather4<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+            for (int bps : {2, 4, 6}) {
+                const double ms = best_ms([&] { tma_gather4<S><<<sms * bps, 256, smb>>>(tm, idx, n, out); });
+                CK(cudaGetLastError());
+                char key[64], what[160];
+                snprintf(key, sizeof key, "tma_gather4_%s_128_b%d", tb.loc, bps);
+                snprintf(what, sizeof what, "TMA tile::gather4 of random 128 B rows from a %.1f MB table, "
+                         "%d blocks/SM x 8 warps x %d sets in flight", tb.bytes / 1048576.0, bps, S);
+                emit(key, (double)n * 128 / ms / 1e6, "GB/s", what);
             }
         }
     }
