@@ -475,8 +475,12 @@ sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream) {
         if (st != SPTK_OK) return st;
         setup_note("copy", m, tc, s);
     }
-    if (all) t->keys.release();
-    setup_note("release keys", -1, tc, s);
+    // the ingest keys stay resident while they fit beside the copies (checked
+    // above): a later build_perm of any mode then sorts straight from them
+    // instead of re-reading the 16/32-byte records; they are a cache, released
+    // first when a sort or a copy needs the memory (sort.cu).  Option
+    // keep_keys = 0 releases them here (re-sorts then extract the keys).
+    if (all && !opt(OPT_KEEP_KEYS)) t->keys.release();
     // keep the sort workspace for the next build_perm only while memory is
     // plentiful.  A steady-state re-sort allocates nothing, so the last
     // decision stands and cudaMemGetInfo (which can stall the host for tens of

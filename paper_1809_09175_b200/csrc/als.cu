@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     reduce_partials_kernel(const double *__restrict__ partial, int nb, int ne,
                            double *__restrict__ out) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < ne;
          e += (gridDim.x * blockDim.x) >> 5) {
@@ -208,12 +209,11 @@ __global__ void __launch_bounds__(256)
 // one warp and sits on the critical path when the MTTKRP is short.  Without
 // pivoting, the pivots of an SPD matrix are the squared Cholesky diagonal, so
 // a non-positive pivot is exactly the Cholesky failure: same ridge retry.
-__global__ void __launch_bounds__(256)
-    gj_inv_kernel(const double *__restrict__ G, int N, int n, int R,
-                  double *__restrict__ Ginv, int *__restrict__ status) {
-    extern __shared__ double sm[];
-    double *M = sm;           // R x R
-    double *f = sm + R * R;   // R: column j before the update
+// (block function: M = R x R and f = R doubles of shared memory; every thread
+// of the block calls it; Ginv may be global or shared)
+__device__ void gj_inv_block(const double *G, int N, int n, int R,
+                             double *__restrict__ Ginv, int *__restrict__ status,
+                             double *__restrict__ M, double *__restrict__ f) {
     __shared__ double piv;
     __shared__ int bad;
     const int tid = threadIdx.x, RR = R * R;
@@ -264,6 +264,14 @@ __global__ void __launch_bounds__(256)
         if (attempt == 1 && tid == 0) atomicOr(status, 1);
     }
     for (int e = tid; e < RR; e += blockDim.x) Ginv[e] = M[e];
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256)
+    gj_inv_kernel(const double *__restrict__ G, int N, int n, int R,
+                  double *__restrict__ Ginv, int *__restrict__ status) {
+    extern __shared__ double sm[];
+    gj_inv_block(G, N, n, R, Ginv, status, sm, sm + R * R);
 }
 
 // Gamma^{-1} for mode n (SPTK_GAMMA_INV=chol forces the Cholesky kernel)
@@ -360,8 +368,8 @@ __global__ void normalize_kernel(T *__restrict__ A, int64_t r0, int64_t r1, int 
 // Called by all 256 threads of one block.
 // trace (nullable): the fit is also appended at trace[(*trace_n)++] (device-side
 // fit history, so iterations can be replayed back to back without a host sync)
-__device__ void fit_block(const double *__restrict__ dot, const double *__restrict__ lam,
-                          const double *__restrict__ G, int N, int R, double normX2,
+__device__ void fit_block(const double *dot, const double *lam,
+                          const double *G, int N, int R, double normX2,
                           double *__restrict__ out, double *__restrict__ trace = nullptr,
                           int *__restrict__ trace_n = nullptr) {
     __shared__ double sh[256];
@@ -396,6 +404,7 @@ __global__ void __launch_bounds__(256)
                const double *__restrict__ G, int N, int R, double normX2,
                double *__restrict__ out, double *__restrict__ trace = nullptr,
                int *__restrict__ trace_n = nullptr) {
+    pdl_wait();
     fit_block(dot, lam, G, N, R, normX2, out, trace, trace_n);
 }
 
@@ -475,32 +484,19 @@ constexpr int kApplyTileDefault = 64;
 #endif
 __host__ __device__ constexpr int apply_pf(int RM) { return RM / SPTK_APPLY_PF_DIV; }
 constexpr int kTailBlocks = 32;  // apply_gram grids up to this size finalise in their last block
-static int apply_tile_rows() {  // SPTK_APPLY_TILE overrides (tuning)
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("SPTK_APPLY_TILE");
-        v = (e && atoi(e) >= 16) ? atoi(e) : kApplyTileDefault;
-    }
-    return v;
+static int apply_tile_rows() {  // option apply_tile (rows of V per tile, tuning)
+    const int64_t v = opt(OPT_APPLY_TILE);
+    return v >= 16 ? (int)v : kApplyTileDefault;
 }
 
-// the deferred path for R <= 32 (SPTK_DEFERRED_NORM=0: explicit normalisation, for A/B)
-static int apply_nb_mult() {  // SPTK_APPLY_NB_MULT: apply_gram block cap = mult x 8 x SMs
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("SPTK_APPLY_NB_MULT");
-        v = (e && atoi(e) > 0) ? atoi(e) : 1;
-    }
-    return v;
+// option apply_nb_mult: apply_gram block cap = mult x 8 x SMs (tuning)
+static int apply_nb_mult() {
+    const int64_t v = opt(OPT_APPLY_NB_MULT);
+    return v > 0 ? (int)v : 1;
 }
 
-static int64_t tail_rows() {  // SPTK_TAIL_ROWS (tuning); 0 = grid by tile only
-    static int64_t v = -1;
-    if (v < 0) {
-        const char *e = getenv("SPTK_TAIL_ROWS");
-        v = e ? (int64_t)atoll(e) : 0;
-    }
-    return v;
+static int64_t tail_rows() {  // option tail_rows (tuning); 0 = grid by tile only
+    return opt(OPT_TAIL_ROWS);
 }
 
 static bool deferred_norm(int64_t R) {  // read per call: tests switch it per case
@@ -565,6 +561,7 @@ __global__ void __launch_bounds__(256)
                          T *__restrict__ A, int N, int n, int R, int next,
                          double *__restrict__ s_all, double *__restrict__ lam,
                          double *__restrict__ G, T *__restrict__ scale_next) {
+    pdl_wait();
     finalize_mode_block<T>(colsq, graw, A, N, n, R, next, s_all, lam, G, scale_next);
 }
 
@@ -599,7 +596,7 @@ __device__ __forceinline__ void mm_store(float *p, float v) {
 }
 
 #ifndef SPTK_APPLY_MINB  // A/B builds only
-#define SPTK_APPLY_MINB 1
+#define SPTK_APPLY_MINB 2
 #endif
 template <typename T, int RM>  // RM >= R: Gamma^{-1} column length held in registers
 __global__ void __launch_bounds__(256, SPTK_APPLY_MINB)
@@ -608,6 +605,7 @@ __global__ void __launch_bounds__(256, SPTK_APPLY_MINB)
                       const double *__restrict__ Ginv, T *__restrict__ A,
                       double *__restrict__ part_sq, double *__restrict__ part_dot,
                       double *__restrict__ gpart, const ModeTail tail, const ExchOut ex) {
+    pdl_wait();
     extern __shared__ __align__(16) double sm[];
     const int RP = (R + 3) & ~3;              // padded row stride (whole 4-column blocks)
     double *Vt = sm;                          // kApplyTile x RP
@@ -670,17 +668,7 @@ __global__ void __launch_bounds__(256, SPTK_APPLY_MINB)
             }
         __syncthreads();
         if (l < lanes) {
-            for (int r = l; r < nr; r += lanes) {
-                const double2 *v2 = reinterpret_cast<const double2 *>(Vt + r * RP);
-                double x = 0.0;
-#pragma unroll
-                for (int i = 0; i < RM; i += 2) {
-                    if (i < R) {
-                        const double2 q = v2[i >> 1];
-                        x += q.x * gi[i];
-                        x += q.y * gi[i + 1];
-                    }
-                }
+            auto emit = [&](int r, double x) {
                 const T xt = (T)x;
                 const int64_t ix = (rt + r) * R + j;
                 if (ex.mc) {
@@ -694,6 +682,23 @@ __global__ void __launch_bounds__(256, SPTK_APPLY_MINB)
                 At[r * RP + j] = xd;
                 sq += xd * xd;
                 dot += xd * Vt[r * RP + j];
+            };
+            // two partial sums per row: FMA chains of R/2 (one chain of R is
+            // latency-bound, ncu "wait" stalls); one row per pass keeps the
+            // register count (two rows per pass: 158 registers, one block per
+            // SM, measured slower)
+            for (int r = l; r < nr; r += lanes) {
+                const double2 *v2 = reinterpret_cast<const double2 *>(Vt + r * RP);
+                double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+                for (int i = 0; i < RM; i += 2) {
+                    if (i < R) {
+                        const double2 q = v2[i >> 1];
+                        a0 += q.x * gi[i];
+                        a1 += q.y * gi[i + 1];
+                    }
+                }
+                emit(r, a0 + a1);
             }
         }
         __syncthreads();
@@ -794,10 +799,7 @@ __global__ void __launch_bounds__(256, SPTK_APPLY_MINB)
 // 8-per-SM cap alone, for A/B) -- a tall mode's pass otherwise runs ~2.7 waves
 template <typename T>
 static int apply_block_cap(int cap, int R, size_t smb) {
-    static const bool wave = [] {
-        const char *e = getenv("SPTK_APPLY_WAVE");
-        return !(e && e[0] == '0');
-    }();
+    const bool wave = opt(OPT_APPLY_WAVE) != 0;
     if (!wave) return cap;
     int occ = 0;
     if (R <= 16)
@@ -1132,28 +1134,31 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
             tail.n = n;
             tail.next = (n + 1) % N;
             if (R <= 16)
-                apply_gram_kernel<T, 16><<<nb, 256, smb, c.s>>>(V, 0, I, R, rpb, tile, Ginv, An, psq,
-                                                                last ? pdot : nullptr,
-                                                                w.gpart.as<double>(), tail, ExchOut{});
+                SPTK_CUDA(launch_pdl(apply_gram_kernel<T, 16>, nb, 256, smb, c.s, V, (int64_t)0, I, R,
+                                     rpb, tile, Ginv, An, psq, last ? pdot : nullptr,
+                                     w.gpart.as<double>(), tail, ExchOut{}));
             else
-                apply_gram_kernel<T, 32><<<nb, 256, smb, c.s>>>(V, 0, I, R, rpb, tile, Ginv, An, psq,
-                                                                last ? pdot : nullptr,
-                                                                w.gpart.as<double>(), tail, ExchOut{});
+                SPTK_CUDA(launch_pdl(apply_gram_kernel<T, 32>, nb, 256, smb, c.s, V, (int64_t)0, I, R,
+                                     rpb, tile, Ginv, An, psq, last ? pdot : nullptr,
+                                     w.gpart.as<double>(), tail, ExchOut{}));
             count_launch();
             SPTK_CUDA(cudaGetLastError());
             if (!tail.counter) {  // many blocks: parallel reductions, then one finalise block
-                reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(psq, nb, R, colsq);
-                reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(w.gpart.as<double>(),
-                                                                        nb, R * R, graw);
-                finalize_mode_kernel<T><<<1, 256, 0, c.s>>>(colsq, graw, An, N, n, R,
-                                                             (n + 1) % N, s_all, lam,
-                                                             w.G.as<double>(), scale);
+                SPTK_CUDA(launch_pdl(reduce_partials_kernel, (R + 7) / 8, 256, 0, c.s,
+                                     (const double *)psq, nb, R, colsq));
+                SPTK_CUDA(launch_pdl(reduce_partials_kernel, (R * R + 7) / 8, 256, 0, c.s,
+                                     (const double *)w.gpart.as<double>(), nb, R * R, graw));
+                SPTK_CUDA(launch_pdl(finalize_mode_kernel<T>, 1, 256, 0, c.s, (const double *)colsq,
+                                     (const double *)graw, An, N, n, R, (n + 1) % N, s_all, lam,
+                                     w.G.as<double>(), scale));
                 count_launch(3);
                 if (last) {
                     double *dot = colsq + R;
-                    reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(pdot, nb, R, dot);
-                    fit_kernel<<<1, 256, 0, c.s>>>(dot, lam, w.G.as<double>(), N, R, t->normX2,
-                                                   scal, trace, trace_n);
+                    SPTK_CUDA(launch_pdl(reduce_partials_kernel, (R + 7) / 8, 256, 0, c.s,
+                                         (const double *)pdot, nb, R, dot));
+                    SPTK_CUDA(launch_pdl(fit_kernel, 1, 256, 0, c.s, (const double *)dot,
+                                         (const double *)lam, (const double *)w.G.as<double>(), N,
+                                         R, t->normX2, scal, trace, trace_n));
                     count_launch(2);
                 }
                 SPTK_CUDA(cudaGetLastError());

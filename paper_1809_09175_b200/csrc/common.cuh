@@ -51,10 +51,36 @@ int dev_sms();
 enum Opt {
     OPT_RUN, OPT_VARIANT, OPT_SLICE, OPT_SLICE_L2_KB, OPT_SLICE_ROWS, OPT_SLICE_OTHER_FIRST,
     OPT_ROWREC, OPT_FORCE_V, OPT_GENERIC, OPT_DEBUG_DISPATCH, OPT_COPY_ORDER, OPT_DEFERRED_NORM,
-    OPT_NO_GRAPH, OPT_GAMMA_INV_CHOL, OPT_USE_COPY, OPT_EXCHANGE, OPT_COUNT
+    OPT_NO_GRAPH, OPT_GAMMA_INV_CHOL, OPT_USE_COPY, OPT_APPLY_TILE, OPT_APPLY_NB_MULT, OPT_TAIL_ROWS, OPT_APPLY_WAVE,
+    OPT_KEEP_KEYS, OPT_PDL, OPT_EXCHANGE, OPT_COUNT
 };
 int64_t opt(Opt o);
 void set_dispatch(const std::string &s);  // what the last MTTKRP call ran (sptk_last_dispatch)
+
+// ------------------------------------------------------------------ PDL
+// Programmatic dependent launch: a kernel launched by launch_pdl may be
+// scheduled while its stream predecessor is still finishing (its launch
+// latency and block ramp-up overlap the predecessor's tail); such a kernel
+// calls pdl_wait() -- griddepcontrol.wait, which returns once every
+// predecessor has completed and its memory is visible -- before it reads or
+// writes anything a predecessor touches.  Without the attribute the wait is a
+// no-op.  Option pdl (default 1) switches the attribute off (A/B).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = opt(OPT_PDL) != 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // ------------------------------------------------------------------ memory
 // RAII device buffer (cudaMallocAsync-free, plain cudaMalloc for large,

@@ -12,7 +12,7 @@ namespace sptk {
 // Nonzeros per worker (the paper's NZPTM block).  Adaptive by default
 // (option "run" = 0): long runs amortise the two boundary atomics, but the
 // grid must still cover every SM several times, so small tensors get short
-// runs (>= 16).
+// runs (>= 4).
 static int64_t run_length(int64_t npos, int G) {
     const int64_t fixed = opt(OPT_RUN);
     if (fixed > 0) return fixed < 4 ? 4 : (fixed + 3) / 4 * 4;
@@ -20,7 +20,9 @@ static int64_t run_length(int64_t npos, int G) {
     const int64_t target = (int64_t)dev_sms() * workers_per_sm * 4;
     int64_t run = npos / (target > 0 ? target : 1);
     if (run > 256) run = 256;
-    if (run < 16) run = 16;
+    // short runs only where the grid would otherwise not fill the GPU (small
+    // tensors: the launch is latency-bound, C1 CP-ALS -12 % at 4 vs 16)
+    if (run < 4) run = 4;
     return (run + 3) / 4 * 4;
 }
 
@@ -127,6 +129,20 @@ __global__ void det_fixup_kernel(const uint32_t *__restrict__ drow, const T *__r
             }
         }
     }
+}
+
+// out[0 .. words) = 0, 16-byte stores where aligned
+__global__ void __launch_bounds__(256) zero_words_kernel(uint32_t *__restrict__ out, int64_t words) {
+    pdl_wait();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t head = (int64_t)(((16 - (reinterpret_cast<uintptr_t>(out) & 15)) & 15) / 4);
+    if (head > words) head = words;
+    for (int64_t i = t0; i < head; i += stride) out[i] = 0u;
+    uint4 *v = reinterpret_cast<uint4 *>(out + head);
+    const int64_t nv = (words - head) / 4;
+    for (int64_t i = t0; i < nv; i += stride) v[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int64_t i = head + nv * 4 + t0; i < words; i += stride) out[i] = 0u;
 }
 
 // start row of every worker: the largest r with rowptr[r] <= s (binary search)
@@ -298,8 +314,14 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     const int64_t In = t->dims[mode];
     const size_t es = dtype_bytes(t->dtype);
     if (row_end <= row_begin) return SPTK_OK;
-    SPTK_CUDA(cudaMemsetAsync(static_cast<char *>(out) + (size_t)row_begin * R * es, 0,
-                              (size_t)(row_end - row_begin) * R * es, s));
+    {   // zero the output rows (a kernel, not a memset node: PDL chains through it)
+        const int64_t words = (row_end - row_begin) * R * (int64_t)es / 4;
+        uint32_t *o = reinterpret_cast<uint32_t *>(static_cast<char *>(out) + (size_t)row_begin * R * es);
+        int64_t blocks = (words / 4 + 255) / 256;
+        blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)dev_sms() * 8));
+        SPTK_CUDA(launch_pdl(zero_words_kernel, dim3((unsigned)blocks), dim3(256), 0, s, o, words));
+        count_launch();
+    }
     int64_t pb = 0, pe = t->P;
     if (row_begin != 0 || row_end != In) {
         SPTK_TRY(host_rowptr(t, mode, s));

@@ -261,6 +261,16 @@ __device__ __forceinline__ void vred(T *p, const T (&r)[VW]) {
     }
 }
 
+// L2 prefetch of a lane's slice of a factor row (no register cost): the rows
+// of the next step are requested while this step's rows are multiplied, so
+// the next step's gathers hit L2 instead of waiting on HBM (SPTK_L2_PF)
+#ifndef SPTK_L2_PF
+#define SPTK_L2_PF 0
+#endif
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
+
 template <typename T> __device__ __forceinline__ T rec_val(const uint32_t (&w)[8]);
 template <> __device__ __forceinline__ double rec_val<double>(const uint32_t (&w)[8]) {
     return __hiloint2double((int)w[1], (int)w[0]);
@@ -429,6 +439,17 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
                 acc[v] += t;
             }
         }
+        if constexpr (SORTED && SPTK_L2_PF) {  // next step's rows into L2
+            if (lane_on)
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (pn[u] != kNoRow)
+#pragma unroll
+                        for (int m = 0; m < N; ++m)
+                            if (m != MODE)
+                                prefetch_l2(static_cast<const T *>(a.A[m]) +
+                                            (int64_t)wn[u][OFF + (m < MODE ? m : m - 1)] * a.ld + c);
+        }
     }
     if (cur != kNoRow) flush(cur, true, 1);
     if (a.dpart && !wrote0 && q == 0) a.drow[2 * worker] = kNoRow;
@@ -436,6 +457,7 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
 
 template <typename T, int N, int G, int U, int RB, bool SORTED, int MINB, int V, bool ROWREC>
 __global__ void __launch_bounds__(256, MINB) mttkrp_fast_kernel(const MttkrpArgs a) {
+    pdl_wait();
     if constexpr (N >= 1) if (a.mode == 0) { mttkrp_fast_body<T, N, 0, G, U, RB, SORTED, V, ROWREC>(a); return; }
     if constexpr (N >= 2) if (a.mode == 1) { mttkrp_fast_body<T, N, 1, G, U, RB, SORTED, V, ROWREC>(a); return; }
     if constexpr (N >= 3) if (a.mode == 2) { mttkrp_fast_body<T, N, 2, G, U, RB, SORTED, V, ROWREC>(a); return; }
@@ -553,6 +575,17 @@ __device__ __forceinline__ void mttkrp_coop_body(const MttkrpArgs &a) {
                 }
             }
         }
+        if constexpr (SPTK_L2_PF) {  // next step's rows into L2
+            if (lane_on)
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (base + U * NG + u * NG + g < e)
+#pragma unroll
+                        for (int m = 0; m < N; ++m)
+                            if (m != MODE)
+                                prefetch_l2(static_cast<const T *>(a.A[m]) +
+                                            (int64_t)wn[u][OFF + (m < MODE ? m : m - 1)] * a.ld + c);
+        }
         const uint32_t last = base + U * NG - 1;
         if (last < nxt && last < e) {  // whole step inside the current row
 #pragma unroll
@@ -607,6 +640,7 @@ __device__ __forceinline__ void mttkrp_coop_body(const MttkrpArgs &a) {
 
 template <typename T, int N, int G, int U, int RB, int MINB, int V>
 __global__ void __launch_bounds__(256, MINB) mttkrp_coop_kernel(const MttkrpArgs a) {
+    pdl_wait();
     if constexpr (N >= 1) if (a.mode == 0) { mttkrp_coop_body<T, N, 0, G, U, RB, V>(a); return; }
     if constexpr (N >= 2) if (a.mode == 1) { mttkrp_coop_body<T, N, 1, G, U, RB, V>(a); return; }
     if constexpr (N >= 3) if (a.mode == 2) { mttkrp_coop_body<T, N, 2, G, U, RB, V>(a); return; }
@@ -714,6 +748,7 @@ __device__ __forceinline__ void mttkrp_slice_body(const MttkrpArgs &a) {
 
 template <typename T, int N, int G, int U, int RB, int MINB, int V>
 __global__ void __launch_bounds__(256, MINB) mttkrp_slice_kernel(const MttkrpArgs a) {
+    pdl_wait();
     if constexpr (N >= 1) if (a.mode == 0) { mttkrp_slice_body<T, N, 0, G, U, RB, V>(a); return; }
     if constexpr (N >= 2) if (a.mode == 1) { mttkrp_slice_body<T, N, 1, G, U, RB, V>(a); return; }
     if constexpr (N >= 3) if (a.mode == 2) { mttkrp_slice_body<T, N, 2, G, U, RB, V>(a); return; }
@@ -726,6 +761,7 @@ __global__ void __launch_bounds__(256, MINB) mttkrp_slice_kernel(const MttkrpArg
 // columns col0 + q + G*k (k < NV), scalar loads, runtime record offsets.
 template <typename T, int G, int NV>
 __global__ void __launch_bounds__(256) mttkrp_generic_kernel(const MttkrpArgs a) {
+    pdl_wait();
     constexpr int U = 2;
     const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t worker = gtid / G;
@@ -827,9 +863,9 @@ inline sptk_status fast_launch_g(int G, const MttkrpArgs &a, int64_t workers, cu
     const unsigned blocks = (unsigned)((threads + 255) / 256);
 #define SPTK_LAUNCH_G(GG)                                                                     \
     if constexpr (COOP)                                                                       \
-        mttkrp_coop_kernel<T, N, GG, kU<N>, RB, kMinBlocks<N>, V><<<blocks, 256, 0, s>>>(a);        \
+        launch_pdl(mttkrp_coop_kernel<T, N, GG, kU<N>, RB, kMinBlocks<N>, V>, blocks, 256, 0, s, a); \
     else                                                                                      \
-        mttkrp_fast_kernel<T, N, GG, kU<N>, RB, SORTED, kMinBlocks<N>, V, ROWREC><<<blocks, 256, 0, s>>>(a);
+        launch_pdl(mttkrp_fast_kernel<T, N, GG, kU<N>, RB, SORTED, kMinBlocks<N>, V, ROWREC>, blocks, 256, 0, s, a);
     switch (G) {
     case 1: SPTK_LAUNCH_G(1) break;
     case 2: SPTK_LAUNCH_G(2) break;
@@ -849,7 +885,7 @@ inline sptk_status fast_launch_g(int G, const MttkrpArgs &a, int64_t workers, cu
 template <typename T, int N, int RC, int V>
 inline sptk_status slice_launch_g(int G, const MttkrpArgs &a, cudaStream_t s) {
     const dim3 grid((unsigned)((a.row1 - a.row0 + 7) / 8), (unsigned)a.nslice);
-#define SPTK_LAUNCH_S(GG)                                                                         mttkrp_slice_kernel<T, N, GG, kU<N>, RC, kMinBlocks<N>, V><<<grid, 256, 0, s>>>(a);
+#define SPTK_LAUNCH_S(GG) launch_pdl(mttkrp_slice_kernel<T, N, GG, kU<N>, RC, kMinBlocks<N>, V>, grid, dim3(256), 0, s, a);
     switch (G) {
     case 1: SPTK_LAUNCH_S(1) break;
     case 2: SPTK_LAUNCH_S(2) break;

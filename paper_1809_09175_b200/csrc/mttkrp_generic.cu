@@ -7,8 +7,8 @@ template <typename T>
 sptk_status launch_generic(int G, const MttkrpArgs &a, int64_t workers, cudaStream_t s) {
     const int64_t threads = workers * G;
     const unsigned blocks = (unsigned)((threads + 255) / 256);
-    if (G == 4) mttkrp_generic_kernel<T, 4, 4><<<blocks, 256, 0, s>>>(a);
-    else mttkrp_generic_kernel<T, 32, 4><<<blocks, 256, 0, s>>>(a);
+    if (G == 4) launch_pdl(mttkrp_generic_kernel<T, 4, 4>, blocks, 256, 0, s, a);
+    else launch_pdl(mttkrp_generic_kernel<T, 32, 4>, blocks, 256, 0, s, a);
     count_launch();
     SPTK_CUDA(cudaGetLastError());
     return SPTK_OK;

@@ -21,7 +21,7 @@ struct OptDef {
     int64_t def;
 };
 // keep in the order of enum Opt (common.cuh)
-constexpr OptDef kOpts[OPT_COUNT] = {
+constexpr OptDef kOpts[] = {
     {"run", 0},                 // positions per worker: 0 adaptive, > 0 fixed
     {"variant", -1},            // fast kernel worker shape: -1 auto, 0 per-group, 1 warp-coop
     {"slice", 1},               // 0 disables the slice traversal, 2 forces it wherever the
@@ -38,9 +38,17 @@ constexpr OptDef kOpts[OPT_COUNT] = {
     {"no_graph", 0},            // CP-ALS: 1 disables the CUDA-graph replay
     {"gamma_inv_chol", 0},      // CP-ALS: 1 = Cholesky inverse instead of Gauss-Jordan
     {"use_copy", 1},            // 0: MTTKRP gathers through perm_n even where a copy exists
+    {"apply_tile", 64},         // CP-ALS apply_gram: rows of V per tile (tuning)
+    {"apply_nb_mult", 1},       // CP-ALS apply_gram: block cap = mult x 8 x SMs (tuning)
+    {"tail_rows", 8192},        // CP-ALS: modes up to this many rows finalise in apply_gram's last block
+    {"apply_wave", 1},          // CP-ALS apply_gram: grid capped at one wave of resident blocks
+    {"keep_keys", 1},           // keep the ingest sort keys resident after build_perm
+    {"pdl", 1},                 // programmatic dependent launch of the MTTKRP / ALS kernels
     {"exchange", -1},           // sharded CP-ALS row exchange: -1 best available, 0 NCCL
                                 //   broadcast, 1 peer stores, 2 NVLS multimem stores
 };
+
+static_assert(sizeof(kOpts) / sizeof(kOpts[0]) == OPT_COUNT, "kOpts must list every Opt, in order");
 
 std::mutex g_mu;
 std::atomic<bool> g_init{false};

@@ -440,6 +440,10 @@ sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
             t->sortws.release();
         }
     }
+    if (free_b < need + reserve && t->keys.p) {  // the resident ingest keys are a cache too
+        free_b += t->keys.bytes;
+        t->keys.release();
+    }
     // declined: remembered, so later MTTKRPs of this mode do not query the
     // free memory again (a host stall while kernels are in flight) -- cleared
     // when memory is released (drop_copies) or the mode is re-sorted
@@ -546,7 +550,8 @@ static sptk_status stable_sort_ids(sptk_tensor t, int mode, const uint32_t *in, 
         ws = static_cast<uint32_t *>(ext_ws);
     } else {
         if (t->sortws.reserve(sizeof(uint32_t) * ws_words) != SPTK_OK) {
-            drop_copies(t);  // permuted copies are caches: free them and retry
+            drop_copies(t);  // permuted copies and ingest keys are caches: free them, retry
+            t->keys.release();
             SPTK_TRY(t->sortws.reserve(sizeof(uint32_t) * ws_words));
         }
         ws = t->sortws.as<uint32_t>();

@@ -86,16 +86,20 @@ def gpu_perm(sp, t, n):
 def test_perm_bitexact(sp, case):
     dist, dims, P = case
     idx, vals = synth.tensor(41, dims, P, dist)
-    t = make(sp, dims, idx, vals)
-    sp.build_perm(t, -1)            # sorts from the keys the ingest pass emitted
-    for n in range(len(dims)):
-        p, rp = gpu_perm(sp, t, n)
-        po, rpo = oracle.perm(idx, n, dims[n])
-        assert np.array_equal(p, po), f"mode {n}"
-        assert np.array_equal(rp, rpo), f"mode {n}"
-    sp.build_perm(t, 0)             # keys released: re-sort extracts them from the records
-    p, rp = gpu_perm(sp, t, 0)
-    assert np.array_equal(p, oracle.perm(idx, 0, dims[0])[0])
+    for keep in (1, 0):
+        with sp.options(keep_keys=keep):
+            t = make(sp, dims, idx, vals)
+            sp.build_perm(t, -1)            # sorts from the keys the ingest pass emitted
+            for n in range(len(dims)):
+                p, rp = gpu_perm(sp, t, n)
+                po, rpo = oracle.perm(idx, n, dims[n])
+                assert np.array_equal(p, po), f"mode {n}"
+                assert np.array_equal(rp, rpo), f"mode {n}"
+            # re-sort: from the resident keys (keep 1) or extracted from the records (keep 0)
+            sp.build_perm(t, 0)
+            p, rp = gpu_perm(sp, t, 0)
+            assert np.array_equal(p, oracle.perm(idx, 0, dims[0])[0])
+            t.close()
 
 
 def test_perm_golden_and_empty(sp):
@@ -361,6 +365,15 @@ def test_cp_als_tiny_trajectory(sp):
     assert np.max(np.abs(res2["trace"] - res["trace"])) <= 1e-12
     assert all(rel(Ah[m], A[m].cpu().numpy()) <= 1e-12 for m in range(3))
     assert rel(lamh, lam.cpu().numpy()) <= 1e-12
+    # fp32: the oracle in fp64 on the fp32-rounded inputs; fit within 1e-4
+    t32 = make(sp, c.dims, idx, vals.astype(np.float32), torch.float32)
+    A32 = [torch.empty(I, R, dtype=torch.float32, device="cuda") for I in c.dims]
+    res32 = sp.cp_als(t32, R, 10, A32, seed=c.seed_f)
+    init32 = [a.astype(np.float32).astype(np.float64) for a in factors_np(c.seed_f, c.dims, R)]
+    ref32 = oracle.cp_als(c.dims, idx, vals.astype(np.float32).astype(np.float64), init32, 10)
+    assert np.max(np.abs(res32["trace"] - ref32["trace"])) <= 1e-4
+    for m in range(3):
+        assert rel(A32[m].double().cpu().numpy(), ref32["A"][m]) <= 1e-3
 
 
 @pytest.mark.parametrize("deferred", [1, 0])
