@@ -261,16 +261,6 @@ __device__ __forceinline__ void vred(T *p, const T (&r)[VW]) {
     }
 }
 
-// L2 prefetch of a lane's slice of a factor row (no register cost): the rows
-// of the next step are requested while this step's rows are multiplied, so
-// the next step's gathers hit L2 instead of waiting on HBM (SPTK_L2_PF)
-#ifndef SPTK_L2_PF
-#define SPTK_L2_PF 0
-#endif
-__device__ __forceinline__ void prefetch_l2(const void *p) {
-    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
-}
-
 template <typename T> __device__ __forceinline__ T rec_val(const uint32_t (&w)[8]);
 template <> __device__ __forceinline__ double rec_val<double>(const uint32_t (&w)[8]) {
     return __hiloint2double((int)w[1], (int)w[0]);
@@ -439,17 +429,6 @@ __device__ __forceinline__ void mttkrp_fast_body(const MttkrpArgs &a) {
                 acc[v] += t;
             }
         }
-        if constexpr (SORTED && SPTK_L2_PF) {  // next step's rows into L2
-            if (lane_on)
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (pn[u] != kNoRow)
-#pragma unroll
-                        for (int m = 0; m < N; ++m)
-                            if (m != MODE)
-                                prefetch_l2(static_cast<const T *>(a.A[m]) +
-                                            (int64_t)wn[u][OFF + (m < MODE ? m : m - 1)] * a.ld + c);
-        }
     }
     if (cur != kNoRow) flush(cur, true, 1);
     if (a.dpart && !wrote0 && q == 0) a.drow[2 * worker] = kNoRow;
@@ -574,17 +553,6 @@ __device__ __forceinline__ void mttkrp_coop_body(const MttkrpArgs &a) {
                     t[u][v] = p;
                 }
             }
-        }
-        if constexpr (SPTK_L2_PF) {  // next step's rows into L2
-            if (lane_on)
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (base + U * NG + u * NG + g < e)
-#pragma unroll
-                        for (int m = 0; m < N; ++m)
-                            if (m != MODE)
-                                prefetch_l2(static_cast<const T *>(a.A[m]) +
-                                            (int64_t)wn[u][OFF + (m < MODE ? m : m - 1)] * a.ld + c);
         }
         const uint32_t last = base + U * NG - 1;
         if (last < nxt && last < e) {  // whole step inside the current row

@@ -1,7 +1,5 @@
-set -x
-nproc; free -g; nvidia-smi --query-gpu=name,memory.total,clocks.max.sm --format=csv
-python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/r2_smoke.log 2>&1
-python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/r2_bench0.json 2> gpurun_out/r2_bench0.err
-python bench.py --config delicious --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r2_bench_del.json 2> gpurun_out/r2_bench_del.err
-python bench.py --config lbnl --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/r2_bench_lbnl.json 2>&1
-python bench.py --config tiny --rank 8 --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/r2_bench_tiny.json 2>&1
+python -c "import paper_1809_09175_b200 as sp; print(sp.version())" > gpurun_out/fb_build.log 2>&1
+for k in 1 2 3; do python tools/first_build.py nell2 1; done > gpurun_out/fb_lazy.log 2>&1
+for k in 1 2 3; do CUDA_MODULE_LOADING=EAGER python tools/first_build.py nell2 1; done > gpurun_out/fb_eager.log 2>&1
+python tools/first_build.py nell2 3 > gpurun_out/fb_same.log 2>&1
+python tools/als_sweep.py tiny 8 f64 "" "run=16" "run=4" > gpurun_out/fb_tiny.log 2>&1
