@@ -279,6 +279,36 @@ using namespace sptk;
         if ((t)->poisoned) return fail(SPTK_ECUDA, "tensor handle poisoned by an earlier CUDA error"); \
     } while (0)
 
+namespace sptk {
+size_t owned_bytes(sptk_tensor t) {
+    size_t b = t->rec.bytes;
+    for (int m = 0; m < t->N; ++m)
+        b += t->perm[m].bytes + t->rowptr[m].bytes + t->srec[m].bytes + t->wrow[m].bytes +
+             t->soff[m].bytes;
+    b += t->sortws.bytes + t->keys.bytes + t->det_row.bytes + t->det_part.bytes;
+    const ALSWork &w = t->als;
+    b += w.V.bytes + w.G.bytes + w.L.bytes + w.partial.bytes + w.colsq.bytes + w.lam.bytes +
+         w.scal.bytes + w.stage.bytes + w.lamT.bytes + w.gpart.bytes + w.trace.bytes + w.scl.bytes;
+    return b;
+}
+
+bool device_free(sptk_tensor t, size_t *free_b, size_t *total_b) {
+    if (t->ledger) {
+        const size_t owned = owned_bytes(t);
+        const size_t grew = owned > t->ledger_owned0 ? owned - t->ledger_owned0 : 0;
+        const size_t shrank = owned < t->ledger_owned0 ? t->ledger_owned0 - owned : 0;
+        *free_b = t->ledger_free0 + shrank - std::min(t->ledger_free0 + shrank, grew);
+        *total_b = t->ledger_total;
+        return true;
+    }
+    if (cudaMemGetInfo(free_b, total_b) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return true;
+}
+}  // namespace sptk
+
 extern "C" {
 
 const char *sptk_version(void) { return "sptk 0.1 sm_100a"; }
@@ -393,16 +423,10 @@ sptk_status sptk_sptensor_info(sptk_tensor t, int *nmodes, int64_t *dims, int64_
     return SPTK_OK;
 }
 
+
 sptk_status sptk_sptensor_device_bytes(sptk_tensor t, int64_t *bytes) {
     if (!t || !bytes) return fail(SPTK_EINVAL, "null argument");
-    int64_t b = t->rec.bytes;
-    for (int m = 0; m < t->N; ++m)
-        b += t->perm[m].bytes + t->rowptr[m].bytes + t->srec[m].bytes + t->wrow[m].bytes;
-    b += t->sortws.bytes + t->keys.bytes;
-    const ALSWork &w = t->als;
-    b += w.V.bytes + w.G.bytes + w.L.bytes + w.partial.bytes + w.colsq.bytes + w.lam.bytes +
-         w.scal.bytes + w.stage.bytes + w.lamT.bytes;
-    *bytes = b;
+    *bytes = (int64_t)owned_bytes(t);
     return SPTK_OK;
 }
 
@@ -443,6 +467,17 @@ sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     const int m0 = mode < 0 ? 0 : mode, m1 = mode < 0 ? t->N : mode + 1;
     double tc = setup_clock(s);
+    // one memory query, while the GPU is idle; the rest of the call keeps a ledger
+    struct LedgerScope {
+        sptk_tensor t;
+        ~LedgerScope() { t->ledger = false; }
+    } ledger_scope{t};
+    if (cudaMemGetInfo(&t->ledger_free0, &t->ledger_total) == cudaSuccess) {
+        t->ledger_owned0 = owned_bytes(t);
+        t->ledger = true;
+    } else {
+        cudaGetLastError();
+    }
     // what this call may allocate: the sort workspace, copies, (released) keys
     const void *ws0 = t->sortws.p;
     const size_t ws_bytes0 = t->sortws.bytes;
@@ -461,10 +496,7 @@ sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream) {
         // they also speed up the copies' secondary sorts; keep them through
         // the copies only if every copy (+ its order buffer) fits beside them
         size_t free_b = 0, total_b = 0;
-        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
-            cudaGetLastError();
-            free_b = 0;
-        }
+        if (!device_free(t, &free_b, &total_b)) free_b = 0;
         const size_t copies = (size_t)(m1 - m0) * (compact_bytes(t->dtype, t->N) + 4) * t->P;
         if (free_b < copies + std::max<size_t>(total_b / 32, (size_t)4 << 30)) t->keys.release();
     }
@@ -483,19 +515,15 @@ sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream) {
     if (all && !opt(OPT_KEEP_KEYS)) t->keys.release();
     // keep the sort workspace for the next build_perm only while memory is
     // plentiful.  A steady-state re-sort allocates nothing, so the last
-    // decision stands and cudaMemGetInfo (which can stall the host for tens of
-    // ms while the sort is in flight: profiles/r01/perm_timing_async.log) is skipped.
+    // decision stands (the ledger replaces cudaMemGetInfo, which can stall the
+    // host for tens of ms while the sort is in flight: profiles/r01/perm_timing_async.log).
     int copies1 = 0;
     for (int m = 0; m < t->N; ++m) copies1 += t->has_srec[m] ? 1 : 0;
     const bool allocated = t->sortws.p != ws0 || t->sortws.bytes != ws_bytes0 ||
                            copies1 != copies0 || keys0 != (t->keys.p != nullptr);
     size_t free_b = 0, total_b = 0;
     if (!t->sortws.p || !allocated) return SPTK_OK;
-    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-        if (free_b < total_b / 4) t->sortws.release();
-    } else {
-        cudaGetLastError();
-    }
+    if (device_free(t, &free_b, &total_b) && free_b < total_b / 4) t->sortws.release();
     return SPTK_OK;
 }
 

@@ -163,6 +163,12 @@ struct sptk_tensor_s {
     bool perm_gather_only = false;              // SPTK_CREATE_PERM_GATHER
     std::vector<uint32_t> host_rowptr[sptk::kMaxModes];  // for partitioning (lazy)
     double normX2 = 0.0;
+    // memory ledger of one build_perm call: the free device memory is queried
+    // once when the call starts (the GPU is idle then) and afterwards estimated
+    // from what the handle itself allocates or releases -- cudaMemGetInfo with
+    // kernels in flight stalls the host for milliseconds
+    bool ledger = false;
+    size_t ledger_free0 = 0, ledger_total = 0, ledger_owned0 = 0;
     bool poisoned = false;
     int device = 0;
     sptk::ALSWork als;
@@ -231,6 +237,9 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
                           const void *lambda, void *out, int64_t row_begin, int64_t row_end,
                           cudaStream_t s);
 sptk_status host_rowptr(sptk_tensor t, int mode, cudaStream_t s);
+size_t owned_bytes(sptk_tensor t);  // device bytes held by the handle
+// free / total device memory: from the ledger inside build_perm, else queried
+bool device_free(sptk_tensor t, size_t *free_b, size_t *total_b);
 sptk_status comm_bcast_rows(sptk_comm c, void *buf, int64_t R, sptk_dtype dt,
                             const int64_t *bounds, cudaStream_t s);
 sptk_status comm_allreduce_f64(sptk_comm c, double *buf, int64_t count, cudaStream_t s);

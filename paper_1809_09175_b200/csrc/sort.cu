@@ -411,10 +411,7 @@ sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
     const int rc = compact_bytes(t->dtype, t->N);
     const size_t need = (size_t)rc * (size_t)std::max<int64_t>(p1 - p0, 1);
     size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
-        cudaGetLastError();
-        return SPTK_OK;
-    }
+    if (!device_free(t, &free_b, &total_b)) return SPTK_OK;
     const size_t reserve = std::max<size_t>(total_b / 32, (size_t)4 << 30);
     int a = copy_secondary_mode(t, mode);
     if (a >= 0 && !t->has_perm[a]) a = -1;
