@@ -297,8 +297,8 @@ sptk_status sptk_set_tuning(int variant, int64_t run);
  *   copy_order 1 (0: permuted copies in perm_n order), deferred_norm 1,
  *   no_graph 0, gamma_inv_chol 0, use_copy 1 (0: gather the records through
  *   perm_n, the paper's traversal, even where a permuted copy exists),
- *   apply_tile 64, apply_nb_mult 1, tail_rows 8192, apply_wave 1 (CP-ALS glue
- *   tuning), keep_keys 1 (the sort keys emitted at ingest stay resident after
+ *   apply_tile 64, apply_nb_mult 1, tail_rows 8192, apply_wave 1, apply_warp 1
+ *   (CP-ALS glue tuning), keep_keys 1 (the sort keys emitted at ingest stay resident after
  *   build_perm while memory allows; 0 releases them), pdl 1 (programmatic dependent launch of the MTTKRP and CP-ALS
  *   kernels: a kernel's launch overlaps its predecessor's tail), exchange -1 (sharded CP-ALS row exchange: -1 best available,
  *   0 NCCL broadcast, 1 peer stores, 2 NVLS multimem; sptk_comm_exchange).

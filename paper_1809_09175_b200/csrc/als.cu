@@ -595,6 +595,54 @@ __device__ __forceinline__ void mm_store(float *p, float v) {
     asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
+// The tail of a mode update in the LAST block of an apply kernel to finish
+// (tail.counter != NULL): reduce every block's partials in block order (eight
+// interleaved sums combined in a fixed order: deterministic), finalise the
+// mode (lambda, scales, normalised Gram, the next MTTKRP's weights) and, after
+// the last mode, the fit.  Called by every thread of every block.
+template <typename T>
+__device__ void apply_tail(const ModeTail &tail, T *__restrict__ A, int R,
+                           const double *part_sq, const double *part_dot, const double *gpart) {
+    if (!tail.counter) return;
+    const int tid = threadIdx.x;
+    __shared__ int last_block;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last_block = atomicAdd(tail.counter, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!last_block) return;
+    __threadfence();
+    const int nb = gridDim.x, RR = R * R;
+    auto sum_parts = [&](const double *part, int stride, int e) {
+        double acc[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] = 0.0;
+        int b = 0;
+        for (; b + 7 < nb; b += 8) {  // 8 independent loads in flight per thread
+            double v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = __ldcg(part + (int64_t)(b + k) * stride + e);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[k] += v[k];
+        }
+        for (; b < nb; ++b) acc[0] += __ldcg(part + (int64_t)b * stride + e);
+        return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    };
+    for (int e = tid; e < R; e += blockDim.x) {
+        tail.colsq[e] = sum_parts(part_sq, R, e);
+        if (part_dot) tail.colsq[R + e] = sum_parts(part_dot, R, e);
+    }
+    for (int e = tid; e < RR; e += blockDim.x) tail.graw[e] = sum_parts(gpart, RR, e);
+    __threadfence_block();
+    __syncthreads();
+    finalize_mode_block<T>(tail.colsq, tail.graw, A, tail.N, tail.n, R, tail.next, tail.s_all,
+                           tail.lam, tail.G, static_cast<T *>(tail.scale_next));
+    if (part_dot)
+        fit_block(tail.colsq + R, tail.lam, tail.G, tail.N, R, tail.normX2, tail.fit, tail.trace,
+                  tail.trace_n);
+    if (tid == 0) *tail.counter = 0;  // ready for the next launch (graph replays)
+}
+
 #ifndef SPTK_APPLY_MINB  // A/B builds only
 #define SPTK_APPLY_MINB 2
 #endif
@@ -752,47 +800,130 @@ __global__ void __launch_bounds__(256, SPTK_APPLY_MINB)
         for (int gg = 0; gg < groups; ++gg) acc += gs[((size_t)gg * nblk + b) * 16 + q];
         if (a < R && c < R) gp[a * R + c] = gp[c * R + a] = acc;
     }
-    if (!tail.counter) return;
-    // the last block to finish reduces every block's partials (block order,
-    // four interleaved sums combined in a fixed order: deterministic) and
-    // finalises the mode: lambda, scales, normalised Gram, next MTTKRP's
-    // weights, and the fit after the last mode
-    __shared__ int last_block;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) last_block = atomicAdd(tail.counter, 1) == (int)gridDim.x - 1;
-    __syncthreads();
-    if (!last_block) return;
-    __threadfence();
-    const int nb = gridDim.x, RR = R * R;
-    auto sum_parts = [&](const double *part, int stride, int e) {
-        double acc[8];
+    apply_tail<T>(tail, A, R, part_sq, part_dot, gpart);
+}
+
+// Warp-private variant of apply_gram (round 2; option apply_warp): no block-wide
+// barrier inside the row loop.  A warp takes groups of 32/LR consecutive rows
+// (LR = R rounded up to 8/16/32 lanes, lane = (row slot, column j)), stages the
+// V rows and the A_raw rows it computes in its own shared-memory tile, reads
+// them back as broadcasts (two columns per 128-bit load), and keeps column j
+// of Gamma^{-1} and row j of the Gram partial in registers: A_raw(r, j) =
+// sum_i V(r, i) Gamma^{-1}(i, j) in two partial sums, G_raw(j, b) += A(r, j)
+// A(r, b) for every b.  The next group's V is loaded before the current one is
+// used.  Partials are reduced across row slots (shuffles) and warps (shared
+// memory) in a fixed order, then the same per-block partials / last-block tail
+// as apply_gram.  The smem-tile kernel above synchronises the block three
+// times per 64-row tile; on LBNL's 868K-row mode it ran at 2.1 TB/s (ncu:
+// 16 warps/SM, "wait" and barrier stalls).
+template <int LR>
+__host__ __device__ constexpr size_t apply_warp_smem_doubles() {
+    return (size_t)8 * 2 * 32 + (size_t)8 * LR * LR + (size_t)2 * 8 * LR;
+}
+
+template <typename T, int LR>
+__global__ void __launch_bounds__(256, 2)
+    apply_gram_warp_kernel(const T *__restrict__ V, int64_t r_begin, int64_t r_end, int R,
+                           const double *__restrict__ Ginv, T *__restrict__ A,
+                           double *__restrict__ part_sq, double *__restrict__ part_dot,
+                           double *__restrict__ gpart, const ModeTail tail, const ExchOut ex) {
+    pdl_wait();
+    constexpr int RPW = 32 / LR;
+    extern __shared__ __align__(16) double wsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+    const int rs = lane / LR, j = lane % LR;
+    double *Vw = wsm + warp * 64;            // [RPW][LR] V rows of the group
+    double *Aw = Vw + 32;                    // [RPW][LR] A_raw rows of the group
+    double *gs = wsm + 8 * 64;               // [8][LR][LR] per-warp Gram sums
+    double *ss = gs + 8 * LR * LR;           // [8][LR] column sums of squares
+    double *ds = ss + 8 * LR;                // [8][LR] column dots with V
+    double gi[LR], g[LR];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] = 0.0;
-        int b = 0;
-        for (; b + 7 < nb; b += 8) {  // 8 independent loads in flight per thread
-            double v[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = __ldcg(part + (int64_t)(b + k) * stride + e);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) acc[k] += v[k];
-        }
-        for (; b < nb; ++b) acc[0] += __ldcg(part + (int64_t)b * stride + e);
-        return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-    };
-    for (int e = tid; e < R; e += blockDim.x) {
-        tail.colsq[e] = sum_parts(part_sq, R, e);
-        if (part_dot) tail.colsq[R + e] = sum_parts(part_dot, R, e);
+    for (int i = 0; i < LR; ++i) {
+        gi[i] = (i < R && j < R) ? Ginv[i * R + j] : 0.0;
+        g[i] = 0.0;
     }
-    for (int e = tid; e < RR; e += blockDim.x) tail.graw[e] = sum_parts(gpart, RR, e);
-    __threadfence_block();
+    double sq = 0.0, dot = 0.0;
+    const int64_t ngroups = (r_end - r_begin + RPW - 1) / RPW;
+    const int64_t wstride = (int64_t)gridDim.x * 8;
+    auto load_v = [&](int64_t grp) {
+        const int64_t r = r_begin + grp * RPW + rs;
+        return (grp < ngroups && r < r_end && j < R) ? (double)V[r * R + j] : 0.0;
+    };
+    int64_t grp = blockIdx.x * (int64_t)8 + warp;
+    double vnext = load_v(grp);
+    for (; grp < ngroups; grp += wstride) {
+        const double v = vnext;
+        vnext = load_v(grp + wstride);
+        const int64_t r = r_begin + grp * RPW + rs;
+        const bool on = r < r_end && j < R;
+        Vw[rs * LR + j] = v;
+        __syncwarp();
+        double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < LR; i += 2) {
+            const double2 q = *reinterpret_cast<const double2 *>(Vw + rs * LR + i);
+            x0 += q.x * gi[i];
+            x1 += q.y * gi[i + 1];
+        }
+        double xd = 0.0;
+        if (on) {
+            const T xt = (T)(x0 + x1);
+            const int64_t ix = r * R + j;
+            if (ex.mc) {
+                mm_store(reinterpret_cast<T *>(ex.mc) + ix, xt);
+            } else if (ex.np) {
+                for (int p = 0; p < ex.np; ++p) reinterpret_cast<T *>(ex.peer[p])[ix] = xt;
+            } else {
+                A[ix] = xt;
+            }
+            xd = (double)xt;
+        }
+        Aw[rs * LR + j] = xd;
+        __syncwarp();
+        sq += xd * xd;
+        dot += xd * v;
+#pragma unroll
+        for (int b = 0; b < LR; b += 2) {
+            const double2 q = *reinterpret_cast<const double2 *>(Aw + rs * LR + b);
+            g[b] += xd * q.x;
+            g[b + 1] += xd * q.y;
+        }
+        __syncwarp();
+    }
+    if (ex.np || ex.mc) __threadfence_system();  // replicas written before the all-reduce
+    // fixed-order reduction: row slots (shuffles), then warps (shared memory)
+#pragma unroll
+    for (int o = LR; o < 32; o <<= 1) {
+        sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        dot += __shfl_xor_sync(0xffffffffu, dot, o);
+#pragma unroll
+        for (int b = 0; b < LR; ++b) g[b] += __shfl_xor_sync(0xffffffffu, g[b], o);
+    }
+    if (rs == 0) {
+#pragma unroll
+        for (int b = 0; b < LR; ++b) gs[(warp * LR + j) * LR + b] = g[b];
+        ss[warp * LR + j] = sq;
+        ds[warp * LR + j] = dot;
+    }
     __syncthreads();
-    finalize_mode_block<T>(tail.colsq, tail.graw, A, tail.N, tail.n, R, tail.next, tail.s_all,
-                           tail.lam, tail.G, static_cast<T *>(tail.scale_next));
-    if (part_dot)
-        fit_block(tail.colsq + R, tail.lam, tail.G, tail.N, R, tail.normX2, tail.fit, tail.trace,
-                  tail.trace_n);
-    if (tid == 0) *tail.counter = 0;  // ready for the next launch (graph replays)
+    const int RR = R * R;
+    for (int e = tid; e < RR; e += blockDim.x) {
+        const int a = e / R, b = e % R;
+        double acc = 0.0;
+        for (int w = 0; w < 8; ++w) acc += gs[(w * LR + a) * LR + b];
+        gpart[(int64_t)blockIdx.x * RR + e] = acc;
+    }
+    for (int c = tid; c < R; c += blockDim.x) {
+        double a2 = 0.0, d2 = 0.0;
+        for (int w = 0; w < 8; ++w) {
+            a2 += ss[w * LR + c];
+            d2 += ds[w * LR + c];
+        }
+        part_sq[(int64_t)blockIdx.x * R + c] = a2;
+        if (part_dot) part_dot[(int64_t)blockIdx.x * R + c] = d2;
+    }
+    apply_tail<T>(tail, A, R, part_sq, part_dot, gpart);
 }
 
 // apply_gram grid cap: one full wave of resident blocks (SPTK_APPLY_WAVE=0: the
@@ -1000,6 +1131,89 @@ struct AlsCtx {
     std::vector<size_t> off;               // byte offset of A_m in c.comm->sym
 };
 
+// Plan and launch of the apply pass over rows [r0, r1): the warp-private kernel
+// (option apply_warp, default) or the shared-memory tile kernel.  small: the
+// caller wants at most kTailBlocks blocks (the last one finalises the mode).
+struct ApplyPlan {
+    bool warp = false;
+    int LR = 16, tile = 0, nb = 1;
+    int64_t rpb = 0;
+    size_t smb = 0;
+};
+
+template <typename T, int LR>
+static int warp_apply_cap(size_t smb) {
+    static int occ = -1;
+    if (occ < 0) {
+        cudaFuncSetAttribute(apply_gram_warp_kernel<T, LR>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, apply_gram_warp_kernel<T, LR>, 256,
+                                                          smb) != cudaSuccess || occ < 1) {
+            cudaGetLastError();
+            occ = 1;
+        }
+    }
+    return occ * dev_sms();
+}
+
+template <typename T>
+static ApplyPlan plan_apply(AlsCtx &c, int64_t rows, int R, bool small) {
+    ApplyPlan p;
+    // the warp kernel for R <= 16 (LBNL -0.6 %, C1 -1.7 %, NELL-2 and Delicious
+    // neutral); at R = 32 its 64 register-held doubles spill (+2.8 %)
+    p.warp = opt(OPT_APPLY_WARP) != 0 && R <= 16;
+    if (p.warp) {
+        p.LR = R <= 8 ? 8 : R <= 16 ? 16 : 32;
+        int cap = 0;
+        if (p.LR == 8) {
+            p.smb = sizeof(double) * apply_warp_smem_doubles<8>();
+            cap = warp_apply_cap<T, 8>(p.smb);
+        } else if (p.LR == 16) {
+            p.smb = sizeof(double) * apply_warp_smem_doubles<16>();
+            cap = warp_apply_cap<T, 16>(p.smb);
+        } else {
+            p.smb = sizeof(double) * apply_warp_smem_doubles<32>();
+            cap = warp_apply_cap<T, 32>(p.smb);
+        }
+        const int64_t groups = (rows + 32 / p.LR - 1) / (32 / p.LR);
+        int64_t nb = std::min<int64_t>(cap, (groups + 7) / 8);
+        if (small) nb = std::min<int64_t>(nb, kTailBlocks);
+        p.nb = (int)std::max<int64_t>(nb, 1);
+        return p;
+    }
+    p.tile = std::min(apply_tile_rows(), apply_pf(R <= 16 ? 16 : 32) * 256 / R);
+    p.smb = sizeof(double) * (2 * p.tile * ((R + 3) & ~3) + 4 * 256);
+    int nb = (int)std::min<int64_t>(apply_block_cap<T>(c.nb_apply, R, p.smb),
+                                    (rows + p.tile - 1) / p.tile);
+    if (small) nb = std::min(nb, kTailBlocks);
+    if (nb < 1) nb = 1;
+    p.rpb = (rows + nb - 1) / nb;
+    p.nb = (int)((rows + p.rpb - 1) / p.rpb);
+    return p;
+}
+
+template <typename T>
+static cudaError_t run_apply(const ApplyPlan &p, cudaStream_t s, const T *V, int64_t r0,
+                             int64_t r1, int R, const double *Ginv, T *An, double *psq,
+                             double *pdot, double *gpart, const ModeTail &tail,
+                             const ExchOut &ex) {
+    if (p.warp) {
+        if (p.LR == 8)
+            return launch_pdl(apply_gram_warp_kernel<T, 8>, p.nb, 256, p.smb, s, V, r0, r1, R, Ginv,
+                              An, psq, pdot, gpart, tail, ex);
+        if (p.LR == 16)
+            return launch_pdl(apply_gram_warp_kernel<T, 16>, p.nb, 256, p.smb, s, V, r0, r1, R, Ginv,
+                              An, psq, pdot, gpart, tail, ex);
+        return launch_pdl(apply_gram_warp_kernel<T, 32>, p.nb, 256, p.smb, s, V, r0, r1, R, Ginv,
+                          An, psq, pdot, gpart, tail, ex);
+    }
+    if (R <= 16)
+        return launch_pdl(apply_gram_kernel<T, 16>, p.nb, 256, p.smb, s, V, r0, r1, R, p.rpb,
+                          p.tile, Ginv, An, psq, pdot, gpart, tail, ex);
+    return launch_pdl(apply_gram_kernel<T, 32>, p.nb, 256, p.smb, s, V, r0, r1, R, p.rpb, p.tile,
+                      Ginv, An, psq, pdot, gpart, tail, ex);
+}
+
 // G_m = A_m^T A_m (fixed-order reduction of per-block partials in `part`,
 // default w.partial; the fused path passes w.gpart so w.partial keeps the
 // fit's column partials)
@@ -1106,15 +1320,10 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
         double *pdot = psq + c.part_stride;
         double *colsq = w.colsq.as<double>();
         if (deferred) {  // one pass: A_raw, its Gram partials, column partials; R x R finalise
-            const int tile = std::min(apply_tile_rows(), apply_pf(R <= 16 ? 16 : 32) * 256 / R);
-            const size_t smb = sizeof(double) * (2 * tile * ((R + 3) & ~3) + 4 * 256);
-            int nb = (int)std::min<int64_t>(apply_block_cap<T>(c.nb_apply, R, smb), (I + tile - 1) / tile);
             // modes up to tail_rows() rows: few fat blocks, so the mode tail
             // (reductions, finalise, fit) runs in the last block, no extra launches
-            if (I <= tail_rows()) nb = std::min(nb, kTailBlocks);
-            if (nb < 1) nb = 1;
-            const int64_t rpb = (I + nb - 1) / nb;
-            nb = (int)((I + rpb - 1) / rpb);
+            const ApplyPlan ap = plan_apply<T>(c, I, R, I <= tail_rows());
+            const int nb = ap.nb;
             // few blocks (small modes): the last block reduces and finalises
             // in place; many blocks: a single block's reduction is latency-
             // bound (measured slower than the parallel reduction kernels)
@@ -1133,14 +1342,8 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
             tail.N = N;
             tail.n = n;
             tail.next = (n + 1) % N;
-            if (R <= 16)
-                SPTK_CUDA(launch_pdl(apply_gram_kernel<T, 16>, nb, 256, smb, c.s, V, (int64_t)0, I, R,
-                                     rpb, tile, Ginv, An, psq, last ? pdot : nullptr,
-                                     w.gpart.as<double>(), tail, ExchOut{}));
-            else
-                SPTK_CUDA(launch_pdl(apply_gram_kernel<T, 32>, nb, 256, smb, c.s, V, (int64_t)0, I, R,
-                                     rpb, tile, Ginv, An, psq, last ? pdot : nullptr,
-                                     w.gpart.as<double>(), tail, ExchOut{}));
+            SPTK_CUDA(run_apply<T>(ap, c.s, V, 0, I, R, Ginv, An, psq, last ? pdot : nullptr,
+                                   w.gpart.as<double>(), tail, ExchOut{}));
             count_launch();
             SPTK_CUDA(cudaGetLastError());
             if (!tail.counter) {  // many blocks: parallel reductions, then one finalise block
@@ -1249,13 +1452,8 @@ static sptk_status enqueue_iteration_sharded(AlsCtx &c) {
         SPTK_CUDA(cudaStreamWaitEvent(c.s, w.ev_inv, 0));
         T *An = static_cast<T *>(c.A[n]);
         if (rows > 0) {
-            const int tile = std::min(apply_tile_rows(), apply_pf(R <= 16 ? 16 : 32) * 256 / R);
-            const size_t smb = sizeof(double) * (2 * tile * ((R + 3) & ~3) + 4 * 256);
-            int nb = (int)std::min<int64_t>(apply_block_cap<T>(c.nb_apply, R, smb),
-                                            (rows + tile - 1) / tile);
-            if (nb < 1) nb = 1;
-            const int64_t rpb = (rows + nb - 1) / nb;
-            nb = (int)((rows + rpb - 1) / rpb);
+            const ApplyPlan ap = plan_apply<T>(c, rows, R, false);
+            const int nb = ap.nb;
             ExchOut ex{};
             if (sm.exchange == 2) {
                 ex.mc = sm.mc + c.off[n];
@@ -1264,14 +1462,8 @@ static sptk_status enqueue_iteration_sharded(AlsCtx &c) {
                 for (int p = 0; p < sm.npeer; ++p) ex.peer[p] = sm.peer[p] + c.off[n];
             }
             ModeTail tail{};  // counter NULL: partials reduced below, across ranks
-            if (R <= 16)
-                apply_gram_kernel<T, 16><<<nb, 256, smb, c.s>>>(V, r0, r1, R, rpb, tile, Ginv, An,
-                                                                psq, last ? pdot : nullptr,
-                                                                w.gpart.as<double>(), tail, ex);
-            else
-                apply_gram_kernel<T, 32><<<nb, 256, smb, c.s>>>(V, r0, r1, R, rpb, tile, Ginv, An,
-                                                                psq, last ? pdot : nullptr,
-                                                                w.gpart.as<double>(), tail, ex);
+            SPTK_CUDA(run_apply<T>(ap, c.s, V, r0, r1, R, Ginv, An, psq, last ? pdot : nullptr,
+                                   w.gpart.as<double>(), tail, ex));
             reduce_partials_kernel<<<(R + 7) / 8, 256, 0, c.s>>>(psq, nb, R, ared);
             reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(w.gpart.as<double>(), nb,
                                                                     R * R, ared + 2 * R);

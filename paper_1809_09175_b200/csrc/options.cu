@@ -42,6 +42,7 @@ constexpr OptDef kOpts[] = {
     {"apply_nb_mult", 1},       // CP-ALS apply_gram: block cap = mult x 8 x SMs (tuning)
     {"tail_rows", 8192},        // CP-ALS: modes up to this many rows finalise in apply_gram's last block
     {"apply_wave", 1},          // CP-ALS apply_gram: grid capped at one wave of resident blocks
+    {"apply_warp", 1},          // CP-ALS: warp-private apply_gram kernel (0: shared-memory tiles)
     {"keep_keys", 1},           // keep the ingest sort keys resident after build_perm
     {"pdl", 1},                 // programmatic dependent launch of the MTTKRP / ALS kernels
     {"exchange", -1},           // sharded CP-ALS row exchange: -1 best available, 0 NCCL

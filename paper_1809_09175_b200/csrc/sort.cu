@@ -41,7 +41,14 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 
 // Lanes of the warp holding the same digit (bits < 9), from `bits` ballots
 // instead of __match_any_sync (MATCH is a slow MIO op); `valid` lanes only.
+#ifndef SPTK_SORT_MATCH  // A/B: one MATCH.ANY instead of `bits` ballots
+#define SPTK_SORT_MATCH 0
+#endif
 __device__ __forceinline__ uint32_t digit_peers(uint32_t digit, int bits, bool valid) {
+    if (SPTK_SORT_MATCH) {
+        const uint32_t key = valid ? digit : 0x100u + (threadIdx.x & 31);  // invalid lanes unique
+        return __match_any_sync(0xffffffffu, key) & __ballot_sync(0xffffffffu, valid);
+    }
     uint32_t peers = __ballot_sync(0xffffffffu, valid);
     for (int b = 0; b < bits; ++b) {
         const bool on = (digit >> b) & 1u;
