@@ -294,7 +294,9 @@ sptk_status sptk_set_tuning(int variant, int64_t run);
  *   factor exceeds it), slice_rows 0 (auto), slice_other_first -1 (auto),
  *   rowrec 1, force_v 0 (cap of the lane vector width in elements),
  *   generic 0 (1 forces the generic scalar kernel), debug_dispatch 0,
- *   copy_order 1 (0: permuted copies in perm_n order), deferred_norm 1,
+ *   copy_order 1 (secondary order of the permuted copies: 1 by balance --
+ *   the largest other factor for power-law modes, else the shortest one
+ *   >= 2048 rows; 2 always the shortest; 0 none, perm_n order), deferred_norm 1,
  *   no_graph 0, gamma_inv_chol 0, use_copy 1 (0: gather the records through
  *   perm_n, the paper's traversal, even where a permuted copy exists),
  *   apply_tile 64, apply_nb_mult 1, tail_rows 8192, apply_wave 1, apply_warp 1

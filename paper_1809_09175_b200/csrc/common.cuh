@@ -154,6 +154,7 @@ struct sptk_tensor_s {
     sptk::DevBuf soff[sptk::kMaxModes];         // slice offsets (slice kernel, cached)
     int64_t soff_key[sptk::kMaxModes][4] = {{-1, -1, -1, -1}};  // (row0, row1, nslice, S)
     int64_t row_max[sptk::kMaxModes] = {-1, -1, -1, -1, -1, -1};  // max nnz of a row (lazy)
+    sptk::DevBuf rowmax_dev;                    // uint32[kMaxModes]: longest row, set by build_perm
     sptk::DevBuf sortws;                        // radix-sort workspace (cached)
     sptk::DevBuf keys;                          // uint32[N][P] sort keys emitted at ingest
                                                 // (consumed by build_perm, then released)
@@ -238,6 +239,7 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
                           cudaStream_t s);
 sptk_status host_rowptr(sptk_tensor t, int mode, cudaStream_t s);
 size_t owned_bytes(sptk_tensor t);  // device bytes held by the handle
+int64_t row_max(sptk_tensor t, int mode, cudaStream_t s);  // longest row of a sorted mode
 // free / total device memory: from the ledger inside build_perm, else queried
 bool device_free(sptk_tensor t, size_t *free_b, size_t *total_b);
 sptk_status comm_bcast_rows(sptk_comm c, void *buf, int64_t R, sptk_dtype dt,

@@ -269,17 +269,8 @@ static int slice_count(sptk_tensor t, int mode, int64_t r0, int64_t r1, int64_t 
     }
     if (nnz < 32 * K * rows) return 0;
     if (((rows + 7) / 8) * K < 2 * (int64_t)dev_sms()) return 0;
-    if (t->row_max[mode] < 0) {
-        if (host_rowptr(t, mode, s) != SPTK_OK) {
-            set_error("");
-            return 0;
-        }
-        const std::vector<uint32_t> &h = t->host_rowptr[mode];
-        int64_t mx = 0;
-        for (int64_t r = 0; r < t->dims[mode]; ++r) mx = std::max<int64_t>(mx, h[r + 1] - h[r]);
-        t->row_max[mode] = mx;
-    }
-    if (t->row_max[mode] * rows > 2 * nnz) return 0;  // longest row > 2x the mean
+    const int64_t mx = row_max(t, mode, s);
+    if (mx < 0 || mx * rows > 2 * nnz) return 0;  // longest row > 2x the mean
     *S = sa;
     return (int)K;
 }

@@ -33,7 +33,8 @@ constexpr OptDef kOpts[] = {
     {"force_v", 0},             // cap of the lane vector width (elements), 0 = none
     {"generic", 0},             // 1 forces the generic (scalar, runtime-N) kernel
     {"debug_dispatch", 0},      // one stderr line per MTTKRP launch
-    {"copy_order", 1},          // 0: permuted copies in perm_n order (no secondary key)
+    {"copy_order", 1},          // copies' secondary key: 1 by balance (largest factor for
+                                //   power-law modes), 2 always the shortest, 0 none
     {"deferred_norm", 1},       // CP-ALS deferred column normalisation (R <= 32)
     {"no_graph", 0},            // CP-ALS: 1 disables the CUDA-graph replay
     {"gamma_inv_chol", 0},      // CP-ALS: 1 = Cholesky inverse instead of Gauss-Jordan

@@ -41,14 +41,9 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 
 // Lanes of the warp holding the same digit (bits < 9), from `bits` ballots
 // instead of __match_any_sync (MATCH is a slow MIO op); `valid` lanes only.
-#ifndef SPTK_SORT_MATCH  // A/B: one MATCH.ANY instead of `bits` ballots
-#define SPTK_SORT_MATCH 0
-#endif
+// (measured round 2: one __match_any_sync instead is 1.5x slower per pass,
+// profiles/r02/ab_sort_match.log)
 __device__ __forceinline__ uint32_t digit_peers(uint32_t digit, int bits, bool valid) {
-    if (SPTK_SORT_MATCH) {
-        const uint32_t key = valid ? digit : 0x100u + (threadIdx.x & 31);  // invalid lanes unique
-        return __match_any_sync(0xffffffffu, key) & __ballot_sync(0xffffffffu, valid);
-    }
     uint32_t peers = __ballot_sync(0xffffffffu, valid);
     for (int b = 0; b < bits; ++b) {
         const bool on = (digit >> b) & 1u;
@@ -307,6 +302,18 @@ __global__ void rowptr_from_sorted(const uint32_t *__restrict__ keys, int64_t P,
     }
 }
 
+// out = max over rows of rowptr[r + 1] - rowptr[r] (the longest row)
+__global__ void row_max_kernel(const uint32_t *__restrict__ rowptr, int64_t In,
+                               uint32_t *__restrict__ out) {
+    uint32_t m = 0;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < In;
+         r += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, __ldg(rowptr + r + 1) - __ldg(rowptr + r));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
 __global__ void iota_kernel(uint32_t *__restrict__ out, int64_t P) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -363,9 +370,30 @@ static sptk_status stable_sort_ids(sptk_tensor t, int mode, const uint32_t *in, 
                                    uint32_t **keys_out, cudaStream_t s, void *ext_ws = nullptr,
                                    size_t ext_bytes = 0);
 
-// Secondary key of the copy order: the shortest other mode whose factor does
-// not stay L1-resident (>= 2048 rows, 256 KB at R = 16 fp64), or -1.
-static int copy_secondary_mode(sptk_tensor t, int mode) {
+// The longest row of `mode` (computed on the device at build_perm; one 4-byte
+// read, cached).  -1 if unavailable.
+int64_t row_max(sptk_tensor t, int mode, cudaStream_t s) {
+    if (t->row_max[mode] >= 0) return t->row_max[mode];
+    if (!t->has_perm[mode] || !t->rowmax_dev.p) return -1;
+    uint32_t h = 0;
+    if (cudaMemcpyAsync(&h, t->rowmax_dev.as<uint32_t>() + mode, sizeof h, cudaMemcpyDeviceToHost,
+                        s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    t->row_max[mode] = h;
+    return h;
+}
+
+// Secondary key of the copy order.  Balanced modes (longest row <= 2x the
+// mean: the slice traversal applies) take the shortest other mode whose factor
+// does not stay L1-resident (>= 2048 rows, 256 KB at R = 16 fp64) -- the factor
+// the slice windows sweep.  Imbalanced (power-law) modes, which use the
+// per-group / cooperative kernels, take the LARGEST other mode: a row's gathers
+// of the biggest factor then go in increasing row order (Delicious mode 3
+// -8 %, profiles/r02/ab_copy_secondary.log).  -1: no secondary order.
+static int copy_secondary_mode(sptk_tensor t, int mode, cudaStream_t s) {
     if (!opt(OPT_COPY_ORDER)) return -1;
     // SPTK_COPY_SEC=a0,a1,...: per-mode override (tuning; -1 = none)
     if (const char *o = getenv("SPTK_COPY_SEC")) {
@@ -384,9 +412,13 @@ static int copy_secondary_mode(sptk_tensor t, int mode) {
             }
         }
     }
+    const int64_t mx = row_max(t, mode, s);
+    const bool imbalanced = opt(OPT_COPY_ORDER) == 1 && mx >= 0 && mx * t->dims[mode] > 2 * t->P;
     int a = -1;
-    for (int m = 0; m < t->N; ++m)
-        if (m != mode && t->dims[m] >= 2048 && (a < 0 || t->dims[m] < t->dims[a])) a = m;
+    for (int m = 0; m < t->N; ++m) {
+        if (m == mode || t->dims[m] < 2048) continue;
+        if (a < 0 || (imbalanced ? t->dims[m] > t->dims[a] : t->dims[m] < t->dims[a])) a = m;
+    }
     return a;
 }
 
@@ -420,7 +452,7 @@ sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
     size_t free_b = 0, total_b = 0;
     if (!device_free(t, &free_b, &total_b)) return SPTK_OK;
     const size_t reserve = std::max<size_t>(total_b / 32, (size_t)4 << 30);
-    int a = copy_secondary_mode(t, mode);
+    int a = copy_secondary_mode(t, mode, s);
     if (a >= 0 && !t->has_perm[a]) a = -1;
     // The secondary sort (over all P ids) runs inside the copy's own buffer
     // (>= 16 B = 4 words per nonzero, the sort needs ~3.1) before the copy
@@ -625,12 +657,16 @@ sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s) {
         count_launch(3);
         SPTK_CUDA(cudaGetLastError());
         t->has_perm[mode] = true;
+        t->row_max[mode] = P;  // the single row holds every nonzero
         return SPTK_OK;
     }
     uint32_t *keys = nullptr;
     SPTK_TRY(stable_sort_ids(t, mode, nullptr, perm, &keys, s));
     rowptr_from_sorted<<<grid_for(In + 1), 256, 0, s>>>(keys, P, In, rowptr);
-    count_launch();
+    SPTK_TRY(t->rowmax_dev.reserve(sizeof(uint32_t) * kMaxModes));
+    SPTK_CUDA(cudaMemsetAsync(t->rowmax_dev.as<uint32_t>() + mode, 0, sizeof(uint32_t), s));
+    row_max_kernel<<<grid_for(In), 256, 0, s>>>(rowptr, In, t->rowmax_dev.as<uint32_t>() + mode);
+    count_launch(2);
     SPTK_CUDA(cudaGetLastError());
     t->has_perm[mode] = true;
     return SPTK_OK;
