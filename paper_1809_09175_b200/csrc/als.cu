@@ -1711,7 +1711,60 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int64_t launches_per_iter = 0;
-    for (it = 0; it < max_iters; ++it) {
+    bool fast_done = false;
+    if (use_graph && tol <= 0.0) {
+        // No convergence test: iteration 0 runs eagerly (its host side builds
+        // every cache the launches read) WITHOUT waiting for it; iteration 1 is
+        // captured while the GPU runs it, and the graph is replayed for the rest
+        // back to back.  One host synchronisation per call; the fits come from
+        // the device-side history (the capture no longer leaves the GPU idle:
+        // C1 at K = 20 iterations per call ran 0.084 ms/iter vs 0.073 amortised).
+        const int64_t l0 = profile().launches;
+        st = enqueue_iteration<T>(c);
+        const int64_t l1 = profile().launches;
+        bool ok = st == SPTK_OK &&
+                  cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        sptk_status est = ok ? enqueue_iteration<T>(c) : SPTK_ECUDA;
+        if (st == SPTK_OK) {
+            cudaGraph_t g = nullptr;
+            const bool ended = ok && cudaStreamEndCapture(s, &g) == cudaSuccess;
+            ok = ok && est == SPTK_OK && ended && g &&
+                 cudaGraphInstantiate(&exec, g, 0) == cudaSuccess;
+            graph = g;
+            launches_per_iter = profile().launches - l1;
+            if (!ok) {  // eager launches for the rest of the call
+                cudaGetLastError();
+                set_error("");
+                if (exec) cudaGraphExecDestroy(exec);
+                exec = nullptr;
+                profile().launches = l1;
+            }
+            (void)l0;
+            for (int k = 1; k < max_iters && st == SPTK_OK; ++k) {
+                if (exec) {
+                    profile().launches += launches_per_iter;
+                    if (cudaGraphLaunch(exec, s) != cudaSuccess)
+                        st = cuda_fail(cudaGetLastError(), "cudaGraphLaunch(ALS iteration)");
+                } else {
+                    st = enqueue_iteration<T>(c);
+                }
+            }
+        }
+        int bad = 0;
+        if (st == SPTK_OK) st = complete_iteration(c, &fit, &bad);
+        if (st == SPTK_OK) {
+            std::vector<double> hist((size_t)max_iters);
+            SPTK_CUDA(cudaMemcpy(hist.data(), w.trace.p, sizeof(double) * max_iters,
+                                 cudaMemcpyDeviceToHost));
+            if (bad) st = fail(SPTK_ESINGULAR, "Gamma is singular after the ridge retry");
+            if (fit_trace)
+                for (int k = 0; k < max_iters; ++k) fit_trace[k] = hist[k];
+            fit = hist[max_iters - 1];
+        }
+        it = max_iters;
+        fast_done = true;  // the loop below has nothing left to run
+    }
+    for (it = fast_done ? max_iters : 0; it < max_iters; ++it) {
         int bad = 0;
         if (use_graph && it >= 1) {
             if (!exec) {
