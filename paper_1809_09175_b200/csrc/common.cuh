@@ -55,6 +55,7 @@ enum Opt {
     OPT_KEEP_KEYS, OPT_PDL, OPT_EXCHANGE, OPT_COUNT
 };
 int64_t opt(Opt o);
+uint64_t options_generation();  // bumped by every sptk_set_option / sptk_reset_options
 void set_dispatch(const std::string &s);  // what the last MTTKRP call ran (sptk_last_dispatch)
 
 // ------------------------------------------------------------------ PDL
@@ -122,7 +123,22 @@ struct ALSWork {
     cudaStream_t side = nullptr;              // Cholesky / inverse, overlapped with MTTKRP
     cudaEvent_t ev_gram = nullptr, ev_inv = nullptr;
     double *hres = nullptr;                   // pinned: fit, inner, ||M||^2, ..., status
+    // the instantiated iteration graph of the last sptk_cp_als call, replayed
+    // by the next call when nothing it captured has changed (key: every buffer
+    // address and cache key it reads, the stream, the options generation)
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<uint64_t> graph_key;
+    int64_t launches_per_iter = 0;
+    void drop_graph() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        exec = nullptr;
+        graph = nullptr;
+        graph_key.clear();
+    }
     ~ALSWork() {
+        drop_graph();
         if (hres) cudaFreeHost(hres);
         if (ev_gram) cudaEventDestroy(ev_gram);
         if (ev_inv) cudaEventDestroy(ev_inv);

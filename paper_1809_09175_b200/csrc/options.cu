@@ -82,6 +82,7 @@ int find(const char *name) {
 }
 
 thread_local std::string g_dispatch;
+std::atomic<uint64_t> g_gen{0};
 }  // namespace
 
 int64_t opt(Opt o) {
@@ -94,6 +95,8 @@ int64_t opt(Opt o) {
 
 void set_dispatch(const std::string &s) { g_dispatch = s; }
 
+uint64_t options_generation() { return g_gen.load(std::memory_order_relaxed); }
+
 }  // namespace sptk
 
 using namespace sptk;
@@ -103,7 +106,7 @@ extern "C" sptk_status sptk_set_option(const char *name, int64_t value) {
     if (i < 0) return fail(SPTK_EINVAL, std::string("unknown option '") + (name ? name : "") + "'");
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g_init) init_locked();
-    g_val[i] = value;
+    if (g_val[i].exchange(value) != value) ++g_gen;
     return SPTK_OK;
 }
 
@@ -118,6 +121,7 @@ extern "C" sptk_status sptk_get_option(const char *name, int64_t *value) {
 extern "C" sptk_status sptk_reset_options(void) {
     std::lock_guard<std::mutex> lk(g_mu);
     init_locked();
+    ++g_gen;
     return SPTK_OK;
 }
 
