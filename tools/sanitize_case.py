@@ -70,3 +70,31 @@ for det in (False, True):
     t.close()
 torch.cuda.synchronize()
 print("sanitize case done")
+
+# round 2 paths: forced slice / L2-window slice, options, sharded CP-ALS through a
+# 1-rank communicator (peer-store and broadcast exchange), cached graph replay
+t = sp.sptensor_create(dims, torch.from_numpy(idx.astype(np.int64)).cuda(),
+                       torch.from_numpy(vals).cuda())
+sp.build_perm(t, -1)
+A = [torch.rand(I, 16, dtype=torch.float64, device="cuda") for I in dims]
+for kv in ({"slice": 2}, {"slice": 2, "slice_l2_kb": 16}, {"use_copy": 0}, {"generic": 1},
+           {"force_v": 1}):
+    with sp.options(**kv):
+        for n in range(3):
+            out = torch.empty(dims[n], 16, dtype=torch.float64, device="cuda")
+            sp.mttkrp(t, n, A, out)
+F = [torch.empty(I, 16, dtype=torch.float64, device="cuda") for I in dims]
+sp.cp_als(t, 16, 6, F, seed=1)
+sp.cp_als(t, 16, 6, F, seed=1)          # replays the cached graph
+os.environ["SPTK_FORCE_SHARDED"] = "1"
+try:
+    comm = sp.comm_create(sp.comm_unique_id(), 1, 0)
+    for ex in (1, 0):
+        with sp.options(exchange=ex):
+            sp.cp_als(t, 16, 6, F, seed=1, comm=comm)
+    comm.close()
+except sp.SptkError as e:
+    print("NCCL unavailable:", e)
+t.close()
+torch.cuda.synchronize()
+print("sanitize case done (round 2 paths)")
