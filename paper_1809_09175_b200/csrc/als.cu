@@ -41,11 +41,22 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
+// Entry (row, col) of an I x Rl factor takes counter row*Rl + col; it is
+// stored at row*ld + col (ld > Rl: padded rank, pad columns written 0).
 template <typename T>
-__global__ void init_factor_kernel(uint64_t seed, uint64_t stream, int64_t n, T *__restrict__ out) {
+__global__ void init_factor_kernel(uint64_t seed, uint64_t stream, int64_t I, int Rl, int ld,
+                                   T *__restrict__ out) {
+    const int64_t n = I * ld;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t d = splitmix64(seed ^ ((uint64_t)i * 0x9E3779B97F4A7C15ull) ^
+        const int64_t row = i / ld;
+        const int col = (int)(i - row * ld);
+        if (col >= Rl) {
+            out[i] = T(0);
+            continue;
+        }
+        const uint64_t k = (uint64_t)(row * Rl + col);
+        const uint64_t d = splitmix64(seed ^ (k * 0x9E3779B97F4A7C15ull) ^
                                       (stream * 0xD1B54A32D192ED03ull));
         out[i] = (T)((double)(d >> 11) * 0x1.0p-53);
     }
@@ -114,7 +125,7 @@ __global__ void __launch_bounds__(256)
 // One block.  Shared memory: R x R (L in the lower triangle, L^{-1}
 // transposed in the strict upper triangle) + R (diagonal of L^{-1}).
 __global__ void __launch_bounds__(256)
-    chol_inv_kernel(const double *__restrict__ G, int N, int n, int R,
+    chol_inv_kernel(const double *__restrict__ G, int N, int n, int R, int Rl,
                     double *__restrict__ Ginv, int *__restrict__ status) {
     extern __shared__ double sm[];
     double *L = sm;             // R x R
@@ -122,7 +133,8 @@ __global__ void __launch_bounds__(256)
     __shared__ int bad;
     __shared__ double ridge;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    auto gamma = [&](int i, int j) {
+    auto gamma = [&](int i, int j) {  // padded rank (i or j >= Rl): identity block
+        if (i >= Rl || j >= Rl) return i == j ? 1.0 : 0.0;
         double h = 1.0;
         for (int m = 0; m < N; ++m)
             if (m != n) h *= G[(int64_t)m * R * R + i * R + j];
@@ -136,7 +148,7 @@ __global__ void __launch_bounds__(256)
     for (int attempt = 0; attempt < 2; ++attempt) {
         for (int e = tid; e < R * R; e += blockDim.x) {
             const int i = e / R, j = e % R;
-            if (j <= i) L[e] = gamma(i, j) + (i == j ? ridge : 0.0);
+            if (j <= i) L[e] = gamma(i, j) + (i == j && i < Rl ? ridge : 0.0);
         }
         __syncthreads();
         if (warp == 0) {  // left-looking in-place Cholesky by one warp
@@ -168,8 +180,8 @@ __global__ void __launch_bounds__(256)
         if (attempt == 0) {
             if (tid == 0) {
                 double tr = 0.0;
-                for (int j = 0; j < R; ++j) tr += gamma(j, j);
-                ridge = 1e-12 * (tr / (double)R);
+                for (int j = 0; j < Rl; ++j) tr += gamma(j, j);
+                ridge = 1e-12 * (tr / (double)Rl);
                 bad = 0;
             }
             __syncthreads();
@@ -211,7 +223,10 @@ __global__ void __launch_bounds__(256)
 // a non-positive pivot is exactly the Cholesky failure: same ridge retry.
 // (block function: M = R x R and f = R doubles of shared memory; every thread
 // of the block calls it; Ginv may be global or shared)
-__device__ void gj_inv_block(const double *G, int N, int n, int R,
+// Padded rank (R > Rl: columns Rl..R-1 of every factor are zero, DESIGN.md
+// §4 "odd R"): Gamma's pad block is the identity, so Gamma^{-1} is
+// diag(Gamma_Rl^{-1}, I) and the pad columns of V Gamma^{-1} stay zero.
+__device__ void gj_inv_block(const double *G, int N, int n, int R, int Rl,
                              double *__restrict__ Ginv, int *__restrict__ status,
                              double *__restrict__ M, double *__restrict__ f) {
     __shared__ double piv;
@@ -220,20 +235,26 @@ __device__ void gj_inv_block(const double *G, int N, int n, int R,
     for (int attempt = 0; attempt < 2; ++attempt) {
         double ridge = 0.0;
         if (attempt) {
-            double tr = 0.0;  // every thread: trace of Gamma (R products, tiny)
-            for (int j = 0; j < R; ++j) {
+            double tr = 0.0;  // every thread: trace of Gamma (Rl products, tiny)
+            for (int j = 0; j < Rl; ++j) {
                 double h = 1.0;
                 for (int m = 0; m < N; ++m)
                     if (m != n) h *= G[(int64_t)m * RR + j * R + j];
                 tr += h;
             }
-            ridge = 1e-12 * (tr / (double)R);
+            ridge = 1e-12 * (tr / (double)Rl);
         }
         for (int e = tid; e < RR; e += blockDim.x) {
+            const int i = e / R, k = e % R;
             double h = 1.0;
-            for (int m = 0; m < N; ++m)
-                if (m != n) h *= G[(int64_t)m * RR + e];
-            M[e] = h + ((e / R == e % R) ? ridge : 0.0);
+            if (i >= Rl || k >= Rl) {
+                h = i == k ? 1.0 : 0.0;
+            } else {
+                for (int m = 0; m < N; ++m)
+                    if (m != n) h *= G[(int64_t)m * RR + e];
+                if (i == k) h += ridge;
+            }
+            M[e] = h;
         }
         if (tid == 0) bad = 0;
         __syncthreads();
@@ -268,19 +289,20 @@ __device__ void gj_inv_block(const double *G, int N, int n, int R,
 }
 
 __global__ void __launch_bounds__(256)
-    gj_inv_kernel(const double *__restrict__ G, int N, int n, int R,
+    gj_inv_kernel(const double *__restrict__ G, int N, int n, int R, int Rl,
                   double *__restrict__ Ginv, int *__restrict__ status) {
     extern __shared__ double sm[];
-    gj_inv_block(G, N, n, R, Ginv, status, sm, sm + R * R);
+    gj_inv_block(G, N, n, R, Rl, Ginv, status, sm, sm + R * R);
 }
 
-// Gamma^{-1} for mode n (SPTK_GAMMA_INV=chol forces the Cholesky kernel)
-static void launch_ginv(const double *G, int N, int n, int R, double *Ginv, int *status,
+// Gamma^{-1} for mode n (SPTK_GAMMA_INV=chol forces the Cholesky kernel);
+// R = the padded rank (row stride), Rl <= R the rank of the decomposition
+static void launch_ginv(const double *G, int N, int n, int R, int Rl, double *Ginv, int *status,
                         cudaStream_t s) {
     if (opt(OPT_GAMMA_INV_CHOL))
-        chol_inv_kernel<<<1, 256, sizeof(double) * (R * R + R), s>>>(G, N, n, R, Ginv, status);
+        chol_inv_kernel<<<1, 256, sizeof(double) * (R * R + R), s>>>(G, N, n, R, Rl, Ginv, status);
     else
-        gj_inv_kernel<<<1, 256, sizeof(double) * (R * R + R), s>>>(G, N, n, R, Ginv, status);
+        gj_inv_kernel<<<1, 256, sizeof(double) * (R * R + R), s>>>(G, N, n, R, Rl, Ginv, status);
 }
 
 // A_raw(k,:) = V(k,:) Gamma^{-1} for rows [r0, r1); per-block partial column
@@ -346,8 +368,9 @@ __global__ void __launch_bounds__(256)
 
 // lambda_j = ||A_raw(:,j)||_2 from colsq; A(:,j) /= lambda_j; a zero column
 // becomes e_1 with lambda_j = 0.  Block 0 also writes lambda.
+// Pad columns (j >= Rl, padded rank) stay zero with lambda_j = 0.
 template <typename T>
-__global__ void normalize_kernel(T *__restrict__ A, int64_t r0, int64_t r1, int R,
+__global__ void normalize_kernel(T *__restrict__ A, int64_t r0, int64_t r1, int R, int Rl,
                                  const double *__restrict__ colsq, double *__restrict__ lam) {
     if (blockIdx.x == 0)
         for (int j = threadIdx.x; j < R; j += blockDim.x) lam[j] = sqrt(colsq[j]);
@@ -358,7 +381,8 @@ __global__ void normalize_kernel(T *__restrict__ A, int64_t r0, int64_t r1, int 
         const int j = (int)(i % R);
         const double l = sqrt(colsq[j]);
         T *a = A + k * R + j;
-        if (l == 0.0) *a = (T)(k == 0 ? 1.0 : 0.0);
+        if (j >= Rl) *a = T(0);
+        else if (l == 0.0) *a = (T)(k == 0 ? 1.0 : 0.0);
         else *a = (T)((double)*a / l);
     }
 }
@@ -415,7 +439,7 @@ __global__ void __launch_bounds__(256)
 //       order by reduce_partials_kernel); block 0 writes lambda.
 template <typename T, int KE>
 __global__ void __launch_bounds__(256)
-    finish_kernel(T *__restrict__ A, int64_t I, int R, int64_t rows_per_block,
+    finish_kernel(T *__restrict__ A, int64_t I, int R, int Rl, int64_t rows_per_block,
                   const double *__restrict__ colsq, double *__restrict__ gpart,
                   double *__restrict__ lam) {
     constexpr int TR = kGramTileRows;
@@ -443,7 +467,8 @@ __global__ void __launch_bounds__(256)
                 T v = *a;
                 if (e0 == 0) {  // normalise once (first entry chunk); later chunks re-read
                     const double l = lam_s[x % R];
-                    v = (l == 0.0) ? (T)(rt + x / R == 0 ? 1.0 : 0.0) : (T)((double)v / l);
+                    if (x % R >= Rl) v = T(0);  // pad column (padded rank)
+                    else v = (l == 0.0) ? (T)(rt + x / R == 0 ? 1.0 : 0.0) : (T)((double)v / l);
                     *a = v;
                 }
                 tile[x] = (double)v;
@@ -516,7 +541,7 @@ static bool deferred_norm(int64_t R) {  // read per call: tests switch it per ca
 template <typename T>
 __device__ void finalize_mode_block(const double *__restrict__ colsq,
                                     const double *__restrict__ graw, T *__restrict__ A, int N,
-                                    int n, int R, int next, double *__restrict__ s_all,
+                                    int n, int R, int Rl, int next, double *__restrict__ s_all,
                                     double *__restrict__ lam, double *__restrict__ G,
                                     T *__restrict__ scale_next) {
     __shared__ double sn[128];
@@ -524,10 +549,13 @@ __device__ void finalize_mode_block(const double *__restrict__ colsq,
     __shared__ int zero[128];
     const int tid = threadIdx.x;
     for (int j = tid; j < R; j += blockDim.x) {
-        const double l = sqrt(colsq[j]);
+        // pad column of a padded rank (j >= Rl): zero, lambda 0, scale 0 --
+        // its Gram entries and the next MTTKRP's weight stay 0
+        const bool pad = j >= Rl;
+        const double l = pad ? 0.0 : sqrt(colsq[j]);
         lam[j] = l;
-        zero[j] = !(l > 0.0);
-        sn[j] = l > 0.0 ? 1.0 / l : 1.0;
+        zero[j] = !pad && !(l > 0.0);
+        sn[j] = pad ? 0.0 : (l > 0.0 ? 1.0 / l : 1.0);
         row0[j] = (double)A[j];
     }
     __syncthreads();
@@ -558,11 +586,11 @@ __device__ void finalize_mode_block(const double *__restrict__ colsq,
 template <typename T>
 __global__ void __launch_bounds__(256)
     finalize_mode_kernel(const double *__restrict__ colsq, const double *__restrict__ graw,
-                         T *__restrict__ A, int N, int n, int R, int next,
+                         T *__restrict__ A, int N, int n, int R, int Rl, int next,
                          double *__restrict__ s_all, double *__restrict__ lam,
                          double *__restrict__ G, T *__restrict__ scale_next) {
     pdl_wait();
-    finalize_mode_block<T>(colsq, graw, A, N, n, R, next, s_all, lam, G, scale_next);
+    finalize_mode_block<T>(colsq, graw, A, N, n, R, Rl, next, s_all, lam, G, scale_next);
 }
 
 // Where the last block of apply_gram leaves the mode's results (counter NULL:
@@ -577,6 +605,7 @@ struct ModeTail {
     void *scale_next;      // R values of the tensor dtype
     double normX2;
     int N, n, next;
+    int Rl;                // rank of the decomposition (< R: padded rank)
 };
 
 // Where apply_gram also stores the rows it computes (sharded CP-ALS with the
@@ -635,7 +664,8 @@ __device__ void apply_tail(const ModeTail &tail, T *__restrict__ A, int R,
     for (int e = tid; e < RR; e += blockDim.x) tail.graw[e] = sum_parts(gpart, RR, e);
     __threadfence_block();
     __syncthreads();
-    finalize_mode_block<T>(tail.colsq, tail.graw, A, tail.N, tail.n, R, tail.next, tail.s_all,
+    finalize_mode_block<T>(tail.colsq, tail.graw, A, tail.N, tail.n, R, tail.Rl, tail.next,
+                           tail.s_all,
                            tail.lam, tail.G, static_cast<T *>(tail.scale_next));
     if (part_dot)
         fit_block(tail.colsq + R, tail.lam, tail.G, tail.N, R, tail.normX2, tail.fit, tail.trace,
@@ -1117,7 +1147,8 @@ static int grid_for(int64_t n, int per = 256) {
 
 struct AlsCtx {
     sptk_tensor t;
-    int64_t R;
+    int64_t R;                             // row stride of the factors: the padded rank
+    int64_t Rl;                            // rank of the decomposition (<= R)
     cudaStream_t s;
     sptk_comm comm;
     std::vector<void *> A;                 // device factor pointers
@@ -1308,7 +1339,7 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
         // side stream: Gamma^{-1} for mode n once G_{n-1} is final
         SPTK_CUDA(cudaEventRecord(w.ev_gram, c.s));
         SPTK_CUDA(cudaStreamWaitEvent(w.side, w.ev_gram, 0));
-        launch_ginv(w.G.as<double>(), N, n, R, Ginv, status, w.side);
+        launch_ginv(w.G.as<double>(), N, n, R, (int)c.Rl, Ginv, status, w.side);
         count_launch();
         SPTK_CUDA(cudaGetLastError());
         SPTK_CUDA(cudaEventRecord(w.ev_inv, w.side));
@@ -1342,6 +1373,7 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
             tail.N = N;
             tail.n = n;
             tail.next = (n + 1) % N;
+            tail.Rl = (int)c.Rl;
             SPTK_CUDA(run_apply<T>(ap, c.s, V, 0, I, R, Ginv, An, psq, last ? pdot : nullptr,
                                    w.gpart.as<double>(), tail, ExchOut{}));
             count_launch();
@@ -1352,7 +1384,8 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
                 SPTK_CUDA(launch_pdl(reduce_partials_kernel, (R * R + 7) / 8, 256, 0, c.s,
                                      (const double *)w.gpart.as<double>(), nb, R * R, graw));
                 SPTK_CUDA(launch_pdl(finalize_mode_kernel<T>, 1, 256, 0, c.s, (const double *)colsq,
-                                     (const double *)graw, An, N, n, R, (n + 1) % N, s_all, lam,
+                                     (const double *)graw, An, N, n, R, (int)c.Rl, (n + 1) % N,
+                                     s_all, lam,
                                      w.G.as<double>(), scale));
                 count_launch(3);
                 if (last) {
@@ -1377,17 +1410,17 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
                 nf = (int)((I + fpb - 1) / fpb);
                 const size_t fsm = sizeof(double) * (R + kGramTileRows * R);
                 if (R <= 16)
-                    finish_kernel<T, 1><<<nf, 256, fsm, c.s>>>(An, I, R, fpb, colsq,
+                    finish_kernel<T, 1><<<nf, 256, fsm, c.s>>>(An, I, R, (int)c.Rl, fpb, colsq,
                                                                w.gpart.as<double>(), lam);
                 else
-                    finish_kernel<T, 4><<<nf, 256, fsm, c.s>>>(An, I, R, fpb, colsq,
+                    finish_kernel<T, 4><<<nf, 256, fsm, c.s>>>(An, I, R, (int)c.Rl, fpb, colsq,
                                                                w.gpart.as<double>(), lam);
                 reduce_partials_kernel<<<(R * R + 7) / 8, 256, 0, c.s>>>(
                     w.gpart.as<double>(), nf, R * R, w.G.as<double>() + (int64_t)n * R * R);
                 count_launch(2);
             } else {        // large R: normalise, tiled Gram
                 normalize_kernel<T><<<grid_for(std::max<int64_t>(I, 1) * R), 256, 0, c.s>>>(
-                    An, 0, I, R, colsq, lam);
+                    An, 0, I, R, (int)c.Rl, colsq, lam);
                 count_launch();
                 SPTK_CUDA(cudaGetLastError());
                 SPTK_TRY(gram<T>(c, n, w.gpart.as<double>()));
@@ -1444,7 +1477,7 @@ static sptk_status enqueue_iteration_sharded(AlsCtx &c) {
         const int64_t r0 = c.b[n][rank], r1 = c.b[n][rank + 1], rows = r1 - r0;
         SPTK_CUDA(cudaEventRecord(w.ev_gram, c.s));
         SPTK_CUDA(cudaStreamWaitEvent(w.side, w.ev_gram, 0));
-        launch_ginv(w.G.as<double>(), N, n, R, Ginv, status, w.side);
+        launch_ginv(w.G.as<double>(), N, n, R, (int)c.Rl, Ginv, status, w.side);
         count_launch();
         SPTK_CUDA(cudaGetLastError());
         SPTK_CUDA(cudaEventRecord(w.ev_inv, w.side));
@@ -1479,7 +1512,7 @@ static sptk_status enqueue_iteration_sharded(AlsCtx &c) {
         SPTK_TRY(comm_allreduce_f64(c.comm, ared, 2 * R + (int64_t)R * R, c.s));
         if (sm.exchange == 0)
             SPTK_TRY(comm_bcast_rows(c.comm, An, c.R, t->dtype, c.b[n].data(), c.s));
-        finalize_mode_kernel<T><<<1, 256, 0, c.s>>>(ared, ared + 2 * R, An, N, n, R, (n + 1) % N,
+        finalize_mode_kernel<T><<<1, 256, 0, c.s>>>(ared, ared + 2 * R, An, N, n, R, (int)c.Rl, (n + 1) % N,
                                                      s_all, lam, w.G.as<double>(), scale);
         count_launch();
         if (last) {
@@ -1534,7 +1567,7 @@ static sptk_status als_iteration(AlsCtx &c, double *fit_host, int *status_host) 
         // (the event was recorded there, before the row broadcast)
         if (n == 0) SPTK_CUDA(cudaEventRecord(w.ev_gram, c.s));
         SPTK_CUDA(cudaStreamWaitEvent(w.side, w.ev_gram, 0));
-        launch_ginv(w.G.as<double>(), N, n, R, Ginv, status, w.side);
+        launch_ginv(w.G.as<double>(), N, n, R, (int)c.Rl, Ginv, status, w.side);
         count_launch();
         SPTK_CUDA(cudaGetLastError());
         SPTK_CUDA(cudaEventRecord(w.ev_inv, w.side));
@@ -1560,7 +1593,7 @@ static sptk_status als_iteration(AlsCtx &c, double *fit_host, int *status_host) 
         }
         if (multi) SPTK_TRY(comm_allreduce_f64(c.comm, colsq, last ? 2 * R : R, c.s));
         normalize_kernel<T><<<grid_for(std::max<int64_t>(rows, 1) * R), 256, 0, c.s>>>(
-            An, r0, r1, R, colsq, lam);
+            An, r0, r1, R, (int)c.Rl, colsq, lam);
         count_launch();
         SPTK_CUDA(cudaGetLastError());
         // G_n = sum over ranks of the Gram matrix of each rank's own normalised
@@ -1594,6 +1627,7 @@ static std::vector<uint64_t> graph_key(AlsCtx &c, cudaStream_t s) {
     auto add = [&](uint64_t v) { k.push_back(v); };
     auto addp = [&](const void *p) { k.push_back((uint64_t)(uintptr_t)p); };
     add((uint64_t)c.R);
+    add((uint64_t)c.Rl);
     add((uint64_t)t->N);
     add((uint64_t)t->dtype);
     addp(s);
@@ -1635,13 +1669,35 @@ static std::vector<uint64_t> graph_key(AlsCtx &c, cudaStream_t s) {
     return k;
 }
 
+// Row stride of CP-ALS's factors for rank Rl (DESIGN.md §4 "odd R"): the
+// MTTKRP's lanes load 32-byte vectors (V = 32 / sizeof(T) columns), which a
+// row of Rl columns cannot use unless Rl is a multiple of V (or a power of two
+// below it) -- R = 17 in fp64 ran 4.8x slower than R = 16 on 8-byte lanes.
+// Other ranks run on factors padded with zero columns to the next multiple of
+// min(V, pow2ceil(Rl)); the pad columns stay exactly zero through every step
+// (Gamma's pad block is the identity, lambda_pad = 0, scale_pad = 0), so the
+// decomposition is the rank-Rl one.  Option pad_rank = 0: stride Rl.
 template <typename T>
-static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double tol, uint64_t seed,
+static int64_t padded_rank(int64_t Rl) {
+    const int64_t V = 32 / (int64_t)sizeof(T);
+    int64_t p2 = 1;
+    while (p2 < Rl) p2 <<= 1;
+    if (!opt(OPT_PAD_RANK) || Rl % V == 0 || p2 == Rl) return Rl;
+    // pad_rank > 1: pad to a multiple of that many columns instead (A/B)
+    const int64_t q = std::max<int64_t>(std::min(V, p2), opt(OPT_PAD_RANK));
+    return std::min<int64_t>((Rl + q - 1) / q * q, kMaxAlsRank);
+}
+
+template <typename T>
+static sptk_status cp_als_impl(sptk_tensor t, int64_t Rl, int max_iters, double tol, uint64_t seed,
                                const void *const *init, void *const *factors_out,
                                void *lambda_out, double *fit_out, int *iters_out,
                                double *fit_trace, sptk_comm comm, cudaStream_t s) {
     const int N = t->N;
     const size_t es = sizeof(T);
+    // R: the factors' row stride inside the iteration (padded rank), Rl the rank
+    const int64_t R = padded_rank<T>(Rl);
+    const bool padded = R != Rl;
     ALSWork &w = t->als;
     int64_t Imax = 0, Isum = 0;
     for (int m = 0; m < N; ++m) {
@@ -1651,6 +1707,7 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     AlsCtx c;
     c.t = t;
     c.R = R;
+    c.Rl = Rl;
     c.s = s;
     c.comm = comm;
     // enough blocks to cover tall factors (LBNL's 868K-row mode) in one wave
@@ -1689,9 +1746,9 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
     c.sym_iter = multi && deferred_norm(R);
     std::vector<bool> host_out(N);
     bool any_host = false;
-    for (int m = 0; m < N; ++m) {
-        host_out[m] = c.sym_iter || !is_device_ptr(factors_out[m]);
-        any_host = any_host || !is_device_ptr(factors_out[m]);
+    for (int m = 0; m < N; ++m) {  // padded: staged, copied out with stride Rl
+        host_out[m] = c.sym_iter || padded || !is_device_ptr(factors_out[m]);
+        any_host = any_host || padded || !is_device_ptr(factors_out[m]);
     }
     c.A.resize(N);
     if (c.sym_iter) {
@@ -1719,9 +1776,15 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
         const size_t bytes = es * t->dims[m] * R;
         if (!init || !init[m]) {
             init_factor_kernel<T><<<grid_for(t->dims[m] * R), 256, 0, s>>>(
-                seed, (uint64_t)(N + 1 + m), t->dims[m] * R, static_cast<T *>(c.A[m]));
+                seed, (uint64_t)(N + 1 + m), t->dims[m], (int)Rl, (int)R,
+                static_cast<T *>(c.A[m]));
             count_launch();
             SPTK_CUDA(cudaGetLastError());
+        } else if (padded) {  // rows of Rl into rows of R, pad columns zero
+            SPTK_CUDA(cudaMemsetAsync(c.A[m], 0, bytes, s));
+            if (t->dims[m] > 0)
+                SPTK_CUDA(cudaMemcpy2DAsync(c.A[m], es * R, init[m], es * Rl, es * Rl, t->dims[m],
+                                            cudaMemcpyDefault, s));
         } else if (init[m] != c.A[m]) {
             SPTK_CUDA(cudaMemcpyAsync(c.A[m], init[m], bytes, cudaMemcpyDefault, s));
         }
@@ -1919,15 +1982,18 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t R, int max_iters, double t
         SPTK_CUDA(cudaStreamSynchronize(s));
     }
     for (int m = 0; m < N; ++m)
-        if (host_out[m])
+        if (host_out[m] && padded && t->dims[m] > 0)  // drop the pad columns
+            SPTK_CUDA(cudaMemcpy2DAsync(factors_out[m], es * Rl, c.A[m], es * R, es * Rl,
+                                        t->dims[m], cudaMemcpyDefault, s));
+        else if (host_out[m])
             SPTK_CUDA(cudaMemcpyAsync(factors_out[m], c.A[m], es * t->dims[m] * R,
                                       cudaMemcpyDefault, s));
     if (lambda_out) {
-        cast_kernel<T><<<(unsigned)((R + 127) / 128), 128, 0, s>>>(w.lam.as<double>(), (int)R,
-                                                                  w.lamT.as<T>());
+        cast_kernel<T><<<(unsigned)((Rl + 127) / 128), 128, 0, s>>>(w.lam.as<double>(), (int)Rl,
+                                                                   w.lamT.as<T>());
         count_launch();
         SPTK_CUDA(cudaGetLastError());
-        SPTK_CUDA(cudaMemcpyAsync(lambda_out, w.lamT.p, es * R, cudaMemcpyDefault, s));
+        SPTK_CUDA(cudaMemcpyAsync(lambda_out, w.lamT.p, es * Rl, cudaMemcpyDefault, s));
     }
     if (any_host || (lambda_out && !is_device_ptr(lambda_out)))
         SPTK_CUDA(cudaStreamSynchronize(s));

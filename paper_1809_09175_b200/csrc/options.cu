@@ -48,6 +48,9 @@ constexpr OptDef kOpts[] = {
     {"pdl", 1},                 // programmatic dependent launch of the MTTKRP / ALS kernels
     {"exchange", -1},           // sharded CP-ALS row exchange: -1 best available, 0 NCCL
                                 //   broadcast, 1 peer stores, 2 NVLS multimem stores
+    {"pad_rank", 1},            // CP-ALS: R not a multiple of the 32-byte lane vector runs on
+                                //   factors padded with zero columns (0: stride R)
+    {"sort_v1", 0},             // 1: round-1 radix downsweep (A/B)
 };
 
 static_assert(sizeof(kOpts) / sizeof(kOpts[0]) == OPT_COUNT, "kOpts must list every Opt, in order");

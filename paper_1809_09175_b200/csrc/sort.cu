@@ -21,7 +21,13 @@
 namespace sptk {
 
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;                              // keys per thread
+#ifndef SPTK_SORT_ITEMS  // A/B builds only
+#define SPTK_SORT_ITEMS 16
+#endif
+#ifndef SPTK_DS_MINB     // A/B builds only: min resident blocks of the leaner downsweep
+#define SPTK_DS_MINB 1
+#endif
+constexpr int kSortItems = SPTK_SORT_ITEMS;                 // keys per thread
 constexpr int kSortTile = kSortThreads * kSortItems;        // 4096
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kWarpChunk = kSortTile / kSortWarps;          // 512 keys per warp
@@ -186,6 +192,162 @@ __global__ void __launch_bounds__(kSortThreads)
         keys_out[g] = k;
         vals_out[g] = sval[j];
     }
+}
+
+// Leaner pass (round 2): the ranking produces the per-warp digit counts
+// itself (no shared-memory atomics), the digit width is a template parameter
+// (unrolled ballots), full tiles skip every bounds test, one shared load per
+// key finds its tile position (warp base folded into the digit start) and one
+// per key its global position (delta = global run start - tile start), and
+// the last pass of a sort whose keys are not wanted writes values only.
+// (round-1 kernel above: 4.6 warp instructions per key, issue-bound at
+// 73 % issue-active, 0.43 of HBM; profiles/r02/prof_radix_raw.csv)
+template <int DB>
+struct DownsweepSmem {
+    uint32_t wbase[kSortWarps][1 << DB];  // per-warp running count, then tile position base
+    int32_t delta[1 << DB];               // global run start - tile start of each digit
+    uint32_t wsum[kSortWarps];
+    uint32_t skey[kSortTile];
+    uint32_t sval[kSortTile];
+};
+
+template <int DB, bool FULL>
+__device__ __forceinline__ void downsweep_body(DownsweepSmem<DB> &sm, const uint32_t *__restrict__ keys_in,
+                                               const uint32_t *__restrict__ vals_in, uint32_t P,
+                                               int shift, uint32_t ntiles,
+                                               const uint32_t *__restrict__ offsets,
+                                               uint32_t *__restrict__ keys_out,
+                                               uint32_t *__restrict__ vals_out) {
+    constexpr int ND = 1 << DB;
+    constexpr uint32_t MASK = ND - 1;
+    auto &wbase = sm.wbase;
+    auto &delta = sm.delta;
+    auto &wsum = sm.wsum;
+    auto &skey = sm.skey;
+    auto &sval = sm.sval;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int d = lane; d < ND; d += 32) wbase[warp][d] = 0;
+    __syncwarp();
+    const uint32_t tile0 = blockIdx.x * (uint32_t)kSortTile;
+    const uint32_t tile_n = FULL ? (uint32_t)kSortTile : P - tile0;
+    const uint32_t base = tile0 + warp * (uint32_t)kWarpChunk;
+    const uint32_t lt = lanemask_lt();
+    uint32_t key[kSortItems], val[kSortItems];
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        const uint32_t i = base + r * 32 + lane;
+        if (FULL || i < P) {
+            key[r] = __ldg(keys_in + i);
+            val[r] = vals_in ? __ldg(vals_in + i) : i;
+        } else {
+            key[r] = 0xffffffffu;
+            val[r] = 0;
+        }
+    }
+    // A: stable rank of every key among the equal digits of its warp chunk
+    //    (rounds of 32 in storage order, per-bit ballots); the running count
+    //    of each digit ends as the warp's digit histogram
+    uint32_t rank[kSortItems];
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        const bool valid = FULL || base + r * 32 + lane < P;
+        const uint32_t digit = (key[r] >> shift) & MASK;
+        uint32_t peers = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+        for (int b = 0; b < DB; ++b)  // LOP3->P, VOTE, predicated NOT, AND per bit
+            asm("{\n\t.reg .pred p;\n\t.reg .b32 m;\n\t"
+                "and.b32 m, %1, %2;\n\t"
+                "setp.ne.u32 p, m, 0;\n\t"
+                "vote.sync.ballot.b32 m, p, 0xffffffff;\n\t"
+                "@!p not.b32 m, m;\n\t"
+                "and.b32 %0, %0, m;\n\t}"
+                : "+r"(peers) : "r"(digit), "r"(1u << b));
+        const uint32_t below = __popc(peers & lt);
+        uint32_t c = 0;
+        if (valid) c = wbase[warp][digit];
+        __syncwarp();
+        if (valid && below == 0) wbase[warp][digit] = c + __popc(peers);
+        __syncwarp();
+        rank[r] = c + below;
+    }
+    __syncthreads();
+    // B: per digit, the exclusive scan over warps and over digits: wbase :=
+    //    tile position of the warp's first key of the digit; delta := global
+    //    start of the digit's run of this tile - its tile start
+    {
+        const int d = threadIdx.x;  // kSortThreads == 256 >= ND
+        uint32_t tot = 0;
+        if (d < ND) {
+#pragma unroll
+            for (int w = 0; w < kSortWarps; ++w) {
+                const uint32_t c = wbase[w][d];
+                wbase[w][d] = tot;
+                tot += c;
+            }
+        }
+        uint32_t inc = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        if (lane == 31) wsum[warp] = inc;
+        __syncthreads();
+        uint32_t wpre = 0;
+#pragma unroll
+        for (int w = 0; w < kSortWarps; ++w)
+            if (w < warp) wpre += wsum[w];
+        if (d < ND) {
+            const uint32_t lstart = wpre + inc - tot;
+#pragma unroll
+            for (int w = 0; w < kSortWarps; ++w) wbase[w][d] += lstart;
+            delta[d] = (int32_t)(offsets[(size_t)d * ntiles + blockIdx.x] - lstart);
+        }
+    }
+    __syncthreads();
+    // C: tile-local scatter into shared memory
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        if (FULL || base + r * 32 + lane < P) {
+            const uint32_t pos = wbase[warp][(key[r] >> shift) & MASK] + rank[r];
+            skey[pos] = key[r];
+            sval[pos] = val[r];
+        }
+    }
+    __syncthreads();
+    // D: coalesced write-out of the digit runs
+#pragma unroll 4
+    for (uint32_t j = threadIdx.x; j < tile_n; j += kSortThreads) {
+        const uint32_t k = skey[j];
+        const uint32_t g = (uint32_t)((int32_t)j + delta[(k >> shift) & MASK]);
+        if (keys_out) keys_out[g] = k;
+        vals_out[g] = sval[j];
+    }
+}
+
+template <int DB>
+__global__ void __launch_bounds__(kSortThreads, SPTK_DS_MINB)
+    radix_downsweep2(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
+                     uint32_t P, int shift, uint32_t ntiles, const uint32_t *__restrict__ offsets,
+                     uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out) {
+    __shared__ DownsweepSmem<DB> sm;
+    if ((blockIdx.x + 1) * (uint64_t)kSortTile <= P)
+        downsweep_body<DB, true>(sm, keys_in, vals_in, P, shift, ntiles, offsets, keys_out, vals_out);
+    else
+        downsweep_body<DB, false>(sm, keys_in, vals_in, P, shift, ntiles, offsets, keys_out, vals_out);
+}
+
+static cudaError_t launch_downsweep2(int db, unsigned grid, cudaStream_t s, const uint32_t *kin,
+                                     const uint32_t *vin, uint32_t P, int shift, uint32_t ntiles,
+                                     const uint32_t *offsets, uint32_t *kout, uint32_t *vout) {
+#define SPTK_DS(D) \
+    case D: radix_downsweep2<D><<<grid, kSortThreads, 0, s>>>(kin, vin, P, shift, ntiles, offsets, kout, vout); break;
+    switch (db) {
+        SPTK_DS(1) SPTK_DS(2) SPTK_DS(3) SPTK_DS(4) SPTK_DS(5) SPTK_DS(6) SPTK_DS(7) SPTK_DS(8)
+    default: return cudaErrorInvalidValue;
+    }
+#undef SPTK_DS
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------ exclusive scan
@@ -624,8 +786,16 @@ static sptk_status stable_sort_ids(sptk_tensor t, int mode, const uint32_t *in, 
         count_launch();
         SPTK_CUDA(cudaGetLastError());
         SPTK_TRY(exclusive_scan(counts, ntiles * ((int64_t)1 << db), tmp, s));
-        radix_downsweep<<<(unsigned)ntiles, kSortThreads, 0, s>>>(
-            kin, vin, (uint32_t)P, shift, db, (uint32_t)ntiles, counts, kout, vout);
+        if (opt(OPT_SORT_V1)) {
+            radix_downsweep<<<(unsigned)ntiles, kSortThreads, 0, s>>>(
+                kin, vin, (uint32_t)P, shift, db, (uint32_t)ntiles, counts, kout, vout);
+        } else {
+            // the last pass writes the keys only if the caller wants them
+            const bool keys_needed = keys_out || p + 1 < npass;
+            SPTK_CUDA(launch_downsweep2(db, (unsigned)ntiles, s, kin, vin, (uint32_t)P, shift,
+                                        (uint32_t)ntiles, counts, keys_needed ? kout : nullptr,
+                                        vout));
+        }
         count_launch();
         SPTK_CUDA(cudaGetLastError());
         kin = kout;

@@ -781,6 +781,51 @@ def test_cp_als_large_rank_tiled_glue(sp, R):
         assert rel(F[m].cpu().numpy(), ref["A"][m]) <= 1e-6
 
 
+@pytest.mark.parametrize("R,dtype,deferred", [
+    (3, torch.float64, 1), (5, torch.float64, 1), (17, torch.float64, 1), (17, torch.float64, 0),
+    (33, torch.float64, 1), (5, torch.float32, 1), (12, torch.float32, 1), (12, torch.float32, 0),
+])
+def test_cp_als_padded_rank(sp, R, dtype, deferred):
+    """R not a multiple of the 32-byte lane vector: CP-ALS runs on factors
+    padded with zero columns (DESIGN.md §4 "odd R").  The trajectory, the
+    factors and lambda follow the oracle's rank-R run; pad_rank=0 (stride R,
+    narrow lanes) gives the same result to rounding; device and host outputs
+    agree."""
+    dims = (150, 170, 130)
+    idx, vals = synth.unique_tensor(41, dims, 20000)
+    f32 = dtype == torch.float32
+    v = vals.astype(np.float32).astype(np.float64) if f32 else vals
+    init = factors_np(42, dims, R)
+    if f32:
+        init = [a.astype(np.float32).astype(np.float64) for a in init]
+    ref = oracle.cp_als(dims, idx, v, init, 8)
+    t = make(sp, dims, idx, vals.astype(np.float32) if f32 else vals, dtype)
+    out = {}
+    for pad in (1, 0):
+        with sp.options(pad_rank=pad, deferred_norm=deferred):
+            F = [torch.full((I, R), float("nan"), dtype=dtype, device="cuda") for I in dims]
+            lam = torch.full((R,), float("nan"), dtype=dtype, device="cuda")
+            res = sp.cp_als(t, R, 8, F, seed=42, lambda_out=lam)
+            out[pad] = (res, [f.double().cpu().numpy() for f in F], lam.double().cpu().numpy())
+    res, F, lam = out[1]
+    tf, tl = (1e-4, 1e-3) if f32 else (1e-9, 1e-8)
+    assert np.max(np.abs(res["trace"] - ref["trace"])) <= tf
+    assert rel(lam, ref["lam"]) <= tl
+    for m in range(3):
+        assert rel(F[m], ref["A"][m]) <= tl, m
+    res0, F0, lam0 = out[0]
+    tp = 1e-4 if f32 else 1e-10
+    assert np.max(np.abs(res0["trace"] - res["trace"])) <= tp
+    for m in range(3):
+        assert rel(F0[m], F[m]) <= (1e-3 if f32 else 1e-9)
+    # host buffers (staged, strided copy-out) and the generator's init (no init)
+    Fh = [np.full((I, R), np.nan, dtype=np.float32 if f32 else np.float64) for I in dims]
+    resh = sp.cp_als(t, R, 8, Fh, seed=42)
+    assert np.max(np.abs(resh["trace"] - res["trace"])) <= tp
+    for m in range(3):
+        assert rel(Fh[m], F[m]) <= (1e-3 if f32 else 1e-9)
+
+
 @pytest.mark.parametrize("exchange", [0, 1])
 def test_sharded_zero_column_e1(sp, monkeypatch, exchange):
     """A zero initial column through the sharded deferred path: every Gamma

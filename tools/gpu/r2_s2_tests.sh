@@ -1,0 +1,3 @@
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/s2_smoke.log 2>&1
+timeout 3000 python -m pytest tests/ -x -q -m gpu -rs > gpurun_out/s2_tests.log 2>&1
+python bench.py > gpurun_out/s2_default.json 2> gpurun_out/s2_default.err
