@@ -303,7 +303,11 @@ sptk_status sptk_set_tuning(int variant, int64_t run);
  *   (CP-ALS glue tuning), keep_keys 1 (the sort keys emitted at ingest stay resident after
  *   build_perm while memory allows; 0 releases them), pdl 1 (programmatic dependent launch of the MTTKRP and CP-ALS
  *   kernels: a kernel's launch overlaps its predecessor's tail), exchange -1 (sharded CP-ALS row exchange: -1 best available,
- *   0 NCCL broadcast, 1 peer stores, 2 NVLS multimem; sptk_comm_exchange).
+ *   0 NCCL broadcast, 1 peer stores, 2 NVLS multimem; sptk_comm_exchange),
+ *   pad_rank 1 (CP-ALS with R not a multiple of the 32-byte lane vector runs
+ *   on internally padded factors whose pad columns stay zero -- the output is
+ *   the rank-R result; 0: stride R; > 1: pad to a multiple of that many
+ *   columns), sort_v1 0 (1: the round-1 radix downsweep, A/B).
  * Every choice gives the same result up to summation order; options change
  * which kernel computes it.  Not synchronised with calls in flight on other
  * threads.  SPTK_EINVAL for an unknown name. */

@@ -82,12 +82,18 @@ def gpu_perm(sp, t, n):
     ("powerlaw", (532000, 1400, 2), 50000),
     ("uniform", (1, 7, 2), 999),                          # I_n = 1 (0 key bits)
     ("uniform", (3, 4), 1),
+    ("uniform", (4000, 2, 3), 60 * 4096 + 5),              # many tiles: look-back chains
+    ("uniform", (5000, 300, 7), 700 * 4096 + 3),           # > 2 tiles per persistent block
 ])
-def test_perm_bitexact(sp, case):
+@pytest.mark.parametrize("sort", [{}, {"sort_onesweep": 1}, {"sort_v1": 1}, {"sort_pipe": 1}])
+def test_perm_bitexact(sp, case, sort):
+    """Every radix variant (the default, the onesweep passes with decoupled
+    look-back, the round-1 downsweep, the persistent bulk-copy pipeline --
+    incl. misaligned key slices, P % 4 != 0) gives the oracle's stable order."""
     dist, dims, P = case
     idx, vals = synth.tensor(41, dims, P, dist)
     for keep in (1, 0):
-        with sp.options(keep_keys=keep):
+        with sp.options(keep_keys=keep, **sort):
             t = make(sp, dims, idx, vals)
             sp.build_perm(t, -1)            # sorts from the keys the ingest pass emitted
             for n in range(len(dims)):
