@@ -1159,6 +1159,18 @@ struct AlsCtx {
     int nb_apply = 0;                      // block cap of apply_gram
     // sharded deferred path: factor replicas in the comm's symmetric buffer
     bool sym_iter = false;
+    // pre-zeroed MTTKRP outputs (single GPU): mode n writes V buffer vb[n];
+    // consecutive modes use different buffers, and the buffer a mode's apply
+    // has just released is zeroed on the side stream for its next user while
+    // the next MTTKRP runs -- the zeroing (LBNL's 868K-row mode: 111 MB,
+    // 17 us) leaves the critical path.  zsame[m]: mode m's buffer is zeroed
+    // earlier in the same iteration (its MTTKRP waits for ev_zero[m]);
+    // otherwise in the previous iteration (graph launches are serialised).
+    bool prezero = false;
+    void *vbuf[3] = {};
+    int vb[kMaxModes] = {};
+    int znext[kMaxModes] = {};  // the mode whose buffer is zeroed when mode n starts
+    bool zsame[kMaxModes] = {};
     std::vector<size_t> off;               // byte offset of A_m in c.comm->sym
 };
 
@@ -1326,7 +1338,6 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
     double *scal = w.scal.as<double>();
     int *status = reinterpret_cast<int *>(scal + 8);
     double *Ginv = w.L.as<double>();
-    T *V = w.V.as<T>();
     double *s_all = w.scl.as<double>();                      // N x R column scales
     double *graw = s_all + (size_t)N * R;                    // R x R Gram of A_raw
     T *scale = reinterpret_cast<T *>(graw + (size_t)R * R);  // R: next MTTKRP's weights
@@ -1336,6 +1347,7 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
     for (int n = 0; n < N; ++n) {
         const bool last = n == N - 1;
         const int64_t I = t->dims[n];
+        T *V = c.prezero ? static_cast<T *>(c.vbuf[c.vb[n]]) : w.V.as<T>();
         // side stream: Gamma^{-1} for mode n once G_{n-1} is final
         SPTK_CUDA(cudaEventRecord(w.ev_gram, c.s));
         SPTK_CUDA(cudaStreamWaitEvent(w.side, w.ev_gram, 0));
@@ -1343,8 +1355,16 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
         count_launch();
         SPTK_CUDA(cudaGetLastError());
         SPTK_CUDA(cudaEventRecord(w.ev_inv, w.side));
+        if (c.prezero) {  // the buffer mode n-1's apply released, for its next user
+            const int m = c.znext[n];
+            SPTK_CUDA(cudaMemsetAsync(c.vbuf[c.vb[m]], 0, sizeof(T) * (size_t)t->dims[m] * R,
+                                      w.side));
+            if (c.zsame[m]) SPTK_CUDA(cudaEventRecord(w.ev_zero[m], w.side));
+            if (c.zsame[n]) SPTK_CUDA(cudaStreamWaitEvent(c.s, w.ev_zero[n], 0));
+        }
         // V = MTTKRP with the normalised factors: raw factors, column scales at the flush
-        SPTK_TRY(mttkrp_launch(t, n, c.R, c.A.data(), deferred ? scale : nullptr, V, 0, I, c.s));
+        SPTK_TRY(mttkrp_launch(t, n, c.R, c.A.data(), deferred ? scale : nullptr, V, 0, I, c.s,
+                               c.prezero));
         SPTK_CUDA(cudaStreamWaitEvent(c.s, w.ev_inv, 0));
         T *An = static_cast<T *>(c.A[n]);
         double *psq = w.partial.as<double>();
@@ -1435,6 +1455,10 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
             }
         }
         SPTK_CUDA(cudaGetLastError());
+    }
+    if (c.prezero) {  // join the side stream's last zeroing (graph capture needs every fork joined)
+        SPTK_CUDA(cudaEventRecord(w.ev_join, w.side));
+        SPTK_CUDA(cudaStreamWaitEvent(c.s, w.ev_join, 0));
     }
     // fit and status to pinned host memory (a graph-capturable copy)
     SPTK_CUDA(cudaMemcpyAsync(w.hres, scal, sizeof(double) * 9, cudaMemcpyDeviceToHost, c.s));
@@ -1634,6 +1658,8 @@ static std::vector<uint64_t> graph_key(AlsCtx &c, cudaStream_t s) {
     addp(c.comm);
     add(options_generation());
     add(c.sym_iter);
+    add(c.prezero);
+    for (const void *p : c.vbuf) addp(p);
     add((uint64_t)c.part_stride);
     add((uint64_t)c.nb_apply);
     add((uint64_t)c.nblocks);
@@ -1735,6 +1761,8 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t Rl, int max_iters, double 
         SPTK_CUDA(cudaStreamCreateWithFlags(&w.side, cudaStreamNonBlocking));
         SPTK_CUDA(cudaEventCreateWithFlags(&w.ev_gram, cudaEventDisableTiming));
         SPTK_CUDA(cudaEventCreateWithFlags(&w.ev_inv, cudaEventDisableTiming));
+        SPTK_CUDA(cudaEventCreateWithFlags(&w.ev_join, cudaEventDisableTiming));
+        for (cudaEvent_t &e : w.ev_zero) SPTK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     SPTK_CUDA(cudaMemsetAsync(w.scal.p, 0, sizeof(double) * 16, s));
     w.R = R;
@@ -1800,6 +1828,34 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t Rl, int max_iters, double 
         }
     }
     for (int m = 0; m < N; ++m) SPTK_TRY(gram<T>(c, m));
+    // pre-zeroed MTTKRP output buffers (AlsCtx::prezero): 2 for even N, a third
+    // for the last mode of odd N; buffer b holds the longest of its modes
+    c.prezero = !multi && opt(OPT_PREZERO) != 0;
+    if (c.prezero) {
+        int64_t rows[3] = {0, 0, 0};
+        for (int n = 0; n < N; ++n) {
+            c.vb[n] = (N % 2 == 1 && n == N - 1) ? 2 : n % 2;
+            rows[c.vb[n]] = std::max(rows[c.vb[n]], t->dims[n]);
+        }
+        c.vbuf[0] = w.V.p;
+        if (w.V2.reserve(es * std::max<int64_t>(rows[1], 1) * R) != SPTK_OK ||
+            (rows[2] && w.V3.reserve(es * rows[2] * R) != SPTK_OK)) {
+            set_error("");  // no room: zero inside each MTTKRP launch instead
+            c.prezero = false;
+        }
+        c.vbuf[1] = w.V2.p;
+        c.vbuf[2] = rows[2] ? w.V3.p : nullptr;
+        for (int n = 0; n < N && c.prezero; ++n) {
+            const int p = (n + N - 1) % N;  // its apply has released buffer vb[p]
+            int k = 1;
+            while (c.vb[(p + k) % N] != c.vb[p]) ++k;
+            const int m = (p + k) % N;      // the next mode writing that buffer
+            c.znext[n] = m;
+            c.zsame[m] = p == N - 1 || p + k <= N - 1;
+        }
+        for (int b = 0; b < 3 && c.prezero; ++b)
+            if (rows[b]) SPTK_CUDA(cudaMemsetAsync(c.vbuf[b], 0, es * rows[b] * R, s));
+    }
     // deferred normalisation state (single GPU, R <= 32): all scales 1, and the
     // first MTTKRP's column weights 1
     const bool deferred = (!multi || c.sym_iter) && deferred_norm(R);

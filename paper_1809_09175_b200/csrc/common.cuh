@@ -52,7 +52,7 @@ enum Opt {
     OPT_RUN, OPT_VARIANT, OPT_SLICE, OPT_SLICE_L2_KB, OPT_SLICE_ROWS, OPT_SLICE_OTHER_FIRST,
     OPT_ROWREC, OPT_FORCE_V, OPT_GENERIC, OPT_DEBUG_DISPATCH, OPT_COPY_ORDER, OPT_DEFERRED_NORM,
     OPT_NO_GRAPH, OPT_GAMMA_INV_CHOL, OPT_USE_COPY, OPT_APPLY_TILE, OPT_APPLY_NB_MULT, OPT_TAIL_ROWS, OPT_APPLY_WAVE, OPT_APPLY_WARP,
-    OPT_KEEP_KEYS, OPT_PDL, OPT_EXCHANGE, OPT_PAD_RANK, OPT_SORT_V1, OPT_SORT_ONESWEEP, OPT_SORT_PIPE, OPT_COUNT
+    OPT_KEEP_KEYS, OPT_PDL, OPT_EXCHANGE, OPT_PAD_RANK, OPT_SORT_V1, OPT_PREZERO, OPT_COUNT
 };
 int64_t opt(Opt o);
 uint64_t options_generation();  // bumped by every sptk_set_option / sptk_reset_options
@@ -108,6 +108,7 @@ bool is_device_ptr(const void *p);
 struct ALSWork {
     int64_t R = 0;
     DevBuf V;         // Imax x R (T)
+    DevBuf V2, V3;    // further MTTKRP output buffers (pre-zeroed V, see als.cu)
     DevBuf G;         // N x R x R (f64) Gram matrices
     DevBuf L;         // R x R (f64) Cholesky factor of Gamma
     DevBuf partial;   // per-block partial sums (f64)
@@ -121,7 +122,8 @@ struct ALSWork {
     DevBuf scl;       // deferred normalisation: s_m = 1/lambda_m (N x R f64), then the
                       // next MTTKRP's column scale prod_{m != n} s_m (R, tensor dtype)
     cudaStream_t side = nullptr;              // Cholesky / inverse, overlapped with MTTKRP
-    cudaEvent_t ev_gram = nullptr, ev_inv = nullptr;
+    cudaEvent_t ev_gram = nullptr, ev_inv = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_zero[8] = {};              // mode n's V buffer zeroed (side stream)
     double *hres = nullptr;                   // pinned: fit, inner, ||M||^2, ..., status
     // the instantiated iteration graph of the last sptk_cp_als call, replayed
     // by the next call when nothing it captured has changed (key: every buffer
@@ -142,6 +144,9 @@ struct ALSWork {
         if (hres) cudaFreeHost(hres);
         if (ev_gram) cudaEventDestroy(ev_gram);
         if (ev_inv) cudaEventDestroy(ev_inv);
+        if (ev_join) cudaEventDestroy(ev_join);
+        for (cudaEvent_t e : ev_zero)
+            if (e) cudaEventDestroy(e);
         if (side) cudaStreamDestroy(side);
     }
 };
@@ -250,9 +255,11 @@ sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s);
 sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s);
 void drop_copies(sptk_tensor t);
 sptk_status merge_duplicates(sptk_tensor t, bool error_only, cudaStream_t s);
+// out_zeroed: the caller already zeroed rows [row_begin, row_end) of out
+// (CP-ALS zeroes the next mode's V buffer off the critical path)
 sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const *factors,
                           const void *lambda, void *out, int64_t row_begin, int64_t row_end,
-                          cudaStream_t s);
+                          cudaStream_t s, bool out_zeroed = false);
 sptk_status host_rowptr(sptk_tensor t, int mode, cudaStream_t s);
 size_t owned_bytes(sptk_tensor t);  // device bytes held by the handle
 int64_t row_max(sptk_tensor t, int mode, cudaStream_t s);  // longest row of a sorted mode

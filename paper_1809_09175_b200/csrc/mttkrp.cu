@@ -301,11 +301,11 @@ static sptk_status slice_offsets(sptk_tensor t, int mode, int64_t r0, int64_t r1
 
 sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const *factors,
                           const void *lambda, void *out, int64_t row_begin, int64_t row_end,
-                          cudaStream_t s) {
+                          cudaStream_t s, bool out_zeroed) {
     const int64_t In = t->dims[mode];
     const size_t es = dtype_bytes(t->dtype);
     if (row_end <= row_begin) return SPTK_OK;
-    {   // zero the output rows (a kernel, not a memset node: PDL chains through it)
+    if (!out_zeroed) {   // zero the output rows (a kernel, not a memset node: PDL chains through it)
         const int64_t words = (row_end - row_begin) * R * (int64_t)es / 4;
         uint32_t *o = reinterpret_cast<uint32_t *>(static_cast<char *>(out) + (size_t)row_begin * R * es);
         int64_t blocks = (words / 4 + 255) / 256;

@@ -51,8 +51,7 @@ constexpr OptDef kOpts[] = {
     {"pad_rank", 1},            // CP-ALS: R not a multiple of the 32-byte lane vector runs on
                                 //   factors padded with zero columns (0: stride R)
     {"sort_v1", 0},             // 1: round-1 radix downsweep (A/B)
-    {"sort_onesweep", 0},       // 1: onesweep radix passes (decoupled look-back, no upsweep/scan)
-    {"sort_pipe", 0},           // 1: persistent downsweep, next tile bulk-copied during the ranking
+    {"prezero", 1},             // CP-ALS: MTTKRP outputs zeroed on the side stream, off the critical path
 };
 
 static_assert(sizeof(kOpts) / sizeof(kOpts[0]) == OPT_COUNT, "kOpts must list every Opt, in order");

@@ -36,7 +36,7 @@ constexpr int kScanChunk = 4096;
 // radix-sort workspace in 32-bit words: keys x2, values, digit counts, scan sums
 static size_t sort_ws_words(int64_t P) {
     const size_t nP = (size_t)P, ncnt = (size_t)((P + kSortTile - 1) / kSortTile) * 256;
-    return 3 * nP + ncnt + (ncnt + kScanChunk - 1) / kScanChunk + 64 + 4 * 256 + 64;
+    return 3 * nP + ncnt + (ncnt + kScanChunk - 1) / kScanChunk + 64;
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -207,39 +207,16 @@ struct DownsweepSmem {
     uint32_t wbase[kSortWarps][1 << DB];  // per-warp running count, then tile position base
     int32_t delta[1 << DB];               // global run start - tile start of each digit
     uint32_t wsum[kSortWarps];
-    uint32_t gsum[kSortWarps];
-    uint32_t tile;                        // onesweep: this block's tile (arrival order)
     uint32_t skey[kSortTile];
     uint32_t sval[kSortTile];
 };
 
-// Onesweep status word of (tile, digit): bits 31-30 the flag (0 not yet,
-// 1 the tile's own count, 2 the inclusive prefix over tiles 0..t), bits 29-0
-// the count (P < 2^30 on this path).
-constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCountMask = (1u << 30) - 1;
-__device__ __forceinline__ void st_status(uint32_t *p, uint32_t v) {
-    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_status(const uint32_t *p) {
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-// ONE = false: the digit runs' global starts come from the upsweep + scan
-// (`offsets`, digit-major over tiles).  ONE = true (onesweep): the tile is
-// taken in arrival order (atomic counter, so every earlier tile is running or
-// done), its digit counts are published to `status` and each digit's start is
-// the pass's global digit start (exclusive scan of `ghist`) plus a decoupled
-// look-back over the earlier tiles' published counts -- no upsweep, no scan.
-template <int DB, bool FULL, bool ONE>
+template <int DB, bool FULL>
 __device__ __forceinline__ void downsweep_body(DownsweepSmem<DB> &sm, uint32_t tile,
                                                const uint32_t *__restrict__ keys_in,
                                                const uint32_t *__restrict__ vals_in, uint32_t P,
                                                int shift, uint32_t ntiles,
                                                const uint32_t *__restrict__ offsets,
-                                               const uint32_t *__restrict__ ghist,
-                                               uint32_t *__restrict__ status,
                                                uint32_t *__restrict__ keys_out,
                                                uint32_t *__restrict__ vals_out) {
     constexpr int ND = 1 << DB;
@@ -321,44 +298,11 @@ __device__ __forceinline__ void downsweep_body(DownsweepSmem<DB> &sm, uint32_t t
 #pragma unroll
         for (int w = 0; w < kSortWarps; ++w)
             if (w < warp) wpre += wsum[w];
-        if constexpr (!ONE) {
-            if (d < ND) {
-                const uint32_t lstart = wpre + inc - tot;
+        if (d < ND) {
+            const uint32_t lstart = wpre + inc - tot;
 #pragma unroll
-                for (int w = 0; w < kSortWarps; ++w) wbase[w][d] += lstart;
-                delta[d] = (int32_t)(offsets[(size_t)d * ntiles + tile] - lstart);
-            }
-        } else {
-            if (d < ND) st_status(status + (size_t)tile * ND + d, (tile ? kFlagAgg : kFlagInc) | tot);
-            // the pass's global start of digit d: exclusive scan of ghist
-            const uint32_t gh = d < ND ? __ldg(ghist + d) : 0u;
-            uint32_t ginc = gh;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t u = __shfl_up_sync(0xffffffffu, ginc, o);
-                if (lane >= o) ginc += u;
-            }
-            if (lane == 31) sm.gsum[warp] = ginc;
-            __syncthreads();
-            uint32_t gpre = 0;
-#pragma unroll
-            for (int w = 0; w < kSortWarps; ++w)
-                if (w < warp) gpre += sm.gsum[w];
-            if (d < ND) {
-                const uint32_t lstart = wpre + inc - tot;
-#pragma unroll
-                for (int w = 0; w < kSortWarps; ++w) wbase[w][d] += lstart;
-                uint32_t excl = 0;  // keys of digit d in tiles 0..tile-1
-                for (int64_t j = (int64_t)tile - 1; j >= 0;) {
-                    const uint32_t v = ld_status(status + (size_t)j * ND + d);
-                    if (!(v >> 30)) continue;  // not published yet: spin
-                    excl += v & kCountMask;
-                    if (v & kFlagInc) break;
-                    --j;
-                }
-                if (tile) st_status(status + (size_t)tile * ND + d, kFlagInc | (excl + tot));
-                delta[d] = (int32_t)(gpre + ginc - gh + excl - lstart);
-            }
+            for (int w = 0; w < kSortWarps; ++w) wbase[w][d] += lstart;
+            delta[d] = (int32_t)(offsets[(size_t)d * ntiles + tile] - lstart);
         }
     }
     __syncthreads();
@@ -389,278 +333,11 @@ __global__ void __launch_bounds__(kSortThreads, SPTK_DS_MINB)
                      uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out) {
     __shared__ DownsweepSmem<DB> sm;
     if ((blockIdx.x + 1) * (uint64_t)kSortTile <= P)
-        downsweep_body<DB, true, false>(sm, blockIdx.x, keys_in, vals_in, P, shift, ntiles, offsets,
-                                        nullptr, nullptr, keys_out, vals_out);
+        downsweep_body<DB, true>(sm, blockIdx.x, keys_in, vals_in, P, shift, ntiles, offsets,
+                                 keys_out, vals_out);
     else
-        downsweep_body<DB, false, false>(sm, blockIdx.x, keys_in, vals_in, P, shift, ntiles, offsets,
-                                         nullptr, nullptr, keys_out, vals_out);
-}
-
-// ---------------------------------------------------- pipelined downsweep
-// Persistent variant: each block walks tiles blockIdx.x, +gridDim.x, ...; the
-// next tile's keys (and values) are fetched by the bulk-copy engine
-// (cp.async.bulk, mbarrier completion) into the other of two shared-memory
-// stages while this tile is ranked and scattered, so HBM reads stay in
-// flight through the ranking (the one-tile-per-block kernels above load a
-// tile, then compute with nothing in flight: long-scoreboard-bound at ~3 TB/s,
-// profiles/r02/s2).  Keys and values are read from the stage, so the ranks are
-// the only per-key registers.  An array not 16-byte aligned (a mode's slice
-// of the ingest keys, P % 4 != 0) is copied from the aligned address below it
-// (up to 3 extra words, read at an offset); the partial last tile is loaded
-// by the threads.
-template <int DB>
-struct PipeSmem {
-    uint32_t in_key[2][kSortTile + 4];
-    uint32_t in_val[2][kSortTile + 4];
-    uint32_t skey[kSortTile];
-    uint32_t sval[kSortTile];
-    uint32_t wbase[kSortWarps][1 << DB];
-    int32_t delta[1 << DB];
-    uint32_t wsum[kSortWarps];
-    alignas(8) uint64_t bar[2];
-};
-
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-        ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
-        "r"((uint32_t)__cvta_generic_to_shared(bar))
-        : "memory");
-}
-__device__ __forceinline__ void bar_expect(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                 ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile("{\n\t.reg .pred p;\n"
-                 "WAIT%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-                 "@!p bra WAIT%=;\n\t}"
-                 ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(parity) : "memory");
-}
-
-template <int DB>
-__global__ void __launch_bounds__(kSortThreads, 2)
-    radix_downsweep_pipe(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
-                         uint32_t P, int shift, uint32_t ntiles,
-                         const uint32_t *__restrict__ offsets, uint32_t *__restrict__ keys_out,
-                         uint32_t *__restrict__ vals_out) {
-    constexpr int ND = 1 << DB;
-    constexpr uint32_t MASK = ND - 1;
-    extern __shared__ __align__(128) unsigned char smraw[];
-    PipeSmem<DB> &sm = *reinterpret_cast<PipeSmem<DB> *>(smraw);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t lt = lanemask_lt();
-    // word offset of each array from the 16-byte boundary below it
-    const uint32_t koff = (uint32_t)(reinterpret_cast<uintptr_t>(keys_in) & 15) >> 2;
-    const uint32_t voff = vals_in ? (uint32_t)(reinterpret_cast<uintptr_t>(vals_in) & 15) >> 2 : 0u;
-    const uint32_t *kbase = keys_in - koff, *vbase = vals_in ? vals_in - voff : nullptr;
-    if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;"
-                     ::"r"((uint32_t)__cvta_generic_to_shared(&sm.bar[0])));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;"
-                     ::"r"((uint32_t)__cvta_generic_to_shared(&sm.bar[1])));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    // full tiles whose (over-)read stays inside [0, P)
-    auto bulk_ok = [&](uint32_t t) {
-        return (uint64_t)(t + 1) * kSortTile + ((koff | voff) ? 4 : 0) <= P;
-    };
-    auto issue = [&](uint32_t t, int st) {  // thread 0: start the bulk copy of tile t
-        const uint32_t kb = (kSortTile + (koff ? 4u : 0u)) * 4u;
-        const uint32_t vb = vals_in ? (kSortTile + (voff ? 4u : 0u)) * 4u : 0u;
-        bar_expect(&sm.bar[st], kb + vb);
-        bulk_g2s(sm.in_key[st], kbase + (size_t)t * kSortTile, kb, &sm.bar[st]);
-        if (vals_in) bulk_g2s(sm.in_val[st], vbase + (size_t)t * kSortTile, vb, &sm.bar[st]);
-    };
-    uint32_t phase = 0;  // bit st: parity of the next completion of stage st's barrier
-    uint32_t t = blockIdx.x;
-    if (t < ntiles && tid == 0 && bulk_ok(t)) issue(t, 0);
-    for (int k = 0; t < ntiles; t += gridDim.x, ++k) {
-        const int st = k & 1;
-        const uint32_t nx = t + gridDim.x;
-        if (nx < ntiles && tid == 0 && bulk_ok(nx)) issue(nx, st ^ 1);
-        const uint32_t tile0 = t * (uint32_t)kSortTile;
-        const uint32_t tile_n = min((uint32_t)kSortTile, P - tile0);
-        const uint32_t *ik = sm.in_key[st] + koff;
-        const uint32_t *iv = sm.in_val[st] + voff;
-        if (bulk_ok(t)) {
-            bar_wait(&sm.bar[st], (phase >> st) & 1u);
-            phase ^= 1u << st;
-        } else {  // partial last tile: the threads load it
-            uint32_t *ikw = sm.in_key[st] + koff, *ivw = sm.in_val[st] + voff;
-            for (uint32_t j = tid; j < tile_n; j += kSortThreads) {
-                ikw[j] = __ldg(keys_in + tile0 + j);
-                if (vals_in) ivw[j] = __ldg(vals_in + tile0 + j);
-            }
-            for (uint32_t j = tile_n + tid; j < (uint32_t)kSortTile; j += kSortThreads) ikw[j] = 0u;
-            __syncthreads();
-        }
-        for (int d = lane; d < ND; d += 32) sm.wbase[warp][d] = 0;
-        __syncwarp();
-        // A: stable rank among the equal digits of the warp's 512-key chunk
-        const uint32_t wb = warp * (uint32_t)kWarpChunk;
-        uint32_t rank[kSortItems];
-#pragma unroll
-        for (int r = 0; r < kSortItems; ++r) {
-            const uint32_t j = wb + r * 32 + lane;
-            const bool valid = j < tile_n;
-            const uint32_t digit = (ik[j] >> shift) & MASK;
-            uint32_t peers = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-            for (int b = 0; b < DB; ++b)
-                asm("{\n\t.reg .pred p;\n\t.reg .b32 m;\n\t"
-                    "and.b32 m, %1, %2;\n\t"
-                    "setp.ne.u32 p, m, 0;\n\t"
-                    "vote.sync.ballot.b32 m, p, 0xffffffff;\n\t"
-                    "@!p not.b32 m, m;\n\t"
-                    "and.b32 %0, %0, m;\n\t}"
-                    : "+r"(peers) : "r"(digit), "r"(1u << b));
-            const uint32_t below = __popc(peers & lt);
-            uint32_t c = 0;
-            if (valid) c = sm.wbase[warp][digit];
-            __syncwarp();
-            if (valid && below == 0) sm.wbase[warp][digit] = c + __popc(peers);
-            __syncwarp();
-            rank[r] = c + below;
-        }
-        __syncthreads();
-        // B: tile positions of each warp's digit runs, global run starts
-        {
-            const int d = tid;
-            uint32_t tot = 0;
-            if (d < ND) {
-#pragma unroll
-                for (int w = 0; w < kSortWarps; ++w) {
-                    const uint32_t c = sm.wbase[w][d];
-                    sm.wbase[w][d] = tot;
-                    tot += c;
-                }
-            }
-            uint32_t inc = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += u;
-            }
-            if (lane == 31) sm.wsum[warp] = inc;
-            __syncthreads();
-            uint32_t wpre = 0;
-#pragma unroll
-            for (int w = 0; w < kSortWarps; ++w)
-                if (w < warp) wpre += sm.wsum[w];
-            if (d < ND) {
-                const uint32_t lstart = wpre + inc - tot;
-#pragma unroll
-                for (int w = 0; w < kSortWarps; ++w) sm.wbase[w][d] += lstart;
-                sm.delta[d] = (int32_t)(offsets[(size_t)d * ntiles + t] - lstart);
-            }
-        }
-        __syncthreads();
-        // C: scatter the stage into tile order
-#pragma unroll
-        for (int r = 0; r < kSortItems; ++r) {
-            const uint32_t j = wb + r * 32 + lane;
-            if (j < tile_n) {
-                const uint32_t key = ik[j];
-                const uint32_t pos = sm.wbase[warp][(key >> shift) & MASK] + rank[r];
-                sm.skey[pos] = key;
-                sm.sval[pos] = vals_in ? iv[j] : tile0 + j;
-            }
-        }
-        __syncthreads();
-        // D: coalesced write-out of the digit runs
-#pragma unroll 4
-        for (uint32_t j = tid; j < tile_n; j += kSortThreads) {
-            const uint32_t key = sm.skey[j];
-            const uint32_t g = (uint32_t)((int32_t)j + sm.delta[(key >> shift) & MASK]);
-            if (keys_out) keys_out[g] = key;
-            vals_out[g] = sm.sval[j];
-        }
-        __syncthreads();  // skey/sval and this stage are free again
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-}
-
-static cudaError_t launch_downsweep_pipe(int db, cudaStream_t s, const uint32_t *kin,
-                                         const uint32_t *vin, uint32_t P, int shift,
-                                         uint32_t ntiles, const uint32_t *offsets, uint32_t *kout,
-                                         uint32_t *vout) {
-    static bool attr[64][9] = {};  // per device, per digit width
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)dev_sms() * 2);
-#define SPTK_DP(D)                                                                                \
-    case D: {                                                                                     \
-        const size_t smb = sizeof(PipeSmem<D>);                                                   \
-        if (dev < 64 && !attr[dev][D]) {                                                          \
-            cudaFuncSetAttribute(radix_downsweep_pipe<D>,                                         \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);          \
-            attr[dev][D] = true;                                                                  \
-        }                                                                                         \
-        radix_downsweep_pipe<D><<<grid, kSortThreads, smb, s>>>(kin, vin, P, shift, ntiles,      \
-                                                                offsets, kout, vout);             \
-        break;                                                                                    \
-    }
-    switch (db) {
-        SPTK_DP(1) SPTK_DP(2) SPTK_DP(3) SPTK_DP(4) SPTK_DP(5) SPTK_DP(6) SPTK_DP(7) SPTK_DP(8)
-    default: return cudaErrorInvalidValue;
-    }
-#undef SPTK_DP
-    return cudaGetLastError();
-}
-
-// One onesweep pass; status = ntiles x 2^DB words + the tile counter, zeroed.
-template <int DB>
-__global__ void __launch_bounds__(kSortThreads, SPTK_DS_MINB)
-    radix_onesweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
-                   uint32_t P, int shift, uint32_t ntiles, const uint32_t *__restrict__ ghist,
-                   uint32_t *__restrict__ status, uint32_t *__restrict__ keys_out,
-                   uint32_t *__restrict__ vals_out) {
-    __shared__ DownsweepSmem<DB> sm;
-    if (threadIdx.x == 0) sm.tile = atomicAdd(status + (size_t)ntiles * (1u << DB), 1u);
-    __syncthreads();
-    const uint32_t tile = sm.tile;
-    if ((tile + 1) * (uint64_t)kSortTile <= P)
-        downsweep_body<DB, true, true>(sm, tile, keys_in, vals_in, P, shift, ntiles, nullptr, ghist,
-                                       status, keys_out, vals_out);
-    else
-        downsweep_body<DB, false, true>(sm, tile, keys_in, vals_in, P, shift, ntiles, nullptr, ghist,
-                                        status, keys_out, vals_out);
-}
-
-// ghist[p][d] = number of keys whose pass-p digit is d (all passes, one read)
-__global__ void __launch_bounds__(256)
-    radix_hist_all(const uint32_t *__restrict__ keys, uint32_t P, int npass, int dbits, int bits,
-                   uint32_t *__restrict__ ghist) {
-    __shared__ uint32_t h[4][256];
-    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
-    __syncthreads();
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
-        const uint32_t k = __ldg(keys + i);
-        for (int p = 0; p < npass; ++p) {
-            const int shift = p * dbits;
-            const int db = (shift + dbits > bits) ? bits - shift : dbits;
-            atomicAdd(&h[p][(k >> shift) & ((1u << db) - 1)], 1u);
-        }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < npass * 256; i += blockDim.x)
-        if ((&h[0][0])[i]) atomicAdd(ghist + i, (&h[0][0])[i]);
-}
-
-static cudaError_t launch_onesweep(int db, unsigned grid, cudaStream_t s, const uint32_t *kin,
-                                   const uint32_t *vin, uint32_t P, int shift, uint32_t ntiles,
-                                   const uint32_t *ghist, uint32_t *status, uint32_t *kout,
-                                   uint32_t *vout) {
-#define SPTK_OS(D) \
-    case D: radix_onesweep<D><<<grid, kSortThreads, 0, s>>>(kin, vin, P, shift, ntiles, ghist, status, kout, vout); break;
-    switch (db) {
-        SPTK_OS(1) SPTK_OS(2) SPTK_OS(3) SPTK_OS(4) SPTK_OS(5) SPTK_OS(6) SPTK_OS(7) SPTK_OS(8)
-    default: return cudaErrorInvalidValue;
-    }
-#undef SPTK_OS
-    return cudaGetLastError();
+        downsweep_body<DB, false>(sm, blockIdx.x, keys_in, vals_in, P, shift, ntiles, offsets,
+                                  keys_out, vals_out);
 }
 
 static cudaError_t launch_downsweep2(int db, unsigned grid, cudaStream_t s, const uint32_t *kin,
@@ -1102,34 +779,6 @@ static sptk_status stable_sort_ids(sptk_tensor t, int mode, const uint32_t *in, 
         SPTK_CUDA(cudaGetLastError());
     }
     const uint32_t *kin = k0, *vin = in;
-    // onesweep (P < 2^30: 30-bit status counts): one histogram of every
-    // pass's digits, then one kernel per pass -- status words in the counts
-    // region (ntiles x 2^db + the tile counter <= ntiles x 256 + 1 words)
-    if (opt(OPT_SORT_ONESWEEP) && !opt(OPT_SORT_V1) && P < ((int64_t)1 << 30)) {
-        uint32_t *ghist = tmp + (ncnt + kScanChunk - 1) / kScanChunk + 64;
-        SPTK_CUDA(cudaMemsetAsync(ghist, 0, sizeof(uint32_t) * 4 * 256, s));
-        radix_hist_all<<<(unsigned)std::min<int64_t>((int64_t)dev_sms() * 8, (P + 255) / 256), 256, 0,
-                         s>>>(kin, (uint32_t)P, npass, dbits, bits, ghist);
-        count_launch();
-        SPTK_CUDA(cudaGetLastError());
-        for (int p = 0; p < npass; ++p) {
-            const int shift = p * dbits;
-            const int db = bits == 0 ? 1 : ((shift + dbits > bits) ? bits - shift : dbits);
-            uint32_t *kout = kbuf[(npass - 1 - p) & 1];
-            uint32_t *vout = vbuf[((npass - 1 - p) & 1) ^ 1];
-            const bool keys_needed = keys_out || p + 1 < npass;
-            SPTK_CUDA(cudaMemsetAsync(counts, 0,
-                                      sizeof(uint32_t) * ((size_t)ntiles * ((size_t)1 << db) + 1), s));
-            SPTK_CUDA(launch_onesweep(db, (unsigned)ntiles, s, kin, vin, (uint32_t)P, shift,
-                                      (uint32_t)ntiles, ghist + 256 * p, counts,
-                                      keys_needed ? kout : nullptr, vout));
-            count_launch();
-            kin = kout;
-            vin = vout;
-        }
-        if (keys_out) *keys_out = const_cast<uint32_t *>(kin);
-        return SPTK_OK;
-    }
     for (int p = 0; p < npass; ++p) {
         const int shift = p * dbits;
         const int db = bits == 0 ? 1 : ((shift + dbits > bits) ? bits - shift : dbits);
@@ -1143,10 +792,6 @@ static sptk_status stable_sort_ids(sptk_tensor t, int mode, const uint32_t *in, 
         if (opt(OPT_SORT_V1)) {
             radix_downsweep<<<(unsigned)ntiles, kSortThreads, 0, s>>>(
                 kin, vin, (uint32_t)P, shift, db, (uint32_t)ntiles, counts, kout, vout);
-        } else if (opt(OPT_SORT_PIPE)) {
-            const bool keys_needed = keys_out || p + 1 < npass;
-            SPTK_CUDA(launch_downsweep_pipe(db, s, kin, vin, (uint32_t)P, shift, (uint32_t)ntiles,
-                                            counts, keys_needed ? kout : nullptr, vout));
         } else {
             // the last pass writes the keys only if the caller wants them
             const bool keys_needed = keys_out || p + 1 < npass;

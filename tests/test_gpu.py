@@ -85,11 +85,11 @@ def gpu_perm(sp, t, n):
     ("uniform", (4000, 2, 3), 60 * 4096 + 5),              # many tiles: look-back chains
     ("uniform", (5000, 300, 7), 700 * 4096 + 3),           # > 2 tiles per persistent block
 ])
-@pytest.mark.parametrize("sort", [{}, {"sort_onesweep": 1}, {"sort_v1": 1}, {"sort_pipe": 1}])
+@pytest.mark.parametrize("sort", [{}, {"sort_v1": 1}])
 def test_perm_bitexact(sp, case, sort):
-    """Every radix variant (the default, the onesweep passes with decoupled
-    look-back, the round-1 downsweep, the persistent bulk-copy pipeline --
-    incl. misaligned key slices, P % 4 != 0) gives the oracle's stable order."""
+    """Both radix downsweeps (the default, the round-1 kernel) give the
+    oracle's stable order, incl. misaligned key slices (P % 4 != 0) and
+    partial last tiles."""
     dist, dims, P = case
     idx, vals = synth.tensor(41, dims, P, dist)
     for keep in (1, 0):
@@ -830,6 +830,28 @@ def test_cp_als_padded_rank(sp, R, dtype, deferred):
     assert np.max(np.abs(resh["trace"] - res["trace"])) <= tp
     for m in range(3):
         assert rel(Fh[m], F[m]) <= (1e-3 if f32 else 1e-9)
+
+
+@pytest.mark.parametrize("dims", [(90, 70), (60, 50, 40), (30, 25, 20, 15), (12, 11, 10, 9, 8)])
+def test_cp_als_prezeroed_outputs(sp, dims):
+    """The MTTKRP outputs zeroed on the side stream for the next mode (two
+    buffers for even N, three for odd N; some zeroed in the same iteration,
+    some in the previous one) give the oracle's trajectory, like zeroing in
+    every launch (prezero=0), eagerly and through the replayed graph."""
+    P = min(int(np.prod(dims)) // 3, 4000)
+    idx, vals = synth.unique_tensor(51, dims, P)
+    R = 8
+    ref = oracle.cp_als(dims, idx, vals, factors_np(52, dims, R), 7)
+    t = make(sp, dims, idx, vals)
+    for opts in ({}, {"prezero": 0}, {"no_graph": 1}):
+        with sp.options(**opts):
+            F = [torch.full((I, R), float("nan"), dtype=torch.float64, device="cuda") for I in dims]
+            res = sp.cp_als(t, R, 7, F, seed=52)
+            res2 = sp.cp_als(t, R, 7, F, seed=52)   # a second call replays the cached graph
+        for r in (res, res2):
+            assert np.max(np.abs(r["trace"] - ref["trace"])) <= 1e-9, opts
+        for m in range(len(dims)):
+            assert rel(F[m].cpu().numpy(), ref["A"][m]) <= 1e-8, (opts, m)
 
 
 @pytest.mark.parametrize("exchange", [0, 1])
