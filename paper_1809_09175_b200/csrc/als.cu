@@ -295,12 +295,85 @@ __global__ void __launch_bounds__(256)
     gj_inv_block(G, N, n, R, Rl, Ginv, status, sm, sm + R * R);
 }
 
+// The same unpivoted Gauss-Jordan (same ridge retry, padded-rank identity
+// block) by ONE warp for R <= 32: lane i holds row i of Gamma in registers;
+// each pivot step broadcasts the pivot row by shuffles and updates every row
+// in parallel -- no block barriers, one FP64 division per step per lane.  The
+// 256-thread kernel above spends 3 block barriers and a serial thread-0
+// division per step: 10-16 us for R = 16 in the LBNL timeline
+// (profiles/r02/s2/timeline_lbnl.log), longer than a short MTTKRP.
+template <int LR>
+__global__ void __launch_bounds__(32)
+    gj_inv_warp_kernel(const double *__restrict__ G, int N, int n, int R, int Rl,
+                       double *__restrict__ Ginv, int *__restrict__ status) {
+    const int i = threadIdx.x;  // row
+    const int RR = R * R;
+    double m[LR];
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        double ridge = 0.0;
+        if (attempt) {  // 1e-12 tr(Gamma_Rl) / Rl, as the oracle
+            double d = 1.0;
+            if (i < Rl) {
+                for (int q = 0; q < N; ++q)
+                    if (q != n) d *= G[(int64_t)q * RR + i * R + i];
+            } else {
+                d = 0.0;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            ridge = 1e-12 * (d / (double)Rl);
+        }
+#pragma unroll
+        for (int k = 0; k < LR; ++k) {
+            double h;
+            if (i >= R || k >= R) {
+                h = 0.0;
+            } else if (i >= Rl || k >= Rl) {
+                h = i == k ? 1.0 : 0.0;
+            } else {
+                h = 1.0;
+                for (int q = 0; q < N; ++q)
+                    if (q != n) h *= G[(int64_t)q * RR + i * R + k];
+                if (i == k) h += ridge;
+            }
+            m[k] = h;
+        }
+        bool bad = false;
+#pragma unroll
+        for (int j = 0; j < LR; ++j) {  // unrolled: m[] stays in registers
+            if (j >= R) break;
+            const double p = __shfl_sync(0xffffffffu, m[j], j);
+            bad |= !(p > 0.0);
+            const double rp = 1.0 / (p > 0.0 ? p : 1.0);
+            const double f = m[j];  // this row's multiplier (row j: the pivot itself)
+#pragma unroll
+            for (int k = 0; k < LR; ++k) {
+                const double rk = __shfl_sync(0xffffffffu, m[k], j) * rp;  // new pivot row
+                const double rkj = (k == j) ? rp : rk;
+                m[k] = (i == j) ? rkj : ((k == j) ? 0.0 : m[k]) - f * rkj;
+            }
+        }
+        if (!bad) break;
+        if (attempt == 1 && i == 0) atomicOr(status, 1);
+    }
+    if (i < R)
+#pragma unroll
+        for (int k = 0; k < LR; ++k)
+            if (k < R) Ginv[i * R + k] = m[k];
+}
+
 // Gamma^{-1} for mode n (SPTK_GAMMA_INV=chol forces the Cholesky kernel);
 // R = the padded rank (row stride), Rl <= R the rank of the decomposition
 static void launch_ginv(const double *G, int N, int n, int R, int Rl, double *Ginv, int *status,
                         cudaStream_t s) {
     if (opt(OPT_GAMMA_INV_CHOL))
         chol_inv_kernel<<<1, 256, sizeof(double) * (R * R + R), s>>>(G, N, n, R, Rl, Ginv, status);
+    else if (opt(OPT_GJ_WARP) && R <= 8)
+        gj_inv_warp_kernel<8><<<1, 32, 0, s>>>(G, N, n, R, Rl, Ginv, status);
+    else if (opt(OPT_GJ_WARP) && R <= 16)
+        gj_inv_warp_kernel<16><<<1, 32, 0, s>>>(G, N, n, R, Rl, Ginv, status);
+    else if (opt(OPT_GJ_WARP) && R <= 32)
+        gj_inv_warp_kernel<32><<<1, 32, 0, s>>>(G, N, n, R, Rl, Ginv, status);
     else
         gj_inv_kernel<<<1, 256, sizeof(double) * (R * R + R), s>>>(G, N, n, R, Rl, Ginv, status);
 }
@@ -956,6 +1029,224 @@ __global__ void __launch_bounds__(256, 2)
     apply_tail<T>(tail, A, R, part_sq, part_dot, gpart);
 }
 
+// ------------------------------------------ apply_gram on the FP64 tensor cores
+// R = 8 RB (8 or 16).  The warp-private kernel above issues 16 + 16 DFMA per
+// row in dependent chains and holds Gamma^{-1} and the Gram row in 64
+// registers (2 blocks/SM): on LBNL's 868K-row mode it ran at 22 % of the FP64
+// pipe and 1.8 TB/s (110-117 us for 222 MB).  Here a warp takes 8 rows at a
+// time and both products are DMMA (mma.sync m8n8k4 f64; the fp64 path of the
+// B200 tensor cores -- tcgen05 has no f64 kind):
+//   A_raw(8 x R) = V(8 x R) Gamma^{-1}(R x R): RB n-blocks x 2RB k-steps,
+//     Gamma^{-1} held as B fragments (2 RB^2 doubles per lane);
+//   G_raw += A_raw^T A_raw over the 8 rows: the RB(RB+1)/2 upper 8x8 blocks
+//     x 2 k-steps, A_raw re-read from shared memory in operand layout;
+// colsq = diag(G_raw); dot(A_raw, V) from the result fragments.  The V tile
+// (8 rows, contiguous since the row stride is R) is one coalesced load per
+// lane, prefetched a tile ahead.  Same per-block partials / tail / exchange
+// stores as the kernels above; a fixed summation order (deterministic).
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// shared-memory row stride of the V / A_raw tiles: 8RB + 4 doubles, so that
+// the fragment loads (8 rows x 4 columns) and stores hit distinct banks per
+// half-warp (a 128-byte row stride put all 8 rows of a column in one bank:
+// 8-way conflicts on every fragment access)
+template <int RB>
+__host__ __device__ constexpr int mma_tile_stride() { return 8 * RB + 4; }
+template <int RB>
+__host__ __device__ constexpr size_t apply_mma_smem_doubles() {
+    // per warp: V tile + A_raw tile (8 rows each); per block: 8 Gram partials
+    // (8RB)^2 + colsq / dot partials 2 x 8 x 8RB
+    return (size_t)8 * 2 * 8 * mma_tile_stride<RB>() + (size_t)8 * (8 * RB) * (8 * RB) +
+           (size_t)2 * 8 * (8 * RB);
+}
+
+#ifndef SPTK_APPLY_MMA_PF  // A/B builds only
+#define SPTK_APPLY_MMA_PF 4
+#endif
+#ifndef SPTK_APPLY_MMA_MINB
+#define SPTK_APPLY_MMA_MINB 2
+#endif
+constexpr int kApplyMmaPf = SPTK_APPLY_MMA_PF;
+
+template <typename T, int RB>
+__global__ void __launch_bounds__(256, SPTK_APPLY_MMA_MINB)
+    apply_gram_mma_kernel(const T *__restrict__ V, int64_t r_begin, int64_t r_end, int R,
+                          const double *__restrict__ Ginv, T *__restrict__ A,
+                          double *__restrict__ part_sq, double *__restrict__ part_dot,
+                          double *__restrict__ gpart, const ModeTail tail, const ExchOut ex) {
+    pdl_wait();
+    constexpr int RR = 8 * RB;       // == R
+    constexpr int PL = RR * 8 / 32;  // V / A_raw tile doubles per lane (2 RB)
+    constexpr int NB = RB * (RB + 1) / 2;
+    extern __shared__ __align__(16) double msm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+    const int g = lane >> 2, q = lane & 3;
+    constexpr int S = mma_tile_stride<RB>();
+    double *vt = msm + warp * 2 * 8 * S;    // [8][S]
+    double *at = vt + 8 * S;                // [8][S]
+    double *gs = msm + 8 * 2 * 8 * S;       // [8 warps][RR][RR]
+    double *ss = gs + 8 * RR * RR;          // [8][RR] colsq partials
+    double *ds = ss + 8 * RR;               // [8][RR] dot partials
+    // Gamma^{-1} as B fragments: gib[ks][nb] = Ginv[4ks + q][8nb + g]
+    double gib[2 * RB][RB];
+#pragma unroll
+    for (int ks = 0; ks < 2 * RB; ++ks)
+#pragma unroll
+        for (int nb = 0; nb < RB; ++nb) gib[ks][nb] = Ginv[(4 * ks + q) * RR + 8 * nb + g];
+    double gacc[NB][2];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) gacc[b][0] = gacc[b][1] = 0.0;
+    double dacc[RB][2];
+#pragma unroll
+    for (int nb = 0; nb < RB; ++nb) dacc[nb][0] = dacc[nb][1] = 0.0;
+    const int64_t ntile = (r_end - r_begin + 7) / 8;
+    const int64_t wstride = (int64_t)gridDim.x * 8;
+    // lane's slice of a V tile: row lane / (32/8... ) -- tile doubles [PL*lane, PL*lane + PL)
+    auto load_tile = [&](int64_t ti, double (&v)[PL]) {
+        const int64_t e0 = (r_begin + ti * 8) * RR + (int64_t)lane * PL;  // element index
+        const int64_t lim = r_end * RR;
+        if (ti < ntile && e0 + PL <= lim) {
+            if constexpr (sizeof(T) == 8 && PL == 4) {
+                const double4 x = *reinterpret_cast<const double4 *>(V + e0);
+                v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+            } else if constexpr (sizeof(T) == 8 && PL == 2) {
+                const double2 x = *reinterpret_cast<const double2 *>(V + e0);
+                v[0] = x.x; v[1] = x.y;
+            } else {
+#pragma unroll
+                for (int k = 0; k < PL; ++k) v[k] = (double)V[e0 + k];
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < PL; ++k) v[k] = (ti < ntile && e0 + k < lim) ? (double)V[e0 + k] : 0.0;
+        }
+    };
+    // V tiles kApplyMmaPf ahead (1 KB per warp each): one tile in flight per
+    // warp kept the tall LBNL mode at ~3.4 TB/s
+    int64_t ti0 = blockIdx.x * (int64_t)8 + warp;
+    double vn[kApplyMmaPf][PL];
+#pragma unroll
+    for (int u = 0; u < kApplyMmaPf; ++u) load_tile(ti0 + u * wstride, vn[u]);
+    for (; ti0 < ntile; ti0 += kApplyMmaPf * wstride)
+#pragma unroll
+    for (int u = 0; u < kApplyMmaPf; ++u) {
+        const int64_t ti = ti0 + u * wstride;
+        if (ti >= ntile) break;
+        {   // the lane's PL consecutive doubles: row lane / (RR / PL), padded stride
+            const int e = lane * PL, row = e / RR, col = e % RR;
+#pragma unroll
+            for (int k = 0; k < PL; ++k) vt[row * S + col + k] = vn[u][k];
+        }
+        load_tile(ti + kApplyMmaPf * wstride, vn[u]);
+        __syncwarp();
+        // A_raw = V Gamma^{-1}: D fragment (row g, cols 8nb + 2q + {0,1})
+        double d[RB][2];
+#pragma unroll
+        for (int nb = 0; nb < RB; ++nb) d[nb][0] = d[nb][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 2 * RB; ++ks) {
+            const double a = vt[g * S + 4 * ks + q];
+#pragma unroll
+            for (int nb = 0; nb < RB; ++nb) dmma(d[nb][0], d[nb][1], a, gib[ks][nb]);
+        }
+        const int64_t r = r_begin + ti * 8 + g;
+        const bool on = r < r_end;
+#pragma unroll
+        for (int nb = 0; nb < RB; ++nb) {
+            const int c = 8 * nb + 2 * q;
+            const T x0 = (T)d[nb][0], x1 = (T)d[nb][1];
+            double y0 = 0.0, y1 = 0.0;
+            if (on) {
+                const int64_t ix = r * RR + c;
+                if (ex.mc) {
+                    mm_store(reinterpret_cast<T *>(ex.mc) + ix, x0);
+                    mm_store(reinterpret_cast<T *>(ex.mc) + ix + 1, x1);
+                } else if (ex.np) {
+                    for (int p = 0; p < ex.np; ++p) {
+                        reinterpret_cast<T *>(ex.peer[p])[ix] = x0;
+                        reinterpret_cast<T *>(ex.peer[p])[ix + 1] = x1;
+                    }
+                } else if constexpr (sizeof(T) == 8) {
+                    *reinterpret_cast<double2 *>(A + ix) = make_double2(x0, x1);
+                } else {
+                    *reinterpret_cast<float2 *>(A + ix) = make_float2(x0, x1);
+                }
+                y0 = (double)x0;
+                y1 = (double)x1;
+            }
+            // the Gram and the fit use the stored (T-rounded) values
+            *reinterpret_cast<double2 *>(at + g * S + c) = make_double2(y0, y1);
+            dacc[nb][0] += y0 * vt[g * S + c];
+            dacc[nb][1] += y1 * vt[g * S + c + 1];
+        }
+        __syncwarp();
+        // G_raw += A_raw^T A_raw: operand fragments f[ks][b] = A_raw[4ks + q][8b + g]
+        double f[2][RB];
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+            for (int b = 0; b < RB; ++b) f[ks][b] = at[(4 * ks + q) * S + 8 * b + g];
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+            int bi = 0;
+#pragma unroll
+            for (int mb = 0; mb < RB; ++mb)
+#pragma unroll
+                for (int nb = mb; nb < RB; ++nb, ++bi) dmma(gacc[bi][0], gacc[bi][1], f[ks][mb], f[ks][nb]);
+        }
+        __syncwarp();
+    }
+    if (ex.np || ex.mc) __threadfence_system();  // replicas written before the all-reduce
+    // per-warp Gram (both triangles) and column partials to shared memory
+    {
+        double *gw = gs + warp * RR * RR;
+        int bi = 0;
+#pragma unroll
+        for (int mb = 0; mb < RB; ++mb)
+#pragma unroll
+            for (int nb = mb; nb < RB; ++nb, ++bi)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int a = 8 * mb + g, b = 8 * nb + 2 * q + e;
+                    gw[a * RR + b] = gacc[bi][e];
+                    if (mb != nb) gw[b * RR + a] = gacc[bi][e];
+                }
+        // dot: sum the 8 row slots (lanes of equal q) in a fixed shuffle order
+#pragma unroll
+        for (int nb = 0; nb < RB; ++nb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                double x = dacc[nb][e];
+#pragma unroll
+                for (int o = 4; o < 32; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+                if (g == 0) ds[warp * RR + 8 * nb + 2 * q + e] = x;
+            }
+    }
+    __syncthreads();
+    for (int c = tid; c < RR; c += blockDim.x)
+        for (int w = 0; w < 8; ++w) ss[w * RR + c] = gs[(w * RR + c) * RR + c];  // colsq = diag
+    __syncthreads();
+    const int RRR = RR * RR;
+    for (int e = tid; e < RRR; e += blockDim.x) {
+        double acc = 0.0;
+        for (int w = 0; w < 8; ++w) acc += gs[w * RRR + e];
+        gpart[(int64_t)blockIdx.x * RRR + e] = acc;
+    }
+    for (int c = tid; c < RR; c += blockDim.x) {
+        double a2 = 0.0, d2 = 0.0;
+        for (int w = 0; w < 8; ++w) {
+            a2 += ss[w * RR + c];
+            d2 += ds[w * RR + c];
+        }
+        part_sq[(int64_t)blockIdx.x * RR + c] = a2;
+        if (part_dot) part_dot[(int64_t)blockIdx.x * RR + c] = d2;
+    }
+    apply_tail<T>(tail, A, RR, part_sq, part_dot, gpart);
+}
+
 // apply_gram grid cap: one full wave of resident blocks (SPTK_APPLY_WAVE=0: the
 // 8-per-SM cap alone, for A/B) -- a tall mode's pass otherwise runs ~2.7 waves
 template <typename T>
@@ -1178,6 +1469,7 @@ struct AlsCtx {
 // (option apply_warp, default) or the shared-memory tile kernel.  small: the
 // caller wants at most kTailBlocks blocks (the last one finalises the mode).
 struct ApplyPlan {
+    bool mma = false;   // apply_gram_mma_kernel (R = 8 or 16)
     bool warp = false;
     int LR = 16, tile = 0, nb = 1;
     int64_t rpb = 0;
@@ -1199,9 +1491,40 @@ static int warp_apply_cap(size_t smb) {
     return occ * dev_sms();
 }
 
+template <typename T, int RB>
+static int mma_apply_cap(size_t smb) {
+    static int occ[64] = {};  // per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 64) dev = 0;
+    if (occ[dev] < 1) {
+        cudaFuncSetAttribute(apply_gram_mma_kernel<T, RB>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[dev], apply_gram_mma_kernel<T, RB>,
+                                                          256, smb) != cudaSuccess ||
+            occ[dev] < 1) {
+            cudaGetLastError();
+            occ[dev] = 1;
+        }
+    }
+    return occ[dev] * dev_sms();
+}
+
 template <typename T>
 static ApplyPlan plan_apply(AlsCtx &c, int64_t rows, int R, bool small) {
     ApplyPlan p;
+    // FP64 tensor-core apply for R = 8 / 16 (R is the padded rank here)
+    p.mma = opt(OPT_APPLY_MMA) != 0 && (R == 8 || R == 16);
+    if (p.mma) {
+        p.LR = R;
+        p.smb = sizeof(double) * (R == 8 ? apply_mma_smem_doubles<1>() : apply_mma_smem_doubles<2>());
+        const int cap = R == 8 ? mma_apply_cap<T, 1>(p.smb) : mma_apply_cap<T, 2>(p.smb);
+        const int64_t tiles = (rows + 7) / 8;
+        int64_t nb = std::min<int64_t>(cap, (tiles + 7) / 8);
+        if (small) nb = std::min<int64_t>(nb, kTailBlocks);
+        p.nb = (int)std::max<int64_t>(nb, 1);
+        return p;
+    }
     // the warp kernel for R <= 16 (LBNL -0.6 %, C1 -1.7 %, NELL-2 and Delicious
     // neutral); at R = 32 its 64 register-held doubles spill (+2.8 %)
     p.warp = opt(OPT_APPLY_WARP) != 0 && R <= 16;
@@ -1240,6 +1563,13 @@ static cudaError_t run_apply(const ApplyPlan &p, cudaStream_t s, const T *V, int
                              int64_t r1, int R, const double *Ginv, T *An, double *psq,
                              double *pdot, double *gpart, const ModeTail &tail,
                              const ExchOut &ex) {
+    if (p.mma) {
+        if (p.LR == 8)
+            return launch_pdl(apply_gram_mma_kernel<T, 1>, p.nb, 256, p.smb, s, V, r0, r1, R, Ginv,
+                              An, psq, pdot, gpart, tail, ex);
+        return launch_pdl(apply_gram_mma_kernel<T, 2>, p.nb, 256, p.smb, s, V, r0, r1, R, Ginv, An,
+                          psq, pdot, gpart, tail, ex);
+    }
     if (p.warp) {
         if (p.LR == 8)
             return launch_pdl(apply_gram_warp_kernel<T, 8>, p.nb, 256, p.smb, s, V, r0, r1, R, Ginv,
@@ -1758,7 +2088,14 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t Rl, int max_iters, double 
     SPTK_TRY(w.scl.reserve(sizeof(double) * ((size_t)N * R + (size_t)R * R + R + 1)));
     if (!w.hres) SPTK_CUDA(cudaMallocHost(&w.hres, sizeof(double) * 16));
     if (!w.side) {
-        SPTK_CUDA(cudaStreamCreateWithFlags(&w.side, cudaStreamNonBlocking));
+        // highest priority: the one-block inverse is scheduled at the next
+        // block retirement of the MTTKRP it overlaps (at default priority it
+        // waited for the MTTKRP's last wave: 10-15 us per mode on the LBNL
+        // critical path, profiles/r02/s2/timeline_lbnl.log)
+        int lo = 0, hi = 0;
+        SPTK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        SPTK_CUDA(cudaStreamCreateWithPriority(&w.side, cudaStreamNonBlocking,
+                                               opt(OPT_SIDE_PRIO) ? hi : 0));
         SPTK_CUDA(cudaEventCreateWithFlags(&w.ev_gram, cudaEventDisableTiming));
         SPTK_CUDA(cudaEventCreateWithFlags(&w.ev_inv, cudaEventDisableTiming));
         SPTK_CUDA(cudaEventCreateWithFlags(&w.ev_join, cudaEventDisableTiming));

@@ -854,6 +854,23 @@ def test_cp_als_prezeroed_outputs(sp, dims):
             assert rel(F[m].cpu().numpy(), ref["A"][m]) <= 1e-8, (opts, m)
 
 
+@pytest.mark.parametrize("R", [8, 16, 24, 32])
+@pytest.mark.parametrize("inv", [{}, {"gj_warp": 0}, {"gamma_inv_chol": 1}])
+def test_cp_als_inverse_kernels(sp, R, inv):
+    """The one-warp Gauss-Jordan (default for R <= 32), the 256-thread one and
+    the Cholesky inverse all follow the oracle's trajectory."""
+    dims = (90, 80, 70)
+    idx, vals = synth.unique_tensor(61, dims, 6000)
+    ref = oracle.cp_als(dims, idx, vals, factors_np(62, dims, R), 6)
+    t = make(sp, dims, idx, vals)
+    with sp.options(**inv):
+        F = [torch.empty(I, R, dtype=torch.float64, device="cuda") for I in dims]
+        res = sp.cp_als(t, R, 6, F, seed=62)
+    assert np.max(np.abs(res["trace"] - ref["trace"])) <= 1e-9
+    for m in range(3):
+        assert rel(F[m].cpu().numpy(), ref["A"][m]) <= 1e-7, m
+
+
 @pytest.mark.parametrize("exchange", [0, 1])
 def test_sharded_zero_column_e1(sp, monkeypatch, exchange):
     """A zero initial column through the sharded deferred path: every Gamma
