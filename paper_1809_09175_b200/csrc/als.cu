@@ -323,20 +323,25 @@ __global__ void __launch_bounds__(32)
             for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
             ridge = 1e-12 * (d / (double)Rl);
         }
+        // Gamma row i: the loads of every mode issued together (unrolled over
+        // kMaxModes), then the Hadamard products
+#pragma unroll
+        for (int k = 0; k < LR; ++k) m[k] = 1.0;
+#pragma unroll
+        for (int q = 0; q < kMaxModes; ++q) {
+            if (q >= N || q == n) continue;
+            double gq[LR];
+#pragma unroll
+            for (int k = 0; k < LR; ++k)
+                gq[k] = (i < Rl && k < Rl) ? __ldg(G + (int64_t)q * RR + i * R + k) : 1.0;
+#pragma unroll
+            for (int k = 0; k < LR; ++k) m[k] *= gq[k];
+        }
 #pragma unroll
         for (int k = 0; k < LR; ++k) {
-            double h;
-            if (i >= R || k >= R) {
-                h = 0.0;
-            } else if (i >= Rl || k >= Rl) {
-                h = i == k ? 1.0 : 0.0;
-            } else {
-                h = 1.0;
-                for (int q = 0; q < N; ++q)
-                    if (q != n) h *= G[(int64_t)q * RR + i * R + k];
-                if (i == k) h += ridge;
-            }
-            m[k] = h;
+            if (i >= R || k >= R) m[k] = 0.0;
+            else if (i >= Rl || k >= Rl) m[k] = i == k ? 1.0 : 0.0;
+            else if (i == k) m[k] += ridge;
         }
         bool bad = false;
 #pragma unroll
@@ -1458,10 +1463,12 @@ struct AlsCtx {
     // earlier in the same iteration (its MTTKRP waits for ev_zero[m]);
     // otherwise in the previous iteration (graph launches are serialised).
     bool prezero = false;
+    bool copy_fit = true;  // per-iteration D2H of (fit, status) inside the iteration
     void *vbuf[3] = {};
     int vb[kMaxModes] = {};
     int znext[kMaxModes] = {};  // the mode whose buffer is zeroed when mode n starts
     bool zsame[kMaxModes] = {};
+    bool pz[kMaxModes] = {};    // mode m's output is pre-zeroed (>= 256 MB; smaller ones zero in-launch)
     std::vector<size_t> off;               // byte offset of A_m in c.comm->sym
 };
 
@@ -1522,6 +1529,7 @@ static ApplyPlan plan_apply(AlsCtx &c, int64_t rows, int R, bool small) {
         const int64_t tiles = (rows + 7) / 8;
         int64_t nb = std::min<int64_t>(cap, (tiles + 7) / 8);
         if (small) nb = std::min<int64_t>(nb, kTailBlocks);
+        if (tiles <= 64) nb = 1;  // <= 8 tiles per warp: one block, no cross-block reduction
         p.nb = (int)std::max<int64_t>(nb, 1);
         return p;
     }
@@ -1687,14 +1695,16 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
         SPTK_CUDA(cudaEventRecord(w.ev_inv, w.side));
         if (c.prezero) {  // the buffer mode n-1's apply released, for its next user
             const int m = c.znext[n];
-            SPTK_CUDA(cudaMemsetAsync(c.vbuf[c.vb[m]], 0, sizeof(T) * (size_t)t->dims[m] * R,
-                                      w.side));
-            if (c.zsame[m]) SPTK_CUDA(cudaEventRecord(w.ev_zero[m], w.side));
-            if (c.zsame[n]) SPTK_CUDA(cudaStreamWaitEvent(c.s, w.ev_zero[n], 0));
+            if (c.pz[m]) {
+                SPTK_CUDA(cudaMemsetAsync(c.vbuf[c.vb[m]], 0, sizeof(T) * (size_t)t->dims[m] * R,
+                                          w.side));
+                if (c.zsame[m]) SPTK_CUDA(cudaEventRecord(w.ev_zero[m], w.side));
+            }
+            if (c.pz[n] && c.zsame[n]) SPTK_CUDA(cudaStreamWaitEvent(c.s, w.ev_zero[n], 0));
         }
         // V = MTTKRP with the normalised factors: raw factors, column scales at the flush
         SPTK_TRY(mttkrp_launch(t, n, c.R, c.A.data(), deferred ? scale : nullptr, V, 0, I, c.s,
-                               c.prezero));
+                               c.prezero && c.pz[n]));
         SPTK_CUDA(cudaStreamWaitEvent(c.s, w.ev_inv, 0));
         T *An = static_cast<T *>(c.A[n]);
         double *psq = w.partial.as<double>();
@@ -1790,8 +1800,11 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
         SPTK_CUDA(cudaEventRecord(w.ev_join, w.side));
         SPTK_CUDA(cudaStreamWaitEvent(c.s, w.ev_join, 0));
     }
-    // fit and status to pinned host memory (a graph-capturable copy)
-    SPTK_CUDA(cudaMemcpyAsync(w.hres, scal, sizeof(double) * 9, cudaMemcpyDeviceToHost, c.s));
+    // fit and status to pinned host memory (a graph-capturable copy); the
+    // no-convergence-test path reads the device fit history instead and copies
+    // the (sticky) status once after the last replay
+    if (c.copy_fit)
+        SPTK_CUDA(cudaMemcpyAsync(w.hres, scal, sizeof(double) * 9, cudaMemcpyDeviceToHost, c.s));
     return SPTK_OK;
 }
 
@@ -1989,6 +2002,8 @@ static std::vector<uint64_t> graph_key(AlsCtx &c, cudaStream_t s) {
     add(options_generation());
     add(c.sym_iter);
     add(c.prezero);
+    for (int n = 0; n < t->N; ++n) add(c.pz[n]);
+    add(c.copy_fit);
     for (const void *p : c.vbuf) addp(p);
     add((uint64_t)c.part_stride);
     add((uint64_t)c.nb_apply);
@@ -2088,14 +2103,16 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t Rl, int max_iters, double 
     SPTK_TRY(w.scl.reserve(sizeof(double) * ((size_t)N * R + (size_t)R * R + R + 1)));
     if (!w.hres) SPTK_CUDA(cudaMallocHost(&w.hres, sizeof(double) * 16));
     if (!w.side) {
-        // highest priority: the one-block inverse is scheduled at the next
-        // block retirement of the MTTKRP it overlaps (at default priority it
-        // waited for the MTTKRP's last wave: 10-15 us per mode on the LBNL
-        // critical path, profiles/r02/s2/timeline_lbnl.log)
+        // highest priority on tensors with long MTTKRPs: the one-block inverse
+        // is then scheduled at the next block retirement of the MTTKRP it
+        // overlaps (at default priority it waited for the MTTKRP's last wave:
+        // LBNL 0.583 -> 0.516 ms/iter); on tiny tensors, where every kernel is
+        // a few us, the prioritised stream measured slower (C1 0.075 -> 0.113)
         int lo = 0, hi = 0;
         SPTK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        SPTK_CUDA(cudaStreamCreateWithPriority(&w.side, cudaStreamNonBlocking,
-                                               opt(OPT_SIDE_PRIO) ? hi : 0));
+        const int64_t sp = opt(OPT_SIDE_PRIO);
+        const bool prio = sp == 1 || (sp < 0 && t->P >= ((int64_t)1 << 20));
+        SPTK_CUDA(cudaStreamCreateWithPriority(&w.side, cudaStreamNonBlocking, prio ? hi : 0));
         SPTK_CUDA(cudaEventCreateWithFlags(&w.ev_gram, cudaEventDisableTiming));
         SPTK_CUDA(cudaEventCreateWithFlags(&w.ev_inv, cudaEventDisableTiming));
         SPTK_CUDA(cudaEventCreateWithFlags(&w.ev_join, cudaEventDisableTiming));
@@ -2190,6 +2207,16 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t Rl, int max_iters, double 
             c.znext[n] = m;
             c.zsame[m] = p == N - 1 || p + k <= N - 1;
         }
+        // only outputs of >= 256 MB (Delicious' 17M- and 2.5M-row modes: -1 %);
+        // below that an in-launch zero costs less than a side-stream memset
+        // and its dependency (LBNL's 111 MB mode: +1.2 % pre-zeroed, C1 +4 %,
+        // profiles/r02/s2/ab_glue_s13.log)
+        bool any = false;
+        for (int n = 0; n < N; ++n) {
+            c.pz[n] = es * (size_t)t->dims[n] * R >= ((size_t)256 << 20);
+            any = any || c.pz[n];
+        }
+        c.prezero = c.prezero && any;
         for (int b = 0; b < 3 && c.prezero; ++b)
             if (rows[b]) SPTK_CUDA(cudaMemsetAsync(c.vbuf[b], 0, es * rows[b] * R, s));
     }
@@ -2219,6 +2246,7 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t Rl, int max_iters, double 
     int64_t launches_per_iter = 0;
     bool fast_done = false;
     if (use_graph && tol <= 0.0) {
+        c.copy_fit = c.sym_iter;  // single GPU: no per-iteration copy (the sharded one keeps its own)
         // No convergence test.  If the previous call captured this same
         // iteration (same buffers, caches, stream and options: graph_key), its
         // graph is replayed from iteration 0.  Otherwise iteration 0 runs
@@ -2263,6 +2291,10 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t Rl, int max_iters, double 
                 st = enqueue_iteration<T>(c);
             }
         }
+        if (st == SPTK_OK && !c.copy_fit &&
+            cudaMemcpyAsync(w.hres, w.scal.p, sizeof(double) * 9, cudaMemcpyDeviceToHost, s) !=
+                cudaSuccess)
+            st = cuda_fail(cudaGetLastError(), "fit/status copy");
         int bad = 0;
         if (st == SPTK_OK) st = complete_iteration(c, &fit, &bad);
         if (st == SPTK_OK) {

@@ -54,7 +54,8 @@ constexpr OptDef kOpts[] = {
     {"prezero", 1},             // CP-ALS: MTTKRP outputs zeroed on the side stream, off the critical path
     {"apply_mma", 1},           // CP-ALS apply_gram on the FP64 tensor cores (DMMA) for R = 8 / 16
     {"gj_warp", 1},             // CP-ALS: one-warp register Gauss-Jordan inverse for R <= 32
-    {"side_prio", 1},           // CP-ALS: side stream (inverse, zeroing) at the highest priority
+    {"side_prio", -1},          // CP-ALS side stream (inverse, zeroing) at the highest priority:
+                                //   -1 for tensors of >= 2^20 nonzeros, 1 always, 0 never
 };
 
 static_assert(sizeof(kOpts) / sizeof(kOpts[0]) == OPT_COUNT, "kOpts must list every Opt, in order");

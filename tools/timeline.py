@@ -41,11 +41,15 @@ for e in prof.events():
         continue
     ev.append((e.time_range.start, e.time_range.end, getattr(e, "device_resource_id", 0), e.name))
 ev.sort()
-# the last iteration: from the last fit/copy boundary -- split on the D2H memcpy of the fit
-cuts = [i for i, x in enumerate(ev) if "Memcpy DtoH" in x[3] or "memcpy" in x[3].lower() and "DtoH" in x[3]]
-lo = cuts[-3] + 1 if len(cuts) >= 3 else 0
-hi = cuts[-2] + 1 if len(cuts) >= 2 else len(ev)
-sel = ev[lo:hi]
+# one iteration: the graph replays identical iterations, so the op-name
+# sequence is periodic at the end (after dropping the trailing status copy);
+# take the last period
+body = list(ev)
+while body and ("Memcpy" in body[-1][3] or "scale_columns" in body[-1][3]):
+    body.pop()  # the status copy and the final column scaling follow the last iteration
+names = [x[3] for x in body]
+per = next((q for q in range(2, len(names) // 2 + 1) if names[-q:] == names[-2 * q:-q]), len(names))
+sel = body[-per:]
 t0 = sel[0][0]
 last_end = {}
 busy = 0.0
