@@ -52,7 +52,7 @@ enum Opt {
     OPT_RUN, OPT_VARIANT, OPT_SLICE, OPT_SLICE_L2_KB, OPT_SLICE_ROWS, OPT_SLICE_OTHER_FIRST,
     OPT_ROWREC, OPT_FORCE_V, OPT_GENERIC, OPT_DEBUG_DISPATCH, OPT_COPY_ORDER, OPT_DEFERRED_NORM,
     OPT_NO_GRAPH, OPT_GAMMA_INV_CHOL, OPT_USE_COPY, OPT_APPLY_TILE, OPT_APPLY_NB_MULT, OPT_TAIL_ROWS, OPT_APPLY_WAVE, OPT_APPLY_WARP,
-    OPT_KEEP_KEYS, OPT_PDL, OPT_EXCHANGE, OPT_PAD_RANK, OPT_SORT_V1, OPT_PREZERO, OPT_APPLY_MMA, OPT_GJ_WARP, OPT_SIDE_PRIO, OPT_COUNT
+    OPT_KEEP_KEYS, OPT_PDL, OPT_EXCHANGE, OPT_PAD_RANK, OPT_SORT_V1, OPT_PREZERO, OPT_APPLY_MMA, OPT_GJ_WARP, OPT_SIDE_PRIO, OPT_WIN, OPT_COUNT
 };
 int64_t opt(Opt o);
 uint64_t options_generation();  // bumped by every sptk_set_option / sptk_reset_options
@@ -172,6 +172,7 @@ struct sptk_tensor_s {
                                                 // permuted positions [copy_p0, copy_p1)
     int shard_n = 1, shard_r = 0;               // sptk_sptensor_set_shard
     bool copy_rowrec[sptk::kMaxModes] = {false};  // copy records carry the row index
+    bool copy_win[sptk::kMaxModes] = {false};     // copy in window-major order (sort.cu)
     sptk::DevBuf soff[sptk::kMaxModes];         // slice offsets (slice kernel, cached)
     int64_t soff_key[sptk::kMaxModes][4] = {{-1, -1, -1, -1}};  // (row0, row1, nslice, S)
     int64_t row_max[sptk::kMaxModes] = {-1, -1, -1, -1, -1, -1};  // max nnz of a row (lazy)

@@ -324,8 +324,12 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     SPTK_TRY(ensure_sorted_copy(t, mode, s));
     // the copy serves this call if it covers the call's positions (a shard's
     // copy covers only its own row range)
-    const bool copy = t->has_srec[mode] && pb >= t->copy_p0[mode] && pe <= t->copy_p1[mode] &&
-                      opt(OPT_USE_COPY) != 0;
+    bool copy = t->has_srec[mode] && pb >= t->copy_p0[mode] && pe <= t->copy_p1[mode] &&
+                opt(OPT_USE_COPY) != 0;
+    // a window-major copy holds rows out of order: only whole-mode calls, on
+    // the cooperative kernel reading rows from the records
+    const bool win = copy && t->copy_win[mode];
+    if (win && (row_begin != 0 || row_end != In)) copy = false;
     MttkrpArgs a{};
     a.rec = t->rec.as<uint8_t>();  // the paper's traversal: gather through perm_n
     a.perm = t->perm[mode].as<uint32_t>();
@@ -337,6 +341,7 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     a.rb = t->rec_bytes;
     for (int m = 0; m < t->N; ++m) a.A[m] = (m == mode) ? nullptr : factors[m];
     a.lambda = lambda;
+
     a.out = out;
 
     // Lane vector width V: the widest power of two <= 32 bytes that divides R
@@ -363,7 +368,14 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     // warp-cooperative steps pay off when rows are long (few boundary steps)
     const int64_t rows = row_end - row_begin;
     int var = 0;
-    if (fast && copy && G0 < 32) {
+    if (win && copy && !(fast && G0 < 32)) copy = false;  // no cooperative kernel for this R
+    if (fast && copy && win) {
+        var = 1;
+        // ~512 positions per warp: the chunks in flight then span about one
+        // window of the secondary factor (in-flight positions x 16 B of A_a)
+        a.run = std::max<int64_t>(1, 512 / (32 / G0));
+        a.win = 1;
+    } else if (fast && copy && G0 < 32) {
         var = variant_setting();
         // measured (profiles/r01/sweep_*.log): a win for >= 4 groups per warp on
         // rows averaging >= 64 nonzeros, a loss on short rows and for 2 groups
@@ -383,7 +395,7 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     }
     a.rowrec = copy && t->copy_rowrec[mode] && var == 0 && opt(OPT_ROWREC) != 0;
     if (fast && copy) {  // stream the compact permuted copy instead
-        SPTK_TRY(worker_rows(t, mode, pb, pe, chunk, workers, s));
+        if (!a.win) SPTK_TRY(worker_rows(t, mode, pb, pe, chunk, workers, s));
         // indexed by absolute position: base shifted back by the copy's first position
         a.rec = t->srec[mode].as<uint8_t>() -
                 (size_t)t->copy_p0[mode] * compact_bytes(t->dtype, t->N);
@@ -395,7 +407,7 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
     // slice traversal: one column tile (R <= 32 V), 32-byte vectors, the copy
     int64_t S = 0;
     int K = 0;
-    if (fast && copy && R <= 32 * V)
+    if (fast && copy && !a.win && R <= 32 * V)
         K = slice_count(t, mode, row_begin, row_end, pe - pb, R * (int64_t)es, s, &S);
     if (K > 0) {
         SPTK_TRY(slice_offsets(t, mode, row_begin, row_end, K, S, s));
@@ -412,6 +424,7 @@ sptk_status mttkrp_launch(sptk_tensor t, int mode, int64_t R, const void *const 
         static const char *kind[] = {"fast", "coop", "slice"};
         std::string d = !fast ? "generic" : !copy ? "perm_gather" : kind[var];
         if (fast && copy && var == 0 && a.rowrec) d += "_rowrec";
+        if (a.win) d += "_window";
         if (var == 2 && t->dims[a.sec] * R * (int64_t)es > slice_l2_bytes()) d += "_l2window";
         if (t->deterministic) d += "+det";
         d += " V" + std::to_string(fast ? V : 1);

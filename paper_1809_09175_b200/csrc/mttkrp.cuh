@@ -62,6 +62,10 @@ struct MttkrpArgs {
     int nslice, sec;
     int other_first;             // slice kernel: non-secondary gathers L2 evict_first
     int rowrec;                  // per-group kernel: row index stored in the copy's spare word
+    // coop kernel over a window-major copy (order: window of l_sec, l_n,
+    // l_sec; sort.cu): rows from the records' spare word, not monotonic, so
+    // every flush is a red.add
+    int win = 0;
 };
 
 // ----------------------------------------------------------------- loads
@@ -501,8 +505,16 @@ __device__ __forceinline__ void mttkrp_coop_body(const MttkrpArgs &a) {
         else ld_rec16_p(rec + (size_t)pos * 16, r, pol_stream);
     };
 
-    uint32_t row = __ldg(a.wrow + warp_id);
-    uint32_t nxt = __ldg(a.rowptr + row + 1);
+    constexpr int RW = OFF + N - 1;  // spare record word: the position's row (window-major copy)
+    const bool win = a.win != 0;
+    uint32_t row, nxt;
+    if (win) {
+        row = __ldg(reinterpret_cast<const uint32_t *>(rec + (size_t)s * RB) + RW);
+        nxt = 0;
+    } else {
+        row = __ldg(a.wrow + warp_id);
+        nxt = __ldg(a.rowptr + row + 1);
+    }
     const uint32_t first = row;
     T acc[V];
 #pragma unroll
@@ -555,7 +567,16 @@ __device__ __forceinline__ void mttkrp_coop_body(const MttkrpArgs &a) {
             }
         }
         const uint32_t last = base + U * NG - 1;
-        if (last < nxt && last < e) {  // whole step inside the current row
+        bool inside;
+        if (win) {  // every position of the step in the current row (rows from the records)
+            bool ok = last < e;
+#pragma unroll
+            for (int u = 0; u < U; ++u) ok = ok && w[u][RW] == row;
+            inside = __all_sync(0xffffffffu, ok);
+        } else {
+            inside = last < nxt && last < e;
+        }
+        if (inside) {  // whole step inside the current row
 #pragma unroll
             for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -573,10 +594,19 @@ __device__ __forceinline__ void mttkrp_coop_body(const MttkrpArgs &a) {
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+            const uint32_t myrow = w[u][RW];
             for (int gg = 0; gg < NG; ++gg) {
                 const uint32_t pos = base + u * NG + gg;
                 if (pos >= e) break;
-                if (pos >= nxt) {
+                if (win) {
+                    const uint32_t prow = __shfl_sync(0xffffffffu, myrow, gg * G);
+                    if (prow != row) {
+                        flush(row, tot, true, 0);
+#pragma unroll
+                        for (int v = 0; v < V; ++v) tot[v] = T(0);
+                        row = prow;
+                    }
+                } else if (pos >= nxt) {
                     flush(row, tot, row == first, 0);
 #pragma unroll
                     for (int v = 0; v < V; ++v) tot[v] = T(0);

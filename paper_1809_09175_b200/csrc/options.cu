@@ -56,6 +56,8 @@ constexpr OptDef kOpts[] = {
     {"gj_warp", 1},             // CP-ALS: one-warp register Gauss-Jordan inverse for R <= 32
     {"side_prio", -1},          // CP-ALS side stream (inverse, zeroing) at the highest priority:
                                 //   -1 for tensors of >= 2^20 nonzeros, 1 always, 0 never
+    {"win", 0},                 // > 0: window-major copies for modes with few rows whose secondary
+                                //   factor spans >= 2 x win L2 windows (power-law tensors)
 };
 
 static_assert(sizeof(kOpts) / sizeof(kOpts[0]) == OPT_COUNT, "kOpts must list every Opt, in order");

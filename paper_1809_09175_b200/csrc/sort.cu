@@ -533,7 +533,7 @@ static int grid_for(int64_t n) {
 
 static sptk_status stable_sort_ids(sptk_tensor t, int mode, const uint32_t *in, uint32_t *out,
                                    uint32_t **keys_out, cudaStream_t s, void *ext_ws = nullptr,
-                                   size_t ext_bytes = 0);
+                                   size_t ext_bytes = 0, int kshift = 0);
 
 // The longest row of `mode` (computed on the device at build_perm; one 4-byte
 // read, cached).  -1 if unavailable.
@@ -666,12 +666,41 @@ sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
         else set_error("");
     }
     t->copy_sec[mode] = -1;
+    t->copy_win[mode] = false;
     t->soff_key[mode][0] = -1;
     if (ordp) {
         SPTK_TRY(stable_sort_ids(t, mode, t->perm[a].as<uint32_t>(), ordp, nullptr, s,
                                  ws_in_copy ? t->srec[mode].p : nullptr, ws_in_copy ? need : 0));
         order = ordp;
         t->copy_sec[mode] = a;
+    }
+    // Window-major order (option win; SURVEY §8(a) a4-a5 on power-law tensors):
+    // for a mode with few output rows whose secondary factor far exceeds L2,
+    // the (l_n, l_a) order is re-sorted stably by the window of l_a (2^wshift
+    // rows of A_a, an L2-sized slice at 128-byte rows), giving (window, l_n,
+    // l_a).  The cooperative kernel then streams the copy in order with short
+    // per-warp chunks, so the positions in flight gather A_a rows from about
+    // one window, which stays in L2; every row is reached once per window and
+    // flushed with red.add (I_n x windows flushes, few when I_n is small).
+    const int vwd = dtype_bytes(t->dtype) / 4;
+    if (ordp && opt(OPT_WIN) && !t->deterministic && whole && rc / 4 >= vwd + t->N) {
+        int wshift = 0;
+        const int64_t wrows = std::max<int64_t>(1, (int64_t)opt(OPT_SLICE_L2_KB) * 1024 / 128);
+        while (((int64_t)2 << wshift) <= wrows) ++wshift;
+        const int64_t nwin = (t->dims[a] + ((int64_t)1 << wshift) - 1) >> wshift;
+        if (nwin >= 2 * (int64_t)opt(OPT_WIN) && t->dims[mode] * nwin * 64 <= t->P) {
+            DevBuf ord2;
+            if (ord2.reserve(order_bytes) == SPTK_OK) {
+                SPTK_TRY(stable_sort_ids(t, a, ordp, ord2.as<uint32_t>(), nullptr, s,
+                                         ws_in_copy ? t->srec[mode].p : nullptr,
+                                         ws_in_copy ? need : 0, wshift));
+                SPTK_CUDA(cudaMemcpyAsync(ordp, ord2.p, order_bytes, cudaMemcpyDeviceToDevice, s));
+                SPTK_CUDA(cudaStreamSynchronize(s));  // ord2 is freed on return
+                t->copy_win[mode] = true;
+            } else {
+                set_error("");
+            }
+        }
     }
     const int vw = dtype_bytes(t->dtype) / 4;
     const int64_t np = p1 - p0;
@@ -703,6 +732,7 @@ void drop_copies(sptk_tensor t) {
         t->wrow[m].release();
         t->wrow_key[m][0] = -1;
         t->copy_sec[m] = -1;
+        t->copy_win[m] = false;
         t->soff[m].release();
         t->soff_key[m][0] = -1;
         t->copy_declined[m] = false;
@@ -733,12 +763,14 @@ __global__ void __launch_bounds__(256) gather_keys(const uint32_t *__restrict__ 
 // Uses the handle's cached workspace.
 // ext_ws (optional, >= sort_ws_words(P) words): scratch to use instead of the
 // handle's cached workspace (the copy buffer about to be overwritten).
+// kshift > 0: sort by l >> kshift only (the window index of the window-major
+// copy order)
 static sptk_status stable_sort_ids(sptk_tensor t, int mode, const uint32_t *in, uint32_t *out,
                                    uint32_t **keys_out, cudaStream_t s, void *ext_ws,
-                                   size_t ext_bytes) {
+                                   size_t ext_bytes, int kshift) {
     const int64_t P = t->P, In = t->dims[mode];
     int bits = 0;
-    while (bits < 32 && ((uint64_t)(In - 1) >> bits) != 0) ++bits;
+    while (bits < 32 && ((uint64_t)(In - 1) >> (bits + kshift)) != 0) ++bits;
     const int npass = bits == 0 ? 1 : (bits + 7) / 8;
     const int dbits = bits == 0 ? 1 : (bits + npass - 1) / npass;
     const int64_t ntiles = (P + kSortTile - 1) / kSortTile;
@@ -780,8 +812,8 @@ static sptk_status stable_sort_ids(sptk_tensor t, int mode, const uint32_t *in, 
     }
     const uint32_t *kin = k0, *vin = in;
     for (int p = 0; p < npass; ++p) {
-        const int shift = p * dbits;
-        const int db = bits == 0 ? 1 : ((shift + dbits > bits) ? bits - shift : dbits);
+        const int db = bits == 0 ? 1 : ((p * dbits + dbits > bits) ? bits - p * dbits : dbits);
+        const int shift = kshift + p * dbits;
         uint32_t *kout = kbuf[(npass - 1 - p) & 1];
         uint32_t *vout = vbuf[((npass - 1 - p) & 1) ^ 1];
         radix_upsweep<<<(unsigned)ntiles, kSortThreads, 0, s>>>(kin, (uint32_t)P, shift, db,

@@ -871,6 +871,47 @@ def test_cp_als_inverse_kernels(sp, R, inv):
         assert rel(F[m].cpu().numpy(), ref["A"][m]) <= 1e-7, m
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_window_major_copy(sp, dtype):
+    """Window-major permuted copy (option win): a power-law 4-way tensor whose
+    3rd mode has few rows and whose secondary factor spans many (shrunken)
+    L2 windows.  The cooperative kernel reads rows from the records and
+    red.adds every flush; MTTKRP of every mode and the CP-ALS trajectory
+    follow the oracle, and a row sub-range call falls back to the perm
+    gather."""
+    dims = (3000, 200000, 40, 24)
+    P = 600000
+    idx, vals = synth.tensor(71, dims, P, "powerlaw")
+    f32 = dtype == torch.float32
+    v = vals.astype(np.float32).astype(np.float64) if f32 else vals
+    R = 16
+    A = factors_np(72, dims, R)
+    if f32:
+        A = [a.astype(np.float32).astype(np.float64) for a in A]
+    with sp.options(win=1, slice_l2_kb=512):
+        t = make(sp, dims, idx, vals.astype(np.float32) if f32 else vals, dtype)
+        sp.build_perm(t, -1)
+        for n in range(4):
+            out = gpu_mttkrp(sp, t, n, A, R, dtype)
+            kind = sp.last_dispatch()
+            if n == 3 and not f32:  # fp32 N=4 records (16 B) have no spare row word
+                assert "window" in kind, kind
+            Vo = oracle.mttkrp(dims, idx, v, A, n)
+            assert rel(out, Vo) <= TOL[dtype], (n, kind)
+        # rows [5, 20) of mode 3: the window-major copy cannot serve a sub-range
+        out = torch.full((dims[3], R), float("nan"), dtype=dtype, device="cuda")
+        sp.mttkrp_rows(t, 3, [dev(a, dtype) for a in A], out, 5, 20)
+        Vo = oracle.mttkrp(dims, idx, v, A, 3)
+        assert rel(out[5:20].double().cpu().numpy(), Vo[5:20]) <= TOL[dtype]
+        assert "window" not in sp.last_dispatch()
+        if not f32:
+            ref = oracle.cp_als(dims, idx, vals, factors_np(72, dims, R), 4)
+            F = [torch.empty(I, R, dtype=dtype, device="cuda") for I in dims]
+            res = sp.cp_als(t, R, 4, F, seed=72)
+            assert np.max(np.abs(res["trace"] - ref["trace"])) <= 1e-9
+        t.close()
+
+
 @pytest.mark.parametrize("exchange", [0, 1])
 def test_sharded_zero_column_e1(sp, monkeypatch, exchange):
     """A zero initial column through the sharded deferred path: every Gamma
