@@ -10,5 +10,6 @@ run --config nell2 --rank 64 --dtype f64 --no-cpu-baseline
 run --config nell2 --rank 16 --dtype f32 --no-cpu-baseline
 run --config nell2 --rank 64 --dtype f32 --no-cpu-baseline
 run --config nell2 --rank 16 --dtype f64 --layout perm_gather --no-cpu-baseline --no-e2e
+run --config nell2 --rank 17 --dtype f64 --no-cpu-baseline --no-e2e
 run --config delicious --rank 16 --steps 20
 run --config amazon --rank 16 --steps 10
