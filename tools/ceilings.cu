@@ -93,6 +93,49 @@ __global__ void __launch_bounds__(256) gather_rows(const uint32_t *__restrict__ 
     if (acc == 1.2345) out[0] = acc;
 }
 
+// The slice MTTKRP's data movement without its arithmetic: per element a
+// 16-byte record {row of A (uint32), row of B (uint32), value (f64)} streamed
+// with L1::no_allocate, one 128-byte row of A from an L1-sized table
+// (L1-allocating: the secondary factor's window) and one of B from an
+// L2-resident table (L1::no_allocate: the other factor); 4 lanes x 32 B per
+// row, U elements in flight per group.  An upper bound for the kernel: its
+// window rows hit L1 only ~35 % of the time (ncu), here always.
+__global__ void __launch_bounds__(256) pair_gather(const uint4 *__restrict__ rec, int64_t n,
+                                                   const double *__restrict__ A,
+                                                   const double *__restrict__ B, double *out) {
+    constexpr int U = 4, G = 4;
+    const int q = threadIdx.x % G;
+    const int64_t g0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+    const int64_t gs = ((int64_t)gridDim.x * blockDim.x) / G;
+    double acc = 0;
+    for (int64_t k = g0; k < n; k += gs * U) {
+        uint32_t ra[U], rb[U];
+        double x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t kk = k + u * gs;
+            uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+            if (kk < n)
+                asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "l"(rec + kk));
+            ra[u] = w0;
+            rb[u] = w1;
+            x[u] = __hiloint2double((int)w3, (int)w2);
+        }
+        double fa[U][4], fb[U][4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            ld32(A + (int64_t)ra[u] * 16 + q * 4, fa[u], true);
+            ld32(B + (int64_t)rb[u] * 16 + q * 4, fb[u], false);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc += x[u] * fa[u][v] * fb[u][v];
+    }
+    if (acc == 1.2345) out[0] = acc;
+}
+
 // TMA gather4: lane 0 of each warp keeps S gather4 copies (4 rows each) in
 // flight into a per-warp smem ring; the warp reads one word of every landed
 // row set (checksum) before re-arming the slot
@@ -249,6 +292,30 @@ int main(int argc, char **argv) {
                 emit(key, (double)n * rb / ms / 1e6, "GB/s", what);
             }
         }
+    }
+    // ---- the slice MTTKRP's access mix (record stream + L1 row + L2 row)
+    {
+        const int64_t np = (int64_t)1 << 26;  // 67M elements, 1 GB of records
+        uint4 *rec;
+        CK(cudaMalloc(&rec, np * 16));
+        std::vector<uint4> hr(np);
+        const int64_t rowsA = (96 << 10) / 128, rowsB = ((int64_t)6400 << 10) / 128;
+        for (int64_t k = 0; k < np; ++k) {
+            const uint64_t r = rng();
+            hr[k] = make_uint4((uint32_t)((r >> 40) % rowsA), (uint32_t)((r & 0xffffffffu) % rowsB), 0u,
+                               0x3ff00000u);  // value 1.0
+        }
+        CK(cudaMemcpy(rec, hr.data(), np * 16, cudaMemcpyHostToDevice));
+        const double *TA = H, *TB = H + (int64_t)(1 << 20);  // disjoint tables in the 4 GB buffer
+        for (int bps : {2, 3, 4}) {
+            const double ms = best_ms([&] { pair_gather<<<sms * bps * 4, 256>>>(rec, np, TA, TB, out); });
+            char key[64], what[200];
+            snprintf(key, sizeof key, "pair_gather_l1_l2_128_x%d", bps);
+            snprintf(what, sizeof what, "slice-MTTKRP mix: 16 B record + 128 B row from 96 KB (L1) + 128 B "
+                     "row from 6.4 MB (L2, no L1); gathered row bytes / time, grid %d x SMs", bps * 4);
+            emit(key, (double)np * 256 / ms / 1e6, "GB/s", what);
+        }
+        cudaFree(rec);
     }
     // ---- TMA gather4 of 128-byte rows (precomputed ids, as above)
     {
