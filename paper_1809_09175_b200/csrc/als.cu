@@ -671,6 +671,55 @@ __global__ void __launch_bounds__(256)
     finalize_mode_block<T>(colsq, graw, A, N, n, R, Rl, next, s_all, lam, G, scale_next);
 }
 
+// A large mode's tail in one launch: every warp reduces one entry of
+// [colsq | graw | dot] over the nb apply blocks' partials (lanes stride over
+// the blocks, fixed shuffle tree: the reduce_partials_kernel order), then the
+// last block to arrive finalises the mode (and, after the last mode, the fit).
+// Replaces 3 (5) dependent launches: reduce colsq, reduce graw, finalise
+// (reduce dot, fit).
+template <typename T>
+__global__ void __launch_bounds__(256)
+    reduce_finalize_kernel(const double *__restrict__ psq, const double *__restrict__ gpart,
+                           const double *__restrict__ pdot, int nb, int R, int Rl,
+                           double *__restrict__ colsq, double *__restrict__ graw, T *__restrict__ A,
+                           int N, int n, int next, double *__restrict__ s_all,
+                           double *__restrict__ lam, double *__restrict__ G,
+                           T *__restrict__ scale_next, int *__restrict__ counter, double normX2,
+                           double *__restrict__ fit, double *__restrict__ trace,
+                           int *__restrict__ trace_n) {
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int RR = R * R, ne = RR + R + (pdot ? R : 0);
+    for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < ne;
+         e += (gridDim.x * blockDim.x) >> 5) {
+        const double *part;
+        int stride, k;
+        double *dst;
+        if (e < R) {
+            part = psq, stride = R, k = e, dst = colsq + e;
+        } else if (e < R + RR) {
+            part = gpart, stride = RR, k = e - R, dst = graw + (e - R);
+        } else {
+            part = pdot, stride = R, k = e - R - RR, dst = colsq + R + (e - R - RR);
+        }
+        double x = 0.0;
+        for (int b = lane; b < nb; b += 32) x += part[(int64_t)b * stride + k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) *dst = x;
+    }
+    __shared__ int last_block;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last_block = atomicAdd(counter, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!last_block) return;
+    __threadfence();
+    finalize_mode_block<T>(colsq, graw, A, N, n, R, Rl, next, s_all, lam, G, scale_next);
+    if (pdot) fit_block(colsq + R, lam, G, N, R, normX2, fit, trace, trace_n);
+    if (threadIdx.x == 0) *counter = 0;  // ready for the next launch (graph replays)
+}
+
 // Where the last block of apply_gram leaves the mode's results (counter NULL:
 // the partials are reduced by separate kernels instead).
 struct ModeTail {
@@ -1738,7 +1787,17 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
                                    w.gpart.as<double>(), tail, ExchOut{}));
             count_launch();
             SPTK_CUDA(cudaGetLastError());
-            if (!tail.counter) {  // many blocks: parallel reductions, then one finalise block
+            if (!tail.counter && opt(OPT_FUSED_REDUCE)) {  // one launch: reductions + finalise
+                const int ne = R * R + R + (last ? R : 0);
+                SPTK_CUDA(launch_pdl(reduce_finalize_kernel<T>, (ne + 7) / 8, 256, 0, c.s,
+                                     (const double *)psq, (const double *)w.gpart.as<double>(),
+                                     (const double *)(last ? pdot : nullptr), nb, R, (int)c.Rl,
+                                     colsq, graw, An, N, n, (n + 1) % N, s_all, lam,
+                                     w.G.as<double>(), scale, reinterpret_cast<int *>(scale + R),
+                                     t->normX2, scal, trace, trace_n));
+                count_launch();
+                SPTK_CUDA(cudaGetLastError());
+            } else if (!tail.counter) {  // many blocks: parallel reductions, then one finalise block
                 SPTK_CUDA(launch_pdl(reduce_partials_kernel, (R + 7) / 8, 256, 0, c.s,
                                      (const double *)psq, nb, R, colsq));
                 SPTK_CUDA(launch_pdl(reduce_partials_kernel, (R * R + 7) / 8, 256, 0, c.s,
@@ -2213,7 +2272,7 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t Rl, int max_iters, double 
         // profiles/r02/s2/ab_glue_s13.log)
         bool any = false;
         for (int n = 0; n < N; ++n) {
-            c.pz[n] = es * (size_t)t->dims[n] * R >= ((size_t)256 << 20);
+            c.pz[n] = opt(OPT_PREZERO) == 2 || es * (size_t)t->dims[n] * R >= ((size_t)256 << 20);
             any = any || c.pz[n];
         }
         c.prezero = c.prezero && any;

@@ -261,6 +261,17 @@ static int slice_count(sptk_tensor t, int mode, int64_t r0, int64_t r1, int64_t 
         const int64_t kfit = std::max<int64_t>(2, nnz / (rows * 96));
         if (kfit < k32) sa = std::min<int64_t>(2 * sa, (t->dims[a] + kfit - 1) / kfit);
     }
+    // small grids (LBNL's 1.6K-row modes: 200 row groups x 2 slices = 400
+    // blocks, 2.7 per SM) fill the GPU unevenly: halve the slices' rows while
+    // the grid is under slice_fill blocks per SM and runs keep >= 64 nonzeros
+    // (measured: 1024-row slices -17 % on those modes, +17 % on the 4.2K-row
+    // ones, profiles/r02/ab_lbnl_slice_rows.log)
+    if (opt(OPT_SLICE_ROWS) <= 0 && t->dims[a] * row_bytes <= slice_l2_bytes()) {
+        const int64_t fill = opt(OPT_SLICE_FILL) * (int64_t)dev_sms();
+        while (sa > 512 && ((rows + 7) / 8) * ((t->dims[a] + sa - 1) / sa) < fill &&
+               nnz >= 64 * ((t->dims[a] + sa / 2 - 1) / (sa / 2)) * rows)
+            sa /= 2;
+    }
     const int64_t K = (t->dims[a] + sa - 1) / sa;
     if (K < 2 || K > 65535) return 0;
     if (opt(OPT_SLICE) == 2) {  // forced (tests): structural conditions only

@@ -51,13 +51,17 @@ constexpr OptDef kOpts[] = {
     {"pad_rank", 1},            // CP-ALS: R not a multiple of the 32-byte lane vector runs on
                                 //   factors padded with zero columns (0: stride R)
     {"sort_v1", 0},             // 1: round-1 radix downsweep (A/B)
-    {"prezero", 1},             // CP-ALS: MTTKRP outputs zeroed on the side stream, off the critical path
+    {"prezero", 1},             // CP-ALS: MTTKRP outputs of >= 256 MB zeroed on the side stream, off
+                                //   the critical path (2: every output, tests)
     {"apply_mma", 1},           // CP-ALS apply_gram on the FP64 tensor cores (DMMA) for R = 8 / 16
     {"gj_warp", 1},             // CP-ALS: one-warp register Gauss-Jordan inverse for R <= 32
     {"side_prio", -1},          // CP-ALS side stream (inverse, zeroing) at the highest priority:
                                 //   -1 for tensors of >= 2^20 nonzeros, 1 always, 0 never
     {"win", 0},                 // > 0: window-major copies for modes with few rows whose secondary
                                 //   factor spans >= 2 x win L2 windows (power-law tensors)
+    {"slice_fill", 6},          // slice traversal: halve the slices until the grid has this many
+                                //   blocks per SM (0 = off)
+    {"fused_reduce", 1},        // CP-ALS: a large mode's reductions + finalise (+ fit) in one launch
 };
 
 static_assert(sizeof(kOpts) / sizeof(kOpts[0]) == OPT_COUNT, "kOpts must list every Opt, in order");

@@ -843,7 +843,7 @@ def test_cp_als_prezeroed_outputs(sp, dims):
     R = 8
     ref = oracle.cp_als(dims, idx, vals, factors_np(52, dims, R), 7)
     t = make(sp, dims, idx, vals)
-    for opts in ({}, {"prezero": 0}, {"no_graph": 1}):
+    for opts in ({"prezero": 2}, {"prezero": 0}, {"prezero": 2, "no_graph": 1}):
         with sp.options(**opts):
             F = [torch.full((I, R), float("nan"), dtype=torch.float64, device="cuda") for I in dims]
             res = sp.cp_als(t, R, 7, F, seed=52)
