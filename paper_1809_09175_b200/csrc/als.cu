@@ -1118,10 +1118,10 @@ __host__ __device__ constexpr size_t apply_mma_smem_doubles() {
 }
 
 #ifndef SPTK_APPLY_MMA_PF  // A/B builds only
-#define SPTK_APPLY_MMA_PF 4
+#define SPTK_APPLY_MMA_PF 1
 #endif
 #ifndef SPTK_APPLY_MMA_MINB
-#define SPTK_APPLY_MMA_MINB 2
+#define SPTK_APPLY_MMA_MINB 3
 #endif
 constexpr int kApplyMmaPf = SPTK_APPLY_MMA_PF;
 
@@ -1178,8 +1178,9 @@ __global__ void __launch_bounds__(256, SPTK_APPLY_MMA_MINB)
             for (int k = 0; k < PL; ++k) v[k] = (ti < ntile && e0 + k < lim) ? (double)V[e0 + k] : 0.0;
         }
     };
-    // V tiles kApplyMmaPf ahead (1 KB per warp each): one tile in flight per
-    // warp kept the tall LBNL mode at ~3.4 TB/s
+    // V tiles kApplyMmaPf ahead (1 KB per warp each; 4 ahead at 2 blocks/SM
+    // measured 2 % slower on LBNL than 1 ahead at 3 blocks/SM once the tile
+    // strides were conflict-free, profiles/r02/s2/ab_apply_mma_variants.log)
     int64_t ti0 = blockIdx.x * (int64_t)8 + warp;
     double vn[kApplyMmaPf][PL];
 #pragma unroll
