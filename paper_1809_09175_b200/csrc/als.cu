@@ -23,6 +23,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 
 #include "common.cuh"
@@ -1535,36 +1536,44 @@ struct ApplyPlan {
 
 template <typename T, int LR>
 static int warp_apply_cap(size_t smb) {
-    static int occ = -1;
-    if (occ < 0) {
+    // per device: the attribute and the occupancy are properties of the
+    // device's context (a process may drive several GPUs)
+    static std::atomic<int> occ[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (occ[dev].load() < 1) {
         cudaFuncSetAttribute(apply_gram_warp_kernel<T, LR>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, apply_gram_warp_kernel<T, LR>, 256,
-                                                          smb) != cudaSuccess || occ < 1) {
+        int o = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, apply_gram_warp_kernel<T, LR>, 256,
+                                                          smb) != cudaSuccess || o < 1) {
             cudaGetLastError();
-            occ = 1;
+            o = 1;
         }
+        occ[dev].store(o);
     }
-    return occ * dev_sms();
+    return occ[dev].load() * dev_sms();
 }
 
 template <typename T, int RB>
 static int mma_apply_cap(size_t smb) {
-    static int occ[64] = {};  // per device
+    static std::atomic<int> occ[64];  // per device (see warp_apply_cap)
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev >= 64) dev = 0;
-    if (occ[dev] < 1) {
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (occ[dev].load() < 1) {
         cudaFuncSetAttribute(apply_gram_mma_kernel<T, RB>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[dev], apply_gram_mma_kernel<T, RB>,
-                                                          256, smb) != cudaSuccess ||
-            occ[dev] < 1) {
+        int o = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, apply_gram_mma_kernel<T, RB>, 256,
+                                                          smb) != cudaSuccess || o < 1) {
             cudaGetLastError();
-            occ[dev] = 1;
+            o = 1;
         }
+        occ[dev].store(o);
     }
-    return occ[dev] * dev_sms();
+    return occ[dev].load() * dev_sms();
 }
 
 template <typename T>
