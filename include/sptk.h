@@ -222,9 +222,12 @@ sptk_status sptk_mttkrp_rows(sptk_tensor t, int mode, int64_t R, const void *con
  *   fit_trace   host double[max_iters] or NULL
  *   comm        NULL or a communicator (row-range sharding of every mode;
  *               factors replicated on all ranks)
- * Requires nmodes >= 2.  Builds missing perms.  Synchronises `stream` once
- * per iteration (the fit).  SPTK_EZERONORM if ||X|| = 0; SPTK_ESINGULAR if
- * Gamma stays singular. */
+ * Any R in 1..128: when R is not a multiple of the 32-byte lane vector the
+ * iteration runs on internally zero-padded factors (option pad_rank) and the
+ * outputs are the rank-R ones, stride R.  Synchronises `stream` once per
+ * iteration (the fit) when tol > 0, once per call otherwise (the fits then
+ * come from a device-side history).  Builds missing perms.  Requires nmodes
+ * >= 2.  SPTK_EZERONORM if ||X|| = 0; SPTK_ESINGULAR if Gamma stays singular. */
 sptk_status sptk_cp_als(sptk_tensor t, int64_t R, int max_iters, double tol, uint64_t seed,
                         const void *const *init, void *const *factors_out, void *lambda_out,
                         double *fit_out, int *iters_out, double *fit_trace, sptk_comm comm,
