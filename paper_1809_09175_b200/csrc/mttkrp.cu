@@ -17,7 +17,9 @@ static int64_t run_length(int64_t npos, int G) {
     const int64_t fixed = opt(OPT_RUN);
     if (fixed > 0) return fixed < 4 ? 4 : (fixed + 3) / 4 * 4;
     const int64_t workers_per_sm = 768 / G;  // ~3 resident 256-thread blocks
-    const int64_t target = (int64_t)dev_sms() * workers_per_sm * 4;
+    // ~2 waves of workers (4 waves: LBNL's 868K-row mode 0.091 ms at 16
+    // positions per worker vs 0.087 at 32, profiles/r02/s2/ab_tall_mode_run.log)
+    const int64_t target = (int64_t)dev_sms() * workers_per_sm * 2;
     int64_t run = npos / (target > 0 ? target : 1);
     if (run > 256) run = 256;
     // short runs only where the grid would otherwise not fill the GPU (small
