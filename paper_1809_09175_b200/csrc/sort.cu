@@ -202,19 +202,17 @@ __global__ void __launch_bounds__(kSortThreads)
 // the last pass of a sort whose keys are not wanted writes values only.
 // (round-1 kernel above: 4.6 warp instructions per key, issue-bound at
 // 73 % issue-active, 0.43 of HBM; profiles/r02/prof_radix_raw.csv)
-// NW warps x IT keys per thread = one kSortTile tile (8 x 16 default; the
-// wide variant 16 x 8 holds half the per-thread arrays: more warps per SM)
-template <int DB, int NW = kSortWarps>
+template <int DB>
 struct DownsweepSmem {
-    uint32_t wbase[NW][1 << DB];  // per-warp running count, then tile position base
-    int32_t delta[1 << DB];       // global run start - tile start of each digit
-    uint32_t wsum[NW];
+    uint32_t wbase[kSortWarps][1 << DB];  // per-warp running count, then tile position base
+    int32_t delta[1 << DB];               // global run start - tile start of each digit
+    uint32_t wsum[kSortWarps];
     uint32_t skey[kSortTile];
     uint32_t sval[kSortTile];
 };
 
-template <int DB, bool FULL, int NW = kSortWarps>
-__device__ __forceinline__ void downsweep_body(DownsweepSmem<DB, NW> &sm, uint32_t tile,
+template <int DB, bool FULL>
+__device__ __forceinline__ void downsweep_body(DownsweepSmem<DB> &sm, uint32_t tile,
                                                const uint32_t *__restrict__ keys_in,
                                                const uint32_t *__restrict__ vals_in, uint32_t P,
                                                int shift, uint32_t ntiles,
@@ -223,7 +221,6 @@ __device__ __forceinline__ void downsweep_body(DownsweepSmem<DB, NW> &sm, uint32
                                                uint32_t *__restrict__ vals_out) {
     constexpr int ND = 1 << DB;
     constexpr uint32_t MASK = ND - 1;
-    constexpr int TH = NW * 32, IT = kSortTile / TH, CH = kSortTile / NW;  // CH keys per warp
     auto &wbase = sm.wbase;
     auto &delta = sm.delta;
     auto &wsum = sm.wsum;
@@ -234,11 +231,11 @@ __device__ __forceinline__ void downsweep_body(DownsweepSmem<DB, NW> &sm, uint32
     __syncwarp();
     const uint32_t tile0 = tile * (uint32_t)kSortTile;
     const uint32_t tile_n = FULL ? (uint32_t)kSortTile : P - tile0;
-    const uint32_t base = tile0 + warp * (uint32_t)CH;
+    const uint32_t base = tile0 + warp * (uint32_t)kWarpChunk;
     const uint32_t lt = lanemask_lt();
-    uint32_t key[IT], val[IT];
+    uint32_t key[kSortItems], val[kSortItems];
 #pragma unroll
-    for (int r = 0; r < IT; ++r) {
+    for (int r = 0; r < kSortItems; ++r) {
         const uint32_t i = base + r * 32 + lane;
         if (FULL || i < P) {
             key[r] = __ldg(keys_in + i);
@@ -251,9 +248,9 @@ __device__ __forceinline__ void downsweep_body(DownsweepSmem<DB, NW> &sm, uint32
     // A: stable rank of every key among the equal digits of its warp chunk
     //    (rounds of 32 in storage order, per-bit ballots); the running count
     //    of each digit ends as the warp's digit histogram
-    uint32_t rank[IT];
+    uint32_t rank[kSortItems];
 #pragma unroll
-    for (int r = 0; r < IT; ++r) {
+    for (int r = 0; r < kSortItems; ++r) {
         const bool valid = FULL || base + r * 32 + lane < P;
         const uint32_t digit = (key[r] >> shift) & MASK;
         uint32_t peers = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
@@ -279,11 +276,11 @@ __device__ __forceinline__ void downsweep_body(DownsweepSmem<DB, NW> &sm, uint32
     //    tile position of the warp's first key of the digit; delta := global
     //    start of the digit's run of this tile - its tile start
     {
-        const int d = threadIdx.x;  // TH >= 256 >= ND
+        const int d = threadIdx.x;  // kSortThreads == 256 >= ND
         uint32_t tot = 0;
         if (d < ND) {
 #pragma unroll
-            for (int w = 0; w < NW; ++w) {
+            for (int w = 0; w < kSortWarps; ++w) {
                 const uint32_t c = wbase[w][d];
                 wbase[w][d] = tot;
                 tot += c;
@@ -299,19 +296,19 @@ __device__ __forceinline__ void downsweep_body(DownsweepSmem<DB, NW> &sm, uint32
         __syncthreads();
         uint32_t wpre = 0;
 #pragma unroll
-        for (int w = 0; w < NW; ++w)
+        for (int w = 0; w < kSortWarps; ++w)
             if (w < warp) wpre += wsum[w];
         if (d < ND) {
             const uint32_t lstart = wpre + inc - tot;
 #pragma unroll
-            for (int w = 0; w < NW; ++w) wbase[w][d] += lstart;
+            for (int w = 0; w < kSortWarps; ++w) wbase[w][d] += lstart;
             delta[d] = (int32_t)(offsets[(size_t)d * ntiles + tile] - lstart);
         }
     }
     __syncthreads();
     // C: tile-local scatter into shared memory
 #pragma unroll
-    for (int r = 0; r < IT; ++r) {
+    for (int r = 0; r < kSortItems; ++r) {
         if (FULL || base + r * 32 + lane < P) {
             const uint32_t pos = wbase[warp][(key[r] >> shift) & MASK] + rank[r];
             skey[pos] = key[r];
@@ -321,7 +318,7 @@ __device__ __forceinline__ void downsweep_body(DownsweepSmem<DB, NW> &sm, uint32
     __syncthreads();
     // D: coalesced write-out of the digit runs
 #pragma unroll 4
-    for (uint32_t j = threadIdx.x; j < tile_n; j += TH) {
+    for (uint32_t j = threadIdx.x; j < tile_n; j += kSortThreads) {
         const uint32_t k = skey[j];
         const uint32_t g = (uint32_t)((int32_t)j + delta[(k >> shift) & MASK]);
         if (keys_out) keys_out[g] = k;
@@ -343,28 +340,11 @@ __global__ void __launch_bounds__(kSortThreads, SPTK_DS_MINB)
                                   keys_out, vals_out);
 }
 
-// the wide variant: 512 threads x 8 keys (option sort_wide; digits <= 7 bits:
-// 16 warps' 8-bit histograms would exceed the 48 KB of static shared memory)
-template <int DB>
-__global__ void __launch_bounds__(512, 2)
-    radix_downsweep2w(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
-                      uint32_t P, int shift, uint32_t ntiles, const uint32_t *__restrict__ offsets,
-                      uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out) {
-    __shared__ DownsweepSmem<DB, 16> sm;
-    if ((blockIdx.x + 1) * (uint64_t)kSortTile <= P)
-        downsweep_body<DB, true, 16>(sm, blockIdx.x, keys_in, vals_in, P, shift, ntiles, offsets,
-                                     keys_out, vals_out);
-    else
-        downsweep_body<DB, false, 16>(sm, blockIdx.x, keys_in, vals_in, P, shift, ntiles, offsets,
-                                      keys_out, vals_out);
-}
-
 static cudaError_t launch_downsweep2(int db, unsigned grid, cudaStream_t s, const uint32_t *kin,
                                      const uint32_t *vin, uint32_t P, int shift, uint32_t ntiles,
                                      const uint32_t *offsets, uint32_t *kout, uint32_t *vout) {
 #define SPTK_DS(D) \
-    case D: if (D <= 7 && opt(OPT_SORT_WIDE)) radix_downsweep2w<(D <= 7 ? D : 7)><<<grid, 512, 0, s>>>(kin, vin, P, shift, ntiles, offsets, kout, vout); \
-            else radix_downsweep2<D><<<grid, kSortThreads, 0, s>>>(kin, vin, P, shift, ntiles, offsets, kout, vout); break;
+    case D: radix_downsweep2<D><<<grid, kSortThreads, 0, s>>>(kin, vin, P, shift, ntiles, offsets, kout, vout); break;
     switch (db) {
         SPTK_DS(1) SPTK_DS(2) SPTK_DS(3) SPTK_DS(4) SPTK_DS(5) SPTK_DS(6) SPTK_DS(7) SPTK_DS(8)
     default: return cudaErrorInvalidValue;
