@@ -97,12 +97,12 @@ def gather_ceilings(row_bytes: int):
     # the slice MTTKRP's own access mix (16 B record + one L1-resident and one
     # L2-resident 128 B row per nonzero, no arithmetic, perfect window hits):
     # the best grid of tools/ceilings.cu's pair_gather runs
-    pair = [v(k) for k in j if k.startswith("pair_gather_l1_l2_128")] if j else []
+    pair = [v(k) for k in j if k.startswith(f"pair_gather_l1_l2_{rb}_")] if j else []
     pair = [x for x in pair if x]
     return {"row_bytes": rb, "l1_resident": v(f"gather_l1_l1_{rb}"),
             "l2_resident": v(f"gather_l2_nol1_{rb}"), "l2_resident_l1alloc": v(f"gather_l2_l1_{rb}"),
             "hbm_resident": v(f"gather_hbm_nol1_{rb}"), "hbm_read": v("hbm_read"),
-            "slice_mix_128": (max(pair) if pair and rb == 128 else None),
+            "slice_mix": (max(pair) if pair else None),
             "source": "profiles/ceilings.json (tools/ceilings.cu)" if j else None}
 
 
@@ -543,8 +543,8 @@ def main():
                                     "ceilings": ceil,
                                     "frac_of_l1_resident": (gather_rate / ceil["l1_resident"]
                                                             if ceil.get("l1_resident") else None),
-                                    "frac_of_slice_mix": (gather_rate / ceil["slice_mix_128"]
-                                                          if ceil.get("slice_mix_128") else None)},
+                                    "frac_of_slice_mix": (gather_rate / ceil["slice_mix"]
+                                                          if ceil.get("slice_mix") else None)},
                          "timing": "per-launch CUDA events in a second K-iteration pass "
                                    "(eager launches), mean over all MTTKRP launches"},
             "clocks": clk.summary(),

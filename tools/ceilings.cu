@@ -100,10 +100,11 @@ __global__ void __launch_bounds__(256) gather_rows(const uint32_t *__restrict__ 
 // L2-resident table (L1::no_allocate: the other factor); 4 lanes x 32 B per
 // row, U elements in flight per group.  An upper bound for the kernel: its
 // window rows hit L1 only ~35 % of the time (ncu), here always.
+template <int G>  // lanes per row: 4 = 128-byte rows (f64 R=16), 2 = 64-byte rows (f32 R=16)
 __global__ void __launch_bounds__(256) pair_gather(const uint4 *__restrict__ rec, int64_t n,
                                                    const double *__restrict__ A,
                                                    const double *__restrict__ B, double *out) {
-    constexpr int U = 4, G = 4;
+    constexpr int U = 4;
     const int q = threadIdx.x % G;
     const int64_t g0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
     const int64_t gs = ((int64_t)gridDim.x * blockDim.x) / G;
@@ -125,8 +126,8 @@ __global__ void __launch_bounds__(256) pair_gather(const uint4 *__restrict__ rec
         double fa[U][4], fb[U][4];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            ld32(A + (int64_t)ra[u] * 16 + q * 4, fa[u], true);
-            ld32(B + (int64_t)rb[u] * 16 + q * 4, fb[u], false);
+            ld32(A + (int64_t)ra[u] * (4 * G) + q * 4, fa[u], true);
+            ld32(B + (int64_t)rb[u] * (4 * G) + q * 4, fb[u], false);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -308,12 +309,21 @@ int main(int argc, char **argv) {
         CK(cudaMemcpy(rec, hr.data(), np * 16, cudaMemcpyHostToDevice));
         const double *TA = H, *TB = H + (int64_t)(1 << 20);  // disjoint tables in the 4 GB buffer
         for (int bps : {2, 3, 4}) {
-            const double ms = best_ms([&] { pair_gather<<<sms * bps * 4, 256>>>(rec, np, TA, TB, out); });
+            const double ms = best_ms([&] { pair_gather<4><<<sms * bps * 4, 256>>>(rec, np, TA, TB, out); });
             char key[64], what[200];
             snprintf(key, sizeof key, "pair_gather_l1_l2_128_x%d", bps);
             snprintf(what, sizeof what, "slice-MTTKRP mix: 16 B record + 128 B row from 96 KB (L1) + 128 B "
                      "row from 6.4 MB (L2, no L1); gathered row bytes / time, grid %d x SMs", bps * 4);
             emit(key, (double)np * 256 / ms / 1e6, "GB/s", what);
+        }
+        // 64-byte rows (fp32 R = 16): the same tables hold twice the rows; ids stay in range
+        for (int bps : {2, 3, 4}) {
+            const double ms = best_ms([&] { pair_gather<2><<<sms * bps * 4, 256>>>(rec, np, TA, TB, out); });
+            char key[64], what[200];
+            snprintf(key, sizeof key, "pair_gather_l1_l2_64_x%d", bps);
+            snprintf(what, sizeof what, "slice-MTTKRP mix, 64 B rows: 16 B record + 64 B row from 48 KB (L1) + "
+                     "64 B row from 3.2 MB (L2, no L1); gathered row bytes / time, grid %d x SMs", bps * 4);
+            emit(key, (double)np * 128 / ms / 1e6, "GB/s", what);
         }
         cudaFree(rec);
     }
