@@ -467,15 +467,21 @@ sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     const int m0 = mode < 0 ? 0 : mode, m1 = mode < 0 ? t->N : mode + 1;
     double tc = setup_clock(s);
-    // one memory query, while the GPU is idle; the rest of the call keeps a ledger
+    // one memory query, while the GPU is idle; the rest of the call keeps a
+    // ledger.  A steady-state re-sort (perm, rowptr, sort workspace and copies
+    // of the modes all present) allocates nothing and decides nothing by free
+    // memory: no query at all (cudaMemGetInfo cost 1 ms of host time inside
+    // the timed re-sort in some processes: 2.1 instead of 1.0 ms per mode,
+    // profiles/r02/s2/bench_all_final.jsonl)
     struct LedgerScope {
         sptk_tensor t;
         ~LedgerScope() { t->ledger = false; }
     } ledger_scope{t};
-    if (cudaMemGetInfo(&t->ledger_free0, &t->ledger_total) == cudaSuccess) {
+    const bool needs_memory = build_needs_memory(t, m0, m1);
+    if (needs_memory && cudaMemGetInfo(&t->ledger_free0, &t->ledger_total) == cudaSuccess) {
         t->ledger_owned0 = owned_bytes(t);
         t->ledger = true;
-    } else {
+    } else if (needs_memory) {
         cudaGetLastError();
     }
     // what this call may allocate: the sort workspace, copies, (released) keys
@@ -492,7 +498,7 @@ sptk_status sptk_build_perm(sptk_tensor t, int mode, void *stream) {
     }
     bool all = true;  // the ingest keys are consumed once every mode is sorted
     for (int m = 0; m < t->N; ++m) all = all && t->has_perm[m];
-    if (all && t->keys.p) {
+    if (all && t->keys.p && needs_memory) {
         // they also speed up the copies' secondary sorts; keep them through
         // the copies only if every copy (+ its order buffer) fits beside them
         size_t free_b = 0, total_b = 0;

@@ -52,7 +52,7 @@ enum Opt {
     OPT_RUN, OPT_VARIANT, OPT_SLICE, OPT_SLICE_L2_KB, OPT_SLICE_ROWS, OPT_SLICE_OTHER_FIRST,
     OPT_ROWREC, OPT_FORCE_V, OPT_GENERIC, OPT_DEBUG_DISPATCH, OPT_COPY_ORDER, OPT_DEFERRED_NORM,
     OPT_NO_GRAPH, OPT_GAMMA_INV_CHOL, OPT_USE_COPY, OPT_APPLY_TILE, OPT_APPLY_NB_MULT, OPT_TAIL_ROWS, OPT_APPLY_WAVE, OPT_APPLY_WARP,
-    OPT_KEEP_KEYS, OPT_PDL, OPT_EXCHANGE, OPT_PAD_RANK, OPT_SORT_V1, OPT_PREZERO, OPT_APPLY_MMA, OPT_GJ_WARP, OPT_SIDE_PRIO, OPT_WIN, OPT_SLICE_FILL, OPT_FUSED_REDUCE, OPT_COUNT
+    OPT_KEEP_KEYS, OPT_PDL, OPT_EXCHANGE, OPT_PAD_RANK, OPT_SORT_V1, OPT_PREZERO, OPT_APPLY_MMA, OPT_GJ_WARP, OPT_SIDE_PRIO, OPT_WIN, OPT_SLICE_FILL, OPT_FUSED_REDUCE, OPT_APPLY_MMA_ROWS, OPT_COUNT
 };
 int64_t opt(Opt o);
 uint64_t options_generation();  // bumped by every sptk_set_option / sptk_reset_options
@@ -254,6 +254,7 @@ sptk_status launch_pack(sptk_tensor t, const void *idx, sptk_idx_type itype, con
                         int *d_flag, double *d_normsq, cudaStream_t s);
 sptk_status build_perm_mode(sptk_tensor t, int mode, cudaStream_t s);
 sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s);
+bool build_needs_memory(sptk_tensor t, int m0, int m1);
 void drop_copies(sptk_tensor t);
 sptk_status merge_duplicates(sptk_tensor t, bool error_only, cudaStream_t s);
 // out_zeroed: the caller already zeroed rows [row_begin, row_end) of out

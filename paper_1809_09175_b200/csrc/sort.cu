@@ -725,6 +725,22 @@ sptk_status ensure_sorted_copy(sptk_tensor t, int mode, cudaStream_t s) {
     return SPTK_OK;
 }
 
+// Would build_perm of modes [m0, m1) allocate anything?  (perm / rowptr of
+// the mode, the sort workspace, a missing copy)
+bool build_needs_memory(sptk_tensor t, int m0, int m1) {
+    const int64_t P = t->P;
+    if (P > 0 && (!t->sortws.p || t->sortws.bytes < sizeof(uint32_t) * sort_ws_words(P)))
+        return true;
+    for (int m = m0; m < m1; ++m) {
+        if (!t->perm[m].p || t->perm[m].bytes < sizeof(uint32_t) * (size_t)std::max<int64_t>(P, 1))
+            return true;
+        if (!t->rowptr[m].p || t->rowptr[m].bytes < sizeof(uint32_t) * (size_t)(t->dims[m] + 1))
+            return true;
+        if (!t->has_srec[m] && !t->copy_declined[m] && !t->perm_gather_only && P > 0) return true;
+    }
+    return false;
+}
+
 void drop_copies(sptk_tensor t) {
     for (int m = 0; m < t->N; ++m) {
         t->srec[m].release();

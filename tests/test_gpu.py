@@ -529,6 +529,28 @@ def test_config_nell2_full_perm_gather(sp):
     full_config_check(sp, "nell2", 16, torch.float64, perm_gather=True)
 
 
+@pytest.mark.parametrize("name,iters", [("lbnl", 3)])  # the oracle takes ~20 s here
+def test_cp_als_full_size(sp, name, iters):
+    """CP-ALS at BASELINE size against the oracle's trajectory: every glue
+    path of the benchmarked iteration runs here -- the tensor-core apply over
+    296 blocks on LBNL's 868K-row mode, the fused reduce + finalise, the
+    small-mode last-block tails, the prioritised side-stream inverse, the
+    filled slice grids, graph replay."""
+    c = synth.CONFIGS[name]
+    idx, vals = synth.tensor(c.seed, c.dims, c.nnz, c.dist)
+    R = 16
+    ref = oracle.cp_als(c.dims, idx, vals, factors_np(c.seed_f, c.dims, R), iters)
+    t = make(sp, c.dims, idx, vals)
+    F = [torch.empty(I, R, dtype=torch.float64, device="cuda") for I in c.dims]
+    lam = torch.empty(R, dtype=torch.float64, device="cuda")
+    res = sp.cp_als(t, R, iters, F, seed=c.seed_f, lambda_out=lam)
+    assert np.max(np.abs(res["trace"] - ref["trace"])) <= 1e-9, (res["trace"], ref["trace"])
+    assert rel(lam.cpu().numpy(), ref["lam"]) <= 1e-8
+    for m in range(c.N):
+        assert rel(F[m].cpu().numpy(), ref["A"][m]) <= 1e-8, m
+    t.close()
+
+
 def test_config_delicious_full(sp):
     full_config_check(sp, "delicious", 16, torch.float64)
 
