@@ -1580,7 +1580,7 @@ template <typename T>
 static ApplyPlan plan_apply(AlsCtx &c, int64_t rows, int R, bool small) {
     ApplyPlan p;
     // FP64 tensor-core apply for R = 8 / 16 (R is the padded rank here)
-    p.mma = opt(OPT_APPLY_MMA) != 0 && (R == 8 || R == 16) && rows >= opt(OPT_APPLY_MMA_ROWS);
+    p.mma = opt(OPT_APPLY_MMA) != 0 && (R == 8 || R == 16);
     if (p.mma) {
         p.LR = R;
         p.smb = sizeof(double) * (R == 8 ? apply_mma_smem_doubles<1>() : apply_mma_smem_doubles<2>());

@@ -62,7 +62,6 @@ constexpr OptDef kOpts[] = {
     {"slice_fill", 6},          // slice traversal: halve the slices until the grid has this many
                                 //   blocks per SM (0 = off)
     {"fused_reduce", 1},        // CP-ALS: a large mode's reductions + finalise (+ fit) in one launch
-    {"apply_mma_rows", 0},      // CP-ALS: the tensor-core apply only for modes of >= this many rows
 };
 
 static_assert(sizeof(kOpts) / sizeof(kOpts[0]) == OPT_COUNT, "kOpts must list every Opt, in order");
