@@ -136,6 +136,22 @@ def test_options_roundtrip_and_unknown_name(sp):
     assert sp.last_dispatch() == ""
 
 
+def test_every_documented_option_exists_with_its_default(sp):
+    """Every option include/sptk.h documents is known to the library, with the
+    documented default (round-2 options included)."""
+    import re
+    hdr = open(os.path.join(ROOT, "include", "sptk.h")).read()
+    doc = hdr[hdr.index("sptk_set_option") - 6000:hdr.index("sptk_status sptk_set_option")]
+    defaults = {"pad_rank": 1, "sort_v1": 0, "prezero": 1, "apply_mma": 1, "gj_warp": 1,
+                "side_prio": -1, "win": 0, "slice_fill": 6, "fused_reduce": 1, "exchange": -1,
+                "pdl": 1, "keep_keys": 1, "tail_rows": 8192, "slice": 1, "slice_l2_kb": 32768}
+    sp.reset_options()
+    for name, value in defaults.items():
+        assert sp.get_option(name) == value, name
+    for name in re.findall(r"\b([a-z][a-z0-9_]+) -?[0-9]+ \(", doc):
+        sp.get_option(name)  # raises SptkError if the library does not know it
+
+
 def test_binding_validates_buffers_before_the_abi(sp):
     """shapes, dtypes, contiguity and placement are checked in the
     binding before raw addresses cross the C ABI (a float32 factor for an f64
