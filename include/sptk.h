@@ -310,15 +310,18 @@ sptk_status sptk_set_tuning(int variant, int64_t run);
  *   pad_rank 1 (CP-ALS with R not a multiple of the 32-byte lane vector runs
  *   on internally padded factors whose pad columns stay zero -- the output is
  *   the rank-R result; 0: stride R; > 1: pad to a multiple of that many
- *   columns), sort_v1 0 (1: the round-1 radix downsweep, A/B), prezero 1
- *   (CP-ALS: MTTKRP outputs of >= 256 MB zeroed on a side stream while the
- *   previous mode runs), apply_mma 1 (CP-ALS V Gamma^{-1} and Gram update on the
+ *   columns), sort_v1 0 (1: the round-1 radix downsweep, A/B),
+ *   prezero 1 (CP-ALS: MTTKRP outputs of >= 256 MB zeroed on a side stream
+ *   while the previous mode runs; 2: every output), apply_mma 1 (CP-ALS V Gamma^{-1} and Gram update on the
  *   FP64 tensor cores for R = 8 / 16), gj_warp 1 (one-warp Gauss-Jordan
  *   Gamma^{-1} for R <= 32), side_prio -1 (the CP-ALS side stream at the highest
  *   priority: -1 for >= 2^20 nonzeros, 1 always, 0 never; read when the handle's
  *   stream is created), win 0 (> 0: window-major permuted copies, built at
  *   build_perm, for modes with few rows whose secondary factor spans >= 2 x win
- *   L2 windows; served by the cooperative kernel).
+ *   L2 windows; served by the cooperative kernel), slice_fill 6 (the slice
+ *   traversal halves its slices until its grid has this many blocks per SM; 0
+ *   off), fused_reduce 1 (CP-ALS: a large mode's reductions, finalisation and
+ *   fit in one launch).
  * Every choice gives the same result up to summation order; options change
  * which kernel computes it.  Not synchronised with calls in flight on other
  * threads.  SPTK_EINVAL for an unknown name. */

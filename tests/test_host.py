@@ -141,7 +141,7 @@ def test_every_documented_option_exists_with_its_default(sp):
     documented default (round-2 options included)."""
     import re
     hdr = open(os.path.join(ROOT, "include", "sptk.h")).read()
-    doc = hdr[hdr.index("sptk_set_option") - 6000:hdr.index("sptk_status sptk_set_option")]
+    doc = hdr[hdr.index("sptk_set_option") - 7000:hdr.index("sptk_status sptk_set_option")]
     defaults = {"pad_rank": 1, "sort_v1": 0, "prezero": 1, "apply_mma": 1, "gj_warp": 1,
                 "side_prio": -1, "win": 0, "slice_fill": 6, "fused_reduce": 1, "exchange": -1,
                 "pdl": 1, "keep_keys": 1, "tail_rows": 8192, "slice": 1, "slice_l2_kb": 32768}
