@@ -587,7 +587,10 @@ constexpr int kApplyTileDefault = 64;
 #define SPTK_APPLY_PF_DIV 4
 #endif
 __host__ __device__ constexpr int apply_pf(int RM) { return RM / SPTK_APPLY_PF_DIV; }
-constexpr int kTailBlocks = 32;  // apply_gram grids up to this size finalise in their last block
+#ifndef SPTK_TAIL_BLOCKS  // A/B builds only
+#define SPTK_TAIL_BLOCKS 32
+#endif
+constexpr int kTailBlocks = SPTK_TAIL_BLOCKS;  // apply_gram grids up to this size finalise in their last block
 static int apply_tile_rows() {  // option apply_tile (rows of V per tile, tuning)
     const int64_t v = opt(OPT_APPLY_TILE);
     return v >= 16 ? (int)v : kApplyTileDefault;
