@@ -852,8 +852,14 @@ constexpr int kNumVariants = 2;
 #ifndef SPTK_KU_WIDE
 #define SPTK_KU_WIDE SPTK_KU
 #endif
-template <int N> constexpr int kU = N <= 3 ? SPTK_KU : SPTK_KU_WIDE;
-template <int N> constexpr int kMinBlocks = N <= 3 ? SPTK_KMINB : SPTK_KMINB_WIDE;
+#ifndef SPTK_KU_5  // N = 5 (LBNL) separately, for A/B builds
+#define SPTK_KU_5 SPTK_KU_WIDE
+#endif
+#ifndef SPTK_KMINB_5
+#define SPTK_KMINB_5 SPTK_KMINB_WIDE
+#endif
+template <int N> constexpr int kU = N <= 3 ? SPTK_KU : (N == 5 ? SPTK_KU_5 : SPTK_KU_WIDE);
+template <int N> constexpr int kMinBlocks = N <= 3 ? SPTK_KMINB : (N == 5 ? SPTK_KMINB_5 : SPTK_KMINB_WIDE);
 
 template <typename T, int N, int RB, bool SORTED, bool COOP, int V, bool ROWREC = false>
 inline sptk_status fast_launch_g(int G, const MttkrpArgs &a, int64_t workers, cudaStream_t s) {
