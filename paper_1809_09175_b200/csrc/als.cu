@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(32)
             double gq[LR];
 #pragma unroll
             for (int k = 0; k < LR; ++k)
-                gq[k] = (i < Rl && k < Rl) ? __ldg(G + (int64_t)q * RR + i * R + k) : 1.0;
+                gq[k] = (i < Rl && k < Rl) ? __ldcg(G + (int64_t)q * RR + i * R + k) : 1.0;
 #pragma unroll
             for (int k = 0; k < LR; ++k) m[k] *= gq[k];
         }
@@ -2374,6 +2374,9 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t Rl, int max_iters, double 
             SPTK_CUDA(cudaMemcpy(hist.data(), w.trace.p, sizeof(double) * max_iters,
                                  cudaMemcpyDeviceToHost));
             if (bad) st = fail(SPTK_ESINGULAR, "Gamma is singular after the ridge retry");
+            for (int k = 0; k < max_iters && st == SPTK_OK; ++k)
+                if (!std::isfinite(hist[k]))
+                    st = fail(SPTK_ESINGULAR, "non-finite fit: Gamma numerically singular");
             if (fit_trace)
                 for (int k = 0; k < max_iters; ++k) fit_trace[k] = hist[k];
             fit = hist[max_iters - 1];
@@ -2439,6 +2442,11 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t Rl, int max_iters, double 
                     for (int k = it; k < max_iters; ++k) fit_trace[k] = hist[k];
                 fit = hist[max_iters - 1];
                 it = max_iters;
+                for (int k = 0; k < max_iters; ++k)
+                    if (!std::isfinite(hist[k])) {
+                        st = fail(SPTK_ESINGULAR, "non-finite fit: Gamma numerically singular");
+                        break;
+                    }
                 break;
             }
             st = complete_iteration(c, &fit, &bad);
@@ -2449,6 +2457,10 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t Rl, int max_iters, double 
     have_fit:
         if (bad) {
             st = fail(SPTK_ESINGULAR, "Gamma is singular after the ridge retry");
+            break;
+        }
+        if (!std::isfinite(fit)) {  // a tiny positive pivot can still overflow Gamma^{-1}
+            st = fail(SPTK_ESINGULAR, "non-finite fit: Gamma numerically singular");
             break;
         }
         if (fit_trace) fit_trace[it] = fit;

@@ -934,6 +934,32 @@ def test_window_major_copy(sp, dtype):
         t.close()
 
 
+def test_cp_als_degenerate_regime_reports_not_nan(sp):
+    """CP-ALS deep into the degenerate regime of a random tensor (LBNL shape:
+    columns collapse to lambda = 0 after ~50 iterations, Gamma can become
+    numerically singular): every call either returns finite fits or raises
+    SPTK_ESINGULAR -- never a silent NaN."""
+    c = synth.CONFIGS["lbnl"]
+    from synth import device
+    idx, val = device.tensor(c.seed, c.dims, c.nnz, c.dist)
+    t = sp.sptensor_create(c.dims, idx, val)
+    sp.build_perm(t, -1)
+    R = 16
+    for its in (60, 90, 120):
+        for prof in (False, True):
+            F = [device.factor(c.seed_f, c.N, m, I, R) for m, I in enumerate(c.dims)]
+            sp.profile_enable(prof)
+            try:
+                res = sp.cp_als(t, R, its, F, init=F)
+                assert np.all(np.isfinite(res["trace"])), res["trace"]
+                assert all(bool(torch.isfinite(f).all()) for f in F)
+            except sp.SptkError as e:
+                assert e.name == "ESINGULAR", e
+            finally:
+                sp.profile_enable(False)
+    t.close()
+
+
 @pytest.mark.parametrize("exchange", [0, 1])
 def test_sharded_zero_column_e1(sp, monkeypatch, exchange):
     """A zero initial column through the sharded deferred path: every Gamma
