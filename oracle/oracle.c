@@ -212,14 +212,17 @@ void oracle_gram(int64_t I, int64_t R, const double *A, double *G)
         }
 }
 
-/* Cholesky G = L L^T in place (lower triangle of L returned in Lout). */
-static int chol(int64_t R, const double *G, double *L)
+/* Cholesky G = L L^T in place (lower triangle of L returned in Lout).
+ * Pivot j fails unless d_j > tau * G_jj (DESIGN.md §2 reading R7: a relative
+ * pivot below 1e-12 is a numerically singular G; tau = 0 is the plain
+ * positive-definiteness test). */
+static int chol(int64_t R, const double *G, double *L, double tau)
 {
     memset(L, 0, sizeof(double) * (size_t)(R * R));
     for (int64_t j = 0; j < R; ++j) {
         double d = G[j * R + j];
         for (int64_t k = 0; k < j; ++k) d -= L[j * R + k] * L[j * R + k];
-        if (!(d > 0.0)) return OR_ESINGULAR;
+        if (!(d > tau * G[j * R + j])) return OR_ESINGULAR;
         const double ljj = sqrt(d);
         L[j * R + j] = ljj;
         for (int64_t i = j + 1; i < R; ++i) {
@@ -247,20 +250,21 @@ static void chol_apply(int64_t R, const double *L, const double *b, double *x)
 }
 
 /* Cholesky factorisation of an SPD matrix with one ridge retry
- * (G + 1e-12 * (tr G / R) * I), then row-wise solves X = B G^{-1}
- * for nrhs rows of B (nrhs x R).  S:347. */
+ * (G + 1e-12 * (tr G / R) * I) when a pivot fails the relative test
+ * (DESIGN.md §2 R7; the retry tests d_j > 0), then row-wise solves
+ * X = B G^{-1} for nrhs rows of B (nrhs x R).  S:347. */
 int oracle_chol_solve(int64_t R, const double *G, int64_t nrhs, const double *B, double *X)
 {
     double *L = (double *)malloc(sizeof(double) * (size_t)(R * R));
     double *Gr = (double *)malloc(sizeof(double) * (size_t)(R * R));
     if (!L || !Gr) { free(L); free(Gr); return OR_ENOMEM; }
-    int st = chol(R, G, L);
+    int st = chol(R, G, L, 1e-12);
     if (st != OR_OK) {
         double tr = 0.0;
         for (int64_t j = 0; j < R; ++j) tr += G[j * R + j];
         memcpy(Gr, G, sizeof(double) * (size_t)(R * R));
         for (int64_t j = 0; j < R; ++j) Gr[j * R + j] += 1e-12 * (tr / (double)R);
-        st = chol(R, Gr, L);
+        st = chol(R, Gr, L, 0.0);
     }
     if (st == OR_OK)
         for (int64_t k = 0; k < nrhs; ++k) chol_apply(R, L, B + k * R, X + k * R);

@@ -121,6 +121,15 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Pivot test of the first factorisation attempt (DESIGN.md §2 reading R7, as
+// the oracle): pivot j counts as a failure unless d_j > kPivotRel * Gamma_jj.
+// d_j / Gamma_jj is the squared sine of the angle between column j and the
+// span of the columns before it; below 1e-12 Gamma is numerically singular
+// (duplicate CP components: cond ~ 1e300 on LBNL after 5 iterations) and its
+// inverse amplifies rounding without bound, so the ridge retry takes over.
+// The retry keeps the plain d_j > 0 test.
+constexpr double kPivotRel = 1e-12;
+
 // Gamma = Hadamard_{m != n} G_m; Cholesky Gamma = L L^T (one ridge retry with
 // 1e-12 tr(Gamma)/R, as the oracle); Gamma^{-1} = L^{-T} L^{-1} -> Ginv.
 // One block.  Shared memory: R x R (L in the lower triangle, L^{-1}
@@ -147,6 +156,7 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
     for (int attempt = 0; attempt < 2; ++attempt) {
+        const double tau = attempt == 0 ? kPivotRel : 0.0;
         for (int e = tid; e < R * R; e += blockDim.x) {
             const int i = e / R, j = e % R;
             if (j <= i) L[e] = gamma(i, j) + (i == j && i < Rl ? ridge : 0.0);
@@ -158,8 +168,9 @@ __global__ void __launch_bounds__(256)
                 for (int k = lane; k < j; k += 32) d += L[j * R + k] * L[j * R + k];
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-                d = L[j * R + j] - d;
-                if (!(d > 0.0)) {
+                const double gjj = L[j * R + j];
+                d = gjj - d;
+                if (!(d > tau * gjj)) {
                     if (lane == 0) bad = 1;
                     d = 1.0;
                 }
@@ -262,10 +273,15 @@ __device__ void gj_inv_block(const double *G, int N, int n, int R, int Rl,
         for (int j = 0; j < R; ++j) {
             if (tid == 0) {
                 double p = M[j * R + j];
-                if (!(p > 0.0)) {
-                    bad = 1;
-                    p = 1.0;
+                double gjj = 0.0;  // relative pivot test (first attempt): Gamma_jj
+                if (!attempt) {
+                    gjj = 1.0;
+                    if (j < Rl)
+                        for (int m = 0; m < N; ++m)
+                            if (m != n) gjj *= G[(int64_t)m * RR + j * R + j];
                 }
+                if (!(p > kPivotRel * gjj)) bad = 1;
+                if (!(p > 0.0)) p = 1.0;
                 piv = 1.0 / p;
             }
             for (int i = tid; i < R; i += blockDim.x) f[i] = M[i * R + j];
@@ -344,12 +360,16 @@ __global__ void __launch_bounds__(32)
             else if (i >= Rl || k >= Rl) m[k] = i == k ? 1.0 : 0.0;
             else if (i == k) m[k] += ridge;
         }
+        double dii = 0.0;  // Gamma_ii (relative pivot test, first attempt only)
+#pragma unroll
+        for (int k = 0; k < LR; ++k)
+            if (k == i && !attempt) dii = m[k];
         bool bad = false;
 #pragma unroll
         for (int j = 0; j < LR; ++j) {  // unrolled: m[] stays in registers
             if (j >= R) break;
             const double p = __shfl_sync(0xffffffffu, m[j], j);
-            bad |= !(p > 0.0);
+            bad |= !(p > kPivotRel * __shfl_sync(0xffffffffu, dii, j));
             const double rp = 1.0 / (p > 0.0 ? p : 1.0);
             const double f = m[j];  // this row's multiplier (row j: the pivot itself)
 #pragma unroll

@@ -221,6 +221,31 @@ def test_chol_solve_ridge_branch():
     assert resid(G2) >= 0.05                      # the unridged matrix
 
 
+def test_chol_solve_relative_pivot_takes_ridge():
+    """DESIGN.md §2 R7: a pivot d_j <= 1e-12 Gamma_jj is a failure even when
+    positive (a numerically singular Gamma, e.g. duplicate CP components).
+    Pinned by the 2 x 2 closed form [[a, c], [c, a]]^{-1} = [[a, -c], [-c, a]]
+    / (a^2 - c^2): with c = 1 - 2^-46 the pivot is ~2.8e-14 (ridge: a = 1 +
+    1e-12); with c = 1 - 2^-34 it is ~1.2e-10 (no ridge: a = 1).  The
+    subtraction a - c loses ~4 (resp. ~6) digits, hence the tolerances; the
+    unridged and ridged answers differ by ~36x and ~1.017x resp."""
+    B = np.array([[1.0, 0.0]])
+
+    def closed(a, c):
+        return np.array([[a, -c]]) / ((a - c) * (a + c))
+
+    c = 1.0 - 2.0 ** -46
+    G = np.array([[1.0, c], [c, 1.0]])
+    X = oracle.chol_solve(G, B)
+    np.testing.assert_allclose(X, closed(1.0 + 1e-12, c), rtol=1e-3)
+    assert not np.allclose(X, closed(1.0, c), rtol=0.5)   # the plain solve is ~36x larger
+    c = 1.0 - 2.0 ** -34
+    G = np.array([[1.0, c], [c, 1.0]])
+    X = oracle.chol_solve(G, B)
+    np.testing.assert_allclose(X, closed(1.0, c), rtol=1e-5)
+    assert not np.allclose(X, closed(1.0 + 1e-12, c), rtol=1e-3)  # no ridge here
+
+
 # ------------------------------------------------------------------- CP-ALS
 def _dense_as_sparse(T):
     idx = np.argwhere(T != 0).astype(np.uint32)
