@@ -208,8 +208,11 @@ sptk_status sptk_mttkrp_rows(sptk_tensor t, int mode, int64_t R, const void *con
  * Bader): textbook alternating least squares, readings in DESIGN.md §2.
  * For it < max_iters, for n = 0..N-1: V = MTTKRP(n); Gamma = Hadamard of
  * A_m^T A_m (m != n); A_n = V Gamma^{-1} (Gamma SPD: inverse by unpivoted
- * Gauss-Jordan, whose pivots are the squared Cholesky diagonal, so a
- * non-positive pivot = Cholesky failure; one ridge retry with 1e-12 tr(Gamma)/R); lambda = column 2-norms; normalise.  fit = 1 - ||X - M||
+ * Gauss-Jordan, whose pivots are the squared Cholesky diagonal; a pivot
+ * d_j <= 1e-12 Gamma_jj is a failure (numerically singular Gamma, e.g.
+ * duplicate components: DESIGN.md §2 R7); one ridge retry with
+ * 1e-12 tr(Gamma)/R, which needs only d_j > 0); lambda = column 2-norms;
+ * normalise.  fit = 1 - ||X - M||
  * / ||X|| after each iteration; stop when tol > 0 and |fit - fit_prev| < tol.
  *   init        HOST array of nmodes pointers (device or host) with the
  *               initial factors, or NULL: A_m(r, c) = U[0,1) drawn from the
@@ -227,7 +230,8 @@ sptk_status sptk_mttkrp_rows(sptk_tensor t, int mode, int64_t R, const void *con
  * outputs are the rank-R ones, stride R.  Synchronises `stream` once per
  * iteration (the fit) when tol > 0, once per call otherwise (the fits then
  * come from a device-side history).  Builds missing perms.  Requires nmodes
- * >= 2.  SPTK_EZERONORM if ||X|| = 0; SPTK_ESINGULAR if Gamma stays singular. */
+ * >= 2.  SPTK_EZERONORM if ||X|| = 0; SPTK_ESINGULAR if Gamma stays singular
+ * or the fit is not finite. */
 sptk_status sptk_cp_als(sptk_tensor t, int64_t R, int max_iters, double tol, uint64_t seed,
                         const void *const *init, void *const *factors_out, void *lambda_out,
                         double *fit_out, int *iters_out, double *fit_trace, sptk_comm comm,
