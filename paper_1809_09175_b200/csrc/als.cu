@@ -695,12 +695,23 @@ __global__ void __launch_bounds__(256)
     finalize_mode_block<T>(colsq, graw, A, N, n, R, Rl, next, s_all, lam, G, scale_next);
 }
 
-// A large mode's tail in one launch: every warp reduces one entry of
-// [colsq | graw | dot] over the nb apply blocks' partials (lanes stride over
-// the blocks, fixed shuffle tree: the reduce_partials_kernel order), then the
-// last block to arrive finalises the mode (and, after the last mode, the fit).
-// Replaces 3 (5) dependent launches: reduce colsq, reduce graw, finalise
-// (reduce dot, fit).
+// A large mode's tail in one launch: block g reduces four consecutive
+// entries of one of [colsq | graw | dot] over the nb apply blocks' partials,
+// then the last block to arrive finalises the mode (and, after the last mode,
+// the fit).  Replaces 3 (5) dependent launches: reduce colsq, reduce graw,
+// finalise (reduce dot, fit).
+// Reduction layout: lane (s, q) = (lane >> 2, lane & 3) of warp w reads entry
+// k0 + q of blocks b = 8w + s + 64i -- four adjacent entries of a block's
+// partial row are one 32-byte sector, so every sector fetched is used (the
+// previous one-warp-per-entry layout read a sector per element: 4x the L2
+// traffic at R = 16, 15 us for LBNL's 1184 partial rows); four accumulators
+// per thread, then a fixed shuffle tree over s and a fixed sum over the 8
+// warps: deterministic.
+constexpr int kRedQ = 4;  // entries per reduction block
+__host__ __device__ inline int reduce_groups(int R, bool dot) {
+    const int gs = (R + kRedQ - 1) / kRedQ;
+    return gs + (R * R + kRedQ - 1) / kRedQ + (dot ? gs : 0);
+}
 template <typename T>
 __global__ void __launch_bounds__(256)
     reduce_finalize_kernel(const double *__restrict__ psq, const double *__restrict__ gpart,
@@ -712,25 +723,45 @@ __global__ void __launch_bounds__(256)
                            double *__restrict__ fit, double *__restrict__ trace,
                            int *__restrict__ trace_n) {
     pdl_wait();
-    const int lane = threadIdx.x & 31;
-    const int RR = R * R, ne = RR + R + (pdot ? R : 0);
-    for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < ne;
-         e += (gridDim.x * blockDim.x) >> 5) {
-        const double *part;
-        int stride, k;
-        double *dst;
-        if (e < R) {
-            part = psq, stride = R, k = e, dst = colsq + e;
-        } else if (e < R + RR) {
-            part = gpart, stride = RR, k = e - R, dst = graw + (e - R);
-        } else {
-            part = pdot, stride = R, k = e - R - RR, dst = colsq + R + (e - R - RR);
+    __shared__ double wsum[8][kRedQ];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int RR = R * R, gs = (R + kRedQ - 1) / kRedQ, gg = (RR + kRedQ - 1) / kRedQ;
+    int g = blockIdx.x;
+    const double *part;
+    int stride;
+    double *dst;
+    if (g < gs) {
+        part = psq, stride = R, dst = colsq;
+    } else if ((g -= gs) < gg) {
+        part = gpart, stride = RR, dst = graw;
+    } else {
+        g -= gg;
+        part = pdot, stride = R, dst = colsq + R;
+    }
+    const int k = g * kRedQ + (lane & 3);
+    const bool on = k < stride;  // stride = the array's entry count
+    double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
+    if (on) {
+        const double *p = part + k;
+        int b = 8 * w + (lane >> 2);
+        for (; b + 192 < nb; b += 256) {
+            x0 += p[(int64_t)b * stride];
+            x1 += p[(int64_t)(b + 64) * stride];
+            x2 += p[(int64_t)(b + 128) * stride];
+            x3 += p[(int64_t)(b + 192) * stride];
         }
-        double x = 0.0;
-        for (int b = lane; b < nb; b += 32) x += part[(int64_t)b * stride + k];
+        for (; b < nb; b += 64) x0 += p[(int64_t)b * stride];
+    }
+    double x = (x0 + x1) + (x2 + x3);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if (lane == 0) *dst = x;
+    for (int o = 4; o < 32; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane < kRedQ) wsum[w][lane] = x;
+    __syncthreads();
+    if (threadIdx.x < kRedQ && g * kRedQ + (int)threadIdx.x < stride) {
+        double t = 0.0;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) t += wsum[v][threadIdx.x];
+        dst[g * kRedQ + threadIdx.x] = t;
     }
     __shared__ int last_block;
     __threadfence();
@@ -1821,8 +1852,7 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
             count_launch();
             SPTK_CUDA(cudaGetLastError());
             if (!tail.counter && opt(OPT_FUSED_REDUCE)) {  // one launch: reductions + finalise
-                const int ne = R * R + R + (last ? R : 0);
-                SPTK_CUDA(launch_pdl(reduce_finalize_kernel<T>, (ne + 7) / 8, 256, 0, c.s,
+                SPTK_CUDA(launch_pdl(reduce_finalize_kernel<T>, reduce_groups(R, last), 256, 0, c.s,
                                      (const double *)psq, (const double *)w.gpart.as<double>(),
                                      (const double *)(last ? pdot : nullptr), nb, R, (int)c.Rl,
                                      colsq, graw, An, N, n, (n + 1) % N, s_all, lam,
