@@ -325,7 +325,8 @@ sptk_status sptk_set_tuning(int variant, int64_t run);
  *   L2 windows; served by the cooperative kernel), slice_fill 6 (the slice
  *   traversal halves its slices until its grid has this many blocks per SM; 0
  *   off), fused_reduce 1 (CP-ALS: a large mode's reductions, finalisation and
- *   fit in one launch).
+ *   fit in one launch), prezero_mb 256 (with prezero 1: the MTTKRP outputs of
+ *   at least this many MB are zeroed on the side stream).
  * Every choice gives the same result up to summation order; options change
  * which kernel computes it.  Not synchronised with calls in flight on other
  * threads.  SPTK_EINVAL for an unknown name. */

@@ -2335,7 +2335,8 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t Rl, int max_iters, double 
         // profiles/r02/s2/ab_glue_s13.log)
         bool any = false;
         for (int n = 0; n < N; ++n) {
-            c.pz[n] = opt(OPT_PREZERO) == 2 || es * (size_t)t->dims[n] * R >= ((size_t)256 << 20);
+            c.pz[n] = opt(OPT_PREZERO) == 2 ||
+                      es * (size_t)t->dims[n] * R >= ((size_t)std::max<int64_t>(opt(OPT_PREZERO_MB), 0) << 20);
             any = any || c.pz[n];
         }
         c.prezero = c.prezero && any;

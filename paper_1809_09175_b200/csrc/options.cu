@@ -62,6 +62,7 @@ constexpr OptDef kOpts[] = {
     {"slice_fill", 6},          // slice traversal: halve the slices until the grid has this many
                                 //   blocks per SM (0 = off)
     {"fused_reduce", 1},        // CP-ALS: a large mode's reductions + finalise (+ fit) in one launch
+    {"prezero_mb", 256},        // CP-ALS (prezero 1): outputs of at least this many MB are pre-zeroed
 };
 
 static_assert(sizeof(kOpts) / sizeof(kOpts[0]) == OPT_COUNT, "kOpts must list every Opt, in order");
