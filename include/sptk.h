@@ -210,7 +210,7 @@ sptk_status sptk_mttkrp_rows(sptk_tensor t, int mode, int64_t R, const void *con
  * A_m^T A_m (m != n); A_n = V Gamma^{-1} (Gamma SPD: inverse by unpivoted
  * Gauss-Jordan, whose pivots are the squared Cholesky diagonal; a pivot
  * d_j <= 1e-12 Gamma_jj is a failure (numerically singular Gamma, e.g.
- * duplicate components: DESIGN.md §2 R7); one ridge retry with
+ * duplicate components: DESIGN.md §2 Z23); one ridge retry with
  * 1e-12 tr(Gamma)/R, which needs only d_j > 0); lambda = column 2-norms;
  * normalise.  fit = 1 - ||X - M||
  * / ||X|| after each iteration; stop when tol > 0 and |fit - fit_prev| < tol.

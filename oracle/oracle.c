@@ -213,7 +213,7 @@ void oracle_gram(int64_t I, int64_t R, const double *A, double *G)
 }
 
 /* Cholesky G = L L^T in place (lower triangle of L returned in Lout).
- * Pivot j fails unless d_j > tau * G_jj (DESIGN.md §2 reading R7: a relative
+ * Pivot j fails unless d_j > tau * G_jj (DESIGN.md §2 reading Z23: a relative
  * pivot below 1e-12 is a numerically singular G; tau = 0 is the plain
  * positive-definiteness test). */
 static int chol(int64_t R, const double *G, double *L, double tau)
@@ -251,7 +251,7 @@ static void chol_apply(int64_t R, const double *L, const double *b, double *x)
 
 /* Cholesky factorisation of an SPD matrix with one ridge retry
  * (G + 1e-12 * (tr G / R) * I) when a pivot fails the relative test
- * (DESIGN.md §2 R7; the retry tests d_j > 0), then row-wise solves
+ * (DESIGN.md §2 Z23; the retry tests d_j > 0), then row-wise solves
  * X = B G^{-1} for nrhs rows of B (nrhs x R).  S:347. */
 int oracle_chol_solve(int64_t R, const double *G, int64_t nrhs, const double *B, double *X)
 {

@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-// Pivot test of the first factorisation attempt (DESIGN.md §2 reading R7, as
+// Pivot test of the first factorisation attempt (DESIGN.md §2 reading Z23, as
 // the oracle): pivot j counts as a failure unless d_j > kPivotRel * Gamma_jj.
 // d_j / Gamma_jj is the squared sine of the angle between column j and the
 // span of the columns before it; below 1e-12 Gamma is numerically singular

@@ -897,7 +897,7 @@ def test_cp_als_inverse_kernels(sp, R, inv):
 def test_cp_als_duplicate_components(sp, inv):
     """Two identical CP components in the initial factors make every Gamma
     numerically singular (its pivot is rounding noise, often still positive):
-    DESIGN.md §2 R7 sends every inverse kernel to the ridge retry, like the
+    DESIGN.md §2 Z23 sends every inverse kernel to the ridge retry, like the
     oracle, so the trajectory stays finite, the fit rises monotonically (an
     ALS property), and it stays near the oracle's.  The split of the
     duplicate pair amplifies rounding by ~1/ridge = 1e12 (the oracle's pair

@@ -222,7 +222,7 @@ def test_chol_solve_ridge_branch():
 
 
 def test_chol_solve_relative_pivot_takes_ridge():
-    """DESIGN.md §2 R7: a pivot d_j <= 1e-12 Gamma_jj is a failure even when
+    """DESIGN.md §2 Z23: a pivot d_j <= 1e-12 Gamma_jj is a failure even when
     positive (a numerically singular Gamma, e.g. duplicate CP components).
     Pinned by the 2 x 2 closed form [[a, c], [c, a]]^{-1} = [[a, -c], [-c, a]]
     / (a^2 - c^2): with c = 1 - 2^-46 the pivot is ~2.8e-14 (ridge: a = 1 +
