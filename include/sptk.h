@@ -326,7 +326,9 @@ sptk_status sptk_set_tuning(int variant, int64_t run);
  *   traversal halves its slices until its grid has this many blocks per SM; 0
  *   off), fused_reduce 1 (CP-ALS: a large mode's reductions, finalisation and
  *   fit in one launch), prezero_mb 256 (with prezero 1: the MTTKRP outputs of
- *   at least this many MB are zeroed on the side stream).
+ *   at least this many MB are zeroed on the side stream), zero_in_apply 0 (1:
+ *   those outputs are zeroed by extra blocks of the previous mode's apply
+ *   launch instead of a side-stream memset; deferred single-GPU CP-ALS).
  * Every choice gives the same result up to summation order; options change
  * which kernel computes it.  Not synchronised with calls in flight on other
  * threads.  SPTK_EINVAL for an unknown name. */

@@ -797,7 +797,27 @@ struct ExchOut {
     int np = 0;
     char *peer[kMaxPeers] = {};  // A_n on rank p (byte address in this process)
     char *mc = nullptr;          // multicast address of A_n
+    // option zero_in_apply: the last zb blocks of the launch only zero the
+    // next mode's MTTKRP output (zw 16-byte words at zp) and exit
+    int zb = 0;
+    int64_t zw = 0;
+    uint4 *zp = nullptr;
 };
+
+// The zeroing blocks of an apply launch (ExchOut::zb > 0): blocks
+// [gridDim.x - zb, gridDim.x) store zeros over the next mode's output buffer
+// (a buffer of its own) and return; the rest of the kernel
+// sees nb = gridDim.x - zb blocks.  True for a zeroing block.
+__device__ __forceinline__ bool apply_zero_blocks(const ExchOut &ex) {
+    if (!ex.zb) return false;
+    const int z = (int)blockIdx.x - ((int)gridDim.x - ex.zb);
+    if (z < 0) return false;
+    const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
+    for (int64_t i = (int64_t)z * blockDim.x + threadIdx.x; i < ex.zw;
+         i += (int64_t)ex.zb * blockDim.x)
+        ex.zp[i] = zero;
+    return true;
+}
 
 __device__ __forceinline__ void mm_store(double *p, double v) {
     asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
@@ -813,17 +833,18 @@ __device__ __forceinline__ void mm_store(float *p, float v) {
 // the last mode, the fit.  Called by every thread of every block.
 template <typename T>
 __device__ void apply_tail(const ModeTail &tail, T *__restrict__ A, int R,
-                           const double *part_sq, const double *part_dot, const double *gpart) {
+                           const double *part_sq, const double *part_dot, const double *gpart,
+                           int zb = 0) {
     if (!tail.counter) return;
     const int tid = threadIdx.x;
+    const int nb = (int)gridDim.x - zb, RR = R * R;  // apply blocks (zeroing blocks excluded)
     __shared__ int last_block;
     __threadfence();
     __syncthreads();
-    if (tid == 0) last_block = atomicAdd(tail.counter, 1) == (int)gridDim.x - 1;
+    if (tid == 0) last_block = atomicAdd(tail.counter, 1) == nb - 1;
     __syncthreads();
     if (!last_block) return;
     __threadfence();
-    const int nb = gridDim.x, RR = R * R;
     auto sum_parts = [&](const double *part, int stride, int e) {
         double acc[8];
 #pragma unroll
@@ -866,6 +887,7 @@ __global__ void __launch_bounds__(256, SPTK_APPLY_MINB)
                       double *__restrict__ part_sq, double *__restrict__ part_dot,
                       double *__restrict__ gpart, const ModeTail tail, const ExchOut ex) {
     pdl_wait();
+    if (apply_zero_blocks(ex)) return;
     extern __shared__ __align__(16) double sm[];
     const int RP = (R + 3) & ~3;              // padded row stride (whole 4-column blocks)
     double *Vt = sm;                          // kApplyTile x RP
@@ -1012,7 +1034,7 @@ __global__ void __launch_bounds__(256, SPTK_APPLY_MINB)
         for (int gg = 0; gg < groups; ++gg) acc += gs[((size_t)gg * nblk + b) * 16 + q];
         if (a < R && c < R) gp[a * R + c] = gp[c * R + a] = acc;
     }
-    apply_tail<T>(tail, A, R, part_sq, part_dot, gpart);
+    apply_tail<T>(tail, A, R, part_sq, part_dot, gpart, ex.zb);
 }
 
 // Warp-private variant of apply_gram (round 2; option apply_warp): no block-wide
@@ -1040,6 +1062,7 @@ __global__ void __launch_bounds__(256, 2)
                            double *__restrict__ part_sq, double *__restrict__ part_dot,
                            double *__restrict__ gpart, const ModeTail tail, const ExchOut ex) {
     pdl_wait();
+    if (apply_zero_blocks(ex)) return;
     constexpr int RPW = 32 / LR;
     extern __shared__ __align__(16) double wsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
@@ -1057,7 +1080,7 @@ __global__ void __launch_bounds__(256, 2)
     }
     double sq = 0.0, dot = 0.0;
     const int64_t ngroups = (r_end - r_begin + RPW - 1) / RPW;
-    const int64_t wstride = (int64_t)gridDim.x * 8;
+    const int64_t wstride = (int64_t)(gridDim.x - ex.zb) * 8;
     auto load_v = [&](int64_t grp) {
         const int64_t r = r_begin + grp * RPW + rs;
         return (grp < ngroups && r < r_end && j < R) ? (double)V[r * R + j] : 0.0;
@@ -1135,7 +1158,7 @@ __global__ void __launch_bounds__(256, 2)
         part_sq[(int64_t)blockIdx.x * R + c] = a2;
         if (part_dot) part_dot[(int64_t)blockIdx.x * R + c] = d2;
     }
-    apply_tail<T>(tail, A, R, part_sq, part_dot, gpart);
+    apply_tail<T>(tail, A, R, part_sq, part_dot, gpart, ex.zb);
 }
 
 // ------------------------------------------ apply_gram on the FP64 tensor cores
@@ -1187,6 +1210,7 @@ __global__ void __launch_bounds__(256, SPTK_APPLY_MMA_MINB)
                           double *__restrict__ part_sq, double *__restrict__ part_dot,
                           double *__restrict__ gpart, const ModeTail tail, const ExchOut ex) {
     pdl_wait();
+    if (apply_zero_blocks(ex)) return;
     constexpr int RR = 8 * RB;       // == R
     constexpr int PL = RR * 8 / 32;  // V / A_raw tile doubles per lane (2 RB)
     constexpr int NB = RB * (RB + 1) / 2;
@@ -1212,7 +1236,7 @@ __global__ void __launch_bounds__(256, SPTK_APPLY_MMA_MINB)
 #pragma unroll
     for (int nb = 0; nb < RB; ++nb) dacc[nb][0] = dacc[nb][1] = 0.0;
     const int64_t ntile = (r_end - r_begin + 7) / 8;
-    const int64_t wstride = (int64_t)gridDim.x * 8;
+    const int64_t wstride = (int64_t)(gridDim.x - ex.zb) * 8;
     // lane's slice of a V tile: row lane / (32/8... ) -- tile doubles [PL*lane, PL*lane + PL)
     auto load_tile = [&](int64_t ti, double (&v)[PL]) {
         const int64_t e0 = (r_begin + ti * 8) * RR + (int64_t)lane * PL;  // element index
@@ -1354,7 +1378,7 @@ __global__ void __launch_bounds__(256, SPTK_APPLY_MMA_MINB)
         part_sq[(int64_t)blockIdx.x * RR + c] = a2;
         if (part_dot) part_dot[(int64_t)blockIdx.x * RR + c] = d2;
     }
-    apply_tail<T>(tail, A, RR, part_sq, part_dot, gpart);
+    apply_tail<T>(tail, A, RR, part_sq, part_dot, gpart, ex.zb);
 }
 
 // apply_gram grid cap: one full wave of resident blocks (SPTK_APPLY_WAVE=0: the
@@ -1568,6 +1592,7 @@ struct AlsCtx {
     // earlier in the same iteration (its MTTKRP waits for ev_zero[m]);
     // otherwise in the previous iteration (graph launches are serialised).
     bool prezero = false;
+    bool zapply = false;   // option zero_in_apply: pre-zeroing by the previous mode's apply launch
     bool copy_fit = true;  // per-iteration D2H of (fit, status) inside the iteration
     void *vbuf[3] = {};
     int vb[kMaxModes] = {};
@@ -1686,25 +1711,25 @@ static cudaError_t run_apply(const ApplyPlan &p, cudaStream_t s, const T *V, int
                              const ExchOut &ex) {
     if (p.mma) {
         if (p.LR == 8)
-            return launch_pdl(apply_gram_mma_kernel<T, 1>, p.nb, 256, p.smb, s, V, r0, r1, R, Ginv,
+            return launch_pdl(apply_gram_mma_kernel<T, 1>, p.nb + ex.zb, 256, p.smb, s, V, r0, r1, R, Ginv,
                               An, psq, pdot, gpart, tail, ex);
-        return launch_pdl(apply_gram_mma_kernel<T, 2>, p.nb, 256, p.smb, s, V, r0, r1, R, Ginv, An,
+        return launch_pdl(apply_gram_mma_kernel<T, 2>, p.nb + ex.zb, 256, p.smb, s, V, r0, r1, R, Ginv, An,
                           psq, pdot, gpart, tail, ex);
     }
     if (p.warp) {
         if (p.LR == 8)
-            return launch_pdl(apply_gram_warp_kernel<T, 8>, p.nb, 256, p.smb, s, V, r0, r1, R, Ginv,
+            return launch_pdl(apply_gram_warp_kernel<T, 8>, p.nb + ex.zb, 256, p.smb, s, V, r0, r1, R, Ginv,
                               An, psq, pdot, gpart, tail, ex);
         if (p.LR == 16)
-            return launch_pdl(apply_gram_warp_kernel<T, 16>, p.nb, 256, p.smb, s, V, r0, r1, R, Ginv,
+            return launch_pdl(apply_gram_warp_kernel<T, 16>, p.nb + ex.zb, 256, p.smb, s, V, r0, r1, R, Ginv,
                               An, psq, pdot, gpart, tail, ex);
-        return launch_pdl(apply_gram_warp_kernel<T, 32>, p.nb, 256, p.smb, s, V, r0, r1, R, Ginv,
+        return launch_pdl(apply_gram_warp_kernel<T, 32>, p.nb + ex.zb, 256, p.smb, s, V, r0, r1, R, Ginv,
                           An, psq, pdot, gpart, tail, ex);
     }
     if (R <= 16)
-        return launch_pdl(apply_gram_kernel<T, 16>, p.nb, 256, p.smb, s, V, r0, r1, R, p.rpb,
+        return launch_pdl(apply_gram_kernel<T, 16>, p.nb + ex.zb, 256, p.smb, s, V, r0, r1, R, p.rpb,
                           p.tile, Ginv, An, psq, pdot, gpart, tail, ex);
-    return launch_pdl(apply_gram_kernel<T, 32>, p.nb, 256, p.smb, s, V, r0, r1, R, p.rpb, p.tile,
+    return launch_pdl(apply_gram_kernel<T, 32>, p.nb + ex.zb, 256, p.smb, s, V, r0, r1, R, p.rpb, p.tile,
                       Ginv, An, psq, pdot, gpart, tail, ex);
 }
 
@@ -1806,7 +1831,7 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
         count_launch();
         SPTK_CUDA(cudaGetLastError());
         SPTK_CUDA(cudaEventRecord(w.ev_inv, w.side));
-        if (c.prezero) {  // the buffer mode n-1's apply released, for its next user
+        if (c.prezero && !c.zapply) {  // the buffer mode n-1's apply released, for its next user
             const int m = c.znext[n];
             if (c.pz[m]) {
                 SPTK_CUDA(cudaMemsetAsync(c.vbuf[c.vb[m]], 0, sizeof(T) * (size_t)t->dims[m] * R,
@@ -1847,8 +1872,16 @@ static sptk_status enqueue_iteration_fused(AlsCtx &c) {
             tail.n = n;
             tail.next = (n + 1) % N;
             tail.Rl = (int)c.Rl;
+            ExchOut zex{};
+            const int nx = (n + 1) % N;
+            if (c.zapply && c.pz[nx]) {  // zero the next mode's output from extra blocks
+                const size_t bytes = sizeof(T) * (size_t)t->dims[nx] * R;
+                zex.zp = static_cast<uint4 *>(c.vbuf[c.vb[nx]]);
+                zex.zw = (int64_t)(bytes / 16);
+                zex.zb = dev_sms() * 2;
+            }
             SPTK_CUDA(run_apply<T>(ap, c.s, V, 0, I, R, Ginv, An, psq, last ? pdot : nullptr,
-                                   w.gpart.as<double>(), tail, ExchOut{}));
+                                   w.gpart.as<double>(), tail, zex));
             count_launch();
             SPTK_CUDA(cudaGetLastError());
             if (!tail.counter && opt(OPT_FUSED_REDUCE)) {  // one launch: reductions + finalise
@@ -2346,6 +2379,9 @@ static sptk_status cp_als_impl(sptk_tensor t, int64_t Rl, int max_iters, double 
     // deferred normalisation state (single GPU, R <= 32): all scales 1, and the
     // first MTTKRP's column weights 1
     const bool deferred = (!multi || c.sym_iter) && deferred_norm(R);
+    // the fused deferred iteration zeroes a pre-zeroed output from extra
+    // blocks of the previous mode's apply instead of a side-stream memset
+    c.zapply = c.prezero && deferred && !multi && opt(OPT_ZERO_IN_APPLY) != 0;
     if (deferred) {
         double *s_all = w.scl.as<double>();
         fill_f64_kernel<<<(unsigned)((N * R + 255) / 256), 256, 0, s>>>(s_all, N * (int)R, 1.0);

@@ -52,7 +52,7 @@ enum Opt {
     OPT_RUN, OPT_VARIANT, OPT_SLICE, OPT_SLICE_L2_KB, OPT_SLICE_ROWS, OPT_SLICE_OTHER_FIRST,
     OPT_ROWREC, OPT_FORCE_V, OPT_GENERIC, OPT_DEBUG_DISPATCH, OPT_COPY_ORDER, OPT_DEFERRED_NORM,
     OPT_NO_GRAPH, OPT_GAMMA_INV_CHOL, OPT_USE_COPY, OPT_APPLY_TILE, OPT_APPLY_NB_MULT, OPT_TAIL_ROWS, OPT_APPLY_WAVE, OPT_APPLY_WARP,
-    OPT_KEEP_KEYS, OPT_PDL, OPT_EXCHANGE, OPT_PAD_RANK, OPT_SORT_V1, OPT_PREZERO, OPT_APPLY_MMA, OPT_GJ_WARP, OPT_SIDE_PRIO, OPT_WIN, OPT_SLICE_FILL, OPT_FUSED_REDUCE, OPT_PREZERO_MB, OPT_COUNT
+    OPT_KEEP_KEYS, OPT_PDL, OPT_EXCHANGE, OPT_PAD_RANK, OPT_SORT_V1, OPT_PREZERO, OPT_APPLY_MMA, OPT_GJ_WARP, OPT_SIDE_PRIO, OPT_WIN, OPT_SLICE_FILL, OPT_FUSED_REDUCE, OPT_PREZERO_MB, OPT_ZERO_IN_APPLY, OPT_COUNT
 };
 int64_t opt(Opt o);
 uint64_t options_generation();  // bumped by every sptk_set_option / sptk_reset_options

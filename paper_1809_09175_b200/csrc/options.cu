@@ -63,6 +63,7 @@ constexpr OptDef kOpts[] = {
                                 //   blocks per SM (0 = off)
     {"fused_reduce", 1},        // CP-ALS: a large mode's reductions + finalise (+ fit) in one launch
     {"prezero_mb", 256},        // CP-ALS (prezero 1): outputs of at least this many MB are pre-zeroed
+    {"zero_in_apply", 0},       // CP-ALS: pre-zero from extra blocks of the previous mode's apply
 };
 
 static_assert(sizeof(kOpts) / sizeof(kOpts[0]) == OPT_COUNT, "kOpts must list every Opt, in order");

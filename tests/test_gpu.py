@@ -859,13 +859,15 @@ def test_cp_als_prezeroed_outputs(sp, dims):
     """The MTTKRP outputs zeroed on the side stream for the next mode (two
     buffers for even N, three for odd N; some zeroed in the same iteration,
     some in the previous one) give the oracle's trajectory, like zeroing in
-    every launch (prezero=0), eagerly and through the replayed graph."""
+    every launch (prezero=0), eagerly and through the replayed graph; also
+    when the previous mode's apply launch zeroes it (zero_in_apply)."""
     P = min(int(np.prod(dims)) // 3, 4000)
     idx, vals = synth.unique_tensor(51, dims, P)
     R = 8
     ref = oracle.cp_als(dims, idx, vals, factors_np(52, dims, R), 7)
     t = make(sp, dims, idx, vals)
-    for opts in ({"prezero": 2}, {"prezero": 0}, {"prezero": 2, "no_graph": 1}):
+    for opts in ({"prezero": 2}, {"prezero": 0}, {"prezero": 2, "no_graph": 1},
+                 {"prezero": 2, "zero_in_apply": 1}, {"prezero": 2, "zero_in_apply": 1, "no_graph": 1}):
         with sp.options(**opts):
             F = [torch.full((I, R), float("nan"), dtype=torch.float64, device="cuda") for I in dims]
             res = sp.cp_als(t, R, 7, F, seed=52)

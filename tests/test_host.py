@@ -143,7 +143,7 @@ def test_every_documented_option_exists_with_its_default(sp):
     hdr = open(os.path.join(ROOT, "include", "sptk.h")).read()
     doc = hdr[hdr.index("sptk_set_option") - 7000:hdr.index("sptk_status sptk_set_option")]
     defaults = {"pad_rank": 1, "sort_v1": 0, "prezero": 1, "apply_mma": 1, "gj_warp": 1,
-                "side_prio": -1, "win": 0, "slice_fill": 6, "fused_reduce": 1, "prezero_mb": 256, "exchange": -1,
+                "side_prio": -1, "win": 0, "slice_fill": 6, "fused_reduce": 1, "prezero_mb": 256, "zero_in_apply": 0, "exchange": -1,
                 "pdl": 1, "keep_keys": 1, "tail_rows": 8192, "slice": 1, "slice_l2_kb": 32768}
     sp.reset_options()
     for name, value in defaults.items():
