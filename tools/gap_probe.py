@@ -4,6 +4,7 @@ combinations of {restart from the generator factors, continue} x {fit
 history on, off}, interleaved.  Usage: gap_probe.py [config] [K] [rounds]"""
 import os
 import statistics
+import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -28,6 +29,11 @@ F = [f.clone() for f in F0]
 s = torch.cuda.current_stream()
 res = {}
 sp.cp_als(t, R, K, F, init=F, trace=True)
+smi = None
+if os.environ.get("GP_SMI") == "1":  # bench.py's clock sampler, polling every 100 ms
+    smi = subprocess.Popen(["nvidia-smi", "-i", "0", "--query-gpu=clocks.sm,clocks.max.sm,"
+                            "clocks_event_reasons.active", "--format=csv,noheader,nounits",
+                            "-lms", "100"], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
 for r in range(rounds):
     for restart in (True, False):
         for trace in (True, False):
@@ -41,6 +47,8 @@ for r in range(rounds):
             b.record(s)
             torch.cuda.synchronize()
             res.setdefault((restart, trace), []).append(a.elapsed_time(b) / K)
+if smi:
+    smi.terminate()
 for (restart, trace), v in res.items():
-    print(f"{name} K={K} restart={restart} trace={trace}: ms/iter median {statistics.median(v):.4f} "
+    print(f"{name} K={K} smi={smi is not None} restart={restart} trace={trace}: ms/iter median {statistics.median(v):.4f} "
           f"(runs {' '.join(f'{x:.4f}' for x in v)})", flush=True)
