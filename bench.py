@@ -359,10 +359,8 @@ def main():
             reps.append(a.elapsed_time(b))
         perm_ms.append(sorted(reps)[1])
     F = [sdev.factor(c.seed_f, c.N, m, I, R, dtype=tdt) for m, I in enumerate(c.dims)]
-    # every measured pass starts from these generator factors (iterations
-    # 1..K): CP-ALS on the random LBNL-shaped tensor collapses columns after
-    # ~50 iterations (lambda_j -> 0) and can then meet a singular Gamma, so the
-    # passes do not continue each other into that regime
+    # every measured pass starts from these generator factors, so each one
+    # times the same iterations 1..K
     F0 = [f.clone() for f in F]
 
     def reset_factors():
